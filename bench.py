@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""bench.py -- batched additive-kernel MVM throughput on B200 (BASELINE.json metric).
+
+One "step" is one pass of the hot path: a single
+``akm_kernel_mvm_multi`` call through the C ABI producing every product the workload requests
+(e.g. c2: K-hat v and dK-hat/d ell v), on inputs already resident in HBM.  set_points / set_theta
+(S0/S1, once per X / theta) run before the timed region.
+
+  value  = n * r * windows / (device time per step)            [pts/s, whole job over N GPUs]
+  e2e    = the same through the C ABI with pinned HOST V and outputs (H2D + D2H inside the timing)
+  roofline: the dominant kernel (from in-library CUDA events on the launching stream) against the
+           FP64 FMA peak (the path is FP64-ALU bound)
+  cpu_baseline: the float64 dense oracle (oracle/dense.c) on a bounded row sample, rank 0, N = 1
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+Under torchrun (N > 1) every rank runs its own independent RHS block of the same workload
+(weak scaling, no data-path collective) and rank 0 prints the max-over-ranks
+timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+PEAK_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: SMs x FP64 FMA/clk/SM x 2 x max SM clock
+MEASURED_FP64 = {"dfma_tflops": 34.1, "dmma_tflops": 37.1, "source": "profiles/r01_fp64_peaks.txt"}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+
+    @staticmethod
+    def one_shot(gpu_index):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={ClockSampler.Q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20).stdout
+            return [l.strip() for l in out.splitlines() if l.strip()]
+        except Exception:
+            return []
+
+    def summary(self, extra_lines=()):
+        rows = []
+        for line in list(self.lines) + list(extra_lines):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[4:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for _, _, flags in rows:
+            for nm, fl in zip(names, flags[1:5]):
+                if fl.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def algorithmic_counts(wl, info, r, ops):
+    """FP64 flops of spreading / interpolation and minimal bytes of one step."""
+    n, W = wl.n, len(wl.windows)
+    d = [len(w) for w in wl.windows]
+    taps = [(2 * wl.m) ** dw for dw in d]
+    n_ops = len({"K" if o in ("K", "dsf") else o for o in ops})      # distinct operators interpolated
+    spread_flops = sum(2.0 * n * r * t for t in taps)
+    interp_flops = sum(2.0 * n * r * t * n_ops for t in taps)
+    ntap = [int(np.prod(b)) for b in info["box"]]
+    grid_bytes = sum(8.0 * nt * r * (2 + 2 * n_ops) for nt in ntap)
+    bytes_ = 2 * 8.0 * n * sum(d) + 8.0 * n * r * (1 + len(ops)) + grid_bytes
+    return spread_flops, interp_flops, bytes_
+
+
+def run_reference(args, wl):
+    """The reference arm: the CPU float64 dense oracle timed as it stands on bounded row samples."""
+    from oracle import dense_apply
+    X = workloads.make_X(wl)
+    V = workloads.make_V(wl)
+    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    rows_all = workloads.make_rows(wl, wl.n)
+    # calibrate the sample so that each step is ~1-3 s of CPU work
+    t0 = time.perf_counter()
+    dense_apply(X, wl.windows, wl.family, theta, V, rows=rows_all[:64], ops=wl.ops)
+    per_row = (time.perf_counter() - t0) / 64
+    rows_per_step = int(min(wl.n, max(64, 2.0 / max(per_row, 1e-9))))
+    times = []
+    for s in range(args.warmup + args.steps):
+        rows = rows_all[(s * rows_per_step) % max(1, wl.n - rows_per_step + 1):][:rows_per_step]
+        t0 = time.perf_counter()
+        dense_apply(X, wl.windows, wl.family, theta, V, rows=rows, ops=wl.ops)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    full_equiv = t * wl.n / rows_per_step
+    value = wl.units / full_equiv
+    cores = os.cpu_count()
+    sample = f"{rows_per_step} of {wl.n} rows per step (dense direct sums, all {wl.n} columns), extrapolated x{wl.n / rows_per_step:.1f}"
+    line = {
+        "impl": "reference", "metric": "batched K-hat V throughput (n*r*windows pts/s)", "value": value,
+        "unit": "pts/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_equiv * 1e3,
+        "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(wl),
+        "cpu_baseline": {"value": value, "unit": "pts/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "pts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(wl):
+    return {"workload": wl.name, "description": wl.description, "n": wl.n, "r": wl.r, "windows": len(wl.windows),
+            "d": [len(w) for w in wl.windows], "family": "gaussian" if wl.family == 0 else "matern12",
+            "N": wl.N, "sigma_over": wl.sigma_over, "m": wl.m, "ops": list(wl.ops),
+            "l2": "256 MiB written between timed steps (L2 flush)"}
+
+
+def cpu_baseline(wl, budget_s=10.0):
+    from oracle import dense_apply
+    X = workloads.make_X(wl)
+    V = workloads.make_V(wl)
+    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    rows_all = workloads.make_rows(wl, wl.n)
+    t0 = time.perf_counter()
+    dense_apply(X, wl.windows, wl.family, theta, V, rows=rows_all[:32], ops=wl.ops)
+    per_row = max((time.perf_counter() - t0) / 32, 1e-9)
+    nrows = int(min(wl.n, max(32, budget_s / per_row)))
+    t0 = time.perf_counter()
+    dense_apply(X, wl.windows, wl.family, theta, V, rows=rows_all[:nrows], ops=wl.ops)
+    t = time.perf_counter() - t0
+    value = nrows * wl.r * len(wl.windows) / t
+    return {"value": value, "unit": "pts/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{nrows} seeded rows of {wl.n} (all columns) of the dense float64 products {list(wl.ops)}; "
+                      f"{t:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-launches", action="store_true", help="short run for ncu launch lists")
+    args = ap.parse_args()
+    wl = workloads.CONFIGS[args.config]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, wl)
+        return
+
+    import torch
+    import paper_2504_00480_b200 as akm
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    X = workloads.make_X(wl)
+    V = workloads.make_V(wl, seed=2000 + wl.index + 7919 * rank)  # independent RHS block per rank
+    Xd = torch.from_numpy(X).to(dev)
+    Vd = torch.from_numpy(V).to(dev)
+    outs = {op: torch.empty_like(Vd) for op in wl.ops}
+    stream = torch.cuda.current_stream(dev)
+
+    plan = akm.Plan(local)
+    plan.set_points(Xd, wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+    t0 = time.perf_counter()
+    plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    set_theta_ms = (time.perf_counter() - t0) * 1e3
+    info = plan.info()
+
+    def step():
+        plan.mvm_multi(Vd, Y=outs.get("K"), dY_ell=outs.get("dell"), dY_sf=outs.get("dsf"))
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    K = args.steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    plan.stage_times(reset=True)
+    plan.set_profiling(True)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(K):
+        flush.fill_(float(i))
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    sampler.stop()
+    plan.set_profiling(False)
+    tail = ClockSampler.one_shot(local)
+    stages = plan.stage_times(reset=True)
+    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / K
+    value = wl.units * world / (ms_per_step * 1e-3)
+
+    # ---------------- e2e: same call with pinned host V and outputs
+    Vh = torch.from_numpy(V).pin_memory()
+    Oh = {op: torch.empty(V.shape, dtype=torch.float64).pin_memory() for op in wl.ops}
+    for _ in range(3):
+        plan.mvm_multi(Vh, Y=Oh.get("K"), dY_ell=Oh.get("dell"), dY_sf=Oh.get("dsf"), stream=stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    e_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if dist:
+        dist.barrier()
+    for i in range(K):
+        flush.fill_(float(i))
+        e_s[i].record(stream)
+        plan.mvm_multi(Vh, Y=Oh.get("K"), dY_ell=Oh.get("dell"), dY_sf=Oh.get("dsf"), stream=stream.cuda_stream)
+        e_e[i].record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = sum(s.elapsed_time(e) for s, e in zip(e_s, e_e))
+    if dist:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = wl.units * world / (e2e_ms / K * 1e-3)
+
+    # ---------------- roofline of the dominant kernel
+    spread_fl, interp_fl, alg_bytes = algorithmic_counts(wl, info, wl.r, wl.ops)
+    cand = []
+    if stages["spread_launches"]:
+        cand.append(("spread", stages["spread_ms"], stages["spread_launches"], spread_fl))
+    if stages["interp_launches"]:
+        cand.append(("interp", stages["interp_ms"], stages["interp_launches"], interp_fl))
+    name, st_ms, launches, flops = max(cand, key=lambda c: c[1])
+    per_launch_ms = st_ms / launches
+    flops_per_launch = flops / (launches / K)
+    achieved = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
+    peaks = _peaks()
+    stage_total = stages["spread_ms"] + stages["fft_ms"] + stages["interp_ms"] + stages["epilogue_ms"]
+    clocks = sampler.summary(tail)
+
+    line = {
+        "metric": "batched K-hat V throughput (n*r*windows pts/s)",
+        "value": value, "unit": "pts/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": config_dict(wl),
+        "e2e": {"value": e2e_value, "unit": "pts/s", "h2d_bytes_per_step": int(V.nbytes),
+                "d2h_bytes_per_step": int(V.nbytes * len(wl.ops))},
+        "gpu_launches": int(stages["kernel_launches"]),
+        "roofline": {"bound": "alu", "kernel": name, "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
+                     "peak_note": "FP64 FMA: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz; measured DFMA 34.1 / DMMA 37.1 "
+                                  "TFLOP/s (profiles/r01_fp64_peaks.txt)",
+                     "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": per_launch_ms},
+        "stages_ms_per_step": {k: stages[k + "_ms"] / K for k in ("spread", "fft", "interp", "epilogue")},
+        "stage_share": {k: stages[k + "_ms"] / stage_total for k in ("spread", "fft", "interp", "epilogue")},
+        "hbm": {"algorithmic_bytes_per_step": alg_bytes, "achieved_gbs": alg_bytes / (ms_per_step * 1e-3) / 1e9,
+                "peak_gbs": peaks.get("hbm_gbs"), "frac": alg_bytes / (ms_per_step * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)},
+        "set_theta_ms": set_theta_ms,
+        "plan": {"bin": info["bin"], "box": info["box"], "c_w": info["c_w"], "work_items_spread": info["work_items_spread"],
+                 "work_items_interp": info["work_items_interp"], "max_bin_points": info["max_bin_points"]},
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl)
+    plan.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

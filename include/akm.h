@@ -1,0 +1,154 @@
+/*
+ * akm.h -- C ABI of the B200-native additive-kernel MVM (NFFT fast summation).
+ *
+ * The library applies, to an n x r block V, the regularized additive kernel matrix
+ *     Khat = sigma_f^2 (K_1 + ... + K_P) + sigma_eps^2 I
+ * and its hyperparameter derivatives
+ *     dKhat/dell     = sigma_f^2 sum_w K_w^der                             (eq. 2.3)
+ *     dKhat/dsigma_f = 2 sigma_f sum_w K_w,  dKhat/dsigma_eps = 2 sigma_eps I ("straightforward")
+ * where K_w is the Gaussian or Matern(1/2) sub-kernel (eqs. 1.1/2.2) over
+ * feature window W_w of d_w <= 3 coordinates (eq. 2.1).  Each K_w v is evaluated by
+ * NFFT fast summation (eq. 3.3): the window's points are scaled into the ball of
+ * radius 1/4 - eps_B/2, the kernel is replaced by its truncated Fourier series with the
+ * coefficients b_k of eq. (3.2) on N^d frequencies, and the two sums of eq. (3.3)
+ * are done by an adjoint NFFT (spreading with a Kaiser-Bessel window onto the oversampled grid
+ * of (sigma N)^d points, App. A), a d-dimensional DFT, multiplication by b_k and
+ * the window deconvolution, an inverse DFT, and an NFFT (interpolation).  The ell-derivative
+ * uses the derivative kernel's coefficients (eq. 3.5).
+ *
+ * Notation: N = the paper's bandwidth m (Fourier coefficients per axis); m = the paper's window
+ * support parameter s (grid cells on each side); sigma_over = the paper's oversampling sigma.
+ *
+ * Conventions
+ *   - All floating point is IEEE float64.  Row-major n x p (X) and n x r (V, Y) blocks.
+ *   - Pointers: X, V, Y, dY may be DEVICE pointers (cudaMalloc / torch CUDA tensors) or HOST
+ *     pointers (pinned or pageable); host buffers are staged through library-owned device
+ *     memory with cudaMemcpyAsync on the given stream (for pageable memory the call returns
+ *     after the copies complete).  win_feat / win_len / c_w are always host pointers.
+ *   - All calls are stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *     set_points / set_theta synchronise `stream` once (they read back small histograms).
+ *     The MVM calls are asynchronous for device buffers.
+ *   - Ownership: the caller owns X, V, Y, dY and the stream.  The plan owns every workspace
+ *     (scaled/sorted coordinates, permutation, grids, spectra, multiplier tables), grows it on
+ *     demand, and frees it in akm_destroy.  set_points copies what it needs from X.
+ *   - State machine: create -> set_points -> set_theta -> mvm*.  set_points invalidates theta.
+ *     MVM calls before both setters return AKM_ERR_STATE.
+ *   - Errors are returned synchronously; the message of the last error is akm_last_error().
+ *     A device fault surfaces as AKM_ERR_CUDA on the call that observes it.
+ *   - A plan is not thread-safe; distinct plans are independent.
+ */
+#ifndef AKM_H
+#define AKM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct akm_plan akm_plan; /* opaque, library-owned */
+
+typedef enum {
+  AKM_OK = 0,
+  AKM_ERR_INVALID_ARG = 1, /* bad size/stride/window/parameter                              */
+  AKM_ERR_NONFINITE = 2,   /* NaN/Inf in X or theta                                          */
+  AKM_ERR_STATE = 3,       /* call out of order (e.g. mvm before set_theta)                  */
+  AKM_ERR_OOM = 4,         /* device allocation failed                                       */
+  AKM_ERR_CUDA = 5,        /* CUDA runtime / kernel error                                    */
+  AKM_ERR_UNSUPPORTED = 6  /* legal but not implemented (e.g. window support m not in {4,6,8}) */
+} akm_status;
+
+typedef enum { AKM_GAUSSIAN = 0, AKM_MATERN12 = 1 } akm_family;
+typedef enum { AKM_D_ELL = 0, AKM_D_SIGMA_F = 1, AKM_D_SIGMA_EPS = 2 } akm_param;
+
+#define AKM_MAX_WINDOWS 32
+
+typedef struct {
+  int64_t n;
+  int32_t p, P, N, m, n_g;           /* n_g = sigma_over * N (oversampled grid per axis)     */
+  int32_t family;
+  double sigma_f, ell, sigma_eps;
+  int32_t d[AKM_MAX_WINDOWS];        /* window dimensions                                    */
+  double c_w[AKM_MAX_WINDOWS];       /* scale factors: x~ = (x - center_w) / c_w             */
+  double ell_eff[AKM_MAX_WINDOWS];   /* ell / c_w                                            */
+  double radius[AKM_MAX_WINDOWS];    /* R_w = max_i ||x_i^W - center_w||_2 (user units)      */
+  int32_t box[AKM_MAX_WINDOWS][3];   /* grid box extent per axis (leading axes 1 if d < 3)   */
+  int32_t bin[AKM_MAX_WINDOWS];      /* bin edge (grid cells) used by spreading/interpolation */
+  int64_t occupied_bins[AKM_MAX_WINDOWS];
+  int64_t max_bin_points[AKM_MAX_WINDOWS];
+  int64_t work_items_spread, work_items_interp;
+  int64_t workspace_bytes;
+} akm_info;
+
+/* Create an empty plan on CUDA device `device`.  *out receives the plan (NULL on error). */
+akm_status akm_create(akm_plan** out, int device);
+
+/* Set the points and feature windows (eq. 2.1) and the NFFT parameters.
+ *   X        n x p row-major float64, leading dimension ldx >= p (device or host)
+ *   win_feat concatenated 0-based feature ids of the P windows (host), win_len[P] in {1,2,3};
+ *            windows must be pairwise disjoint and ids in [0, p)
+ *   family   AKM_GAUSSIAN (kappa^G) or AKM_MATERN12 (kappa^M)   (eq. 2.2)
+ *   N        even >= 4 (bandwidth, paper's m, index set I_N = {-N/2..N/2-1}^d)
+ *   sigma_over > 1 with sigma_over*N an even integer n_g (oversampling, App. A)
+ *   m        window half-support in grid cells (paper's s); supported: 4, 6, 8; need 4m <= n_g
+ *   eps_B    in [0, 1/2): points are scaled into the ball of radius 1/4 - eps_B/2
+ * Errors: INVALID_ARG (sizes, windows, parameters), NONFINITE (X), UNSUPPORTED (m), OOM, CUDA.
+ * n == 0 is legal (every product is then empty). */
+akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p, int64_t ldx,
+                          const int32_t* win_feat, const int32_t* win_len, int32_t P, int32_t family,
+                          int32_t N, double sigma_over, int32_t m, double eps_B, void* stream);
+
+/* Set theta = (sigma_f, ell, sigma_eps); all must be finite and > 0 (sigma_eps >= 0).
+ * Recomputes the per-window scale factors (reading R2), re-bins the points when a
+ * scale factor changed, and rebuilds the coefficient tables b_k (eq. 3.2) of kappa and
+ * kappa^der at ell_eff = ell / c_w and the multiplier tables (window deconvolution). */
+akm_status akm_set_theta(akm_plan* plan, double sigma_f, double ell, double sigma_eps, void* stream);
+
+/* Y = Khat V.  V: n x r (ld ldv >= r), Y: n x r (ld ldy >= r).  r >= 1. */
+akm_status akm_kernel_mvm(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y, int64_t ldy,
+                          void* stream);
+
+/* dY = (dKhat / d theta_which) V for which in {AKM_D_ELL, AKM_D_SIGMA_F, AKM_D_SIGMA_EPS}. */
+akm_status akm_kernel_deriv_mvm(akm_plan* plan, int32_t which, const double* V, int64_t ldv, int32_t r,
+                                double* dY, int64_t ldy, void* stream);
+
+/* Fused form sharing spreading and the forward DFT: any of Y, dY_ell, dY_sf may be NULL
+ * (at least one non-NULL).  All outputs use the same leading dimension ldy. */
+akm_status akm_kernel_mvm_multi(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y,
+                                double* dY_ell, double* dY_sf, int64_t ldy, void* stream);
+
+/* Plan description (scale factors, grid boxes, bin sizes, workspace). */
+akm_status akm_get_info(const akm_plan* plan, akm_info* out);
+
+/* Test hook: freeze the per-window scale factors c_w (host array of P entries) or restore the
+ * automatic rule (c_w == NULL).  Takes effect at the next akm_set_theta.  Every frozen c_w must
+ * keep all scaled points inside the radius-(1/4 - eps_B/2) ball, else INVALID_ARG. */
+akm_status akm_set_scale_override(akm_plan* plan, const double* c_w);
+
+/* Message of the last error on this plan ("" if none).  Valid until the next call. */
+const char* akm_last_error(const akm_plan* plan);
+
+/* Free the plan and all its device memory (NULL is a no-op).  Synchronises the device. */
+void akm_destroy(akm_plan* plan);
+
+/* Profiling hooks (used by bench.py).  While enabled, every MVM call records CUDA events on the
+ * caller's stream around its stages (spreading S2, DFT/multiply/inverse DFT S3-S5,
+ * interpolation S6, epilogue S7); akm_get_stage_times synchronises on them and returns the
+ * accumulated device milliseconds per stage.  kernel_launches counts the library's own kernel
+ * launches issued by MVM calls (always counted).  reset != 0 clears the accumulators. */
+typedef struct {
+  double spread_ms, fft_ms, interp_ms, epilogue_ms;
+  int64_t calls;
+  int64_t kernel_launches;
+  int64_t spread_launches, interp_launches;
+} akm_stage_times;
+akm_status akm_set_profiling(akm_plan* plan, int32_t enable);
+akm_status akm_get_stage_times(akm_plan* plan, akm_stage_times* out, int32_t reset);
+
+/* Library version string. */
+const char* akm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AKM_H */

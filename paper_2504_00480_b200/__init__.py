@@ -1,0 +1,296 @@
+"""paper_2504_00480_b200 -- B200-native additive-kernel MVM by NFFT fast summation (arXiv 2504.00480).
+
+Thin Python binding of the C ABI in ``include/akm.h`` (``libakm.so``, built in-tree for
+sm_100a by ``_build.py`` / ``__graft_entry__.build()``).  This module only marshals arguments:
+every step of the product runs in the library's CUDA kernels.  There is no CPU fallback -- if
+the shared library is missing, importing the package raises ``ImportError``.
+
+Module-level functions carry the C names (``akm_create``, ``akm_set_points``, ``akm_set_theta``,
+``akm_kernel_mvm``, ``akm_kernel_deriv_mvm``, ``akm_kernel_mvm_multi``, ``akm_get_info``,
+``akm_set_scale_override``, ``akm_last_error``, ``akm_destroy``); ``Plan`` wraps them with
+tensor-friendly signatures.  Arrays may be CUDA torch tensors (device pointers, the caller's
+current stream is used) or host numpy arrays / CPU tensors (the library stages them).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libakm.so")
+
+AKM_OK, AKM_ERR_INVALID_ARG, AKM_ERR_NONFINITE, AKM_ERR_STATE, AKM_ERR_OOM, AKM_ERR_CUDA, AKM_ERR_UNSUPPORTED = range(7)
+STATUS_NAMES = {0: "AKM_OK", 1: "AKM_ERR_INVALID_ARG", 2: "AKM_ERR_NONFINITE", 3: "AKM_ERR_STATE", 4: "AKM_ERR_OOM",
+                5: "AKM_ERR_CUDA", 6: "AKM_ERR_UNSUPPORTED"}
+AKM_GAUSSIAN, AKM_MATERN12 = 0, 1
+AKM_D_ELL, AKM_D_SIGMA_F, AKM_D_SIGMA_EPS = 0, 1, 2
+AKM_MAX_WINDOWS = 32
+
+# names exported by include/akm.h (checked by tests/test_abi_cpu.py)
+ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm", "akm_kernel_deriv_mvm",
+               "akm_kernel_mvm_multi", "akm_get_info", "akm_set_scale_override", "akm_last_error", "akm_destroy",
+               "akm_version", "akm_set_profiling", "akm_get_stage_times")
+
+
+class akm_info(ctypes.Structure):
+    W = AKM_MAX_WINDOWS
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("p", ctypes.c_int32), ("P", ctypes.c_int32), ("N", ctypes.c_int32), ("m", ctypes.c_int32),
+        ("n_g", ctypes.c_int32), ("family", ctypes.c_int32),
+        ("sigma_f", ctypes.c_double), ("ell", ctypes.c_double), ("sigma_eps", ctypes.c_double),
+        ("d", ctypes.c_int32 * W),
+        ("c_w", ctypes.c_double * W),
+        ("ell_eff", ctypes.c_double * W),
+        ("radius", ctypes.c_double * W),
+        ("box", (ctypes.c_int32 * 3) * W),
+        ("bin", ctypes.c_int32 * W),
+        ("occupied_bins", ctypes.c_int64 * W),
+        ("max_bin_points", ctypes.c_int64 * W),
+        ("work_items_spread", ctypes.c_int64),
+        ("work_items_interp", ctypes.c_int64),
+        ("workspace_bytes", ctypes.c_int64),
+    ]
+
+
+class akm_stage_times(ctypes.Structure):
+    _fields_ = [("spread_ms", ctypes.c_double), ("fft_ms", ctypes.c_double), ("interp_ms", ctypes.c_double),
+                ("epilogue_ms", ctypes.c_double), ("calls", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("spread_launches", ctypes.c_int64), ("interp_launches", ctypes.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, d = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    st = ctypes.c_int
+    lib.akm_create.argtypes = [ctypes.POINTER(P), ctypes.c_int]
+    lib.akm_create.restype = st
+    lib.akm_set_points.argtypes = [P, P, i64, i32, i64, P, P, i32, i32, i32, d, i32, d, P]
+    lib.akm_set_points.restype = st
+    lib.akm_set_theta.argtypes = [P, d, d, d, P]
+    lib.akm_set_theta.restype = st
+    lib.akm_kernel_mvm.argtypes = [P, P, i64, i32, P, i64, P]
+    lib.akm_kernel_mvm.restype = st
+    lib.akm_kernel_deriv_mvm.argtypes = [P, i32, P, i64, i32, P, i64, P]
+    lib.akm_kernel_deriv_mvm.restype = st
+    lib.akm_kernel_mvm_multi.argtypes = [P, P, i64, i32, P, P, P, i64, P]
+    lib.akm_kernel_mvm_multi.restype = st
+    lib.akm_get_info.argtypes = [P, ctypes.POINTER(akm_info)]
+    lib.akm_get_info.restype = st
+    lib.akm_set_scale_override.argtypes = [P, P]
+    lib.akm_set_scale_override.restype = st
+    lib.akm_last_error.argtypes = [P]
+    lib.akm_last_error.restype = ctypes.c_char_p
+    lib.akm_destroy.argtypes = [P]
+    lib.akm_destroy.restype = None
+    lib.akm_set_profiling.argtypes = [P, i32]
+    lib.akm_set_profiling.restype = st
+    lib.akm_get_stage_times.argtypes = [P, ctypes.POINTER(akm_stage_times), i32]
+    lib.akm_get_stage_times.restype = st
+    lib.akm_version.argtypes = []
+    lib.akm_version.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = _load()
+
+
+class AkmError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+# ---------------------------------------------------------------- argument marshalling
+def _ptr_ld(a, name):
+    """(pointer, leading dimension, rows, cols, is_cuda_tensor, keepalive) of a 2-D float64 array."""
+    if a is None:
+        return None, 0, 0, 0, False, None
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.dtype != torch.float64:
+                raise TypeError(f"{name} must be float64")
+            if a.dim() == 1:
+                a = a.unsqueeze(1)
+            if a.dim() != 2 or a.stride(1) != 1:
+                raise ValueError(f"{name} must be 2-D with unit column stride")
+            ld = a.stride(0) if a.shape[0] > 1 else a.shape[1]
+            return ctypes.c_void_p(a.data_ptr()), max(ld, a.shape[1]), a.shape[0], a.shape[1], a.is_cuda, a
+    except ImportError:  # pragma: no cover
+        pass
+    arr = np.asarray(a)
+    if arr.dtype != np.float64:
+        raise TypeError(f"{name} must be float64")
+    if arr.ndim == 1:
+        arr = arr[:, None]
+    if arr.ndim != 2 or arr.strides[1] != 8:
+        raise ValueError(f"{name} must be 2-D row-major")
+    ld = arr.strides[0] // 8 if arr.shape[0] > 1 else arr.shape[1]
+    return ctypes.c_void_p(arr.ctypes.data), max(ld, arr.shape[1]), arr.shape[0], arr.shape[1], False, arr
+
+
+def _stream(stream, *tensors):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    for t in tensors:
+        if t is not None and getattr(t, "is_cuda", False):
+            import torch
+            return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+    return ctypes.c_void_p(0)
+
+
+def _check(plan, status):
+    if status != AKM_OK:
+        msg = _lib.akm_last_error(plan).decode() if plan else ""
+        raise AkmError(status, msg)
+
+
+# ---------------------------------------------------------------- C-named functions
+def akm_version() -> str:
+    return _lib.akm_version().decode()
+
+
+def akm_create(device: int = 0):
+    h = ctypes.c_void_p()
+    st = _lib.akm_create(ctypes.byref(h), int(device))
+    if st != AKM_OK:
+        raise AkmError(st, f"akm_create(device={device}) failed")
+    return h
+
+
+def akm_destroy(plan) -> None:
+    _lib.akm_destroy(plan)
+
+
+def akm_last_error(plan) -> str:
+    return _lib.akm_last_error(plan).decode()
+
+
+def akm_set_points(plan, X, windows, family, N, sigma_over, m, eps_B, stream=None):
+    px, ldx, n, p, _, keep = _ptr_ld(X, "X")
+    feat = np.ascontiguousarray([f for w in windows for f in w], dtype=np.int32)
+    lens = np.ascontiguousarray([len(w) for w in windows], dtype=np.int32)
+    st = _lib.akm_set_points(plan, px, n, p, ldx, feat.ctypes.data_as(ctypes.c_void_p),
+                             lens.ctypes.data_as(ctypes.c_void_p), len(windows), int(family), int(N),
+                             float(sigma_over), int(m), float(eps_B), _stream(stream, keep))
+    _check(plan, st)
+
+
+def akm_set_theta(plan, sigma_f, ell, sigma_eps, stream=None):
+    _check(plan, _lib.akm_set_theta(plan, float(sigma_f), float(ell), float(sigma_eps), _stream(stream)))
+
+
+def akm_kernel_mvm(plan, V, Y, stream=None):
+    pv, ldv, n, r, _, kv = _ptr_ld(V, "V")
+    py, ldy, _, _, _, ky = _ptr_ld(Y, "Y")
+    _check(plan, _lib.akm_kernel_mvm(plan, pv, ldv, r, py, ldy, _stream(stream, kv, ky)))
+
+
+def akm_kernel_deriv_mvm(plan, which, V, dY, stream=None):
+    pv, ldv, n, r, _, kv = _ptr_ld(V, "V")
+    py, ldy, _, _, _, ky = _ptr_ld(dY, "dY")
+    _check(plan, _lib.akm_kernel_deriv_mvm(plan, int(which), pv, ldv, r, py, ldy, _stream(stream, kv, ky)))
+
+
+def akm_kernel_mvm_multi(plan, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
+    pv, ldv, n, r, _, kv = _ptr_ld(V, "V")
+    outs = [_ptr_ld(o, "out") for o in (Y, dY_ell, dY_sf)]
+    lds = {o[1] for o in outs if o[0] is not None}
+    if len(lds) > 1:
+        raise ValueError("all outputs of akm_kernel_mvm_multi must share one leading dimension")
+    ldy = lds.pop() if lds else r
+    _check(plan, _lib.akm_kernel_mvm_multi(plan, pv, ldv, r, outs[0][0], outs[1][0], outs[2][0], ldy,
+                                           _stream(stream, kv, *[o[5] for o in outs])))
+
+
+def akm_get_info(plan) -> dict:
+    info = akm_info()
+    _check(plan, _lib.akm_get_info(plan, ctypes.byref(info)))
+    P = info.P
+    return {
+        "n": info.n, "p": info.p, "P": P, "N": info.N, "m": info.m, "n_g": info.n_g, "family": info.family,
+        "theta": (info.sigma_f, info.ell, info.sigma_eps),
+        "d": list(info.d[:P]), "c_w": list(info.c_w[:P]), "ell_eff": list(info.ell_eff[:P]),
+        "radius": list(info.radius[:P]), "box": [tuple(info.box[w]) for w in range(P)], "bin": list(info.bin[:P]),
+        "occupied_bins": list(info.occupied_bins[:P]), "max_bin_points": list(info.max_bin_points[:P]),
+        "work_items_spread": info.work_items_spread, "work_items_interp": info.work_items_interp,
+        "workspace_bytes": info.workspace_bytes,
+    }
+
+
+def akm_set_scale_override(plan, c_w=None):
+    if c_w is None:
+        _check(plan, _lib.akm_set_scale_override(plan, None))
+    else:
+        arr = np.ascontiguousarray(c_w, dtype=np.float64)
+        _check(plan, _lib.akm_set_scale_override(plan, arr.ctypes.data_as(ctypes.c_void_p)))
+
+
+def akm_set_profiling(plan, enable: bool):
+    _check(plan, _lib.akm_set_profiling(plan, 1 if enable else 0))
+
+
+def akm_get_stage_times(plan, reset: bool = False) -> dict:
+    t = akm_stage_times()
+    _check(plan, _lib.akm_get_stage_times(plan, ctypes.byref(t), 1 if reset else 0))
+    return {f[0]: getattr(t, f[0]) for f in akm_stage_times._fields_}
+
+
+# ---------------------------------------------------------------- convenience wrapper
+class Plan:
+    """RAII wrapper: ``Plan(device).set_points(...).set_theta(...)`` then ``mvm`` / ``deriv_mvm`` / ``mvm_multi``."""
+
+    def __init__(self, device: int = 0):
+        self.handle = akm_create(device)
+        self.device = device
+
+    def close(self):
+        if self.handle is not None:
+            akm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_points(self, X, windows, family=AKM_GAUSSIAN, N=32, sigma_over=2.0, m=6, eps_B=1.0 / 16, stream=None):
+        akm_set_points(self.handle, X, windows, family, N, sigma_over, m, eps_B, stream)
+        return self
+
+    def set_theta(self, sigma_f, ell, sigma_eps, stream=None):
+        akm_set_theta(self.handle, sigma_f, ell, sigma_eps, stream)
+        return self
+
+    def set_scale_override(self, c_w=None):
+        akm_set_scale_override(self.handle, c_w)
+        return self
+
+    def mvm(self, V, Y, stream=None):
+        akm_kernel_mvm(self.handle, V, Y, stream)
+        return Y
+
+    def deriv_mvm(self, which, V, dY, stream=None):
+        akm_kernel_deriv_mvm(self.handle, which, V, dY, stream)
+        return dY
+
+    def mvm_multi(self, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
+        akm_kernel_mvm_multi(self.handle, V, Y, dY_ell, dY_sf, stream)
+        return Y, dY_ell, dY_sf
+
+    def info(self):
+        return akm_get_info(self.handle)
+
+    def set_profiling(self, enable=True):
+        akm_set_profiling(self.handle, enable)
+        return self
+
+    def stage_times(self, reset=False):
+        return akm_get_stage_times(self.handle, reset)

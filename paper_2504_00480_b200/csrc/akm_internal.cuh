@@ -1,0 +1,142 @@
+// akm_internal.cuh -- shared definitions of the CUDA implementation behind include/akm.h.
+//
+// Geometry conventions:
+//   * Every window is handled in a "padded 3-D" form: padded axis a in {0,1,2}; the window's
+//     d axes are the last d padded axes, the leading 3-d axes are singletons (length 1, k = 0).
+//   * Scaled grid coordinate of point j along a real axis: u = (x - center) * n_g / c_w
+//     (x~ = (x - center)/c_w in the ball of radius 1/4 - eps_B/2; u = n_g x~).
+//   * Taps (App. A): the point touches grid nodes l = floor(u) - m + 1 + o,
+//     o in [0, 2m).  The window is taken as zero at |u - l| >= m: the closed end of the support
+//     carries weight phi(m/n_g)/phi(0) ~ 3e-11 (m = 6) and matters only for integer u
+//     (reading R3).
+//   * The grid "box" of a window is the range of nodes any point can touch; all grids and
+//     spectra are stored box-local.  cell_t = floor(u_t) - (box_lo_t + m - 1) in [0, ncell_t).
+//   * Bins are B^d blocks of cells; a bin's footprint is F = B + 2m - 1 nodes per real axis.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace akm {
+
+constexpr int kMaxWin = 32;
+constexpr double kPi = 3.14159265358979323846;
+
+// Per-window geometry passed (by value, inside WinTable) to kernels.
+struct WinGeom {
+  int d;
+  int feat[3];          // feature ids of the window's axes, padded axis a -> feat[a] (a >= 3-d)
+  double center[3];     // per padded axis (0 for singleton axes)
+  double scale;         // n_g / c_w
+  int box_lo[3];        // global grid index of box node 0 (0 for singleton axes)
+  int L[3];             // box length (1 for singleton axes)
+  int ncell[3];         // cells per axis (1 for singleton axes)
+  int B;                // bin edge (cells)
+  int F[3];             // bin footprint per axis (1 for singleton axes)
+  int nbin[3];          // bins per axis
+  int K[3];             // spectrum sizes: K[2] = N/2+1; K[0],K[1] = N+1 or 1 (singleton)
+  long long tap_off;    // offset of this window's box in "tap" units (grids are [tap][...])
+  long long ntap;       // L0*L1*L2
+  long long pt_off;     // offset of this window's points in the sorted arrays (w * n)
+  long long a1_off;     // offsets (complex units, per RHS) into the FFT work buffers
+  long long a2_off;
+  long long a3_off;     // [k0][k1][k2]
+  long long c_off;      // OPS-major: [op][L0][K1][K2]
+  long long c2_off;     // [op][L0][L1][K2]
+  long long tw_off[3];  // offsets of twiddle tables (complex) for each padded axis: [K][L]
+  long long d_off;      // offset of this window's multiplier tables [op][K0][K1][K2] (real)
+};
+
+struct WinTable {
+  int P;
+  int N, n_g, m;
+  WinGeom w[kMaxWin];
+};
+
+// One unit of spreading / interpolation work: a chunk of points of one bin.
+struct WorkItem {
+  int win;
+  int bin[3];       // bin coordinates per padded axis
+  int start;        // first sorted point (window-relative)
+  int count;        // number of points
+};
+
+// ------------------------------------------------------------------ device helpers
+// Kaiser-Bessel window (App. A) at a distance delta = n_g * x in grid cells:
+//   phi = (1/pi) sinh(beta sqrt(m^2 - delta^2)) / sqrt(m^2 - delta^2) for |delta| < m,
+//   0 otherwise (truncated; reading R3 for the end point).
+__device__ __forceinline__ double kb_window(double delta, double m, double beta) {
+  const double s = m * m - delta * delta;
+  if (s > 0.0) {
+    const double q = sqrt(s);
+    return sinh(beta * q) / (kPi * q);
+  }
+  return 0.0;
+}
+
+// Modified Bessel I0 by its power series sum_k ((x/2)^{2k} / (k!)^2); x <= ~60 here.
+__host__ __device__ inline double bessel_i0(double x) {
+  const double q = 0.25 * x * x;
+  double term = 1.0, sum = 1.0;
+  for (int k = 1; k < 200; ++k) {
+    term *= q / ((double)k * (double)k);
+    sum += term;
+    if (term < 1e-17 * sum) break;
+  }
+  return sum;
+}
+
+}  // namespace akm
+
+// ------------------------------------------------------------------ launchers (host side)
+// `tab` is the host copy of the window table (sizes for grid dimensions), `dtab` its device copy.
+namespace akm {
+// setup_kernels.cu
+cudaError_t launch_gather_columns(const double* X, long long n, long long ldx, const int* feat, int nf, double* Xc,
+                                  cudaStream_t s);
+cudaError_t launch_window_minmax(const double* X, long long n, long long ldx, const int* feat_dev, int nfeat,
+                                 double* minmax_dev, cudaStream_t s);
+cudaError_t launch_window_radius(const double* X, long long n, long long ldx, const WinTable& tab,
+                                 const WinTable* dtab, double* r2_dev, cudaStream_t s);
+cudaError_t launch_scale_and_key(const double* X, long long n, long long ldx, const WinTable& tab,
+                                 const WinTable* dtab, double* u_tmp, int* key, int* hist, const long long* hist_off,
+                                 int* err_flag, cudaStream_t s);
+cudaError_t launch_scatter(long long n, const WinTable& tab, const WinTable* dtab, const double* u_tmp,
+                           const int* key, int* cursor, const long long* hist_off, double* u_sorted, int* perm,
+                           cudaStream_t s);
+cudaError_t launch_kernel_samples(int family, int d, int N, double ell_eff, int deriv, double* out, cudaStream_t s);
+cudaError_t launch_cos_dft_axis(int d, int N, int axis, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_multiplier(const WinTable& tab, const WinTable* dtab, int win, const double* bK, const double* bL,
+                              int ops_mask, double inv_c, double sigma_over, double* D, cudaStream_t s);
+cudaError_t launch_twiddles(const WinTable& tab, const WinTable* dtab, double2* tw, cudaStream_t s);
+
+// spread.cu
+bool spread_tile_supported(int MT, int NT);
+size_t spread_smem_bytes(int PB, int Mpad, int Npad, int Fmax, int rc);
+cudaError_t launch_spread(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                          const int* perm, const double* V, long long ldv, long long n, int r0, int rc, int r_total,
+                          double* grid, int MT, int NT, int threads, int PB, size_t smem, double beta, cudaStream_t s);
+
+// fft.cu
+cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1,
+                               double2* A2, const double2* tw, int r, long long maxA1, long long maxA2,
+                               cudaStream_t s);
+cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dtab, const double2* A2, double2* A3,
+                                        double2* C, double2* C2, const double2* tw, const double* D, int ops, int dslot0, int r,
+                                        double* H, long long maxA3, long long maxC, long long maxC2,
+                                        long long maxTap, cudaStream_t s);
+cudaError_t launch_zero(double* p, long long count, cudaStream_t s);
+
+// interp.cu
+bool interp_supported(int d, int taps, int ops, int rc);
+int interp_rc_for(int r_remaining);
+size_t interp_smem_bytes(int slab, int ops, int rc);
+cudaError_t launch_interp(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                          const int* perm, const double* H, int d, int taps, int ops, int r, int r0, int rc,
+                          double* part, long long n, double beta, size_t smem, cudaStream_t s);
+cudaError_t launch_epilogue(long long n, int P, int r, int ops, const double* part, const double* V, long long ldv,
+                            double sigma_f, double sigma_eps, double* Y, double* dYl, double* dYsf, long long ldy,
+                            int slotK, int slotL, cudaStream_t s);
+cudaError_t launch_scaled_copy(long long n, int r, double alpha, const double* V, long long ldv, double* Y,
+                               long long ldy, cudaStream_t s);
+}  // namespace akm

@@ -1,0 +1,134 @@
+// interp.cu -- dispatch of the NFFT interpolation kernels (kernel template in
+// interp_impl.cuh) and the epilogue S7: Y = sigma_f^2 S + sigma_eps^2 V, dY_ell = sigma_f^2 S^ell,
+// dY_sf = 2 sigma_f S, with the windows summed in a fixed order.
+#include "akm_internal.cuh"
+
+namespace akm {
+
+cudaError_t launch_interp_d1_t8(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
+                              long long n, double beta, size_t smem, cudaStream_t s);
+cudaError_t launch_interp_d1_t12(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
+                              long long n, double beta, size_t smem, cudaStream_t s);
+cudaError_t launch_interp_d1_t16(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
+                              long long n, double beta, size_t smem, cudaStream_t s);
+cudaError_t launch_interp_d2_t8(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
+                              long long n, double beta, size_t smem, cudaStream_t s);
+cudaError_t launch_interp_d2_t12(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
+                              long long n, double beta, size_t smem, cudaStream_t s);
+cudaError_t launch_interp_d2_t16(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
+                              long long n, double beta, size_t smem, cudaStream_t s);
+cudaError_t launch_interp_d3_t8(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
+                              long long n, double beta, size_t smem, cudaStream_t s);
+cudaError_t launch_interp_d3_t12(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
+                              long long n, double beta, size_t smem, cudaStream_t s);
+cudaError_t launch_interp_d3_t16(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
+                              long long n, double beta, size_t smem, cudaStream_t s);
+
+bool interp_supported(int d, int taps, int ops, int rc) {
+  const bool dt = (d >= 1 && d <= 3) && (taps == 8 || taps == 12 || taps == 16);
+  const bool orc = (ops == 1 || ops == 2) && (rc == 1 || rc == 2 || rc == 4 || rc == 11);
+  return dt && orc;
+}
+
+// Largest instantiated RHS chunk not exceeding r_remaining.
+int interp_rc_for(int r_remaining) {
+  if (r_remaining >= 11) return 11;
+  if (r_remaining >= 4) return 4;
+  if (r_remaining >= 2) return 2;
+  return 1;
+}
+
+size_t interp_smem_bytes(int slab, int ops, int rc) {
+  const int vp = (ops * rc + 1) & ~1;
+  return sizeof(double) * (size_t)slab * vp;
+}
+
+cudaError_t launch_interp(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                          const int* perm, const double* H, int d, int taps, int ops, int r, int r0, int rc,
+                          double* part, long long n, double beta, size_t smem, cudaStream_t s) {
+  if (n_items <= 0) return cudaSuccess;
+  if (d == 1 && taps == 8)
+    return launch_interp_d1_t8(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+  if (d == 1 && taps == 12)
+    return launch_interp_d1_t12(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+  if (d == 1 && taps == 16)
+    return launch_interp_d1_t16(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+  if (d == 2 && taps == 8)
+    return launch_interp_d2_t8(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+  if (d == 2 && taps == 12)
+    return launch_interp_d2_t12(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+  if (d == 2 && taps == 16)
+    return launch_interp_d2_t16(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+  if (d == 3 && taps == 8)
+    return launch_interp_d3_t8(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+  if (d == 3 && taps == 12)
+    return launch_interp_d3_t12(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+  if (d == 3 && taps == 16)
+    return launch_interp_d3_t16(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+  return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------- epilogue (S7)
+// part[(w*n + i)*ops + slot][r] holds S^{w,op}; sums over windows in fixed order (deterministic).
+__global__ void k_epilogue(long long n, int P, int r, int ops, const double* __restrict__ part,
+                           const double* __restrict__ V, long long ldv, double sigma_f, double sigma_eps,
+                           double* __restrict__ Y, double* __restrict__ dYl, double* __restrict__ dYsf,
+                           long long ldy, int slotK, int slotL) {
+  const long long total = n * r;
+  const double sf2 = sigma_f * sigma_f, se2 = sigma_eps * sigma_eps;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx / r;
+    const int c = (int)(idx % r);
+    double sK = 0.0, sL = 0.0;
+    for (int w = 0; w < P; ++w) {
+      const double* pp = part + (((long long)w * n + i) * ops) * r + c;
+      if (slotK >= 0) sK += pp[(long long)slotK * r];
+      if (slotL >= 0) sL += pp[(long long)slotL * r];
+    }
+    if (Y) Y[i * ldy + c] = sf2 * sK + se2 * V[i * ldv + c];
+    if (dYl) dYl[i * ldy + c] = sf2 * sL;
+    if (dYsf) dYsf[i * ldy + c] = 2.0 * sigma_f * sK;
+  }
+}
+
+cudaError_t launch_epilogue(long long n, int P, int r, int ops, const double* part, const double* V, long long ldv,
+                            double sigma_f, double sigma_eps, double* Y, double* dYl, double* dYsf, long long ldy,
+                            int slotK, int slotL, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  long long blocks = (n * r + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_epilogue<<<(int)blocks, 256, 0, s>>>(n, P, r, ops, part, V, ldv, sigma_f, sigma_eps, Y, dYl, dYsf, ldy, slotK,
+                                         slotL);
+  return cudaGetLastError();
+}
+
+__global__ void k_scaled_copy(long long n, int r, double alpha, const double* __restrict__ V, long long ldv,
+                              double* __restrict__ Y, long long ldy) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n * r;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx / r;
+    const int c = (int)(idx % r);
+    Y[i * ldy + c] = alpha * V[i * ldv + c];
+  }
+}
+
+cudaError_t launch_scaled_copy(long long n, int r, double alpha, const double* V, long long ldv, double* Y,
+                               long long ldy, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  long long blocks = (n * r + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_scaled_copy<<<(int)blocks, 256, 0, s>>>(n, r, alpha, V, ldv, Y, ldy);
+  return cudaGetLastError();
+}
+
+}  // namespace akm

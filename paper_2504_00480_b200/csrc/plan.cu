@@ -1,0 +1,961 @@
+// plan.cu -- the C ABI of include/akm.h: plan state, validation, workspace, orchestration.
+//
+// Host code here only validates arguments, sizes buffers, chooses bin sizes / tiles from
+// device-computed histograms, and enqueues the kernels of setup_kernels.cu, spread.cu, fft.cu and
+// interp.cu on the caller's stream.  All per-point, per-grid-node and per-frequency arithmetic
+// of the method runs in those kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/akm.h"
+#include "akm_internal.cuh"
+
+using namespace akm;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  // grow-only; contents are not preserved
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    release();
+    if (need == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc(&p, need);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      return e;
+    }
+    bytes = need;
+    return cudaSuccess;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct Group {  // windows sharing (d, F) -> one spread / interp launch
+  int d = 0, F = 0;
+  std::vector<int> wins;
+  int spread_begin = 0, spread_count = 0;  // slice of the concatenated spread work items
+  int interp_begin = 0, interp_count = 0;
+};
+
+}  // namespace
+
+struct akm_plan {
+  int device = 0;
+  std::string err;
+  bool have_points = false, have_theta = false;
+
+  // problem
+  long long n = 0;
+  int p = 0, P = 0, family = 0, N = 0, m = 0, n_g = 0;
+  double sigma_over = 2.0, eps_B = 0.0, beta = 0.0;
+  std::vector<int> win_len, win_feat;       // as given
+  std::vector<int> feat_used;               // distinct features, compact column order
+  double sigma_f = 1.0, ell = 1.0, sigma_eps = 0.0;
+  std::vector<double> scale_override;       // empty = automatic rule (reading R2)
+
+  // per-window host data
+  std::vector<double> lo, hi;               // [w*3 + a] bounding box (padded axes)
+  std::vector<double> radius;               // R_w
+  std::vector<double> c_w, c_w_binned;      // current scale, scale the bins were built for
+  WinTable tab{};                           // host copy
+  std::vector<WorkItem> items_spread, items_interp;
+  std::vector<Group> groups;
+  std::vector<long long> occupied, maxbin;
+  long long total_taps = 0, szA1 = 0, szA2 = 0, szA3 = 0, szC = 0, szC2 = 0, szTW = 0, szD = 0;
+  long long maxA1 = 0, maxA2 = 0, maxA3 = 0, maxC = 0, maxC2 = 0, maxTap = 0;
+
+  // device buffers
+  DevBuf dtab, Xc, u_tmp, u_sorted, perm, hist, hist_off, err_flag, items_s, items_i, minmax, r2;
+  DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
+  DevBuf stageV, stageY, stageL, stageS;
+  long long r_cap = 0;
+
+  // profiling (akm_set_profiling / akm_get_stage_times): a ring of event sets, drained lazily
+  static constexpr int kRing = 512;
+  struct EvSet { cudaEvent_t e[5]; bool pending = false; };
+  bool profiling = false;
+  std::vector<EvSet> ring;
+  int ring_pos = 0;
+  double stage_ms[4] = {0, 0, 0, 0};
+  long long prof_calls = 0, launches = 0, spread_launches = 0, interp_launches = 0;
+
+  void drain(EvSet& es) {
+    if (!es.pending) return;
+    cudaEventSynchronize(es.e[4]);
+    for (int k = 0; k < 4; ++k) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, es.e[k], es.e[k + 1]) == cudaSuccess) stage_ms[k] += ms;
+      else cudaGetLastError();
+    }
+    es.pending = false;
+  }
+  EvSet* next_set() {
+    if (ring.empty()) {
+      ring.resize(kRing);
+      for (auto& es : ring)
+        for (auto& e : es.e) cudaEventCreate(&e);
+    }
+    EvSet& es = ring[ring_pos];
+    ring_pos = (ring_pos + 1) % kRing;
+    drain(es);
+    es.pending = true;
+    ++prof_calls;
+    return &es;
+  }
+  ~akm_plan() {
+    for (auto& es : ring)
+      for (auto& e : es.e) cudaEventDestroy(e);
+  }
+
+  akm_status fail(akm_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    err = buf;
+    return st;
+  }
+};
+
+#define AKM_CK(call)                                                                              \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) {                                                                      \
+      akm_status st_ = (e_ == cudaErrorMemoryAllocation) ? AKM_ERR_OOM : AKM_ERR_CUDA;            \
+      return plan->fail(st_, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    }                                                                                             \
+  } while (0)
+
+namespace {
+
+bool is_device_ptr(const void* ptr) {
+  if (!ptr) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+bool is_pinned_host(const void* ptr) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+// ================================================================== geometry / binning
+// Build per-window boxes for the current c_w, histogram the points per cell on the device,
+// choose the bin edge B per window from the histogram, lay the cells out bin-major, scatter.
+static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
+  const int P = plan->P, m = plan->m, n_g = plan->n_g;
+  const long long n = plan->n;
+  WinTable& tab = plan->tab;
+  tab.P = P;
+  tab.N = plan->N;
+  tab.n_g = n_g;
+  tab.m = m;
+  // pass 0: boxes and cells (independent of B)
+  std::vector<long long> hoff(P + 1, 0);
+  for (int w = 0; w < P; ++w) {
+    WinGeom& g = tab.w[w];
+    const double c = plan->c_w[w];
+    g.scale = (double)n_g / c;
+    for (int a = 0; a < 3; ++a) {
+      if (a < 3 - g.d) {
+        g.box_lo[a] = 0; g.L[a] = 1; g.ncell[a] = 1; g.K[a] = 1;
+        continue;
+      }
+      // u of the extreme points, computed with the same two IEEE operations as k_scale_and_key
+      // (a subtraction and a multiplication cannot be contracted into an FMA), so floor() agrees
+      // bit for bit; one cell of slack is kept on each side only when the box still fits n_g.
+      const double umin = (plan->lo[w * 3 + a] - g.center[a]) * g.scale;
+      const double umax = (plan->hi[w * 3 + a] - g.center[a]) * g.scale;
+      int fmin = (int)std::floor(umin), fmax = (int)std::floor(umax);
+      if ((fmax - fmin + 2) + 2 * m - 1 <= n_g) {
+        fmin -= 1;
+        fmax += 1;
+      }
+      g.box_lo[a] = fmin - m + 1;
+      g.ncell[a] = fmax - fmin + 1;
+      g.L[a] = g.ncell[a] + 2 * m - 1;
+      g.K[a] = (a == 2) ? plan->N / 2 + 1 : plan->N + 1;
+    }
+    hoff[w + 1] = hoff[w] + (long long)g.ncell[0] * g.ncell[1] * g.ncell[2];
+  }
+  const long long ncells = hoff[P];
+  AKM_CK(plan->hist.ensure(sizeof(int) * std::max<long long>(ncells, 1)));
+  AKM_CK(plan->hist_off.ensure(sizeof(long long) * (P + 1)));
+  AKM_CK(plan->err_flag.ensure(sizeof(int)));
+  AKM_CK(plan->u_tmp.ensure(sizeof(double) * 3 * P * std::max<long long>(n, 1)));
+  AKM_CK(plan->u_sorted.ensure(sizeof(double) * 3 * P * std::max<long long>(n, 1)));
+  AKM_CK(plan->perm.ensure(sizeof(int) * P * std::max<long long>(n, 1)));
+  AKM_CK(plan->dtab.ensure(sizeof(WinTable)));
+  AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
+  AKM_CK(cudaMemcpyAsync(plan->hist_off.p, hoff.data(), sizeof(long long) * (P + 1), cudaMemcpyHostToDevice, s));
+  AKM_CK(cudaMemsetAsync(plan->hist.p, 0, sizeof(int) * std::max<long long>(ncells, 1), s));
+  AKM_CK(cudaMemsetAsync(plan->err_flag.p, 0, sizeof(int), s));
+  const int nf = (int)plan->feat_used.size();
+  AKM_CK(launch_scale_and_key(plan->Xc.as<double>(), n, nf, tab, plan->dtab.as<WinTable>(), plan->u_tmp.as<double>(),
+                              nullptr, plan->hist.as<int>(), plan->hist_off.as<long long>(), plan->err_flag.as<int>(), s));
+  std::vector<int> hist(std::max<long long>(ncells, 1));
+  int errf = 0;
+  AKM_CK(cudaMemcpyAsync(hist.data(), plan->hist.p, sizeof(int) * std::max<long long>(ncells, 1), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaMemcpyAsync(&errf, plan->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaStreamSynchronize(s));
+  if (errf) return plan->fail(AKM_ERR_CUDA, "internal error: a scaled point fell outside its grid box");
+
+  // choose B per window (cost model in FMA-equivalents per RHS)
+  const int taps = 2 * m;
+  std::vector<int> cell_off(std::max<long long>(ncells, 1), 0);
+  plan->items_spread.clear();
+  plan->items_interp.clear();
+  plan->occupied.assign(P, 0);
+  plan->maxbin.assign(P, 0);
+  const long long total_pts = n * P;
+  long long ch_s = total_pts / (148 * 2);
+  ch_s = std::max(32LL, std::min(4096LL, ch_s));
+  const int ch_i = 128;
+  std::vector<std::vector<WorkItem>> its_s(P), its_i(P);
+  for (int w = 0; w < P; ++w) {
+    WinGeom& g = tab.w[w];
+    const int* hc = hist.data() + hoff[w];
+    const int d = g.d;
+    int bestB = 1;
+    double bestCost = 1e300;
+    for (int B : {1, 2, 3, 4, 6, 8}) {
+      const int F = B + 2 * m - 1;
+      double Fd = 1;
+      for (int t = 0; t < d; ++t) Fd *= F;
+      if (Fd > 20000) continue;
+      bool fits = true;
+      for (int a = 3 - d; a < 3; ++a) fits = fits && ((g.ncell[a] + B - 1) / B) * B + 2 * m - 1 <= n_g;
+      if (!fits) continue;
+      int nb[3];
+      for (int a = 0; a < 3; ++a) nb[a] = (g.ncell[a] + B - 1) / (a < 3 - d ? 1 : B);
+      for (int a = 0; a < 3 - d; ++a) nb[a] = 1;
+      std::vector<long long> bc((size_t)nb[0] * nb[1] * nb[2], 0);
+      for (int c0 = 0; c0 < g.ncell[0]; ++c0)
+        for (int c1 = 0; c1 < g.ncell[1]; ++c1)
+          for (int c2 = 0; c2 < g.ncell[2]; ++c2) {
+            const int v = hc[((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2];
+            if (!v) continue;
+            const int b0 = (3 - d > 0) ? 0 : c0 / B, b1 = (3 - d > 1) ? 0 : c1 / B, b2 = c2 / B;
+            bc[((size_t)b0 * nb[1] + b1) * nb[2] + b2] += v;
+          }
+      double chunks_s = 0, chunks_i = 0;
+      for (long long v : bc)
+        if (v) {
+          chunks_s += (double)((v + ch_s - 1) / ch_s);
+          chunks_i += (double)((v + ch_i - 1) / ch_i);
+        }
+      double tapd = 1;
+      for (int t = 0; t < d; ++t) tapd *= taps;
+      const double diverge = (d == 3) ? (double)F / taps : 1.0;
+      const double spread = Fd * ((double)n + 34.0 * chunks_s);
+      const double interp = 2.0 * ((double)n * tapd * diverge + 4.0 * chunks_i * Fd);
+      const double cost = spread + interp;
+      if (cost < bestCost * 0.999) {
+        bestCost = cost;
+        bestB = B;
+      }
+    }
+    // finalize geometry for bestB
+    const int B = bestB;
+    g.B = B;
+    for (int a = 0; a < 3; ++a) {
+      if (a < 3 - d) {
+        g.nbin[a] = 1; g.F[a] = 1;
+        continue;
+      }
+      g.nbin[a] = (g.ncell[a] + B - 1) / B;
+      g.F[a] = B + 2 * m - 1;
+      g.L[a] = g.nbin[a] * B + 2 * m - 1;  // covers the last bin's footprint
+      if (g.L[a] > n_g)
+        return plan->fail(AKM_ERR_UNSUPPORTED,
+                          "window %d: grid box of %d nodes exceeds the oversampled grid (n_g = %d); "
+                          "increase N or sigma_over, or decrease m", w, g.L[a], n_g);
+    }
+    // cell offsets in bin-major order and work items
+    long long pos = 0;
+    const int Bd0 = (3 - d > 0) ? 1 : B, Bd1 = (3 - d > 1) ? 1 : B, Bd2 = B;
+    for (int b0 = 0; b0 < g.nbin[0]; ++b0)
+      for (int b1 = 0; b1 < g.nbin[1]; ++b1)
+        for (int b2 = 0; b2 < g.nbin[2]; ++b2) {
+          const long long start = pos;
+          for (int s0 = 0; s0 < Bd0; ++s0)
+            for (int s1 = 0; s1 < Bd1; ++s1)
+              for (int s2 = 0; s2 < Bd2; ++s2) {
+                const int c0 = b0 * Bd0 + s0, c1 = b1 * Bd1 + s1, c2 = b2 * Bd2 + s2;
+                if (c0 >= g.ncell[0] || c1 >= g.ncell[1] || c2 >= g.ncell[2]) continue;
+                const long long ci = ((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2;
+                cell_off[hoff[w] + ci] = (int)pos;
+                pos += hc[ci];
+              }
+          const long long cnt = pos - start;
+          if (!cnt) continue;
+          plan->occupied[w] += 1;
+          plan->maxbin[w] = std::max(plan->maxbin[w], cnt);
+          for (long long q = 0; q < cnt; q += ch_s)
+            its_s[w].push_back(WorkItem{w, {b0, b1, b2}, (int)(start + q), (int)std::min<long long>(ch_s, cnt - q)});
+          for (long long q = 0; q < cnt; q += ch_i)
+            its_i[w].push_back(WorkItem{w, {b0, b1, b2}, (int)(start + q), (int)std::min<long long>(ch_i, cnt - q)});
+        }
+    if (pos != n) return plan->fail(AKM_ERR_CUDA, "internal error: histogram of window %d holds %lld of %lld points",
+                                    w, pos, n);
+  }
+  // groups of windows with equal (d, F); work items concatenated group by group,
+  // larger chunks first inside a group (better tail behaviour)
+  plan->groups.clear();
+  for (int w = 0; w < P; ++w) {
+    const WinGeom& g = tab.w[w];
+    const int F = g.F[2];
+    Group* grp = nullptr;
+    for (auto& gg : plan->groups)
+      if (gg.d == g.d && gg.F == F) grp = &gg;
+    if (!grp) {
+      plan->groups.push_back(Group{});
+      grp = &plan->groups.back();
+      grp->d = g.d;
+      grp->F = F;
+    }
+    grp->wins.push_back(w);
+  }
+  for (auto& grp : plan->groups) {
+    std::vector<WorkItem> gs, gi;
+    for (int w : grp.wins) {
+      gs.insert(gs.end(), its_s[w].begin(), its_s[w].end());
+      gi.insert(gi.end(), its_i[w].begin(), its_i[w].end());
+    }
+    std::stable_sort(gs.begin(), gs.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
+    std::stable_sort(gi.begin(), gi.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
+    grp.spread_begin = (int)plan->items_spread.size();
+    grp.spread_count = (int)gs.size();
+    grp.interp_begin = (int)plan->items_interp.size();
+    grp.interp_count = (int)gi.size();
+    plan->items_spread.insert(plan->items_spread.end(), gs.begin(), gs.end());
+    plan->items_interp.insert(plan->items_interp.end(), gi.begin(), gi.end());
+  }
+
+  // workspace layout (per RHS) for grids, spectra, twiddles and multipliers
+  long long tap = 0, a1 = 0, a2 = 0, a3 = 0, cc = 0, c2 = 0, twc = 0, dd = 0;
+  plan->maxA1 = plan->maxA2 = plan->maxA3 = plan->maxC = plan->maxC2 = plan->maxTap = 0;
+  for (int w = 0; w < P; ++w) {
+    WinGeom& g = tab.w[w];
+    g.ntap = (long long)g.L[0] * g.L[1] * g.L[2];
+    g.tap_off = tap;
+    tap += g.ntap;
+    g.pt_off = (long long)w * n;
+    const long long s1 = (long long)g.L[0] * g.L[1] * g.K[2];
+    const long long s2 = (long long)g.L[0] * g.K[1] * g.K[2];
+    const long long s3 = (long long)g.K[0] * g.K[1] * g.K[2];
+    g.a1_off = a1; a1 += s1;
+    g.a2_off = a2; a2 += s2;
+    g.a3_off = a3; a3 += s3;
+    g.c_off = cc; cc += 2 * s2;
+    g.c2_off = c2; c2 += 2 * s1;
+    for (int a = 0; a < 3; ++a) {
+      g.tw_off[a] = twc;
+      twc += (long long)g.K[a] * g.L[a];
+    }
+    g.d_off = dd;
+    dd += 2 * s3;
+    plan->maxA1 = std::max(plan->maxA1, s1);
+    plan->maxA2 = std::max(plan->maxA2, s2);
+    plan->maxA3 = std::max(plan->maxA3, s3);
+    plan->maxC = std::max(plan->maxC, s2);
+    plan->maxC2 = std::max(plan->maxC2, s1);
+    plan->maxTap = std::max(plan->maxTap, g.ntap);
+  }
+  plan->total_taps = tap;
+  plan->szA1 = a1; plan->szA2 = a2; plan->szA3 = a3; plan->szC = cc; plan->szC2 = c2; plan->szTW = twc; plan->szD = dd;
+  plan->r_cap = 0;  // grid workspace must be re-sized
+
+  // scatter into bin-major order
+  AKM_CK(cudaMemcpyAsync(plan->hist.p, cell_off.data(), sizeof(int) * std::max<long long>(ncells, 1),
+                         cudaMemcpyHostToDevice, s));
+  AKM_CK(plan->dtab.ensure(sizeof(WinTable)));
+  AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
+  AKM_CK(launch_scatter(n, tab, plan->dtab.as<WinTable>(), plan->u_tmp.as<double>(), nullptr, plan->hist.as<int>(),
+                        plan->hist_off.as<long long>(), plan->u_sorted.as<double>(), plan->perm.as<int>(), s));
+  AKM_CK(plan->items_s.ensure(sizeof(WorkItem) * std::max<size_t>(plan->items_spread.size(), 1)));
+  AKM_CK(plan->items_i.ensure(sizeof(WorkItem) * std::max<size_t>(plan->items_interp.size(), 1)));
+  if (!plan->items_spread.empty())
+    AKM_CK(cudaMemcpyAsync(plan->items_s.p, plan->items_spread.data(), sizeof(WorkItem) * plan->items_spread.size(),
+                           cudaMemcpyHostToDevice, s));
+  if (!plan->items_interp.empty())
+    AKM_CK(cudaMemcpyAsync(plan->items_i.p, plan->items_interp.data(), sizeof(WorkItem) * plan->items_interp.size(),
+                           cudaMemcpyHostToDevice, s));
+  // twiddles
+  AKM_CK(plan->tw.ensure(sizeof(double2) * std::max<long long>(twc, 1)));
+  AKM_CK(launch_twiddles(tab, plan->dtab.as<WinTable>(), plan->tw.as<double2>(), s));
+  AKM_CK(plan->D.ensure(sizeof(double) * std::max<long long>(dd, 1)));
+  AKM_CK(cudaStreamSynchronize(s));  // host vectors (cell_off, items) go out of scope / may change
+  plan->c_w_binned = plan->c_w;
+  return AKM_OK;
+}
+
+// b_k of eq. (3.2) for kappa and kappa^der at ell_eff, then the multiplier tables.
+static akm_status rebuild_tables(akm_plan* plan, cudaStream_t s) {
+  const int N = plan->N;
+  long long maxNd = 1;
+  for (int w = 0; w < plan->P; ++w) {
+    long long v = 1;
+    for (int t = 0; t < plan->tab.w[w].d; ++t) v *= N;
+    maxNd = std::max(maxNd, v);
+  }
+  AKM_CK(plan->bs0.ensure(sizeof(double) * maxNd));
+  AKM_CK(plan->bs1.ensure(sizeof(double) * maxNd));
+  AKM_CK(plan->bs2.ensure(sizeof(double) * maxNd));
+  AKM_CK(plan->bs3.ensure(sizeof(double) * maxNd));
+  for (int w = 0; w < plan->P; ++w) {
+    const int d = plan->tab.w[w].d;
+    const double ell_eff = plan->ell / plan->c_w[w];
+    double* bufs[2] = {plan->bs2.as<double>(), plan->bs3.as<double>()};
+    for (int deriv = 0; deriv < 2; ++deriv) {
+      double* a = plan->bs0.as<double>();
+      double* b = plan->bs1.as<double>();
+      AKM_CK(launch_kernel_samples(plan->family, d, N, ell_eff, deriv, a, s));
+      for (int t = 0; t < d; ++t) {
+        double* out = (t == d - 1) ? bufs[deriv] : b;
+        AKM_CK(launch_cos_dft_axis(d, N, t, a, out, s));
+        std::swap(a, b);
+        if (t == d - 1) break;
+        // after the swap, `a` holds the latest result
+      }
+    }
+    AKM_CK(launch_multiplier(plan->tab, plan->dtab.as<WinTable>(), w, plan->bs2.as<double>(), plan->bs3.as<double>(), 3,
+                             1.0 / plan->c_w[w], plan->sigma_over, plan->D.as<double>(), s));
+  }
+  return AKM_OK;
+}
+
+static akm_status ensure_rhs_workspace(akm_plan* plan, int r) {
+  if (r <= plan->r_cap) return AKM_OK;
+  const long long R = r;
+  AKM_CK(plan->grid.ensure(sizeof(double) * std::max<long long>(plan->total_taps * R, 1)));
+  AKM_CK(plan->H.ensure(sizeof(double) * std::max<long long>(plan->total_taps * 2 * R, 1)));
+  AKM_CK(plan->A1.ensure(sizeof(double2) * std::max<long long>(plan->szA1 * R, 1)));
+  AKM_CK(plan->A2.ensure(sizeof(double2) * std::max<long long>(plan->szA2 * R, 1)));
+  AKM_CK(plan->A3.ensure(sizeof(double2) * std::max<long long>(plan->szA3 * R, 1)));
+  AKM_CK(plan->C.ensure(sizeof(double2) * std::max<long long>(plan->szC * R, 1)));
+  AKM_CK(plan->C2.ensure(sizeof(double2) * std::max<long long>(plan->szC2 * R, 1)));
+  AKM_CK(plan->part.ensure(sizeof(double) * std::max<long long>(plan->P * plan->n * 2 * R, 1)));
+  plan->r_cap = r;
+  return AKM_OK;
+}
+
+// choose the spread register tile for a (M = F^{d-1}) x (Nn = F*rc) footprint matrix
+static bool choose_spread_tile(int M, int Nn, int& MT, int& NT, int& threads) {
+  static const int cand[][2] = {{2, 8}, {2, 16}, {4, 4}, {4, 6}, {4, 8}, {4, 11}, {4, 12}, {4, 16},
+                                {8, 4}, {8, 6}, {8, 8}, {8, 11}, {8, 12}};
+  double best = 1e300;
+  bool found = false;
+  for (auto& c : cand) {
+    const int mt = c[0], nt = c[1];
+    const int TM = (M + mt - 1) / mt, TN = (Nn + nt - 1) / nt;
+    const int thr = TM * TN;
+    if (thr > 256) continue;  // k_spread is compiled with __launch_bounds__(256)
+    const double waste = (double)TM * mt * TN * nt / ((double)M * Nn);
+    const double ldratio = (double)(mt + nt) / (mt * nt);
+    double score = waste * (1.0 + 1.5 * ldratio);
+    if (thr < 64) score *= 1.25;
+    if (score < best) {
+      best = score;
+      MT = mt;
+      NT = nt;
+      threads = ((thr + 31) / 32) * 32;
+      found = true;
+    }
+  }
+  return found;
+}
+
+// ================================================================== the MVM
+static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r, double* Y, double* dYl,
+                          double* dYsf, long long ldy, cudaStream_t s) {
+  const bool needK = (Y != nullptr) || (dYsf != nullptr);
+  const bool needL = dYl != nullptr;
+  const int ops = (needK ? 1 : 0) + (needL ? 1 : 0);
+  const int slotK = needK ? 0 : -1;
+  const int slotL = needL ? (needK ? 1 : 0) : -1;
+  const int dslot0 = needK ? 0 : 1;
+  const long long n = plan->n;
+  if (n == 0) return AKM_OK;
+  akm_status st = ensure_rhs_workspace(plan, r);
+  if (st != AKM_OK) return st;
+  const WinTable* dtab = plan->dtab.as<WinTable>();
+  akm_plan::EvSet* ev = plan->profiling ? plan->next_set() : nullptr;
+  if (ev) AKM_CK(cudaEventRecord(ev->e[0], s));
+  // S2: spread
+  AKM_CK(launch_zero(plan->grid.as<double>(), plan->total_taps * r, s));
+  for (const Group& grp : plan->groups) {
+    const int F = grp.F, d = grp.d;
+    int M = 1;
+    for (int t = 0; t < d - 1; ++t) M *= F;
+    int r0 = 0;
+    while (r0 < r) {
+      // largest RHS chunk (<= 12) whose footprint tile fits one CTA of <= 256 threads
+      int rc = std::min(12, r - r0), MT = 0, NT = 0, threads = 0;
+      while (rc > 1 && !choose_spread_tile(M, F * rc, MT, NT, threads)) --rc;
+      if (!choose_spread_tile(M, F * rc, MT, NT, threads))
+        return plan->fail(AKM_ERR_UNSUPPORTED, "no spread tile for footprint %d x %d", M, F * rc);
+      const int Nn = F * rc;
+      const int TM = (M + MT - 1) / MT, TN = (Nn + NT - 1) / NT;
+      const int Fmax = F;
+      int PB = 32;
+      size_t smem = spread_smem_bytes(PB, TM * MT, TN * NT, Fmax, rc);
+      while (smem > 96 * 1024 && PB > 4) {
+        PB /= 2;
+        smem = spread_smem_bytes(PB, TM * MT, TN * NT, Fmax, rc);
+      }
+      AKM_CK(launch_spread(dtab, plan->items_s.as<WorkItem>() + grp.spread_begin, grp.spread_count,
+                           plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc, r,
+                           plan->grid.as<double>(), MT, NT, threads, PB, smem, plan->beta, s));
+      if (grp.spread_count > 0) {
+        ++plan->launches;
+        ++plan->spread_launches;
+      }
+      r0 += rc;
+    }
+  }
+  if (ev) AKM_CK(cudaEventRecord(ev->e[1], s));
+  // S3-S5: DFT, multiply, inverse DFT
+  AKM_CK(launch_fft_forward(plan->tab, dtab, plan->grid.as<double>(), plan->A1.as<double2>(), plan->A2.as<double2>(),
+                            plan->tw.as<double2>(), r, plan->maxA1, plan->maxA2, s));
+  AKM_CK(launch_fft_multiply_inverse(plan->tab, dtab, plan->A2.as<double2>(), plan->A3.as<double2>(),
+                                     plan->C.as<double2>(), plan->C2.as<double2>(), plan->tw.as<double2>(),
+                                     plan->D.as<double>(), ops, dslot0, r, plan->H.as<double>(), plan->maxA3,
+                                     plan->maxC, plan->maxC2, plan->maxTap, s));
+  plan->launches += 6;
+  if (ev) AKM_CK(cudaEventRecord(ev->e[2], s));
+  // S6: interpolation
+  int r0 = 0;
+  while (r0 < r) {
+    const int rc = interp_rc_for(r - r0);
+    for (const Group& grp : plan->groups) {
+      const int F = grp.F, d = grp.d;
+      const int slab = (d >= 2 ? F : 1) * F;
+      const size_t smem = interp_smem_bytes(slab, ops, rc);
+      if (smem > 200 * 1024) return plan->fail(AKM_ERR_UNSUPPORTED, "interp footprint too large (%zu bytes)", smem);
+      AKM_CK(launch_interp(dtab, plan->items_i.as<WorkItem>() + grp.interp_begin, grp.interp_count,
+                           plan->u_sorted.as<double>(), plan->perm.as<int>(), plan->H.as<double>(), d, 2 * plan->m,
+                           ops, r, r0, rc, plan->part.as<double>(), n, plan->beta, smem, s));
+      if (grp.interp_count > 0) {
+        ++plan->launches;
+        ++plan->interp_launches;
+      }
+    }
+    r0 += rc;
+  }
+  if (ev) AKM_CK(cudaEventRecord(ev->e[3], s));
+  // S7: epilogue
+  AKM_CK(launch_epilogue(n, plan->P, r, ops, plan->part.as<double>(), V, ldv, plan->sigma_f, plan->sigma_eps, Y, dYl,
+                         dYsf, ldy, slotK, slotL, s));
+  ++plan->launches;
+  if (ev) AKM_CK(cudaEventRecord(ev->e[4], s));
+  return AKM_OK;
+}
+
+// host/device staging around run_mvm
+static akm_status mvm_entry(akm_plan* plan, const double* V, long long ldv, int r, double* Y, double* dYl,
+                            double* dYsf, double* dYse, long long ldy, cudaStream_t s) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points || !plan->have_theta)
+    return plan->fail(AKM_ERR_STATE, "kernel_mvm called before set_points and set_theta");
+  if (r < 1 || ldv < r || ldy < r) return plan->fail(AKM_ERR_INVALID_ARG, "bad r/ldv/ldy (r=%d ldv=%lld ldy=%lld)", r, ldv, ldy);
+  if (!Y && !dYl && !dYsf && !dYse) return plan->fail(AKM_ERR_INVALID_ARG, "no output requested");
+  const long long n = plan->n;
+  if (n > 0 && !V) return plan->fail(AKM_ERR_INVALID_ARG, "V is NULL");
+  AKM_CK(cudaSetDevice(plan->device));
+  if (n == 0) return AKM_OK;
+  const bool v_dev = is_device_ptr(V);
+  double* outs[4] = {Y, dYl, dYsf, dYse};
+  bool out_dev[4];
+  bool any_host = !v_dev;
+  for (int k = 0; k < 4; ++k) {
+    out_dev[k] = outs[k] ? is_device_ptr(outs[k]) : true;
+    any_host = any_host || !out_dev[k];
+  }
+  const double* Vd = V;
+  long long ldvd = ldv;
+  if (!v_dev) {
+    AKM_CK(plan->stageV.ensure(sizeof(double) * n * r));
+    AKM_CK(cudaMemcpy2DAsync(plan->stageV.p, sizeof(double) * r, V, sizeof(double) * ldv, sizeof(double) * r, n,
+                             cudaMemcpyHostToDevice, s));
+    Vd = plan->stageV.as<double>();
+    ldvd = r;
+  }
+  DevBuf* stages[4] = {&plan->stageY, &plan->stageL, &plan->stageS, nullptr};
+  double* od[4];
+  long long ldyd = ldy;
+  bool staged = false;
+  for (int k = 0; k < 4; ++k) {
+    od[k] = outs[k];
+    if (outs[k] && !out_dev[k]) staged = true;
+  }
+  if (staged) {
+    // stage every output (one leading dimension for all)
+    ldyd = r;
+    for (int k = 0; k < 4; ++k) {
+      if (!outs[k]) continue;
+      DevBuf* b = stages[k] ? stages[k] : &plan->bs0;
+      if (k == 3) {
+        AKM_CK(plan->bs0.ensure(sizeof(double) * n * r));  // reuse (tables are already built)
+        b = &plan->bs0;
+      }
+      AKM_CK(b->ensure(sizeof(double) * n * r));
+      od[k] = b->as<double>();
+    }
+  }
+  if (od[0] || od[1] || od[2]) {
+    akm_status st = run_mvm(plan, Vd, ldvd, r, od[0], od[1], od[2], ldyd, s);
+    if (st != AKM_OK) return st;
+  }
+  if (od[3]) {
+    AKM_CK(launch_scaled_copy(n, r, 2.0 * plan->sigma_eps, Vd, ldvd, od[3], ldyd, s));
+    ++plan->launches;
+  }
+  if (staged) {
+    for (int k = 0; k < 4; ++k) {
+      if (!outs[k]) continue;
+      AKM_CK(cudaMemcpy2DAsync(outs[k], sizeof(double) * ldy, od[k], sizeof(double) * r, sizeof(double) * r, n,
+                               out_dev[k] ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    }
+  }
+  if (any_host) AKM_CK(cudaStreamSynchronize(s));
+  return AKM_OK;
+}
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* akm_version(void) { return "akm 0.1 (sm_100a, float64 NFFT fast summation)"; }
+
+akm_status akm_create(akm_plan** out, int device) {
+  if (!out) return AKM_ERR_INVALID_ARG;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+    cudaGetLastError();
+    return AKM_ERR_CUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return AKM_ERR_CUDA;
+  akm_plan* p = new (std::nothrow) akm_plan();
+  if (!p) return AKM_ERR_OOM;
+  p->device = device;
+  *out = p;
+  return AKM_OK;
+}
+
+void akm_destroy(akm_plan* plan) {
+  if (!plan) return;
+  cudaSetDevice(plan->device);
+  cudaDeviceSynchronize();
+  delete plan;
+}
+
+const char* akm_last_error(const akm_plan* plan) { return plan ? plan->err.c_str() : "null plan"; }
+
+akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p, int64_t ldx, const int32_t* win_feat,
+                          const int32_t* win_len, int32_t P, int32_t family, int32_t N, double sigma_over, int32_t m,
+                          double eps_B, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  plan->have_points = false;
+  plan->have_theta = false;
+  cudaStream_t s = S(stream);
+  if (n < 0 || n > 2000000000LL) return plan->fail(AKM_ERR_INVALID_ARG, "n out of range (%lld)", (long long)n);
+  if (p < 1 || ldx < p) return plan->fail(AKM_ERR_INVALID_ARG, "bad p/ldx (p=%d ldx=%lld)", p, (long long)ldx);
+  if (P < 1 || P > AKM_MAX_WINDOWS) return plan->fail(AKM_ERR_INVALID_ARG, "P must be in [1, %d]", AKM_MAX_WINDOWS);
+  if (!win_feat || !win_len) return plan->fail(AKM_ERR_INVALID_ARG, "null window arrays");
+  if (family != AKM_GAUSSIAN && family != AKM_MATERN12) return plan->fail(AKM_ERR_INVALID_ARG, "unknown family %d", family);
+  if (N < 4 || (N % 2) != 0) return plan->fail(AKM_ERR_INVALID_ARG, "N must be even and >= 4 (got %d)", N);
+  if (!(sigma_over > 1.0) || !std::isfinite(sigma_over)) return plan->fail(AKM_ERR_INVALID_ARG, "sigma_over must be > 1");
+  const double ngd = sigma_over * N;
+  const int n_g = (int)std::lround(ngd);
+  if (std::fabs(ngd - n_g) > 1e-9 || (n_g % 2) != 0)
+    return plan->fail(AKM_ERR_INVALID_ARG, "sigma_over * N must be an even integer (got %g)", ngd);
+  if (m < 1 || 2 * m >= n_g) return plan->fail(AKM_ERR_INVALID_ARG, "need 1 <= m and 2m < sigma_over*N");
+  if (m != 4 && m != 6 && m != 8) return plan->fail(AKM_ERR_UNSUPPORTED, "window support m = %d not built (4, 6, 8)", m);
+  if (!(eps_B >= 0.0 && eps_B < 0.5)) return plan->fail(AKM_ERR_INVALID_ARG, "eps_B must be in [0, 1/2)");
+  if (n > 0 && !X) return plan->fail(AKM_ERR_INVALID_ARG, "X is NULL");
+  // windows: sizes 1..3, ids in range, pairwise disjoint
+  std::vector<int> lens(win_len, win_len + P);
+  int tot = 0;
+  for (int w = 0; w < P; ++w) {
+    if (lens[w] < 1 || lens[w] > 3) return plan->fail(AKM_ERR_INVALID_ARG, "window %d has size %d (must be 1..3)", w, lens[w]);
+    tot += lens[w];
+  }
+  std::vector<int> feats(win_feat, win_feat + tot);
+  std::set<int> seen;
+  for (int f : feats) {
+    if (f < 0 || f >= p) return plan->fail(AKM_ERR_INVALID_ARG, "feature id %d out of range [0, %d)", f, p);
+    if (!seen.insert(f).second) return plan->fail(AKM_ERR_INVALID_ARG, "windows overlap in feature %d", f);
+  }
+  AKM_CK(cudaSetDevice(plan->device));
+  plan->n = n;
+  plan->p = p;
+  plan->P = P;
+  plan->family = family;
+  plan->N = N;
+  plan->m = m;
+  plan->n_g = n_g;
+  plan->sigma_over = sigma_over;
+  plan->eps_B = eps_B;
+  plan->beta = kPi * (2.0 - 1.0 / sigma_over);
+  plan->win_len = lens;
+  plan->win_feat = feats;
+  plan->feat_used.assign(feats.begin(), feats.end());
+  const int nf = (int)feats.size();
+  // compact copy of the used features: Xc[i][j] = X[i][feats[j]]
+  AKM_CK(plan->Xc.ensure(sizeof(double) * std::max<long long>(n * nf, 1)));
+  if (n > 0) {
+    const double* Xd = X;
+    DevBuf xstage, fdev;
+    if (!is_device_ptr(X)) {
+      AKM_CK(xstage.ensure(sizeof(double) * (size_t)((n - 1) * ldx + p)));
+      AKM_CK(cudaMemcpyAsync(xstage.p, X, sizeof(double) * (size_t)((n - 1) * ldx + p), cudaMemcpyHostToDevice, s));
+      Xd = xstage.as<double>();
+    }
+    AKM_CK(fdev.ensure(sizeof(int) * nf));
+    AKM_CK(cudaMemcpyAsync(fdev.p, feats.data(), sizeof(int) * nf, cudaMemcpyHostToDevice, s));
+    AKM_CK(launch_gather_columns(Xd, n, ldx, fdev.as<int>(), nf, plan->Xc.as<double>(), s));
+    AKM_CK(cudaStreamSynchronize(s));  // the staging buffers are freed on scope exit
+  }
+  // per-window table skeleton (feature -> compact column)
+  WinTable& tab = plan->tab;
+  std::memset(&tab, 0, sizeof(tab));
+  tab.P = P;
+  tab.N = N;
+  tab.n_g = n_g;
+  tab.m = m;
+  int col = 0;
+  for (int w = 0; w < P; ++w) {
+    WinGeom& g = tab.w[w];
+    g.d = lens[w];
+    for (int a = 0; a < 3; ++a) g.feat[a] = 0;
+    for (int t = 0; t < g.d; ++t) g.feat[3 - g.d + t] = col++;
+  }
+  plan->lo.assign(3 * P, 0.0);
+  plan->hi.assign(3 * P, 0.0);
+  plan->radius.assign(P, 0.0);
+  if (n > 0) {
+    std::vector<int> idx(nf);
+    for (int j = 0; j < nf; ++j) idx[j] = j;
+    DevBuf fd;
+    AKM_CK(fd.ensure(sizeof(int) * nf));
+    AKM_CK(cudaMemcpyAsync(fd.p, idx.data(), sizeof(int) * nf, cudaMemcpyHostToDevice, s));
+    AKM_CK(plan->minmax.ensure(sizeof(double) * 3 * nf));
+    AKM_CK(launch_window_minmax(plan->Xc.as<double>(), n, nf, fd.as<int>(), nf, plan->minmax.as<double>(), s));
+    std::vector<double> mm(3 * nf);
+    AKM_CK(cudaMemcpyAsync(mm.data(), plan->minmax.p, sizeof(double) * 3 * nf, cudaMemcpyDeviceToHost, s));
+    AKM_CK(cudaStreamSynchronize(s));
+    for (int j = 0; j < nf; ++j)
+      if (mm[3 * j + 2] != 0.0) return plan->fail(AKM_ERR_NONFINITE, "X has non-finite values in feature %d", feats[j]);
+    for (int w = 0; w < P; ++w) {
+      WinGeom& g = tab.w[w];
+      for (int a = 3 - g.d; a < 3; ++a) {
+        const int j = g.feat[a];
+        plan->lo[w * 3 + a] = mm[3 * j];
+        plan->hi[w * 3 + a] = mm[3 * j + 1];
+        g.center[a] = 0.5 * (mm[3 * j] + mm[3 * j + 1]);  // bounding-box midpoint (reading R2)
+      }
+    }
+    AKM_CK(plan->dtab.ensure(sizeof(WinTable)));
+    AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
+    AKM_CK(plan->r2.ensure(sizeof(double) * P));
+    AKM_CK(launch_window_radius(plan->Xc.as<double>(), n, nf, tab, plan->dtab.as<WinTable>(), plan->r2.as<double>(), s));
+    std::vector<double> r2(P);
+    AKM_CK(cudaMemcpyAsync(r2.data(), plan->r2.p, sizeof(double) * P, cudaMemcpyDeviceToHost, s));
+    AKM_CK(cudaStreamSynchronize(s));
+    for (int w = 0; w < P; ++w) plan->radius[w] = std::sqrt(r2[w]);
+  }
+  plan->c_w.assign(P, 0.0);
+  plan->c_w_binned.assign(P, -1.0);
+  plan->r_cap = 0;
+  plan->have_points = true;
+  return AKM_OK;
+}
+
+akm_status akm_set_scale_override(akm_plan* plan, const double* c_w) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points) return plan->fail(AKM_ERR_STATE, "set_scale_override before set_points");
+  if (!c_w) {
+    plan->scale_override.clear();
+    return AKM_OK;
+  }
+  const double rho = 0.25 - plan->eps_B / 2.0;
+  for (int w = 0; w < plan->P; ++w) {
+    if (!(c_w[w] > 0.0) || !std::isfinite(c_w[w])) return plan->fail(AKM_ERR_INVALID_ARG, "c_w[%d] must be > 0", w);
+    if (plan->radius[w] / c_w[w] > rho * (1.0 + 1e-12))
+      return plan->fail(AKM_ERR_INVALID_ARG, "c_w[%d] = %g puts points outside the radius-%g ball", w, c_w[w], rho);
+  }
+  plan->scale_override.assign(c_w, c_w + plan->P);
+  plan->have_theta = false;
+  return AKM_OK;
+}
+
+akm_status akm_set_theta(akm_plan* plan, double sigma_f, double ell, double sigma_eps, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points) return plan->fail(AKM_ERR_STATE, "set_theta before set_points");
+  if (!std::isfinite(sigma_f) || !std::isfinite(ell) || !std::isfinite(sigma_eps))
+    return plan->fail(AKM_ERR_NONFINITE, "theta has non-finite entries");
+  if (!(sigma_f > 0.0) || !(ell > 0.0) || !(sigma_eps >= 0.0))
+    return plan->fail(AKM_ERR_INVALID_ARG, "need sigma_f > 0, ell > 0, sigma_eps >= 0");
+  cudaStream_t s = S(stream);
+  AKM_CK(cudaSetDevice(plan->device));
+  plan->have_theta = false;
+  plan->sigma_f = sigma_f;
+  plan->ell = ell;
+  plan->sigma_eps = sigma_eps;
+  // scale factors (reading R2): Matern fills the ball; Gaussian additionally keeps ell_eff <= 1/sqrt(2 pi N)
+  const double rho = 0.25 - plan->eps_B / 2.0;
+  bool changed = false;
+  for (int w = 0; w < plan->P; ++w) {
+    double c;
+    if (!plan->scale_override.empty()) {
+      c = plan->scale_override[w];
+    } else {
+      c = plan->radius[w] > 0.0 ? plan->radius[w] / rho : 1.0;
+      if (plan->family == AKM_GAUSSIAN) c = std::max(c, ell * std::sqrt(2.0 * kPi * plan->N));
+    }
+    plan->c_w[w] = c;
+    if (c != plan->c_w_binned[w]) changed = true;
+  }
+  if (plan->n == 0) {
+    plan->have_theta = true;
+    return AKM_OK;
+  }
+  if (changed) {
+    akm_status st = rebuild_bins(plan, s);
+    if (st != AKM_OK) return st;
+  }
+  akm_status st = rebuild_tables(plan, s);
+  if (st != AKM_OK) return st;
+  AKM_CK(cudaGetLastError());
+  plan->have_theta = true;
+  return AKM_OK;
+}
+
+akm_status akm_kernel_mvm(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y, int64_t ldy, void* stream) {
+  if (!Y) {
+    if (plan) plan->fail(AKM_ERR_INVALID_ARG, "Y is NULL");
+    return AKM_ERR_INVALID_ARG;
+  }
+  return mvm_entry(plan, V, ldv, r, Y, nullptr, nullptr, nullptr, ldy, S(stream));
+}
+
+akm_status akm_kernel_deriv_mvm(akm_plan* plan, int32_t which, const double* V, int64_t ldv, int32_t r, double* dY,
+                                int64_t ldy, void* stream) {
+  if (!dY) {
+    if (plan) plan->fail(AKM_ERR_INVALID_ARG, "dY is NULL");
+    return AKM_ERR_INVALID_ARG;
+  }
+  switch (which) {
+    case AKM_D_ELL: return mvm_entry(plan, V, ldv, r, nullptr, dY, nullptr, nullptr, ldy, S(stream));
+    case AKM_D_SIGMA_F: return mvm_entry(plan, V, ldv, r, nullptr, nullptr, dY, nullptr, ldy, S(stream));
+    case AKM_D_SIGMA_EPS: return mvm_entry(plan, V, ldv, r, nullptr, nullptr, nullptr, dY, ldy, S(stream));
+    default:
+      if (plan) plan->fail(AKM_ERR_INVALID_ARG, "unknown derivative parameter %d", which);
+      return AKM_ERR_INVALID_ARG;
+  }
+}
+
+akm_status akm_kernel_mvm_multi(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y, double* dY_ell,
+                                double* dY_sf, int64_t ldy, void* stream) {
+  return mvm_entry(plan, V, ldv, r, Y, dY_ell, dY_sf, nullptr, ldy, S(stream));
+}
+
+akm_status akm_set_profiling(akm_plan* plan, int32_t enable) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->profiling = enable != 0;
+  return AKM_OK;
+}
+
+akm_status akm_get_stage_times(akm_plan* plan, akm_stage_times* out, int32_t reset) {
+  if (!plan || !out) return AKM_ERR_INVALID_ARG;
+  cudaSetDevice(plan->device);
+  for (auto& es : plan->ring) plan->drain(es);
+  out->spread_ms = plan->stage_ms[0];
+  out->fft_ms = plan->stage_ms[1];
+  out->interp_ms = plan->stage_ms[2];
+  out->epilogue_ms = plan->stage_ms[3];
+  out->calls = plan->prof_calls;
+  out->kernel_launches = plan->launches;
+  out->spread_launches = plan->spread_launches;
+  out->interp_launches = plan->interp_launches;
+  if (reset) {
+    for (double& v : plan->stage_ms) v = 0.0;
+    plan->prof_calls = plan->launches = plan->spread_launches = plan->interp_launches = 0;
+  }
+  return AKM_OK;
+}
+
+akm_status akm_get_info(const akm_plan* plan, akm_info* out) {
+  if (!plan || !out) return AKM_ERR_INVALID_ARG;
+  std::memset(out, 0, sizeof(*out));
+  out->n = plan->n;
+  out->p = plan->p;
+  out->P = plan->P;
+  out->N = plan->N;
+  out->m = plan->m;
+  out->n_g = plan->n_g;
+  out->family = plan->family;
+  out->sigma_f = plan->sigma_f;
+  out->ell = plan->ell;
+  out->sigma_eps = plan->sigma_eps;
+  for (int w = 0; w < plan->P && w < AKM_MAX_WINDOWS; ++w) {
+    const WinGeom& g = plan->tab.w[w];
+    out->d[w] = g.d;
+    out->c_w[w] = plan->c_w.empty() ? 0.0 : plan->c_w[w];
+    out->ell_eff[w] = (plan->c_w.empty() || plan->c_w[w] == 0.0) ? 0.0 : plan->ell / plan->c_w[w];
+    out->radius[w] = plan->radius.empty() ? 0.0 : plan->radius[w];
+    for (int a = 0; a < 3; ++a) out->box[w][a] = g.L[a];
+    out->bin[w] = g.B;
+    out->occupied_bins[w] = plan->occupied.empty() ? 0 : plan->occupied[w];
+    out->max_bin_points[w] = plan->maxbin.empty() ? 0 : plan->maxbin[w];
+  }
+  out->work_items_spread = (int64_t)plan->items_spread.size();
+  out->work_items_interp = (int64_t)plan->items_interp.size();
+  long long ws = 0;
+  const DevBuf* bufs[] = {&plan->Xc, &plan->u_tmp, &plan->u_sorted, &plan->perm, &plan->hist, &plan->grid, &plan->H,
+                          &plan->A1, &plan->A2, &plan->A3, &plan->C, &plan->C2, &plan->tw, &plan->D, &plan->part,
+                          &plan->items_s, &plan->items_i};
+  for (const DevBuf* b : bufs) ws += (long long)b->bytes;
+  out->workspace_bytes = ws;
+  return AKM_OK;
+}
+
+}  // extern "C"

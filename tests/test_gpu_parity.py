@@ -1,0 +1,313 @@
+"""GPU parity of the CUDA path (through the C ABI) against the oracle -- SURVEY.md §4 tiers 3-5.
+
+Gates:
+  * method parity vs the float64 dense oracle (eqs. 2.1-2.3): relative Frobenius error over the
+    n x r block of every requested product <= 1e-6 (Gaussian) / 1e-3 (Matern), BASELINE.json
+    north_star; full rows at small n, seeded row samples at BASELINE.json's full sizes;
+  * implementation parity vs the truncated-Fourier oracle (eq. 3.3 evaluated exactly, same
+    scaling reading R2): <= 1e-9 at m = 6 and <= 1e-11 at m = 8 -- the NFFT window error
+    (eq. A.3) of this build is ~1e-12 / ~1e-14, so any wrong constant, sign or index fails.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import workloads
+from oracle import dense_apply
+from oracle import fourier as F
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def akm():
+    import __graft_entry__
+    __graft_entry__.build_library()
+    import paper_2504_00480_b200 as mod
+    return mod
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def gpu_apply(akm, X, windows, family, theta, V, N=32, sigma=2.0, m=6, eps_B=1.0 / 16, ops=("K",), scales=None,
+              host=False):
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    Xa = X if host else torch.from_numpy(np.ascontiguousarray(X)).to(dev)
+    plan.set_points(Xa, windows, family, N, sigma, m, eps_B)
+    if scales is not None:
+        plan.set_scale_override(scales)
+    plan.set_theta(*theta)
+    V = np.ascontiguousarray(V if V.ndim == 2 else V[:, None])
+    if host:
+        Va = V
+        outs = {op: np.zeros_like(V) for op in ops}
+    else:
+        Va = torch.from_numpy(V).to(dev)
+        outs = {op: torch.empty_like(Va) for op in ops}
+    plan.mvm_multi(Va, Y=outs.get("K"), dY_ell=outs.get("dell"), dY_sf=outs.get("dsf"))
+    if not host:
+        torch.cuda.synchronize()
+        outs = {k: v.cpu().numpy() for k, v in outs.items()}
+    info = plan.info()
+    plan.close()
+    return outs, info
+
+
+def _wl_inputs(name, n=None, r=None):
+    wl = workloads.CONFIGS[name]
+    X = workloads.make_X(wl, n=n)
+    V = workloads.make_V(wl, n=n, r=r)
+    return wl, X, V
+
+
+def _theta(wl):
+    return (wl.sigma_f, wl.ell, wl.sigma_eps)
+
+
+def _tol(wl):
+    return 1e-6 if wl.family == 0 else 1e-3
+
+
+# ------------------------------------------------------------------ BASELINE.json configs
+def test_c1_full_vs_dense_and_ndft(akm):
+    wl, X, V = _wl_inputs("c1")
+    out, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B, ("K",))
+    de = dense_apply(X, wl.windows, wl.family, _theta(wl), V, ops=("K",))
+    assert rel(out["K"], de["K"]) <= 1e-6
+    nd = F.additive_fastsum(X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.eps_B, ops=("K",))
+    assert rel(out["K"], nd["K"]) <= 1e-9
+
+
+def test_c2_full_vs_dense(akm):
+    wl, X, V = _wl_inputs("c2")
+    out, info = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B,
+                          ("K", "dell"))
+    de = dense_apply(X, wl.windows, wl.family, _theta(wl), V, ops=("K", "dell"))
+    for op in ("K", "dell"):
+        assert rel(out[op], de[op]) <= 1e-6, (op, rel(out[op], de[op]))
+
+
+def test_c2_generator_vs_ndft(akm):
+    wl, X, V = _wl_inputs("c2", n=3000, r=2)
+    out, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B,
+                       ("K", "dell", "dsf"))
+    nd = F.additive_fastsum(X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.eps_B, ops=("K", "dell", "dsf"))
+    for op in ("K", "dell", "dsf"):
+        assert rel(out[op], nd[op]) <= 1e-9, (op, rel(out[op], nd[op]))
+
+
+def test_c3_rows_vs_dense(akm):
+    wl, X, V = _wl_inputs("c3")
+    out, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B, ("K",))
+    rows = workloads.make_rows(wl, 1024)
+    de = dense_apply(X, wl.windows, wl.family, _theta(wl), V, rows=rows, ops=("K",))
+    assert rel(out["K"][rows], de["K"]) <= 1e-3
+
+
+def test_c3_generator_vs_ndft(akm):
+    wl, X, V = _wl_inputs("c3", n=2000, r=3)
+    out, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B,
+                       ("K", "dell"))
+    nd = F.additive_fastsum(X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.eps_B, ops=("K", "dell"))
+    for op in ("K", "dell"):
+        assert rel(out[op], nd[op]) <= 1e-11, (op, rel(out[op], nd[op]))
+
+
+@pytest.mark.parametrize("name,nrows", [("c4", 192), ("c5", 256)])
+def test_full_size_rows_vs_dense(akm, name, nrows):
+    wl, X, V = _wl_inputs(name)
+    ops = wl.ops
+    out, info = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B, ops)
+    rows = workloads.make_rows(wl, nrows)
+    de = dense_apply(X, wl.windows, wl.family, _theta(wl), V, rows=rows, ops=ops)
+    for op in ops:
+        assert rel(out[op][rows], de[op]) <= _tol(wl), (op, rel(out[op][rows], de[op]))
+
+
+# ------------------------------------------------------------------ properties of the operator
+def test_symmetry_and_linearity(akm):
+    wl, X, _ = _wl_inputs("c2", n=4000)
+    rng = np.random.default_rng(21)
+    U = rng.standard_normal((4000, 2))
+    out, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), U, ops=("K", "dell"))
+    for op in ("K", "dell"):
+        a = U[:, 1] @ out[op][:, 0]
+        b = U[:, 0] @ out[op][:, 1]
+        assert abs(a - b) <= 1e-12 * (abs(a) + np.linalg.norm(out[op])), op
+    W = np.ascontiguousarray(np.stack([2.0 * U[:, 0] - 3.0 * U[:, 1]], axis=1))
+    lin, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), W, ops=("K",))
+    assert rel(lin["K"][:, 0], 2.0 * out["K"][:, 0] - 3.0 * out["K"][:, 1]) <= 1e-13
+
+
+def test_columns_independent_of_batching(akm):
+    wl, X, V = _wl_inputs("c4", n=5000, r=11)
+    th = _theta(wl)
+    batch, _ = gpu_apply(akm, X, wl.windows, wl.family, th, V, ops=("K", "dell"))
+    for c in (0, 5, 10):
+        single, _ = gpu_apply(akm, X, wl.windows, wl.family, th, np.ascontiguousarray(V[:, c:c + 1]), ops=("K", "dell"))
+        for op in ("K", "dell"):
+            assert rel(batch[op][:, c], single[op][:, 0]) <= 1e-13
+
+
+def test_eq35_derivative_matches_finite_difference(akm):
+    """eq. (3.5): at fixed scale factors the NFFT dK/dell product is the ell-derivative of the NFFT K product."""
+    wl, X, V = _wl_inputs("c2", n=3000, r=1)
+    sf, ell, se = _theta(wl)
+    plan_scales = gpu_apply(akm, X, wl.windows, wl.family, (sf, ell, se), V, ops=("K",))[1]["c_w"]
+    h = 1e-5 * ell
+    base, _ = gpu_apply(akm, X, wl.windows, wl.family, (sf, ell, se), V, ops=("dell",), scales=plan_scales)
+    kp, _ = gpu_apply(akm, X, wl.windows, wl.family, (sf, ell + h, se), V, ops=("K",), scales=plan_scales)
+    km, _ = gpu_apply(akm, X, wl.windows, wl.family, (sf, ell - h, se), V, ops=("K",), scales=plan_scales)
+    fd = (kp["K"] - km["K"]) / (2 * h)
+    assert rel(fd, base["dell"]) <= 1e-7
+
+
+@pytest.mark.parametrize("family,m,N", [(0, 4, 16), (1, 6, 32), (0, 8, 32), (1, 8, 16)])
+def test_mixed_window_sizes_vs_ndft(akm, family, m, N):
+    rng = np.random.default_rng(100 + m)
+    n = 700
+    X = rng.random((n, 7))
+    windows = [(0, 1, 2), (3, 4), (6,)]
+    V = rng.standard_normal((n, 3))
+    th = (0.8, 0.35, 0.2)
+    out, _ = gpu_apply(akm, X, windows, family, th, V, N=N, m=m, ops=("K", "dell", "dsf"))
+    nd = F.additive_fastsum(X, windows, family, th, V, N, 1.0 / 16, ops=("K", "dell", "dsf"))
+    tol = {4: 1e-6, 6: 1e-9, 8: 1e-11}[m]
+    for op in ("K", "dell", "dsf"):
+        assert rel(out[op], nd[op]) <= tol, (op, rel(out[op], nd[op]))
+
+
+@pytest.mark.parametrize("r", [1, 2, 3, 5, 12, 13, 23])
+def test_ragged_rhs_counts(akm, r):
+    rng = np.random.default_rng(r)
+    n = 1500
+    X = rng.random((n, 3))
+    V = rng.standard_normal((n, r))
+    th = (1.0, 0.3, 0.1)
+    out, _ = gpu_apply(akm, X, [(0, 1, 2)], 0, th, V, ops=("K", "dell"))
+    nd = F.additive_fastsum(X, [(0, 1, 2)], 0, th, V, 32, 1.0 / 16, ops=("K", "dell"))
+    for op in ("K", "dell"):
+        assert rel(out[op], nd[op]) <= 1e-9
+
+
+def test_strided_inputs_and_outputs(akm):
+    rng = np.random.default_rng(7)
+    n, r = 900, 3
+    X = rng.random((n, 5))
+    Vbig = torch.from_numpy(rng.standard_normal((n, 8))).cuda()
+    V = Vbig[:, 2:5]                       # ld 8, r 3
+    Ybig = torch.zeros((n, 6), dtype=torch.float64, device="cuda")
+    Y = Ybig[:, 1:4]                       # ld 6
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(X).cuda(), [(0, 2), (4,)], 1, 32, 2.0, 6, 1 / 16)
+    plan.set_theta(1.0, 0.5, 0.1)
+    plan.mvm(V, Y)
+    torch.cuda.synchronize()
+    nd = F.additive_fastsum(X, [(0, 2), (4,)], 1, (1.0, 0.5, 0.1), V.cpu().numpy(), 32, 1 / 16, ops=("K",))
+    assert rel(Y.cpu().numpy(), nd["K"]) <= 1e-9
+    assert torch.all(Ybig[:, 0] == 0) and torch.all(Ybig[:, 4:] == 0)
+    plan.close()
+
+
+def test_host_pointer_path_matches_device(akm):
+    wl, X, V = _wl_inputs("c1", n=1200, r=2)
+    dev, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, ops=("K", "dell"))
+    host, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, ops=("K", "dell"), host=True)
+    for op in ("K", "dell"):
+        assert rel(host[op], dev[op]) <= 1e-14
+
+
+def test_small_n_and_degenerate_windows(akm):
+    th = (1.3, 0.4, 0.2)
+    # n = 1: Khat = sigma_f^2 P + sigma_eps^2 up to the method error at r = 0
+    X = np.array([[0.3, 0.7, 0.1]])
+    out, _ = gpu_apply(akm, X, [(0, 1), (2,)], 0, th, np.array([[2.0]]), ops=("K", "dell", "dsf"))
+    assert out["K"][0, 0] == pytest.approx((1.3**2 * 2 + 0.04) * 2.0, rel=1e-6)
+    assert abs(out["dell"][0, 0]) <= 1e-6
+    # all points identical in a window (R_w = 0) and a handful of points
+    rng = np.random.default_rng(3)
+    X = rng.random((7, 4))
+    X[:, 3] = 0.5
+    V = rng.standard_normal((7, 2))
+    for fam in (0, 1):
+        out, _ = gpu_apply(akm, X, [(0, 1, 2), (3,)], fam, th, V, ops=("K",))
+        de = dense_apply(X, [(0, 1, 2), (3,)], fam, th, V, ops=("K",))
+        assert rel(out["K"], de["K"]) <= (1e-6 if fam == 0 else 1e-3)
+
+
+def test_n_zero_is_a_noop(akm):
+    plan = akm.Plan(0)
+    plan.set_points(np.zeros((0, 3)), [(0, 1, 2)], 0)
+    plan.set_theta(1.0, 0.5, 0.1)
+    plan.mvm(np.zeros((0, 2)), np.zeros((0, 2)))
+    plan.close()
+
+
+def test_deriv_entry_points(akm):
+    wl, X, V = _wl_inputs("c2", n=2500, r=2)
+    th = _theta(wl)
+    out, _ = gpu_apply(akm, X, wl.windows, wl.family, th, V, ops=("K", "dell", "dsf"))
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family)
+    plan.set_theta(*th)
+    Vd = torch.from_numpy(V).to(dev)
+    res = {}
+    for which, key in ((akm.AKM_D_ELL, "dell"), (akm.AKM_D_SIGMA_F, "dsf"), (akm.AKM_D_SIGMA_EPS, "dse")):
+        dY = torch.empty_like(Vd)
+        plan.deriv_mvm(which, Vd, dY)
+        res[key] = dY.cpu().numpy()
+    plan.close()
+    assert rel(res["dell"], out["dell"]) <= 1e-13
+    assert rel(res["dsf"], out["dsf"]) <= 1e-13
+    np.testing.assert_array_equal(res["dse"], 2 * th[2] * V)
+
+
+def test_error_codes(akm):
+    plan = akm.Plan(0)
+    with pytest.raises(akm.AkmError) as e:
+        plan.mvm(np.zeros((3, 1)), np.zeros((3, 1)))
+    assert e.value.status == akm.AKM_ERR_STATE
+    X = np.random.default_rng(0).random((10, 4))
+    bad = [
+        (dict(windows=[(0, 1), (1, 2)]), akm.AKM_ERR_INVALID_ARG),     # overlap
+        (dict(windows=[(0, 1, 2, 3)]), akm.AKM_ERR_INVALID_ARG),       # d > 3
+        (dict(windows=[(0, 9)]), akm.AKM_ERR_INVALID_ARG),             # id out of range
+        (dict(windows=[(0,)], N=7), akm.AKM_ERR_INVALID_ARG),          # odd N
+        (dict(windows=[(0,)], sigma_over=1.0), akm.AKM_ERR_INVALID_ARG),
+        (dict(windows=[(0,)], m=5), akm.AKM_ERR_UNSUPPORTED),
+        (dict(windows=[(0,)], eps_B=0.5), akm.AKM_ERR_INVALID_ARG),
+    ]
+    for kw, code in bad:
+        args = dict(windows=[(0,)], family=0, N=32, sigma_over=2.0, m=6, eps_B=1 / 16)
+        args.update(kw)
+        with pytest.raises(akm.AkmError) as e:
+            plan.set_points(X, **args)
+        assert e.value.status == code, kw
+    Xn = X.copy()
+    Xn[3, 1] = np.nan
+    with pytest.raises(akm.AkmError) as e:
+        plan.set_points(Xn, [(1,)], 0)
+    assert e.value.status == akm.AKM_ERR_NONFINITE
+    plan.set_points(X, [(0, 1)], 0)
+    with pytest.raises(akm.AkmError) as e:
+        plan.set_theta(1.0, -0.5, 0.1)
+    assert e.value.status == akm.AKM_ERR_INVALID_ARG
+    with pytest.raises(akm.AkmError) as e:
+        plan.set_theta(1.0, math.inf, 0.1)
+    assert e.value.status == akm.AKM_ERR_NONFINITE
+    with pytest.raises(akm.AkmError) as e:
+        plan.set_scale_override([1e-6])
+    assert e.value.status == akm.AKM_ERR_INVALID_ARG
+    plan.set_theta(1.0, 0.5, 0.1)
+    with pytest.raises(akm.AkmError) as e:
+        plan.mvm(np.zeros((10, 2)), np.zeros((10, 2)))[0:0]
+        akm.akm_kernel_deriv_mvm(plan.handle, 7, np.zeros((10, 1)), np.zeros((10, 1)))
+    assert e.value.status == akm.AKM_ERR_INVALID_ARG
+    plan.close()
