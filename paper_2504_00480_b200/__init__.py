@@ -129,6 +129,8 @@ def _ptr_ld(a, name):
         raise TypeError(f"{name} must be float64")
     if arr.ndim == 1:
         arr = arr[:, None]
+    if arr.ndim == 2 and arr.size == 0:
+        return ctypes.c_void_p(arr.ctypes.data), max(1, arr.shape[1]), arr.shape[0], arr.shape[1], False, arr
     if arr.ndim != 2 or arr.strides[1] != 8:
         raise ValueError(f"{name} must be 2-D row-major")
     ld = arr.strides[0] // 8 if arr.shape[0] > 1 else arr.shape[1]

@@ -20,6 +20,9 @@
 namespace akm {
 
 constexpr int kMaxWin = 32;
+constexpr int kPolyDeg = 14;              // window polynomial degree (see window_taps)
+constexpr int kPolyLen = kPolyDeg + 1;
+constexpr int kMaxTaps = 16;              // 2m <= 16
 constexpr double kPi = 3.14159265358979323846;
 
 // Per-window geometry passed (by value, inside WinTable) to kernels.
@@ -50,6 +53,7 @@ struct WinGeom {
 struct WinTable {
   int P;
   int N, n_g, m;
+  double poly[kMaxTaps * kPolyLen];  // window polynomial coefficients (see window_taps)
   WinGeom w[kMaxWin];
 };
 
@@ -73,6 +77,45 @@ __device__ __forceinline__ double kb_window(double delta, double m, double beta)
   }
   return 0.0;
 }
+
+// Window polynomials: for tap o in [0, 2m) of a point with fractional grid
+// position t = u - floor(u), the weight phi(t + m - 1 - o) is an entire function of t on [0, 1]
+// (sinh(beta q)/q is analytic in q^2 = m^2 - delta^2).  It is replaced by its degree-kPolyDeg
+// Chebyshev interpolant on [0, 1], stored as monomial coefficients in x = 2t - 1 (Horner).
+// Measured max error <= 1e-14 * phi(0) for m in {4,6,8}, sigma in [1.25, 2] (tests/ and
+// tools/ check it against the exact window).
+
+// Evaluate the 2m tap weights of one axis at x = 2 frac(u) - 1 from coefficients c[o*kPolyLen + k].
+template <int TAPS>
+__device__ __forceinline__ void window_taps(const double* __restrict__ c, double x, double* w) {
+#pragma unroll
+  for (int o = 0; o < TAPS; ++o) {
+    double v = c[o * kPolyLen + kPolyDeg];
+#pragma unroll
+    for (int k = kPolyDeg - 1; k >= 0; --k) v = fma(v, x, c[o * kPolyLen + k]);
+    w[o] = v;
+  }
+}
+
+__device__ __forceinline__ double window_tap(const double* __restrict__ c, int o, double x) {
+  double v = c[o * kPolyLen + kPolyDeg];
+#pragma unroll
+  for (int k = kPolyDeg - 1; k >= 0; --k) v = fma(v, x, c[o * kPolyLen + k]);
+  return v;
+}
+
+// FP64 tensor-core MMA (mma.sync.m8n8k4.f64), fragment layout verified on sm_100a by
+// tools/microbench/dmma_layout.cu:  A (8x4 row) a = A[lane>>2][lane&3];  B (4x8 col)
+// b = B[lane&3][lane>>2];  C (8x8) c{0,1} = C[lane>>2][2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// shared-memory row stride (doubles) of a matrix read as MMA fragments: = 4 (mod 16) makes the
+// 4 k-rows x 8 columns of a fragment load hit 32 distinct banks.
+__host__ __device__ constexpr int mma_ld(int cols) { return ((cols + 15) / 16) * 16 + 4; }
 
 // Modified Bessel I0 by its power series sum_k ((x/2)^{2k} / (k!)^2); x <= ~60 here.
 __host__ __device__ inline double bessel_i0(double x) {
@@ -109,6 +152,15 @@ cudaError_t launch_cos_dft_axis(int d, int N, int axis, const double* in, double
 cudaError_t launch_multiplier(const WinTable& tab, const WinTable* dtab, int win, const double* bK, const double* bL,
                               int ops_mask, double inv_c, double sigma_over, double* D, cudaStream_t s);
 cudaError_t launch_twiddles(const WinTable& tab, const WinTable* dtab, double2* tw, cudaStream_t s);
+cudaError_t launch_window_poly(int m, double beta, double* coef, cudaStream_t s);
+
+// spread_mma.cu
+bool spread_mma_choose(int M, int Nn, int& MB, int& NB, int& WM, int& WN);
+size_t spread_mma_smem(int PB, int M, int Nn, int Fmax, int rc);
+cudaError_t launch_spread_mma(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+                              const int* perm, const double* V, long long ldv, long long n, int r0, int rc,
+                              int r_total, double* grid, int MB, int NB, int WM, int WN, int PB, size_t smem,
+                              cudaStream_t s);
 
 // spread.cu
 bool spread_tile_supported(int MT, int NT);
@@ -130,10 +182,9 @@ cudaError_t launch_zero(double* p, long long count, cudaStream_t s);
 // interp.cu
 bool interp_supported(int d, int taps, int ops, int rc);
 int interp_rc_for(int r_remaining);
-size_t interp_smem_bytes(int slab, int ops, int rc);
 cudaError_t launch_interp(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
                           const int* perm, const double* H, int d, int taps, int ops, int r, int r0, int rc,
-                          double* part, long long n, double beta, size_t smem, cudaStream_t s);
+                          double* part, long long n, cudaStream_t s);
 cudaError_t launch_epilogue(long long n, int P, int r, int ops, const double* part, const double* V, long long ldv,
                             double sigma_f, double sigma_eps, double* Y, double* dYl, double* dYsf, long long ldy,
                             int slotK, int slotL, cudaStream_t s);

@@ -4,7 +4,7 @@
 namespace akm {
 cudaError_t launch_interp_d3_t16(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
                               const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
-                              long long n, double beta, size_t smem, cudaStream_t s) {
-  return launch_interp_dt<3, 16>(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, beta, smem, s);
+                              long long n, cudaStream_t s) {
+  return launch_interp_dt<3, 16>(dtab, items, n_items, u_sorted, perm, H, ops, r, r0, rc, part, n, s);
 }
 }  // namespace akm

@@ -234,7 +234,6 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   if (errf) return plan->fail(AKM_ERR_CUDA, "internal error: a scaled point fell outside its grid box");
 
   // choose B per window (cost model in FMA-equivalents per RHS)
-  const int taps = 2 * m;
   std::vector<int> cell_off(std::max<long long>(ncells, 1), 0);
   plan->items_spread.clear();
   plan->items_interp.clear();
@@ -243,7 +242,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   const long long total_pts = n * P;
   long long ch_s = total_pts / (148 * 2);
   ch_s = std::max(32LL, std::min(4096LL, ch_s));
-  const int ch_i = 128;
+  const int ch_i = 128;  // interpolation: one cell per work item (64 thr x 2 pts, or 8 warps x 16 pts on DMMA)
   std::vector<std::vector<WorkItem>> its_s(P), its_i(P);
   for (int w = 0; w < P; ++w) {
     WinGeom& g = tab.w[w];
@@ -258,6 +257,11 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
       if (Fd > 20000) continue;
       bool fits = true;
       for (int a = 3 - d; a < 3; ++a) fits = fits && ((g.ncell[a] + B - 1) / B) * B + 2 * m - 1 <= n_g;
+      {
+        int MB_, NB_, WM_, WN_, Mr = 1;
+        for (int t = 0; t < d - 1; ++t) Mr *= F;
+        fits = fits && spread_mma_choose(Mr, F, MB_, NB_, WM_, WN_);
+      }
       if (!fits) continue;
       int nb[3];
       for (int a = 0; a < 3; ++a) nb[a] = (g.ncell[a] + B - 1) / (a < 3 - d ? 1 : B);
@@ -271,18 +275,13 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
             const int b0 = (3 - d > 0) ? 0 : c0 / B, b1 = (3 - d > 1) ? 0 : c1 / B, b2 = c2 / B;
             bc[((size_t)b0 * nb[1] + b1) * nb[2] + b2] += v;
           }
-      double chunks_s = 0, chunks_i = 0;
+      double chunks_s = 0;
       for (long long v : bc)
-        if (v) {
-          chunks_s += (double)((v + ch_s - 1) / ch_s);
-          chunks_i += (double)((v + ch_i - 1) / ch_i);
-        }
-      double tapd = 1;
-      for (int t = 0; t < d; ++t) tapd *= taps;
-      const double diverge = (d == 3) ? (double)F / taps : 1.0;
-      const double spread = Fd * ((double)n + 34.0 * chunks_s);
-      const double interp = 2.0 * ((double)n * tapd * diverge + 4.0 * chunks_i * Fd);
-      const double cost = spread + interp;
+        if (v) chunks_s += (double)((v + ch_s - 1) / ch_s);
+      // spreading: F^d FMAs per point and RHS, plus one footprint flush of F^d RED.ADD.F64
+      // (~34 FMA-equivalents each, profiles/r01_fp64_peaks.txt) per work item.  Interpolation
+      // works per cell and does not depend on B.
+      const double cost = Fd * ((double)n + 34.0 * chunks_s);
       if (cost < bestCost * 0.999) {
         bestCost = cost;
         bestB = B;
@@ -318,7 +317,10 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
                 if (c0 >= g.ncell[0] || c1 >= g.ncell[1] || c2 >= g.ncell[2]) continue;
                 const long long ci = ((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2;
                 cell_off[hoff[w] + ci] = (int)pos;
-                pos += hc[ci];
+                const int cc = hc[ci];
+                for (int q = 0; q < cc; q += ch_i)
+                  its_i[w].push_back(WorkItem{w, {c0, c1, c2}, (int)(pos + q), std::min(ch_i, cc - q)});
+                pos += cc;
               }
           const long long cnt = pos - start;
           if (!cnt) continue;
@@ -326,8 +328,6 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
           plan->maxbin[w] = std::max(plan->maxbin[w], cnt);
           for (long long q = 0; q < cnt; q += ch_s)
             its_s[w].push_back(WorkItem{w, {b0, b1, b2}, (int)(start + q), (int)std::min<long long>(ch_s, cnt - q)});
-          for (long long q = 0; q < cnt; q += ch_i)
-            its_i[w].push_back(WorkItem{w, {b0, b1, b2}, (int)(start + q), (int)std::min<long long>(ch_i, cnt - q)});
         }
     if (pos != n) return plan->fail(AKM_ERR_CUDA, "internal error: histogram of window %d holds %lld of %lld points",
                                     w, pos, n);
@@ -523,23 +523,20 @@ static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r,
     for (int t = 0; t < d - 1; ++t) M *= F;
     int r0 = 0;
     while (r0 < r) {
-      // largest RHS chunk (<= 12) whose footprint tile fits one CTA of <= 256 threads
-      int rc = std::min(12, r - r0), MT = 0, NT = 0, threads = 0;
-      while (rc > 1 && !choose_spread_tile(M, F * rc, MT, NT, threads)) --rc;
-      if (!choose_spread_tile(M, F * rc, MT, NT, threads))
+      // largest RHS chunk (<= 12) whose footprint fits one CTA of <= 9 warps of DMMA tiles
+      int rc = std::min(12, r - r0), MB = 0, NB = 0, WM = 0, WN = 0;
+      while (rc > 1 && !spread_mma_choose(M, F * rc, MB, NB, WM, WN)) --rc;
+      if (!spread_mma_choose(M, F * rc, MB, NB, WM, WN))
         return plan->fail(AKM_ERR_UNSUPPORTED, "no spread tile for footprint %d x %d", M, F * rc);
-      const int Nn = F * rc;
-      const int TM = (M + MT - 1) / MT, TN = (Nn + NT - 1) / NT;
-      const int Fmax = F;
       int PB = 32;
-      size_t smem = spread_smem_bytes(PB, TM * MT, TN * NT, Fmax, rc);
-      while (smem > 96 * 1024 && PB > 4) {
+      size_t smem = spread_mma_smem(PB, M, F * rc, F, rc);
+      while (smem > 100 * 1024 && PB > 4) {
         PB /= 2;
-        smem = spread_smem_bytes(PB, TM * MT, TN * NT, Fmax, rc);
+        smem = spread_mma_smem(PB, M, F * rc, F, rc);
       }
-      AKM_CK(launch_spread(dtab, plan->items_s.as<WorkItem>() + grp.spread_begin, grp.spread_count,
-                           plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc, r,
-                           plan->grid.as<double>(), MT, NT, threads, PB, smem, plan->beta, s));
+      AKM_CK(launch_spread_mma(dtab, plan->items_s.as<WorkItem>() + grp.spread_begin, grp.spread_count,
+                               plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc, r,
+                               plan->grid.as<double>(), MB, NB, WM, WN, PB, smem, s));
       if (grp.spread_count > 0) {
         ++plan->launches;
         ++plan->spread_launches;
@@ -562,13 +559,9 @@ static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r,
   while (r0 < r) {
     const int rc = interp_rc_for(r - r0);
     for (const Group& grp : plan->groups) {
-      const int F = grp.F, d = grp.d;
-      const int slab = (d >= 2 ? F : 1) * F;
-      const size_t smem = interp_smem_bytes(slab, ops, rc);
-      if (smem > 200 * 1024) return plan->fail(AKM_ERR_UNSUPPORTED, "interp footprint too large (%zu bytes)", smem);
       AKM_CK(launch_interp(dtab, plan->items_i.as<WorkItem>() + grp.interp_begin, grp.interp_count,
-                           plan->u_sorted.as<double>(), plan->perm.as<int>(), plan->H.as<double>(), d, 2 * plan->m,
-                           ops, r, r0, rc, plan->part.as<double>(), n, plan->beta, smem, s));
+                           plan->u_sorted.as<double>(), plan->perm.as<int>(), plan->H.as<double>(), grp.d,
+                           2 * plan->m, ops, r, r0, rc, plan->part.as<double>(), n, s));
       if (grp.interp_count > 0) {
         ++plan->launches;
         ++plan->interp_launches;
@@ -765,6 +758,14 @@ akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p,
     g.d = lens[w];
     for (int a = 0; a < 3; ++a) g.feat[a] = 0;
     for (int t = 0; t < g.d; ++t) g.feat[3 - g.d + t] = col++;
+  }
+  {  // window polynomials (depend on m and sigma only)
+    DevBuf pc;
+    AKM_CK(pc.ensure(sizeof(double) * kMaxTaps * kPolyLen));
+    AKM_CK(cudaMemsetAsync(pc.p, 0, sizeof(double) * kMaxTaps * kPolyLen, s));
+    AKM_CK(launch_window_poly(m, plan->beta, pc.as<double>(), s));
+    AKM_CK(cudaMemcpyAsync(tab.poly, pc.p, sizeof(double) * kMaxTaps * kPolyLen, cudaMemcpyDeviceToHost, s));
+    AKM_CK(cudaStreamSynchronize(s));
   }
   plan->lo.assign(3 * P, 0.0);
   plan->hi.assign(3 * P, 0.0);

@@ -334,4 +334,50 @@ cudaError_t launch_twiddles(const WinTable& tab, const WinTable* dtab, double2* 
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- window polynomials
+// One thread per tap o: Chebyshev interpolation of f_o(t) = phi(t + m - 1 - o), t in [0,1], at
+// kPolyLen Chebyshev nodes (exact sinh form of App. A), converted to monomials in
+// x = 2t - 1.  f_o is sampled with the analytic (untruncated) window: on t in [0,1] the distance
+// |delta| never exceeds m, so this is the window itself.
+__global__ void k_window_poly(int m, double beta, double* __restrict__ coef) {
+  const int o = threadIdx.x;
+  if (o >= 2 * m) return;
+  constexpr int L = kPolyLen;
+  double f[L], a[L], c[L], Tp[L], Tc[L], Tn[L];
+  for (int j = 0; j < L; ++j) {
+    const double xn = cospi(((double)j + 0.5) / L);
+    const double delta = 0.5 * (xn + 1.0) + (double)(m - 1 - o);
+    const double s = (double)m * m - delta * delta;
+    if (s > 0.0) {
+      const double q = sqrt(s);
+      f[j] = sinh(beta * q) / (kPi * q);
+    } else {
+      f[j] = beta / kPi;  // limit q -> 0
+    }
+  }
+  for (int k = 0; k < L; ++k) {
+    double acc = 0.0;
+    for (int j = 0; j < L; ++j) acc += f[j] * cospi((double)k * ((double)j + 0.5) / L);
+    a[k] = acc * 2.0 / L;
+  }
+  a[0] *= 0.5;
+  for (int k = 0; k < L; ++k) { c[k] = 0.0; Tp[k] = 0.0; Tc[k] = 0.0; }
+  Tp[0] = 1.0;  // T_0
+  Tc[1] = 1.0;  // T_1
+  c[0] += a[0];
+  c[1] += a[1];
+  for (int k = 2; k < L; ++k) {
+    Tn[0] = -Tp[0];
+    for (int q = 1; q < L; ++q) Tn[q] = 2.0 * Tc[q - 1] - Tp[q];
+    for (int q = 0; q < L; ++q) c[q] += a[k] * Tn[q];
+    for (int q = 0; q < L; ++q) { Tp[q] = Tc[q]; Tc[q] = Tn[q]; }
+  }
+  for (int k = 0; k < L; ++k) coef[o * L + k] = c[k];
+}
+
+cudaError_t launch_window_poly(int m, double beta, double* coef, cudaStream_t s) {
+  k_window_poly<<<1, 32, 0, s>>>(m, beta, coef);
+  return cudaGetLastError();
+}
+
 }  // namespace akm

@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(256) k_spread(const WinTable* __restrict__ tab
   const bool active = tm < TM;
 
   extern __shared__ double smem[];
-  double* As = smem;                          // [PB][Mpad]  w0 (x) w1
+  double* poly = smem;                        // [2m][kPolyLen] window polynomials
+  double* As = poly + kMaxTaps * kPolyLen;    // [PB][Mpad]  w0 (x) w1
   double* Bs = As + (size_t)PB * Mpad;        // [PB][Npad]  w2 (x) v
   double* Ws = Bs + (size_t)PB * Npad;        // [PB][3][Fmax] window weights
   double* Vs = Ws + (size_t)PB * 3 * Fmax;    // [PB][rc]
@@ -49,6 +50,10 @@ __global__ void __launch_bounds__(256) k_spread(const WinTable* __restrict__ tab
   int org[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) org[a] = g.box_lo[a] + it.bin[a] * g.B;
+
+  const int taps = 2 * tab.m;
+  for (int idx = tid; idx < taps * kPolyLen; idx += blockDim.x) poly[idx] = tab.poly[idx];
+  __syncthreads();
 
   double acc[MT][NT];
 #pragma unroll
@@ -69,7 +74,9 @@ __global__ void __launch_bounds__(256) k_spread(const WinTable* __restrict__ tab
         wv = (o == 0) ? 1.0 : 0.0;  // singleton axis
       } else if (o < g.F[a]) {
         const double u = u_sorted[((long long)it.win * 3 + a) * n + it.start + p0 + p];
-        wv = kb_window(u - (double)(org[a] + o), mm, beta);
+        const double fl = floor(u);
+        const int tap = o - ((int)fl - tab.m + 1 - org[a]);  // tap index of footprint node o
+        if (tap >= 0 && tap < taps) wv = window_tap(poly, tap, 2.0 * (u - fl) - 1.0);
       }
       Ws[idx] = wv;
     }
@@ -150,7 +157,7 @@ bool spread_tile_supported(int MT, int NT) {
 }
 
 size_t spread_smem_bytes(int PB, int Mpad, int Npad, int Fmax, int rc) {
-  return sizeof(double) * (size_t)PB * (size_t)(Mpad + Npad + 3 * Fmax + rc);
+  return sizeof(double) * ((size_t)PB * (size_t)(Mpad + Npad + 3 * Fmax + rc) + kMaxTaps * kPolyLen);
 }
 
 cudaError_t launch_spread(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
