@@ -211,6 +211,7 @@ def main():
 
     import torch
     import paper_2504_00480_b200 as akm
+    from paper_2504_00480_b200 import dist as D   # host-side N > 1 logic only (no kernels)
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -220,7 +221,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     X = workloads.make_X(wl)
-    V = workloads.make_V(wl, seed=2000 + wl.index + 7919 * rank)  # independent RHS block per rank
+    V = workloads.make_V(wl, seed=D.rank_seed(2000 + wl.index, rank))  # independent RHS block per rank
     Xd = torch.from_numpy(X).to(dev)
     Vd = torch.from_numpy(V).to(dev)
     outs = {op: torch.empty_like(Vd) for op in wl.ops}
@@ -233,8 +234,20 @@ def main():
     set_theta_ms = (time.perf_counter() - t0) * 1e3
     info = plan.info()
 
-    def step():
-        plan.mvm_multi(Vd, Y=outs.get("K"), dY_ell=outs.get("dell"), dY_sf=outs.get("dsf"))
+    objective = "cg_iters" in wl.extra          # c5: one Z~ evaluation per step (S8)
+    if objective:
+        cg, lz = wl.extra["cg_iters"], wl.extra["lanczos_steps"]
+        yd, Zd = Vd[:, 0].contiguous(), Vd[:, 1:].contiguous()
+        products_per_step = max(cg, lz)
+        last = {}
+
+        def step():
+            last["out"] = plan.objective_diag(yd, Zd, cg, lz)
+    else:
+        products_per_step = 1
+
+        def step():
+            plan.mvm_multi(Vd, Y=outs.get("K"), dY_ell=outs.get("dell"), dY_sf=outs.get("dsf"))
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     for _ in range(max(args.warmup, 3)):
@@ -264,19 +277,24 @@ def main():
     plan.set_profiling(False)
     tail = ClockSampler.one_shot(local)
     stages = plan.stage_times(reset=True)
-    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = D.max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(starts, ends)), dev)
     ms_per_step = total_ms / K
-    value = wl.units * world / (ms_per_step * 1e-3)
+    value = D.weak_throughput(wl.units * products_per_step, world, ms_per_step)
 
     # ---------------- e2e: same call with pinned host V and outputs
     Vh = torch.from_numpy(V).pin_memory()
     Oh = {op: torch.empty(V.shape, dtype=torch.float64).pin_memory() for op in wl.ops}
+    if objective:
+        yh, Zh = Vh[:, 0].contiguous().pin_memory(), Vh[:, 1:].contiguous().pin_memory()
+
+    def e2e_step():
+        if objective:   # host y, Z in; the objective's terms come back to the host
+            plan.objective_diag(yh, Zh, cg, lz, stream=stream.cuda_stream)
+        else:
+            plan.mvm_multi(Vh, Y=Oh.get("K"), dY_ell=Oh.get("dell"), dY_sf=Oh.get("dsf"), stream=stream.cuda_stream)
+
     for _ in range(3):
-        plan.mvm_multi(Vh, Y=Oh.get("K"), dY_ell=Oh.get("dell"), dY_sf=Oh.get("dsf"), stream=stream.cuda_stream)
+        e2e_step()
     torch.cuda.synchronize(dev)
     e_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     e_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
@@ -285,18 +303,15 @@ def main():
     for i in range(K):
         flush.fill_(float(i))
         e_s[i].record(stream)
-        plan.mvm_multi(Vh, Y=Oh.get("K"), dY_ell=Oh.get("dell"), dY_sf=Oh.get("dsf"), stream=stream.cuda_stream)
+        e2e_step()
         e_e[i].record(stream)
     torch.cuda.synchronize(dev)
-    e2e_ms = sum(s.elapsed_time(e) for s, e in zip(e_s, e_e))
-    if dist:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = wl.units * world / (e2e_ms / K * 1e-3)
+    e2e_ms = D.max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(e_s, e_e)), dev)
+    e2e_value = D.weak_throughput(wl.units * products_per_step, world, e2e_ms / K)
 
     # ---------------- roofline of the dominant kernel
     spread_fl, interp_fl, alg_bytes = algorithmic_counts(wl, info, wl.r, wl.ops)
+    alg_bytes *= products_per_step
     cand = []
     if stages["spread_launches"]:
         cand.append(("spread", stages["spread_ms"], stages["spread_launches"], spread_fl))
@@ -304,7 +319,7 @@ def main():
         cand.append(("interp", stages["interp_ms"], stages["interp_launches"], interp_fl))
     name, st_ms, launches, flops = max(cand, key=lambda c: c[1])
     per_launch_ms = st_ms / launches
-    flops_per_launch = flops / (launches / K)
+    flops_per_launch = flops * products_per_step / (launches / K)
     achieved = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
     peaks = _peaks()
     stage_total = stages["spread_ms"] + stages["fft_ms"] + stages["interp_ms"] + stages["epilogue_ms"]
@@ -316,7 +331,7 @@ def main():
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": config_dict(wl),
         "e2e": {"value": e2e_value, "unit": "pts/s", "h2d_bytes_per_step": int(V.nbytes),
-                "d2h_bytes_per_step": int(V.nbytes * len(wl.ops))},
+                "d2h_bytes_per_step": int(8 * (10 + 2 * wl.r) if objective else V.nbytes * len(wl.ops))},
         "gpu_launches": int(stages["kernel_launches"]),
         "roofline": {"bound": "alu", "kernel": name, "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
@@ -328,10 +343,16 @@ def main():
         "hbm": {"algorithmic_bytes_per_step": alg_bytes, "achieved_gbs": alg_bytes / (ms_per_step * 1e-3) / 1e9,
                 "peak_gbs": peaks.get("hbm_gbs"), "frac": alg_bytes / (ms_per_step * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)},
         "set_theta_ms": set_theta_ms,
+        "products_per_step": products_per_step,
         "plan": {"bin": info["bin"], "box": info["box"], "c_w": info["c_w"], "work_items_spread": info["work_items_spread"],
                  "work_items_interp": info["work_items_interp"], "max_bin_points": info["max_bin_points"]},
         "clocks": clocks,
     }
+    if objective:
+        o = last["out"]
+        line["objective"] = {"Z": o["Z"], "quad": o["quad"], "logdetM": o["logdetM"], "slq": o["slq"],
+                             "cg_relres": o["cg_relres"], "steps": o["steps"], "ms_per_evaluation": ms_per_step,
+                             "ms_per_product": ms_per_step / products_per_step}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl)
     plan.close()

@@ -145,6 +145,38 @@ typedef struct {
 akm_status akm_set_profiling(akm_plan* plan, int32_t enable);
 akm_status akm_get_stage_times(akm_plan* plan, akm_stage_times* out, int32_t reset);
 
+/* One evaluation of the preconditioned objective (eq. 1.4) with the diagonal
+ * preconditioner M = diag(Khat) = (sigma_f^2 P + sigma_eps^2) I (reading R11):
+ *     Z~ = 1/2 ( y^T x + log det M + (1/n_z) sum_i z_i^T logm(M^{-1} Khat) z_i + n log 2 pi ),
+ * x = cg_iters steps of preconditioned CG on Khat x = y from x0 = 0, and each
+ * quadratic form by stochastic Lanczos quadrature: lanczos_steps steps of Lanczos on
+ * M^{-1/2} Khat M^{-1/2} from z_i/||z_i|| with full reorthogonalisation, stopped early on breakdown
+ * beta_j <= 1e-12 ||S q_j|| (reading R14), Gauss quadrature ||z_i||^2 sum_j tau_j^2 log theta_j.
+ * Every Krylov step is ONE product of Khat with the n x (1 + n_z) block [CG direction | Lanczos
+ * vectors] through the NFFT path (columns that finished are zero; reading R11).
+ *   y   n float64 (device or host);  Z  n x n_z row-major probes (ld ldz >= n_z; device or host)
+ *   1 <= n_z <= AKM_MAX_PROBES, 0 <= cg_iters <= 1024, 0 <= lanczos_steps <= 64
+ *   out (host) receives the terms; cg_relres (host, nullable) receives cg_iters relative residuals
+ *   ||y - Khat x_t|| / ||y|| (recursively updated).
+ * Synchronises `stream` before returning.  Workspace: about (lanczos_steps + 4) n (1 + n_z)
+ * doubles on top of the product's.  Errors: STATE, INVALID_ARG, OOM, CUDA; a non-positive Ritz
+ * value or a non-converged tridiagonal eigensolve returns AKM_ERR_NONFINITE. */
+#define AKM_MAX_PROBES 31
+typedef struct {
+  double Z;                       /* Z~(theta), eq. 1.4                                      */
+  double quad;                    /* y^T x                                                    */
+  double logdet_M;                /* n log(sigma_f^2 P + sigma_eps^2)                        */
+  double slq;                     /* (1/n_z) sum_i samples[i]                                 */
+  double n_log_2pi;               /* n log 2 pi                                               */
+  double samples[AKM_MAX_PROBES]; /* z_i^T logm(M^{-1} Khat) z_i estimates                    */
+  int32_t steps[AKM_MAX_PROBES];  /* Lanczos steps used per probe (< lanczos_steps on breakdown) */
+  int32_t n_z, cg_iters, lanczos_steps, products; /* products = Khat block products issued    */
+  double cg_relres;               /* final recursive relative residual                        */
+} akm_objective_out;
+akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                              int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,
+                              void* stream);
+
 /* Library version string. */
 const char* akm_version(void);
 

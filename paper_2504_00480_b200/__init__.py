@@ -31,7 +31,8 @@ AKM_MAX_WINDOWS = 32
 # names exported by include/akm.h (checked by tests/test_abi_cpu.py)
 ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm", "akm_kernel_deriv_mvm",
                "akm_kernel_mvm_multi", "akm_get_info", "akm_set_scale_override", "akm_last_error", "akm_destroy",
-               "akm_version", "akm_set_profiling", "akm_get_stage_times")
+               "akm_version", "akm_set_profiling", "akm_get_stage_times", "akm_objective_diag")
+AKM_MAX_PROBES = 31
 
 
 class akm_info(ctypes.Structure):
@@ -59,6 +60,14 @@ class akm_stage_times(ctypes.Structure):
     _fields_ = [("spread_ms", ctypes.c_double), ("fft_ms", ctypes.c_double), ("interp_ms", ctypes.c_double),
                 ("epilogue_ms", ctypes.c_double), ("calls", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("spread_launches", ctypes.c_int64), ("interp_launches", ctypes.c_int64)]
+
+
+class akm_objective_out(ctypes.Structure):
+    _fields_ = [("Z", ctypes.c_double), ("quad", ctypes.c_double), ("logdet_M", ctypes.c_double),
+                ("slq", ctypes.c_double), ("n_log_2pi", ctypes.c_double),
+                ("samples", ctypes.c_double * AKM_MAX_PROBES), ("steps", ctypes.c_int32 * AKM_MAX_PROBES),
+                ("n_z", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("lanczos_steps", ctypes.c_int32),
+                ("products", ctypes.c_int32), ("cg_relres", ctypes.c_double)]
 
 
 def _load():
@@ -92,6 +101,8 @@ def _load():
     lib.akm_set_profiling.restype = st
     lib.akm_get_stage_times.argtypes = [P, ctypes.POINTER(akm_stage_times), i32]
     lib.akm_get_stage_times.restype = st
+    lib.akm_objective_diag.argtypes = [P, P, P, i64, i32, i32, i32, ctypes.POINTER(akm_objective_out), P, P]
+    lib.akm_objective_diag.restype = st
     lib.akm_version.argtypes = []
     lib.akm_version.restype = ctypes.c_char_p
     return lib
@@ -244,6 +255,19 @@ def akm_get_stage_times(plan, reset: bool = False) -> dict:
     return {f[0]: getattr(t, f[0]) for f in akm_stage_times._fields_}
 
 
+def akm_objective_diag(plan, y, Z, cg_iters=50, lanczos_steps=30, stream=None) -> dict:
+    """eq. (1.4) with M = diag(Khat): CG + SLQ, every Krylov step one block product (include/akm.h)."""
+    py, _, n, _, _, ky = _ptr_ld(y, "y")
+    pz, ldz, _, n_z, _, kz = _ptr_ld(Z, "Z")
+    out = akm_objective_out()
+    hist = (ctypes.c_double * max(int(cg_iters), 1))()
+    _check(plan, _lib.akm_objective_diag(plan, py, pz, ldz, n_z, int(cg_iters), int(lanczos_steps), ctypes.byref(out),
+                                         hist, _stream(stream, ky, kz)))
+    return {"Z": out.Z, "quad": out.quad, "logdetM": out.logdet_M, "slq": out.slq, "n_log_2pi": out.n_log_2pi,
+            "samples": list(out.samples[:n_z]), "steps": list(out.steps[:n_z]), "products": out.products,
+            "cg_relres": out.cg_relres, "cg_hist": [h for h in hist[:cg_iters]]}
+
+
 # ---------------------------------------------------------------- convenience wrapper
 class Plan:
     """RAII wrapper: ``Plan(device).set_points(...).set_theta(...)`` then ``mvm`` / ``deriv_mvm`` / ``mvm_multi``."""
@@ -286,6 +310,9 @@ class Plan:
     def mvm_multi(self, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
         akm_kernel_mvm_multi(self.handle, V, Y, dY_ell, dY_sf, stream)
         return Y, dY_ell, dY_sf
+
+    def objective_diag(self, y, Z, cg_iters=50, lanczos_steps=30, stream=None):
+        return akm_objective_diag(self.handle, y, Z, cg_iters, lanczos_steps, stream)
 
     def info(self):
         return akm_get_info(self.handle)

@@ -24,6 +24,9 @@ constexpr int kPolyDeg = 14;              // window polynomial degree (see windo
 constexpr int kPolyLen = kPolyDeg + 1;
 constexpr int kMaxTaps = 16;              // 2m <= 16
 constexpr double kPi = 3.14159265358979323846;
+constexpr int kKrMaxR = 32;               // Krylov driver: 1 CG column + <= 31 probes
+constexpr int kKrMaxSteps = 64;           // Lanczos steps
+constexpr int kKrMaxIters = 1024;         // CG iterations
 
 // Per-window geometry passed (by value, inside WinTable) to kernels.
 struct WinGeom {
@@ -178,6 +181,26 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
                                         double* H, long long maxA3, long long maxC, long long maxC2,
                                         long long maxTap, cudaStream_t s);
 cudaError_t launch_zero(double* p, long long count, cudaStream_t s);
+
+// krylov.cu (config-5 objective driver)
+size_t kr_state_bytes();
+int kr_blocks();
+cudaError_t launch_kr_col2(long long n, int R, const double* A, const double* B, double* part, cudaStream_t s);
+cudaError_t launch_kr_load(long long n, int R, const double* y, const double* Z, long long ldz, double* B,
+                           double* ybuf, cudaStream_t s);
+cudaError_t launch_kr_init(void* st, const double* part, int R, double c, cudaStream_t s);
+cudaError_t launch_kr_start(long long n, int R, const void* st, double* B, double* W, double* Q0, double* x,
+                            cudaStream_t s);
+cudaError_t launch_kr_after_dots(void* st, const double* part, int R, int cg_iters, int lanczos_steps, cudaStream_t s);
+cudaError_t launch_kr_update(long long n, int R, const void* st, const double* B, const double* KB, double* W,
+                             const double* Qt, const double* Qtm1, double* x, cudaStream_t s);
+cudaError_t launch_kr_reorth(long long n, int R, int nq, const void* st, const double* Q, long long slab, double* W,
+                             double* part, double* h, cudaStream_t s);
+cudaError_t launch_kr_after_norms(void* st, const double* part, int R, cudaStream_t s);
+cudaError_t launch_kr_finalize(long long n, int R, void* st, double* B, const double* W, double* Qn, cudaStream_t s);
+cudaError_t launch_kr_advance(void* st, int R, cudaStream_t s);
+cudaError_t launch_kr_slq_quad(void* st, int R, const double* part_yx, int* err, cudaStream_t s);
+void kr_summary_offsets(size_t* off_quad, size_t* off_samples, size_t* off_steps, size_t* off_hist, size_t* off_znorm);
 
 // interp.cu
 bool interp_supported(int d, int taps, int ops, int rc);

@@ -87,6 +87,7 @@ struct akm_plan {
   DevBuf dtab, Xc, u_tmp, u_sorted, perm, hist, hist_off, err_flag, items_s, items_i, minmax, r2;
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
   DevBuf stageV, stageY, stageL, stageS;
+  DevBuf krB, krKB, krW, krX, krY, krQ, krPart, krH, krState, krErr, krStage;
   long long r_cap = 0;
 
   // profiling (akm_set_profiling / akm_get_stage_times): a ring of event sets, drained lazily
@@ -897,6 +898,133 @@ akm_status akm_kernel_deriv_mvm(akm_plan* plan, int32_t which, const double* V, 
 akm_status akm_kernel_mvm_multi(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y, double* dY_ell,
                                 double* dY_sf, int64_t ldy, void* stream) {
   return mvm_entry(plan, V, ldv, r, Y, dY_ell, dY_sf, nullptr, ldy, S(stream));
+}
+
+akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                              int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,
+                              void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points || !plan->have_theta)
+    return plan->fail(AKM_ERR_STATE, "objective_diag called before set_points and set_theta");
+  if (!out) return plan->fail(AKM_ERR_INVALID_ARG, "out is NULL");
+  if (n_z < 1 || n_z > AKM_MAX_PROBES) return plan->fail(AKM_ERR_INVALID_ARG, "n_z must be in [1, %d]", AKM_MAX_PROBES);
+  if (ldz < n_z) return plan->fail(AKM_ERR_INVALID_ARG, "ldz < n_z");
+  if (cg_iters < 0 || cg_iters > kKrMaxIters) return plan->fail(AKM_ERR_INVALID_ARG, "cg_iters must be in [0, %d]", kKrMaxIters);
+  if (lanczos_steps < 0 || lanczos_steps > kKrMaxSteps)
+    return plan->fail(AKM_ERR_INVALID_ARG, "lanczos_steps must be in [0, %d]", kKrMaxSteps);
+  const long long n = plan->n;
+  if (n < 1) return plan->fail(AKM_ERR_INVALID_ARG, "objective needs n >= 1");
+  if (!y || !Z) return plan->fail(AKM_ERR_INVALID_ARG, "y or Z is NULL");
+  cudaStream_t s = S(stream);
+  AKM_CK(cudaSetDevice(plan->device));
+  const int R = 1 + n_z;
+  const int L = std::max(lanczos_steps, 1);
+  const long long slab = n * R;
+  // stage host inputs
+  const double* yd = y;
+  const double* Zd = Z;
+  long long ldzd = ldz;
+  const bool y_dev = is_device_ptr(y), z_dev = is_device_ptr(Z);
+  if (!y_dev || !z_dev) {
+    AKM_CK(plan->krStage.ensure(sizeof(double) * (size_t)(n + n * n_z)));
+    double* st = plan->krStage.as<double>();
+    if (!y_dev) {
+      AKM_CK(cudaMemcpyAsync(st, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      yd = st;
+    }
+    if (!z_dev) {
+      AKM_CK(cudaMemcpy2DAsync(st + n, sizeof(double) * n_z, Z, sizeof(double) * ldz, sizeof(double) * n_z, n,
+                               cudaMemcpyHostToDevice, s));
+      Zd = st + n;
+      ldzd = n_z;
+    }
+  }
+  const int nblk = kr_blocks();
+  AKM_CK(plan->krB.ensure(sizeof(double) * slab));
+  AKM_CK(plan->krKB.ensure(sizeof(double) * slab));
+  AKM_CK(plan->krW.ensure(sizeof(double) * slab));
+  AKM_CK(plan->krX.ensure(sizeof(double) * n));
+  AKM_CK(plan->krY.ensure(sizeof(double) * n));
+  AKM_CK(plan->krQ.ensure(sizeof(double) * slab * L));
+  AKM_CK(plan->krPart.ensure(sizeof(double) * (size_t)nblk * std::max(2, L) * R));
+  AKM_CK(plan->krH.ensure(sizeof(double) * (size_t)L * R));
+  AKM_CK(plan->krState.ensure(kr_state_bytes()));
+  AKM_CK(plan->krErr.ensure(sizeof(int)));
+  AKM_CK(cudaMemsetAsync(plan->krErr.p, 0, sizeof(int), s));
+  double* B = plan->krB.as<double>();
+  double* KB = plan->krKB.as<double>();
+  double* W = plan->krW.as<double>();
+  double* Q = plan->krQ.as<double>();
+  double* part = plan->krPart.as<double>();
+  void* st = plan->krState.p;
+  // M = diag(Khat): kappa(0) = 1 for every sub-kernel (reading R11)
+  const double c = plan->sigma_f * plan->sigma_f * plan->P + plan->sigma_eps * plan->sigma_eps;
+  AKM_CK(launch_kr_load(n, R, yd, Zd, ldzd, B, plan->krY.as<double>(), s));
+  AKM_CK(launch_kr_col2(n, R, B, B, part, s));
+  AKM_CK(launch_kr_init(st, part, R, c, s));
+  AKM_CK(launch_kr_start(n, R, st, B, W, Q, plan->krX.as<double>(), s));
+  const int T = std::max(cg_iters, lanczos_steps);
+  int products = 0;
+  for (int t = 0; t < T; ++t) {
+    akm_status stt = run_mvm(plan, B, R, R, KB, nullptr, nullptr, R, s);
+    if (stt != AKM_OK) return stt;
+    ++products;
+    AKM_CK(launch_kr_col2(n, R, B, KB, part, s));
+    AKM_CK(launch_kr_after_dots(st, part, R, cg_iters, lanczos_steps, s));
+    const double* Qt = Q + (long long)std::min(t, L - 1) * slab;
+    const double* Qtm1 = (t > 0 && t < L) ? Q + (long long)(t - 1) * slab : nullptr;
+    AKM_CK(launch_kr_update(n, R, st, B, KB, W, Qt, Qtm1, plan->krX.as<double>(), s));
+    if (t + 1 < lanczos_steps) {
+      for (int pass = 0; pass < 2; ++pass)  // classical Gram-Schmidt, twice (reading R11)
+        AKM_CK(launch_kr_reorth(n, R, t + 1, st, Q, slab, W, part, plan->krH.as<double>(), s));
+    }
+    AKM_CK(launch_kr_col2(n, R, W, W, part, s));
+    AKM_CK(launch_kr_after_norms(st, part, R, s));
+    AKM_CK(launch_kr_finalize(n, R, st, B, W, (t + 1 < L) ? Q + (long long)(t + 1) * slab : nullptr, s));
+    AKM_CK(launch_kr_advance(st, R, s));
+    plan->launches += 7 + ((t + 1 < lanczos_steps) ? 6 : 0);
+  }
+  AKM_CK(launch_kr_col2(n, 1, plan->krY.as<double>(), plan->krX.as<double>(), part, s));
+  AKM_CK(launch_kr_slq_quad(st, R, part, plan->krErr.as<int>(), s));
+  size_t o_quad, o_samp, o_steps, o_hist, o_zn;
+  kr_summary_offsets(&o_quad, &o_samp, &o_steps, &o_hist, &o_zn);
+  double quad = 0.0;
+  std::vector<double> samples(R), hist(std::max(cg_iters, 1));
+  std::vector<int> steps(R);
+  int errf = 0;
+  const char* base = static_cast<const char*>(st);
+  AKM_CK(cudaMemcpyAsync(&quad, base + o_quad, sizeof(double), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaMemcpyAsync(samples.data(), base + o_samp, sizeof(double) * R, cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaMemcpyAsync(steps.data(), base + o_steps, sizeof(int) * R, cudaMemcpyDeviceToHost, s));
+  if (cg_iters > 0)
+    AKM_CK(cudaMemcpyAsync(hist.data(), base + o_hist, sizeof(double) * cg_iters, cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaMemcpyAsync(&errf, plan->krErr.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaStreamSynchronize(s));
+  std::memset(out, 0, sizeof(*out));
+  out->quad = quad;
+  out->logdet_M = (double)n * std::log(c);
+  out->n_log_2pi = (double)n * std::log(2.0 * kPi);
+  double acc = 0.0;
+  for (int i = 0; i < n_z; ++i) {
+    out->samples[i] = samples[i + 1];
+    out->steps[i] = steps[i + 1];
+    acc += samples[i + 1];
+  }
+  out->slq = acc / n_z;
+  out->Z = 0.5 * (out->quad + out->logdet_M + out->slq + out->n_log_2pi);
+  out->n_z = n_z;
+  out->cg_iters = cg_iters;
+  out->lanczos_steps = lanczos_steps;
+  out->products = products;
+  // iterations after an exactly-zero residual are not run (history -1): report the last one run
+  out->cg_relres = 1.0;
+  for (int t = 0; t < cg_iters; ++t)
+    if (hist[t] >= 0.0) out->cg_relres = hist[t];
+  if (cg_relres)
+    for (int t = 0; t < cg_iters; ++t) cg_relres[t] = hist[t];
+  if (errf) return plan->fail(AKM_ERR_NONFINITE, "SLQ: tridiagonal eigensolve failed or non-positive Ritz value (flags %d)", errf);
+  return AKM_OK;
 }
 
 akm_status akm_set_profiling(akm_plan* plan, int32_t enable) {

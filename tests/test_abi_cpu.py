@@ -75,3 +75,18 @@ def test_null_plan_is_rejected(lib):
     assert akm._lib.akm_set_theta(None, 1.0, 1.0, 0.1, None) == akm.AKM_ERR_INVALID_ARG
     assert akm._lib.akm_kernel_mvm(None, None, 1, 1, None, 1, None) == akm.AKM_ERR_INVALID_ARG
     akm._lib.akm_destroy(None)  # no-op
+
+
+def test_objective_struct_matches_header_fields(lib):
+    _, akm = lib
+    text = open(HEADER).read()
+    end = text.index("} akm_objective_out;")
+    body = text[text.rindex("typedef struct {", 0, end):end]
+    flat = []
+    for line in body.splitlines():
+        line = line.split("/*")[0]
+        m = re.match(r"\s*(int64_t|int32_t|double)\s+(.*);", line)
+        if m:
+            flat += [v.strip().split("[")[0] for v in m.group(2).split(",")]
+    assert flat == [f[0] for f in akm.akm_objective_out._fields_]
+    assert "#define AKM_MAX_PROBES %d" % akm.AKM_MAX_PROBES in text
