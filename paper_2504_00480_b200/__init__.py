@@ -129,7 +129,7 @@ def _ptr_ld(a, name):
                 raise TypeError(f"{name} must be float64")
             if a.dim() == 1:
                 a = a.unsqueeze(1)
-            if a.dim() != 2 or a.stride(1) != 1:
+            if a.dim() != 2 or (a.stride(1) != 1 and a.shape[1] > 1):
                 raise ValueError(f"{name} must be 2-D with unit column stride")
             ld = a.stride(0) if a.shape[0] > 1 else a.shape[1]
             return ctypes.c_void_p(a.data_ptr()), max(ld, a.shape[1]), a.shape[0], a.shape[1], a.is_cuda, a
@@ -142,7 +142,7 @@ def _ptr_ld(a, name):
         arr = arr[:, None]
     if arr.ndim == 2 and arr.size == 0:
         return ctypes.c_void_p(arr.ctypes.data), max(1, arr.shape[1]), arr.shape[0], arr.shape[1], False, arr
-    if arr.ndim != 2 or arr.strides[1] != 8:
+    if arr.ndim != 2 or (arr.strides[1] != 8 and arr.shape[1] > 1):
         raise ValueError(f"{name} must be 2-D row-major")
     ld = arr.strides[0] // 8 if arr.shape[0] > 1 else arr.shape[1]
     return ctypes.c_void_p(arr.ctypes.data), max(ld, arr.shape[1]), arr.shape[0], arr.shape[1], False, arr

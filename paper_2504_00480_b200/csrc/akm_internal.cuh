@@ -53,6 +53,16 @@ struct WinGeom {
   long long d_off;      // offset of this window's multiplier tables [op][K0][K1][K2] (real)
 };
 
+// Window polynomial coefficients passed BY VALUE as a __grid_constant__ kernel parameter: with
+// compile-time indices the FP64 FMAs read them straight from the constant bank (no smem loads).
+struct PolyParam {
+  double c[kMaxTaps * kPolyLen];
+};
+
+// float-reciprocal integer division for small non-negative operands (a < 2^20, b <= 2^10):
+// exact because the rounding error of (a + 1/2) / b stays far below 1/(2b).
+__device__ __forceinline__ int fdiv(int a, float inv_b) { return (int)(((float)a + 0.5f) * inv_b); }
+
 struct WinTable {
   int P;
   int N, n_g, m;
@@ -97,6 +107,25 @@ __device__ __forceinline__ void window_taps(const double* __restrict__ c, double
 #pragma unroll
     for (int k = kPolyDeg - 1; k >= 0; --k) v = fma(v, x, c[o * kPolyLen + k]);
     w[o] = v;
+  }
+}
+
+// The same polynomials by Estrin's scheme: dependency depth 4 (after x^2, x^4, x^8, shared by all
+// taps) instead of 14.  Used where the weights are evaluated next to DMMA traffic, which stretches
+// every dependent FP64 step to ~135 clk (tools/microbench/dmma_occupancy.cu).
+static_assert(kPolyDeg == 14, "Estrin layout below assumes degree 14");
+template <int TAPS>
+__device__ __forceinline__ void window_taps_estrin(const double* __restrict__ c, double x, double* w) {
+  const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4;
+#pragma unroll
+  for (int o = 0; o < TAPS; ++o) {
+    const double* k = c + o * kPolyLen;
+    const double p0 = fma(k[1], x, k[0]), p1 = fma(k[3], x, k[2]), p2 = fma(k[5], x, k[4]);
+    const double p3 = fma(k[7], x, k[6]), p4 = fma(k[9], x, k[8]), p5 = fma(k[11], x, k[10]);
+    const double p6 = fma(k[13], x, k[12]), p7 = k[14];
+    const double q0 = fma(p1, x2, p0), q1 = fma(p3, x2, p2), q2 = fma(p5, x2, p4), q3 = fma(p7, x2, p6);
+    const double r0 = fma(q1, x4, q0), r1 = fma(q3, x4, q2);
+    w[o] = fma(r1, x8, r0);
   }
 }
 
@@ -158,19 +187,14 @@ cudaError_t launch_twiddles(const WinTable& tab, const WinTable* dtab, double2* 
 cudaError_t launch_window_poly(int m, double beta, double* coef, cudaStream_t s);
 
 // spread_mma.cu
-bool spread_mma_choose(int M, int Nn, int& MB, int& NB, int& WM, int& WN);
+bool spread_mma_choose(int M, int Nn, int Fmax, int rc, int& MB, int& NB, int& WM, int& WN);
 size_t spread_mma_smem(int PB, int M, int Nn, int Fmax, int rc);
-cudaError_t launch_spread_mma(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
+cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
+                              const double* u_sorted,
                               const int* perm, const double* V, long long ldv, long long n, int r0, int rc,
                               int r_total, double* grid, int MB, int NB, int WM, int WN, int PB, size_t smem,
                               cudaStream_t s);
 
-// spread.cu
-bool spread_tile_supported(int MT, int NT);
-size_t spread_smem_bytes(int PB, int Mpad, int Npad, int Fmax, int rc);
-cudaError_t launch_spread(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
-                          const int* perm, const double* V, long long ldv, long long n, int r0, int rc, int r_total,
-                          double* grid, int MT, int NT, int threads, int PB, size_t smem, double beta, cudaStream_t s);
 
 // fft.cu
 cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1,

@@ -77,6 +77,7 @@ struct akm_plan {
   std::vector<double> radius;               // R_w
   std::vector<double> c_w, c_w_binned;      // current scale, scale the bins were built for
   WinTable tab{};                           // host copy
+  PolyParam poly_param{};                   // window polynomials, passed to kernels by value
   std::vector<WorkItem> items_spread, items_interp;
   std::vector<Group> groups;
   std::vector<long long> occupied, maxbin;
@@ -261,7 +262,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
       {
         int MB_, NB_, WM_, WN_, Mr = 1;
         for (int t = 0; t < d - 1; ++t) Mr *= F;
-        fits = fits && spread_mma_choose(Mr, F, MB_, NB_, WM_, WN_);
+        fits = fits && spread_mma_choose(Mr, F, F, 1, MB_, NB_, WM_, WN_);
       }
       if (!fits) continue;
       int nb[3];
@@ -524,18 +525,16 @@ static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r,
     for (int t = 0; t < d - 1; ++t) M *= F;
     int r0 = 0;
     while (r0 < r) {
-      // largest RHS chunk (<= 12) whose footprint fits one CTA of <= 9 warps of DMMA tiles
+      // largest RHS chunk (<= 12) whose footprint accumulator fits the 8 warps' DMMA tiles and whose
+      // panels fit shared memory; split the rest evenly
       int rc = std::min(12, r - r0), MB = 0, NB = 0, WM = 0, WN = 0;
-      while (rc > 1 && !spread_mma_choose(M, F * rc, MB, NB, WM, WN)) --rc;
-      if (!spread_mma_choose(M, F * rc, MB, NB, WM, WN))
+      while (rc > 1 && !spread_mma_choose(M, F * rc, F, rc, MB, NB, WM, WN)) --rc;
+      if (rc < r - r0 && rc > (r - r0 + 1) / 2) rc = (r - r0 + 1) / 2;  // balanced chunks (e.g. 6 + 5)
+      if (!spread_mma_choose(M, F * rc, F, rc, MB, NB, WM, WN))
         return plan->fail(AKM_ERR_UNSUPPORTED, "no spread tile for footprint %d x %d", M, F * rc);
-      int PB = 32;
-      size_t smem = spread_mma_smem(PB, M, F * rc, F, rc);
-      while (smem > 100 * 1024 && PB > 4) {
-        PB /= 2;
-        smem = spread_mma_smem(PB, M, F * rc, F, rc);
-      }
-      AKM_CK(launch_spread_mma(dtab, plan->items_s.as<WorkItem>() + grp.spread_begin, grp.spread_count,
+      const int PB = 0;  // fixed inside the kernel (kSpreadPB)
+      const size_t smem = spread_mma_smem(PB, M, F * rc, F, rc);
+      AKM_CK(launch_spread_mma(dtab, plan->poly_param, plan->items_s.as<WorkItem>() + grp.spread_begin, grp.spread_count,
                                plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc, r,
                                plan->grid.as<double>(), MB, NB, WM, WN, PB, smem, s));
       if (grp.spread_count > 0) {
@@ -767,6 +766,7 @@ akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p,
     AKM_CK(launch_window_poly(m, plan->beta, pc.as<double>(), s));
     AKM_CK(cudaMemcpyAsync(tab.poly, pc.p, sizeof(double) * kMaxTaps * kPolyLen, cudaMemcpyDeviceToHost, s));
     AKM_CK(cudaStreamSynchronize(s));
+    std::memcpy(plan->poly_param.c, tab.poly, sizeof(plan->poly_param.c));
   }
   plan->lo.assign(3 * P, 0.0);
   plan->hi.assign(3 * P, 0.0);

@@ -4,118 +4,244 @@
 //   g^{w,c}_l = sum_j V[j,c] phi~(x~_j^w - l/n_g)
 //
 // Per work item (a chunk of points of one bin of B^d cells) the bin's footprint accumulator is
-//   C[(o0,o1), (o2,c)] = sum_p (w0_p[o0] w1_p[o1]) * (w2_p[o2] v_p[c])   = A'^T B,
-// a GEMM with K = points.  It runs on DMMA (mma.sync.m8n8k4.f64): on B200 DMMA and DFMA share
-// one FP64 pipe (35 TFLOP/s either way, profiles/r01_fp64_peaks.txt) but one DMMA instruction
-// carries 256 FMAs, so operand delivery and issue stop limiting and the accumulator tile lives in
-// MMA fragments (2 doubles per thread per 8x8 tile).  Each warp owns MB x NB tiles of C; the two
-// factor matrices of a batch of PB points are staged in shared memory with row strides = 4 mod 16
-// doubles (conflict-free fragment loads).  Window weights: Horner polynomials (window_taps).
-// The footprint is written once per work item with RED.ADD.F64.
+//   C[(o0,o1), (c,o2)] = sum_p (w0_p[o0] w1_p[o1]) * (v_p[c] w2_p[o2])   = A^T B,
+// a GEMM with K = points, run on DMMA (mma.sync.m8n8k4.f64): on B200 DMMA and DFMA share one FP64
+// pipe (37 TFLOP/s, profiles/r01_fp64_peaks.txt) but one DMMA instruction carries 256 FMAs, so
+// operand delivery and issue stop limiting and the accumulator lives in MMA fragments.
+//
+// Phased design.  Measured on B200 (tools/microbench/dmma_occupancy.cu and the
+// round-1 ncu captures): while one warp streams DMMAs, a DFMA/DMUL of ANOTHER warp on the same SM
+// sub-partition is granted the FP64 pipe only every ~34 clk.  Any scalar FP64 work overlapped with
+// DMMAs of other warps (on-the-fly fragment products, producer warps building panels) therefore
+// starves and stalls the MMAs behind it.  So every batch of PB points runs in two phases, all
+// 8 warps (2 per sub-partition) together:
+//   STAGE  window weights (Estrin polynomials, independent chains) and the two factor panels
+//          A[p][(o0,o1)] = w0 w1, B[p][(o2,c)] = w2 v in shared memory -- no DMMA in flight;
+//   MMA    C += A^T B: fragments are single conflict-free LDS.64 (panel row stride = 4 mod 16
+//          doubles) straight into DMMA -- no scalar FP64 in flight.
+// Raw inputs (grid coordinates, permutation, RHS values gathered through it) stream in through a
+// cp.async ring a few batches ahead, so neither phase waits on global memory.  The footprint is
+// written once per work item with RED.ADD.F64.
+#include <algorithm>
+
 #include "akm_internal.cuh"
 
 namespace akm {
 
+constexpr int kSpreadPB = 64;        // points per batch (16 MMA k-steps)
+constexpr int kSpreadWarps = 8;      // two per SM sub-partition
+constexpr int kSpreadThreads = 32 * kSpreadWarps;
+constexpr int kRing = 4;             // cp.async ring depth (batches)
+
+__device__ __forceinline__ void cpasync8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cpasync4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__host__ __device__ constexpr int spread_ldf(int f) { return (f + 2) & ~1; }  // weight row: even, > f
+
 template <int MB, int NB>
-__global__ void __launch_bounds__(288) k_spread_mma(const WinTable* __restrict__ tabp,
-                                                    const WorkItem* __restrict__ items,
-                                                    const double* __restrict__ u_sorted, const int* __restrict__ perm,
-                                                    const double* __restrict__ V, long long ldv, long long n, int r0,
-                                                    int rc, int r_total, double* __restrict__ grid, int PB, int WN) {
+__global__ void __launch_bounds__(kSpreadThreads, 1) k_spread_mma(const WinTable* __restrict__ tabp,
+                                                                  const WorkItem* __restrict__ items,
+                                                                  const double* __restrict__ u_sorted,
+                                                                  const int* __restrict__ perm,
+                                                                  const double* __restrict__ V, long long ldv,
+                                                                  long long n, int r0, int rc, int r_total,
+                                                                  double* __restrict__ grid, int WN,
+                                                                  const __grid_constant__ PolyParam pp) {
+  constexpr int PB = kSpreadPB;
+  constexpr int NT = kSpreadThreads;
   const WinTable& tab = *tabp;
   const WorkItem it = items[blockIdx.x];
   const WinGeom& g = tab.w[it.win];
-  const int F0 = g.F[0], F1 = g.F[1], F2 = g.F[2];
-  const int Fmax = max(F0, max(F1, F2));
-  const int M = F0 * F1, Nn = F2 * rc;
-  const int TMt = (M + 7) / 8, TNt = (Nn + 7) / 8;
-  const int lda = mma_ld(TMt * 8), ldb = mma_ld(TNt * 8);
+  const int d = g.d;
+  const int F1 = g.F[1];
+  const int Fmax = max(g.F[0], max(F1, g.F[2]));
+  const int LDF = spread_ldf(Fmax);
+  const int M = g.F[0] * F1, Nn = g.F[2] * rc;
+  const int WM = kSpreadWarps / WN;
+  const int lda = mma_ld(WM * MB * 8), ldb = mma_ld(WN * NB * 8);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / WN, wn = warp % WN;
   const int taps = 2 * tab.m;
+  const int nbatch = (it.count + PB - 1) / PB;
+  const float inv_rc = 1.0f / rc, inv_F1 = 1.0f / F1, inv_F2 = 1.0f / g.F[2];
 
   extern __shared__ double smem[];
-  double* poly = smem;                         // [2m][kPolyLen]
-  double* As = poly + kMaxTaps * kPolyLen;     // [PB][lda]  w0 (x) w1
-  double* Bs = As + (size_t)PB * lda;          // [PB][ldb]  w2 (x) v
-  double* Ws = Bs + (size_t)PB * ldb;          // [PB][3][Fmax]
-  double* Vs = Ws + (size_t)PB * 3 * Fmax;     // [PB][rc]
+  double* As = smem;                               // [PB][lda]
+  double* Bs = As + PB * lda;                      // [PB][ldb]
+  double* Ws = Bs + PB * ldb;                      // [3][PB][LDF]  weights on the footprint
+  double* Vring = Ws + 3 * PB * LDF;               // [R][PB][rc]   RHS values        (cp.async ring)
+  double* Uring = Vring + kRing * PB * rc;         // [R][3][PB]    grid coordinates  (cp.async ring)
+  int* Pring = reinterpret_cast<int*>(Uring + kRing * 3 * PB);  // [R][PB] permutation (cp.async ring)
 
   int org[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) org[a] = g.box_lo[a] + it.bin[a] * g.B;
-  for (int idx = tid; idx < taps * kPolyLen; idx += blockDim.x) poly[idx] = tab.poly[idx];
+  // panels: the padding rows / columns (>= M, >= Nn) are never written and stay zero
+  for (int idx = tid; idx < PB * (lda + ldb); idx += NT) As[idx] = 0.0;
 
+  const long long ptbase = (long long)it.win * n + it.start;
+  const double* ubase = u_sorted + (long long)it.win * 3 * n + it.start;
+  // ring schedule: at batch b the permutation of b+3, the coordinates of b+2 and the RHS values of
+  // b+1 (gathered through the permutation, which landed a batch earlier) are issued
+  auto issue_perm = [&](int b) {
+    if (b >= nbatch) return;
+    const int q0 = b * PB, pb = min(PB, it.count - q0);
+    if (tid < pb) cpasync4(Pring + (b % kRing) * PB + tid, perm + ptbase + q0 + tid);
+  };
+  auto issue_u = [&](int b) {
+    if (b >= nbatch) return;
+    const int q0 = b * PB, pb = min(PB, it.count - q0);
+    for (int j = tid; j < 3 * PB; j += NT) {
+      const int a = j / PB, p = j - a * PB;
+      if (a >= 3 - d && p < pb) cpasync8(Uring + ((b % kRing) * 3 + a) * PB + p, ubase + (long long)a * n + q0 + p);
+    }
+  };
+  auto issue_v = [&](int b) {  // needs Pring[b] visible to all threads
+    if (b >= nbatch) return;
+    const int q0 = b * PB, pb = min(PB, it.count - q0);
+    double* Vs = Vring + (b % kRing) * PB * rc;
+    const int* pr = Pring + (b % kRing) * PB;
+    for (int j = tid; j < PB * rc; j += NT) {
+      const int p = fdiv(j, inv_rc), c = j - p * rc;
+      if (p < pb) cpasync8(Vs + j, V + (long long)pr[p] * ldv + r0 + c);
+      else Vs[j] = 0.0;  // absent points: zero (0 * a stale NaN would poison the panel)
+    }
+  };
+  for (int b = 0; b < 3; ++b) issue_perm(b);
+  for (int b = 0; b < 2; ++b) issue_u(b);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  issue_v(0);
+  cp_async_commit();
+
+  const int wm = warp / WN, wn = warp % WN;
   double acc[MB][NB][2];
 #pragma unroll
   for (int i = 0; i < MB; ++i)
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int aoff = (lane & 3) * lda + wm * MB * 8 + (lane >> 2);
+  const int boff = (lane & 3) * ldb + wn * NB * 8 + (lane >> 2);
 
-  const long long ptbase = (long long)it.win * n + it.start;
-  for (int p0 = 0; p0 < it.count; p0 += PB) {
-    const int pb = min(PB, it.count - p0);
-    const int pb4 = (pb + 3) & ~3;
-    __syncthreads();  // poly visible / previous batch consumed
-    // (1) window weights: one thread per (point, axis); Horner polynomials, no divisions
-    for (int pa = tid; pa < pb * 3; pa += blockDim.x) {
-      const int p = pa / 3, a = pa - 3 * p;
-      double* wrow = Ws + (size_t)pa * Fmax;
-      if (a < 3 - g.d) {
-        for (int o = 0; o < Fmax; ++o) wrow[o] = (o == 0) ? 1.0 : 0.0;
-      } else {
-        const double u = u_sorted[((long long)it.win * 3 + a) * n + it.start + p0 + p];
-        const double fl = floor(u);
-        const int s0 = (int)fl - tab.m + 1 - org[a];  // footprint position of the point's tap 0
-        const double x = 2.0 * (u - fl) - 1.0;
-        for (int o = 0; o < Fmax; ++o) {
-          const int tap = o - s0;
-          wrow[o] = (tap >= 0 && tap < taps && o < g.F[a]) ? window_tap(poly, tap, x) : 0.0;
+  for (int b = 0; b < nbatch; ++b) {
+    const int pb = min(PB, it.count - b * PB);
+    const double* Vc = Vring + (b % kRing) * PB * rc;
+    const double* U = Uring + (b % kRing) * 3 * PB;
+    // ---- STAGE.  u(b), V(b) and perm(b+1) have landed (issued >= 1 batch ago); the previous
+    //      batch's MMAs are done (panels free)
+    cp_async_wait<0>();
+    __syncthreads();
+    issue_perm(b + 3);
+    issue_u(b + 2);
+    issue_v(b + 1);
+    cp_async_commit();
+    // window weights: one job per (point, axis) (PB * 3 <= 256 threads), all 2m taps by Estrin
+    // (independent chains of depth 4; coefficients are constant-bank operands)
+    for (int job = tid; job < PB * 3; job += NT) {
+      const int p = job / 3, a = job - 3 * p;
+      double* wrow = Ws + (a * PB + p) * LDF;
+      const int Fa = g.F[a];
+      if (p >= pb || a < 3 - d) {
+        const double fill = (p < pb) ? 1.0 : 0.0;  // singleton axis: F = 1, weight 1
+        for (int o = 0; o < Fa; ++o) wrow[o] = fill;
+        continue;
+      }
+      const double u = U[a * PB + p];
+      const double fl = floor(u);
+      const int s0 = (int)fl - tab.m + 1 - org[a];  // footprint position of the point's tap 0
+      const double x = 2.0 * (u - fl) - 1.0;
+      for (int o = 0; o < s0; ++o) wrow[o] = 0.0;
+      for (int o = s0 + taps; o < Fa; ++o) wrow[o] = 0.0;
+      double wv[kMaxTaps];
+      if (taps == 12) window_taps_estrin<12>(pp.c, x, wv);
+      else if (taps == 8) window_taps_estrin<8>(pp.c, x, wv);
+      else window_taps_estrin<16>(pp.c, x, wv);
+#pragma unroll
+      for (int q = 0; q < kMaxTaps; ++q)
+        if (q < taps) wrow[s0 + q] = wv[q];
+    }
+    __syncthreads();
+    // factor panels.  A[p][o0*F1 + o1] = w0[o0] w1[o1]: one job per (point, o0) writes F1
+    // consecutive doubles; B[p][c*F2 + o2] = v[c] w2[o2] (columns ordered (c, o2)): one job per
+    // (point, c) writes F2 consecutive doubles.  Even runs go as 16-byte vectors (weight rows and
+    // panel rows are 16-byte aligned: LDF, lda, ldb even); consecutive threads take consecutive
+    // points (row strides = 4 mod 16 doubles spread the stores over the banks).
+    {
+      const double* W0 = Ws;
+      const double* W1 = Ws + PB * LDF;
+      const double* W2 = Ws + 2 * PB * LDF;
+      const int F0 = g.F[0], F2 = g.F[2];
+      for (int job = tid; job < PB * F0; job += NT) {
+        const int o0 = job / PB, p = job - o0 * PB;
+        const double w0 = W0[p * LDF + o0];
+        const double* w1 = W1 + p * LDF;
+        double* dst = As + p * lda + o0 * F1;
+        if ((F1 & 1) == 0) {
+          for (int o = 0; o < F1; o += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(w1 + o);
+            *reinterpret_cast<double2*>(dst + o) = make_double2(w0 * t.x, w0 * t.y);
+          }
+        } else {
+          for (int o = 0; o < F1; ++o) dst[o] = w0 * w1[o];
+        }
+      }
+      for (int job = tid; job < PB * rc; job += NT) {
+        const int c = job / PB, p = job - c * PB;
+        const double v = Vc[p * rc + c];
+        const double* w2 = W2 + p * LDF;
+        double* dst = Bs + p * ldb + c * F2;
+        if ((F2 & 1) == 0) {
+          for (int o = 0; o < F2; o += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(w2 + o);
+            *reinterpret_cast<double2*>(dst + o) = make_double2(v * t.x, v * t.y);
+          }
+        } else {
+          for (int o = 0; o < F2; ++o) dst[o] = v * w2[o];
         }
       }
     }
-    for (int pc = tid; pc < pb * rc; pc += blockDim.x) {
-      const int p = pc / rc, c = pc - p * rc;
-      Vs[pc] = V[(long long)perm[ptbase + p0 + p] * ldv + r0 + c];
-    }
     __syncthreads();
-    // (2) factor matrices; each thread owns whole columns (index math once per column)
-    for (int row = tid; row < lda; row += blockDim.x) {
-      const bool ok = row < M;
-      const int o0 = ok ? row / F1 : 0, o1 = ok ? row - (row / F1) * F1 : 0;
-      for (int p = 0; p < pb4; ++p)
-        As[(size_t)p * lda + row] = (ok && p < pb) ? Ws[(p * 3 + 0) * Fmax + o0] * Ws[(p * 3 + 1) * Fmax + o1] : 0.0;
-    }
-    for (int col = tid; col < ldb; col += blockDim.x) {
-      const bool ok = col < Nn;
-      const int o2 = ok ? col / rc : 0, c = ok ? col - (col / rc) * rc : 0;
-      for (int p = 0; p < pb4; ++p)
-        Bs[(size_t)p * ldb + col] = (ok && p < pb) ? Ws[(p * 3 + 2) * Fmax + o2] * Vs[p * rc + c] : 0.0;
-    }
-    __syncthreads();
-    // C += A'^T B over this batch, 4 points per MMA k-step
-    const double* ap = As + (lane & 3) * lda + (wm * MB) * 8 + (lane >> 2);
-    const double* bp = Bs + (lane & 3) * ldb + (wn * NB) * 8 + (lane >> 2);
-    for (int k = 0; k < pb4; k += 4) {
-      double a[MB], b[NB];
+    // ---- MMA
+    const double* ap = As + aoff;
+    const double* bp = Bs + boff;
+    const int ksteps = (pb + 3) >> 2;
+#pragma unroll 1
+    for (int ks = 0; ks < ksteps; ++ks) {
+      double af[MB];
 #pragma unroll
-      for (int i = 0; i < MB; ++i) a[i] = ap[(size_t)k * lda + i * 8];
+      for (int i = 0; i < MB; ++i) af[i] = ap[i * 8];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) b[j] = bp[(size_t)k * ldb + j * 8];
+      for (int j = 0; j < NB; ++j) {
+        const double bfj = bp[j * 8];
 #pragma unroll
-      for (int i = 0; i < MB; ++i)
-#pragma unroll
-        for (int j = 0; j < NB; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int i = 0; i < MB; ++i) dmma(acc[i][j][0], acc[i][j][1], af[i], bfj);
+      }
+      ap += 4 * lda;
+      bp += 4 * ldb;
     }
   }
 
-  // flush: fragment (row = lane>>2, cols 2*(lane&3) + {0,1}) of each owned tile
+  // flush: fragment (row = lane>>2, cols 2*(lane&3) + {0,1}) of each owned tile; table fields are
+  // read once (the atomics would otherwise force re-loads of the global table)
+  const long long L1 = g.L[1], L2 = g.L[2], toff = g.tap_off;
+  const int b0 = org[0] - g.box_lo[0], b1 = org[1] - g.box_lo[1], b2 = org[2] - g.box_lo[2];
+  double* gbase = grid + r0;
+  const int F2 = g.F[2];
 #pragma unroll
   for (int i = 0; i < MB; ++i) {
     const int row = (wm * MB + i) * 8 + (lane >> 2);
     if (row >= M) continue;
-    const long long l0 = org[0] - g.box_lo[0] + row / F1;
-    const long long l1 = org[1] - g.box_lo[1] + row % F1;
+    const int o0 = fdiv(row, inv_F1);
+    const long long line = ((long long)(b0 + o0) * L1 + (b1 + row - o0 * F1)) * L2 + b2;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
 #pragma unroll
@@ -123,66 +249,79 @@ __global__ void __launch_bounds__(288) k_spread_mma(const WinTable* __restrict__
         const int col = (wn * NB + j) * 8 + 2 * (lane & 3) + h;
         const double v = acc[i][j][h];
         if (col >= Nn || v == 0.0) continue;
-        const long long l2 = org[2] - g.box_lo[2] + col / rc;
-        const long long tap = (l0 * g.L[1] + l1) * g.L[2] + l2;
-        atomicAdd(grid + (g.tap_off + tap) * r_total + r0 + col % rc, v);
+        const int c = fdiv(col, inv_F2), o2 = col - c * F2;  // B columns are ordered (c, o2)
+        atomicAdd(gbase + (toff + line + o2) * r_total + c, v);
       }
     }
   }
 }
 
-#define AKM_MMA_TILES(X) X(2, 2) X(3, 2) X(4, 2) X(2, 3) X(3, 3) X(4, 3) X(2, 4) X(3, 4) X(4, 4) X(6, 3) X(3, 6) X(6, 6)
+// (MB, NB) register tiles of the 8 warps (WM x WN = 8); an 8x8 f64 accumulator tile costs 4
+// registers per thread, MB x NB <= 45 keeps a thread under the 255-register cap
+#define AKM_MMA_TILES(X)                                                                                      \
+  X(9, 5) X(5, 9) X(9, 4) X(4, 9) X(6, 6) X(9, 3) X(3, 9) X(6, 3) X(3, 6) X(3, 7) X(7, 3) X(12, 2) X(2, 12)  \
+  X(6, 2) X(2, 6) X(4, 4) X(3, 3) X(4, 2) X(2, 4) X(3, 2) X(2, 3) X(2, 2) X(1, 6) X(1, 3) X(1, 2)
 
-bool spread_mma_choose(int M, int Nn, int& MB, int& NB, int& WM, int& WN) {
-  static const int cand[][2] = {{2, 2}, {3, 2}, {4, 2}, {2, 3}, {3, 3}, {4, 3}, {2, 4}, {3, 4}, {4, 4}, {6, 3}, {3, 6}, {6, 6}};
+static size_t spread_smem_for(int lda, int ldb, int Fmax, int rc) {
+  return sizeof(double) * ((size_t)kSpreadPB * (lda + ldb) + 3 * (size_t)kSpreadPB * spread_ldf(Fmax) +
+                           (size_t)kRing * kSpreadPB * (rc + 3)) +
+         sizeof(int) * (size_t)kRing * kSpreadPB;
+}
+
+bool spread_mma_choose(int M, int Nn, int Fmax, int rc, int& MB, int& NB, int& WM, int& WN) {
+  static const int cand[][2] = {
+#define AKM_PAIR(a, b) {a, b},
+      AKM_MMA_TILES(AKM_PAIR)
+#undef AKM_PAIR
+  };
   const int TMt = (M + 7) / 8, TNt = (Nn + 7) / 8;
   double best = 1e300;
   bool found = false;
   for (auto& c : cand) {
     const int mb = c[0], nb = c[1];
-    const int wm = (TMt + mb - 1) / mb, wn = (TNt + nb - 1) / nb;
-    const int warps = wm * wn;
-    if (warps > 9) continue;  // __launch_bounds__(288)
-    // cost: tile slots issued (incl. empty ones) + operand loads per k-step; prefer >= 4 warps
-    const double slots = (double)warps * mb * nb;
-    const double loads = (double)warps * (mb + nb) * 0.25;
-    double score = slots + loads;
-    if (warps < 4) score *= 1.0 + 0.15 * (4 - warps);
-    if (score < best) {
-      best = score;
-      MB = mb;
-      NB = nb;
-      WM = wm;
-      WN = wn;
-      found = true;
+    for (int wm = 1; wm <= kSpreadWarps; wm *= 2) {
+      const int wn = kSpreadWarps / wm;
+      if (wm * mb < TMt || wn * nb < TNt) continue;
+      // panels (and the worst-case scratch) must fit the 227 KB of a CTA
+      if (spread_smem_for(mma_ld(wm * mb * 8), mma_ld(wn * nb * 8), Fmax, rc) > 224 * 1024) continue;
+      // time ~ DMMA slots per sub-partition (incl. padding tiles) + fragment loads per k-step
+      const double slots = (double)mb * nb;
+      const double score = slots * (1.0 + 0.25 * (double)(mb + nb) / (mb * nb));
+      if (score < best) {
+        best = score;
+        MB = mb;
+        NB = nb;
+        WM = wm;
+        WN = wn;
+        found = true;
+      }
     }
   }
   return found;
 }
 
-size_t spread_mma_smem(int PB, int M, int Nn, int Fmax, int rc) {
-  const int TMt = (M + 7) / 8, TNt = (Nn + 7) / 8;
-  return sizeof(double) * ((size_t)kMaxTaps * kPolyLen +
-                           (size_t)PB * (mma_ld(TMt * 8) + mma_ld(TNt * 8) + 3 * Fmax + rc));
+size_t spread_mma_smem(int /*PB*/, int M, int Nn, int Fmax, int rc) {
+  int MB, NB, WM, WN;
+  if (!spread_mma_choose(M, Nn, Fmax, rc, MB, NB, WM, WN)) return 0;
+  return spread_smem_for(mma_ld(WM * MB * 8), mma_ld(WN * NB * 8), Fmax, rc);
 }
 
-cudaError_t launch_spread_mma(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
-                              const int* perm, const double* V, long long ldv, long long n, int r0, int rc,
-                              int r_total, double* grid, int MB, int NB, int WM, int WN, int PB, size_t smem,
-                              cudaStream_t s) {
+cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
+                              const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
+                              int r0, int rc, int r_total, double* grid, int MB, int NB, int /*WM*/, int WN,
+                              int /*PB*/, size_t smem, cudaStream_t s) {
   if (n_items <= 0) return cudaSuccess;
-  const int threads = 32 * WM * WN;
 #define AKM_CASE(a, b)                                                                                         \
   if (MB == a && NB == b) {                                                                                    \
     static bool attr_set = false;                                                                              \
     if (!attr_set) {                                                                                           \
       cudaError_t e = cudaFuncSetAttribute(k_spread_mma<a, b>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                           200 * 1024);                                                        \
+                                           227 * 1024);                                                        \
       if (e != cudaSuccess) return e;                                                                          \
       attr_set = true;                                                                                         \
     }                                                                                                          \
-    k_spread_mma<a, b><<<n_items, threads, smem, s>>>(dtab, items, u_sorted, perm, V, ldv, n, r0, rc, r_total, \
-                                                      grid, PB, WN);                                           \
+    k_spread_mma<a, b><<<n_items, kSpreadThreads, smem, s>>>(dtab, items, u_sorted, perm, V, ldv, n, r0, rc,   \
+                                                             r_total, grid, WN, pp);                           \
     return cudaGetLastError();                                                                                 \
   }
   AKM_MMA_TILES(AKM_CASE)
