@@ -17,213 +17,228 @@
 //   FE  inverse last axis, Hermitian half-sum (k2 = 0 once, k2 > 0 twice, real part)
 // Only the box (nodes any point can touch) is transformed in and out, so the zero padding of
 // the oversampled grid and the frequencies outside S cost nothing.  Singleton (padded) axes
-// have one node and k = 0 with twiddle 1.  The stage is L2-resident and ~1% of the MVM.
+// have one node and k = 0 with twiddle 1.
+//
+// Every pass is the same batched operation Y[o][k][i] = sum_l M[k][l] X[o][l][i] (o = outer
+// index, i = inner index incl. the RHS), run by one kernel body: a CTA stages the L inputs of 32
+// consecutive columns (o, i) in shared memory with one read of each input, then each thread
+// produces outputs (k, column) with broadcast twiddle reads.  (The first version computed every
+// output straight from global memory and was latency-bound: profiles/r01_launches_c2_summary.txt.)
+#include <algorithm>
+
 #include "akm_internal.cuh"
 
 namespace akm {
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // conj(a) * b
-  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+
+constexpr int kDftThreads = 256;
+
+enum DftMode { kFA = 0, kFB, kFC1, kFC2, kFD, kFE };
+
+struct DftShape {
+  long long O, I;       // outer / inner extents (inner includes the RHS index)
+  int L, K;             // input length along the axis, output length
+  long long xo, xl;     // input strides (elements) of o and l; inner stride 1
+  long long yo, yk;     // output strides of o and k; inner stride 1
+};
+
+__host__ __device__ inline DftShape dft_shape(const WinGeom& g, int mode, int r, int ops) {
+  DftShape s;
+  const long long R = r;
+  switch (mode) {
+    case kFA:   // G[(l0,l1)][l2][c] (real) -> A1[(l0,l1)][k2][c]
+      s.O = (long long)g.L[0] * g.L[1]; s.I = R; s.L = g.L[2]; s.K = g.K[2];
+      s.xo = (long long)g.L[2] * R; s.xl = R; s.yo = (long long)g.K[2] * R; s.yk = R;
+      break;
+    case kFB:   // A1[l0][l1][(k2,c)] -> A2[l0][k1][(k2,c)]
+      s.O = g.L[0]; s.I = (long long)g.K[2] * R; s.L = g.L[1]; s.K = g.K[1];
+      s.xo = (long long)g.L[1] * s.I; s.xl = s.I; s.yo = (long long)g.K[1] * s.I; s.yk = s.I;
+      break;
+    case kFC1:  // A2[l0][(k1,k2,c)] -> A3[k0][(k1,k2,c)]
+      s.O = 1; s.I = (long long)g.K[1] * g.K[2] * R; s.L = g.L[0]; s.K = g.K[0];
+      s.xo = 0; s.xl = s.I; s.yo = 0; s.yk = s.I;
+      break;
+    case kFC2:  // D_op A3[k0][(k1,k2,c)] -> C[op][l0][(k1,k2,c)]   (o = op)
+      s.O = ops; s.I = (long long)g.K[1] * g.K[2] * R; s.L = g.K[0]; s.K = g.L[0];
+      s.xo = 0; s.xl = s.I; s.yo = (long long)g.L[0] * s.I; s.yk = s.I;
+      break;
+    case kFD:   // C[(op,l0)][k1][(k2,c)] -> C2[(op,l0)][l1][(k2,c)]
+      s.O = (long long)ops * g.L[0]; s.I = (long long)g.K[2] * R; s.L = g.K[1]; s.K = g.L[1];
+      s.xo = (long long)g.K[1] * s.I; s.xl = s.I; s.yo = (long long)g.L[1] * s.I; s.yk = s.I;
+      break;
+    default:    // kFE: C2[(op,line)][k2][c] -> H[(line, l2)][op][c] (real)
+      s.O = (long long)ops * g.L[0] * g.L[1]; s.I = R; s.L = g.K[2]; s.K = g.L[2];
+      s.xo = (long long)g.K[2] * R; s.xl = R; s.yo = 0; s.yk = 0;  // output indexed explicitly
+      break;
+  }
+  return s;
 }
 
-// Thread-per-output kernels; blockIdx.y = window.  r = number of RHS (innermost index).
-__global__ void k_fa(const WinTable* __restrict__ tabp, const double* __restrict__ G, double2* __restrict__ A1,
-                     const double2* __restrict__ tw, int r) {
+template <int MODE, int kDftCols>
+__global__ void __launch_bounds__(kDftThreads) k_dft_axis(const WinTable* __restrict__ tabp, const void* __restrict__ Xv,
+                                                          void* __restrict__ Yv, const double2* __restrict__ tw,
+                                                          const double* __restrict__ D, int dslot0, int r, int ops) {
   const WinTable& tab = *tabp;
   const WinGeom& g = tab.w[blockIdx.y];
-  const long long total = (long long)g.L[0] * g.L[1] * g.K[2] * r;
-  const double2* T = tw + g.tw_off[2];
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(idx % r);
-    const long long q = idx / r;
-    const int k2 = (int)(q % g.K[2]);
-    const long long line = q / g.K[2];  // l0*L1 + l1
-    const double* src = G + (g.tap_off + line * g.L[2]) * r + c;
-    const double2* Tk = T + (long long)k2 * g.L[2];
-    double re = 0.0, im = 0.0;
-    for (int l = 0; l < g.L[2]; ++l) {
-      const double v = src[(long long)l * r];
-      const double2 t = Tk[l];
-      re = fma(t.x, v, re);
-      im = fma(t.y, v, im);
+  const DftShape sh = dft_shape(g, MODE, r, ops);
+  const long long ncol = sh.O * sh.I;
+  const long long col0 = (long long)blockIdx.x * kDftCols;
+  if (col0 >= ncol) return;
+  extern __shared__ double2 xs[];  // [L][kDftCols]
+  const int tid = threadIdx.x;
+
+  long long xbase, ybase;  // window-relative base offsets (elements)
+  switch (MODE) {
+    case kFA: xbase = g.tap_off * r; ybase = g.a1_off * r; break;
+    case kFB: xbase = g.a1_off * r; ybase = g.a2_off * r; break;
+    case kFC1: xbase = g.a2_off * r; ybase = g.a3_off * r; break;
+    case kFC2: xbase = g.a3_off * r; ybase = g.c_off * r; break;
+    case kFD: xbase = g.c_off * r; ybase = g.c2_off * r; break;
+    default: xbase = g.c2_off * r; ybase = g.tap_off * (long long)ops * r; break;
+  }
+  // twiddle table of the transformed axis: T[k][l] = e^{-2 pi i k (box_lo + l) / n_g}, [K][L]
+  const int axis = (MODE == kFA || MODE == kFE) ? 2 : (MODE == kFB || MODE == kFD) ? 1 : 0;
+  const double2* T = tw + g.tw_off[axis];
+  const int Lt = g.L[axis];  // row length of the table
+
+  // stage the inputs X[o][l][i] of the CTA's columns (FC2: with D_op applied)
+  const long long kk = (long long)g.K[1] * g.K[2];
+  const long long dper = (long long)g.K[0] * kk;
+  for (int idx = tid; idx < sh.L * kDftCols; idx += kDftThreads) {
+    const int l = idx / kDftCols, j = idx - l * kDftCols;
+    const long long col = col0 + j;
+    double2 v = make_double2(0.0, 0.0);
+    if (col < ncol) {
+      const long long o = col / sh.I, i = col - o * sh.I;
+      const long long off = xbase + o * sh.xo + (long long)l * sh.xl + i;
+      if (MODE == kFA) {
+        v.x = static_cast<const double*>(Xv)[off];
+      } else {
+        v = static_cast<const double2*>(Xv)[off];
+      }
+      if (MODE == kFC2) {  // multiplier D_op[k0 = l][(k1,k2) = i / r]
+        const double dd = D[g.d_off + (dslot0 + o) * dper + (long long)l * kk + i / r];
+        v.x *= dd;
+        v.y *= dd;
+      }
     }
-    A1[(g.a1_off + q) * r + c] = make_double2(re, im);
+    xs[idx] = v;
+  }
+  __syncthreads();
+
+  // outputs (k, column): a warp shares k (broadcast twiddles), lanes take consecutive columns
+  const int j = tid % kDftCols;
+  const long long col = col0 + j;
+  if (col >= ncol) return;
+  const long long o = col / sh.I, i = col - o * sh.I;
+  for (int k = tid / kDftCols; k < sh.K; k += kDftThreads / kDftCols) {
+    // four interleaved partial sums over l (independent FMA chains)
+    double re4[4] = {0.0, 0.0, 0.0, 0.0}, im4[4] = {0.0, 0.0, 0.0, 0.0};
+    if (MODE == kFA || MODE == kFB || MODE == kFC1) {  // forward: M[k][l] = T[k][l]
+      const double2* Tk = T + (long long)k * Lt;
+      int l = 0;
+      for (; l + 4 <= sh.L; l += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 t = Tk[l + q], x = xs[(l + q) * kDftCols + j];
+          re4[q] = fma(t.x, x.x, fma(-t.y, x.y, re4[q]));
+          im4[q] = fma(t.x, x.y, fma(t.y, x.x, im4[q]));
+        }
+      }
+      for (; l < sh.L; ++l) {
+        const double2 t = Tk[l], x = xs[l * kDftCols + j];
+        re4[0] = fma(t.x, x.x, fma(-t.y, x.y, re4[0]));
+        im4[0] = fma(t.x, x.y, fma(t.y, x.x, im4[0]));
+      }
+    } else {  // inverse: M[k][l] = conj(T[l][k]) (k indexes nodes, l frequencies)
+      int l = 0;
+      for (; l + 4 <= sh.L; l += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 t = T[(long long)(l + q) * Lt + k], x = xs[(l + q) * kDftCols + j];
+          if (MODE == kFE) {
+            const double w = (l + q == 0) ? 1.0 : 2.0;  // Hermitian half-sum, real part
+            re4[q] = fma(w, fma(t.x, x.x, t.y * x.y), re4[q]);
+          } else {
+            re4[q] = fma(t.x, x.x, fma(t.y, x.y, re4[q]));
+            im4[q] = fma(t.x, x.y, fma(-t.y, x.x, im4[q]));
+          }
+        }
+      }
+      for (; l < sh.L; ++l) {
+        const double2 t = T[(long long)l * Lt + k], x = xs[l * kDftCols + j];
+        if (MODE == kFE) {
+          const double w = (l == 0) ? 1.0 : 2.0;
+          re4[0] = fma(w, fma(t.x, x.x, t.y * x.y), re4[0]);
+        } else {
+          re4[0] = fma(t.x, x.x, fma(t.y, x.y, re4[0]));
+          im4[0] = fma(t.x, x.y, fma(-t.y, x.x, im4[0]));
+        }
+      }
+    }
+    const double re = (re4[0] + re4[1]) + (re4[2] + re4[3]);
+    const double im = (im4[0] + im4[1]) + (im4[2] + im4[3]);
+    if (MODE == kFE) {
+      // H[(line * L2 + l2) * ops + op][c] with o = op * lines + line
+      const long long lines = (long long)g.L[0] * g.L[1];
+      const long long op = o / lines, line = o - op * lines;
+      static_cast<double*>(Yv)[ybase + ((line * g.L[2] + k) * ops + op) * r + i] = re;
+    } else {
+      static_cast<double2*>(Yv)[ybase + o * sh.yo + (long long)k * sh.yk + i] = make_double2(re, im);
+    }
   }
 }
 
-__global__ void k_fb(const WinTable* __restrict__ tabp, const double2* __restrict__ A1, double2* __restrict__ A2,
-                     const double2* __restrict__ tw, int r) {
-  const WinTable& tab = *tabp;
-  const WinGeom& g = tab.w[blockIdx.y];
-  const long long total = (long long)g.L[0] * g.K[1] * g.K[2] * r;
-  const double2* T = tw + g.tw_off[1];
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long j = idx % ((long long)g.K[2] * r);  // (k2, c)
-    const long long q = idx / ((long long)g.K[2] * r);
-    const int k1 = (int)(q % g.K[1]);
-    const int l0 = (int)(q / g.K[1]);
-    const double2* src = A1 + (g.a1_off + (long long)l0 * g.L[1] * g.K[2]) * r + j;
-    const double2* Tk = T + (long long)k1 * g.L[1];
-    double2 acc = make_double2(0.0, 0.0);
-    for (int l = 0; l < g.L[1]; ++l) {
-      const double2 v = src[(long long)l * g.K[2] * r];
-      const double2 t = Tk[l];
-      acc.x = fma(t.x, v.x, fma(-t.y, v.y, acc.x));
-      acc.y = fma(t.x, v.y, fma(t.y, v.x, acc.y));
-    }
-    A2[g.a2_off * r + idx] = acc;
+// host: grid for one pass = max over windows of the column tiles; smem = max L
+template <int MODE, int COLS>
+static cudaError_t launch_cols(long long tiles, int P, int Lmax, const WinTable* dtab, const void* X, void* Y,
+                               const double2* tw, const double* D, int dslot0, int r, int ops, cudaStream_t s) {
+  const size_t smem = sizeof(double2) * (size_t)Lmax * COLS;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_dft_axis<MODE, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
   }
-}
-
-// FC1: A3[k0][k1][k2][c] = sum_l0 T0[k0][l0] A2[l0][k1][k2][c]
-__global__ void k_fc1(const WinTable* __restrict__ tabp, const double2* __restrict__ A2, double2* __restrict__ A3,
-                      const double2* __restrict__ tw, int r) {
-  const WinTable& tab = *tabp;
-  const WinGeom& g = tab.w[blockIdx.y];
-  const long long plane = (long long)g.K[1] * g.K[2] * r;
-  const long long total = (long long)g.K[0] * plane;
-  const double2* T = tw + g.tw_off[0];
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long j = idx % plane;
-    const int k0 = (int)(idx / plane);
-    const double2* src = A2 + g.a2_off * r + j;
-    const double2* Tk = T + (long long)k0 * g.L[0];
-    double2 acc = make_double2(0.0, 0.0);
-    for (int l = 0; l < g.L[0]; ++l) {
-      const double2 v = src[(long long)l * plane];
-      const double2 t = Tk[l];
-      acc.x = fma(t.x, v.x, fma(-t.y, v.y, acc.x));
-      acc.y = fma(t.x, v.y, fma(t.y, v.x, acc.y));
-    }
-    A3[g.a3_off * r + idx] = acc;
-  }
-}
-
-// FC2: C[op][l0][k1][k2][c] = sum_k0 conj(T0[k0][l0]) D_op[k0][k1][k2] A3[k0][k1][k2][c]
-__global__ void k_fc2(const WinTable* __restrict__ tabp, const double2* __restrict__ A3, double2* __restrict__ C,
-                      const double2* __restrict__ tw, const double* __restrict__ D, int ops, int dslot0, int r) {
-  const WinTable& tab = *tabp;
-  const WinGeom& g = tab.w[blockIdx.y];
-  const long long kplane = (long long)g.K[1] * g.K[2];
-  const long long plane = kplane * r;
-  const long long per_op = (long long)g.L[0] * plane;
-  const long long total = ops * per_op;
-  const long long dper = (long long)g.K[0] * kplane;
-  const double2* T = tw + g.tw_off[0];
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int op = (int)(idx / per_op);
-    const long long rem = idx % per_op;
-    const int l0 = (int)(rem / plane);
-    const long long j = rem % plane;   // (k1, k2, c)
-    const long long kj = j / r;        // (k1, k2)
-    const double2* src = A3 + g.a3_off * r + j;
-    const double* Dk = D + g.d_off + (dslot0 + op) * dper + kj;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int k0 = 0; k0 < g.K[0]; ++k0) {
-      const double2 v = src[(long long)k0 * plane];
-      const double dd = Dk[(long long)k0 * kplane];
-      const double2 t = T[(long long)k0 * g.L[0] + l0];
-      const double2 y = make_double2(dd * v.x, dd * v.y);
-      // conj(t) * y
-      acc.x = fma(t.x, y.x, fma(t.y, y.y, acc.x));
-      acc.y = fma(t.x, y.y, fma(-t.y, y.x, acc.y));
-    }
-    C[g.c_off * r + idx] = acc;
-  }
-}
-
-// FD: C2[op][l0][l1][k2][c] = sum_k1 conj(T1[k1][l1]) C[op][l0][k1][k2][c]
-__global__ void k_fd(const WinTable* __restrict__ tabp, const double2* __restrict__ C, double2* __restrict__ C2,
-                     const double2* __restrict__ tw, int ops, int r) {
-  const WinTable& tab = *tabp;
-  const WinGeom& g = tab.w[blockIdx.y];
-  const long long inner = (long long)g.K[2] * r;
-  const long long per_op = (long long)g.L[0] * g.L[1] * inner;
-  const long long total = ops * per_op;
-  const double2* T = tw + g.tw_off[1];
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int op = (int)(idx / per_op);
-    const long long rem = idx % per_op;
-    const long long j = rem % inner;
-    const long long q = rem / inner;
-    const int l1 = (int)(q % g.L[1]);
-    const int l0 = (int)(q / g.L[1]);
-    const double2* src = C + g.c_off * r + (long long)op * g.L[0] * g.K[1] * inner + (long long)l0 * g.K[1] * inner + j;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int k1 = 0; k1 < g.K[1]; ++k1) {
-      const double2 v = src[(long long)k1 * inner];
-      const double2 t = T[(long long)k1 * g.L[1] + l1];
-      acc.x = fma(t.x, v.x, fma(t.y, v.y, acc.x));
-      acc.y = fma(t.x, v.y, fma(-t.y, v.x, acc.y));
-    }
-    C2[g.c2_off * r + idx] = acc;
-  }
-}
-
-// FE: H[(tap_off + tap) * ops*r + op*r + c] = Re sum_k2 alpha_k2 conj(T2[k2][l2]) C2[op][l0][l1][k2][c]
-__global__ void k_fe(const WinTable* __restrict__ tabp, const double2* __restrict__ C2, double* __restrict__ H,
-                     const double2* __restrict__ tw, int ops, int r) {
-  const WinTable& tab = *tabp;
-  const WinGeom& g = tab.w[blockIdx.y];
-  const long long total = g.ntap * ops * r;
-  const double2* T = tw + g.tw_off[2];
-  const long long lines = (long long)g.L[0] * g.L[1];
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(idx % r);
-    const int op = (int)((idx / r) % ops);
-    const long long tap = idx / ((long long)ops * r);
-    const int l2 = (int)(tap % g.L[2]);
-    const long long line = tap / g.L[2];
-    const double2* src = C2 + (g.c2_off + ((long long)op * lines + line) * g.K[2]) * r + c;
-    double acc = 0.0;
-    for (int k2 = 0; k2 < g.K[2]; ++k2) {
-      const double2 v = src[(long long)k2 * r];
-      const double2 t = T[(long long)k2 * g.L[2] + l2];
-      // Re(conj(t) v) = t.x v.x + t.y v.y
-      const double re = fma(t.x, v.x, t.y * v.y);
-      acc = (k2 == 0) ? re : fma(2.0, re, acc);
-    }
-    H[(g.tap_off + tap) * ops * r + op * r + c] = acc;
-  }
-}
-
-static int blocks_for(long long total) {
-  long long b = (total + 255) / 256;
-  if (b > 148 * 16) b = 148 * 16;
-  if (b < 1) b = 1;
-  return (int)b;
-}
-
-cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1, double2* A2, const double2* tw,
-                               int r, long long maxA1, long long maxA2, cudaStream_t s) {
-  k_fa<<<dim3(blocks_for(maxA1 * r), tab.P), 256, 0, s>>>(dtab, grid, A1, tw, r);
-  k_fb<<<dim3(blocks_for(maxA2 * r), tab.P), 256, 0, s>>>(dtab, A1, A2, tw, r);
+  k_dft_axis<MODE, COLS><<<dim3((unsigned)tiles, P), kDftThreads, smem, s>>>(dtab, X, Y, tw, D, dslot0, r, ops);
   return cudaGetLastError();
 }
 
-cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dtab, const double2* A2, double2* A3, double2* C,
-                                        double2* C2, const double2* tw, const double* D, int ops, int dslot0, int r, double* H,
-                                        long long maxA3, long long maxC, long long maxC2, long long maxTap,
-                                        cudaStream_t s) {
-  k_fc1<<<dim3(blocks_for(maxA3 * r), tab.P), 256, 0, s>>>(dtab, A2, A3, tw, r);
-  k_fc2<<<dim3(blocks_for(maxC * ops * r), tab.P), 256, 0, s>>>(dtab, A3, C, tw, D, ops, dslot0, r);
-  k_fd<<<dim3(blocks_for(maxC2 * ops * r), tab.P), 256, 0, s>>>(dtab, C, C2, tw, ops, r);
-  k_fe<<<dim3(blocks_for(maxTap * ops * r), tab.P), 256, 0, s>>>(dtab, C2, H, tw, ops, r);
-  return cudaGetLastError();
+// columns per CTA: 32 when there are many columns; 8 for small passes (more CTAs, fewer outputs
+// per thread -- the small configurations are latency-bound)
+template <int MODE>
+static cudaError_t launch_pass(const WinTable& tab, const WinTable* dtab, const void* X, void* Y, const double2* tw,
+                               const double* D, int dslot0, int r, int ops, cudaStream_t s) {
+  long long cols = 1, total = 0;
+  int Lmax = 1;
+  for (int w = 0; w < tab.P; ++w) {
+    const DftShape sh = dft_shape(tab.w[w], MODE, r, ops);
+    cols = std::max(cols, sh.O * sh.I);
+    total += sh.O * sh.I;
+    Lmax = std::max(Lmax, sh.L);
+  }
+  if (total >= 148LL * 4 * 32)
+    return launch_cols<MODE, 32>((cols + 31) / 32, tab.P, Lmax, dtab, X, Y, tw, D, dslot0, r, ops, s);
+  return launch_cols<MODE, 8>((cols + 7) / 8, tab.P, Lmax, dtab, X, Y, tw, D, dslot0, r, ops, s);
 }
 
-__global__ void k_zero(double* __restrict__ p, long long count) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
-    p[i] = 0.0;
+cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1, double2* A2,
+                               const double2* tw, int r, long long /*maxA1*/, long long /*maxA2*/, cudaStream_t s) {
+  cudaError_t e = launch_pass<kFA>(tab, dtab, grid, A1, tw, nullptr, 0, r, 1, s);
+  if (e != cudaSuccess) return e;
+  return launch_pass<kFB>(tab, dtab, A1, A2, tw, nullptr, 0, r, 1, s);
+}
+
+cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dtab, const double2* A2, double2* A3,
+                                        double2* C, double2* C2, const double2* tw, const double* D, int ops,
+                                        int dslot0, int r, double* H, long long /*maxA3*/, long long /*maxC*/,
+                                        long long /*maxC2*/, long long /*maxTap*/, cudaStream_t s) {
+  cudaError_t e = launch_pass<kFC1>(tab, dtab, A2, A3, tw, nullptr, 0, r, ops, s);
+  if (e == cudaSuccess) e = launch_pass<kFC2>(tab, dtab, A3, C, tw, D, dslot0, r, ops, s);
+  if (e == cudaSuccess) e = launch_pass<kFD>(tab, dtab, C, C2, tw, nullptr, 0, r, ops, s);
+  if (e == cudaSuccess) e = launch_pass<kFE>(tab, dtab, C2, H, tw, nullptr, 0, r, ops, s);
+  return e;
 }
 
 cudaError_t launch_zero(double* p, long long count, cudaStream_t s) {

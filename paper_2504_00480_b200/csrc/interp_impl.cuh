@@ -2,154 +2,14 @@
 // eq. 3.3).  Instantiated per (D, TAPS) in interp_d<D>_t<TAPS>.cu so the builds run in parallel;
 // dispatched from interp.cu.
 //
-// Design: one CTA of 128 threads per work item = a chunk of <= 256 points of
-// ONE grid cell, two points per thread.  All points of a cell share the footprint of (2m)^d
-// nodes, which is staged in shared memory (whole, or one o0-plane at a time when it exceeds
-// 48 KB); every tap's OPS x RC values are then read once per warp as broadcasts and feed
-// 2 * OPS * RC FMAs.  Window weights come from the Horner polynomials of the window
-// (window_taps).  For OPS*RC <= 10 the tap loop is sum-factorised over the last axis.
+// Two kernels: k_interp_mma (OPS*RC >= 8 values per node: per-cell work items,
+// the tap contraction as a GEMM on DMMA) and k_interp_bin (fewer values: per-bin work items,
+// scalar FP64 with the last axis sum-factorised).  Window weights come from the Chebyshev
+// polynomials of the window (window_taps / window_taps_estrin).
 #pragma once
 #include "akm_internal.cuh"
 
 namespace akm {
-
-template <int D, int TAPS, int OPS, int RC, int PPT>
-__global__ void __launch_bounds__(64) k_interp(const WinTable* __restrict__ tabp, const WorkItem* __restrict__ items,
-                                                const double* __restrict__ u_sorted, const int* __restrict__ perm,
-                                                const double* __restrict__ H, int r, int r0,
-                                                double* __restrict__ part, long long n) {
-  constexpr int V = OPS * RC;           // values per grid node used by this CTA
-  constexpr int VP = (V + 1) & ~1;      // padded to an even count (16-byte rows)
-  constexpr int T0 = (D >= 3) ? TAPS : 1;
-  constexpr int T1 = (D >= 2) ? TAPS : 1;
-  constexpr int SLAB = T1 * TAPS;       // nodes of one o0-plane of the cell footprint
-  constexpr bool FULL = (size_t)T0 * SLAB * VP * sizeof(double) <= 48 * 1024;
-  constexpr int NPL = FULL ? T0 : 1;    // planes staged per pass
-  constexpr bool SUMF = V <= 10;        // sum-factorised tap loop (fewer weight products)
-  const WinTable& tab = *tabp;
-  const WorkItem it = items[blockIdx.x];
-  const WinGeom& g = tab.w[it.win];
-  __shared__ double poly[TAPS * kPolyLen];
-  extern __shared__ double sm[];        // [NPL * SLAB][VP]
-
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < TAPS * kPolyLen; idx += blockDim.x) poly[idx] = tab.poly[idx];
-  __syncthreads();
-
-  // points of this thread (strided so a warp holds consecutive points of the cell)
-  bool has[PPT];
-  long long pidx[PPT];
-  double x0[PPT], w1[PPT][T1], w2[PPT][TAPS];
-#pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    const int q = tid + k * blockDim.x;
-    has[k] = q < it.count;
-    pidx[k] = (long long)it.start + (has[k] ? q : 0);
-    double x[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int a = 3 - D; a < 3; ++a) {
-      const double u = u_sorted[((long long)it.win * 3 + a) * n + pidx[k]];
-      x[a] = 2.0 * (u - floor(u)) - 1.0;
-    }
-    x0[k] = x[0];
-    window_taps<TAPS>(poly, x[2], w2[k]);
-    if (D >= 2) {
-      window_taps<T1>(poly, x[1], w1[k]);
-    } else {
-#pragma unroll
-      for (int o = 0; o < T1; ++o) w1[k][o] = 1.0;
-    }
-  }
-
-  double acc[PPT][V];
-#pragma unroll
-  for (int k = 0; k < PPT; ++k)
-#pragma unroll
-    for (int v = 0; v < V; ++v) acc[k][v] = 0.0;
-
-  const int cell0 = it.bin[0], cell1 = it.bin[1], cell2 = it.bin[2];
-  const long long row_vals = (long long)OPS * r;  // values per node in H
-  for (int pg = 0; pg < T0; pg += NPL) {
-    __syncthreads();
-    for (int idx = tid; idx < NPL * SLAB * V; idx += blockDim.x) {
-      const int t = idx / V, v = idx % V;
-      const int op = v / RC, c = v % RC;
-      const int o0 = pg + t / SLAB;
-      const int o1 = (t % SLAB) / TAPS, o2 = t % TAPS;
-      const long long tap = ((long long)(cell0 + o0) * g.L[1] + (cell1 + o1)) * g.L[2] + (cell2 + o2);
-      sm[t * VP + v] = H[(g.tap_off + tap) * row_vals + op * r + r0 + c];
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int pl = 0; pl < NPL; ++pl) {
-      double wa[PPT];
-#pragma unroll
-      for (int k = 0; k < PPT; ++k) wa[k] = (D >= 3) ? window_tap(poly, pg + pl, x0[k]) : 1.0;
-      const double* plane = sm + pl * SLAB * VP;
-#pragma unroll
-      for (int o1 = 0; o1 < T1; ++o1) {
-        const double* rowp = plane + o1 * TAPS * VP;
-        double w01[PPT];
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) w01[k] = wa[k] * w1[k][o1];
-        if (SUMF) {
-          double t[PPT][V];
-#pragma unroll
-          for (int k = 0; k < PPT; ++k)
-#pragma unroll
-            for (int v = 0; v < V; ++v) t[k][v] = 0.0;
-#pragma unroll
-          for (int o2 = 0; o2 < TAPS; ++o2) {
-            double h[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) h[v] = rowp[o2 * VP + v];
-#pragma unroll
-            for (int k = 0; k < PPT; ++k)
-#pragma unroll
-              for (int v = 0; v < V; ++v) t[k][v] = fma(w2[k][o2], h[v], t[k][v]);
-          }
-#pragma unroll
-          for (int k = 0; k < PPT; ++k)
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc[k][v] = fma(w01[k], t[k][v], acc[k][v]);
-        } else {
-#pragma unroll
-          for (int o2 = 0; o2 < TAPS; ++o2) {
-            double h[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) h[v] = rowp[o2 * VP + v];
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) {
-              const double wt = w01[k] * w2[k][o2];
-#pragma unroll
-              for (int v = 0; v < V; ++v) acc[k][v] = fma(wt, h[v], acc[k][v]);
-            }
-          }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    if (!has[k]) continue;
-    const long long i = perm[(long long)it.win * n + pidx[k]];
-    double* out = part + (((long long)it.win * n + i) * OPS) * r + r0;
-#pragma unroll
-    for (int q = 0; q < OPS; ++q)
-#pragma unroll
-      for (int c = 0; c < RC; ++c) out[(long long)q * r + c] = acc[k][q * RC + c];
-  }
-}
-
-// dynamic shared memory of k_interp<D, TAPS, OPS, RC, *>
-inline size_t interp_smem(int D, int TAPS, int OPS, int RC) {
-  const int V = OPS * RC, VP = (V + 1) & ~1;
-  const int T0 = (D >= 3) ? TAPS : 1, T1 = (D >= 2) ? TAPS : 1;
-  const size_t slab = (size_t)T1 * TAPS;
-  const bool full = (size_t)T0 * slab * VP * sizeof(double) <= 48 * 1024;
-  return (full ? T0 : 1) * slab * VP * sizeof(double);
-}
-
 
 // ---------------------------------------------------------------- FP64 tensor-core variant
 // For OPS*RC >= 8 values per node: per o0-plane of the cell footprint, S[p][v] += sum over the
@@ -290,11 +150,123 @@ inline size_t interp_mma_smem(int D, int TAPS, int OPS, int RC) {
   return 2 * (size_t)T1 * TAPS * mma_ld(NT * 8) * sizeof(double);
 }
 
+
+// ---------------------------------------------------------------- bin-based scalar variant
+// For few values per node (OPS*RC < 8) and sparse cells: one CTA of 128 threads per work item = a
+// chunk of <= 128 points of ONE BIN (B^d cells, the spreading bins), one point per thread.  The
+// bin footprint (F = B + 2m - 1 nodes per axis) streams through shared memory one o0-plane at a
+// time (double-buffered); each thread reads its own 2m x 2m window of the plane at its cell's
+// offset inside the bin.  Points are sorted by cell inside a bin, so the lanes of a warp mostly
+// read the same addresses (broadcasts).  FP64 FMAs per point and value: (2m)^d + (2m)^(d-1).
+template <int D, int TAPS, int OPS, int RC>
+__global__ void __launch_bounds__(128) k_interp_bin(const WinTable* __restrict__ tabp,
+                                                    const WorkItem* __restrict__ items,
+                                                    const double* __restrict__ u_sorted, const int* __restrict__ perm,
+                                                    const double* __restrict__ H, int r, int r0,
+                                                    double* __restrict__ part, long long n) {
+  constexpr int V = OPS * RC;
+  constexpr int VP = (V + 1) & ~1;
+  constexpr int T1 = (D >= 2) ? TAPS : 1;
+  const WinTable& tab = *tabp;
+  const WorkItem it = items[blockIdx.x];
+  const WinGeom& g = tab.w[it.win];
+  const int F0 = g.F[0], F1 = g.F[1], F2 = g.F[2], B = g.B;
+  const int plane = F1 * F2;
+  __shared__ double poly[TAPS * kPolyLen];
+  extern __shared__ double sm[];  // [2][F1*F2][VP]
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < TAPS * kPolyLen; idx += blockDim.x) poly[idx] = tab.poly[idx];
+
+  int org[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) org[a] = g.box_lo[a] + it.bin[a] * (a < 3 - D ? 0 : B);
+  const long long row_vals = (long long)OPS * r;
+  const long long tap0 = g.tap_off + ((long long)(org[0] - g.box_lo[0]) * g.L[1] + (org[1] - g.box_lo[1])) * g.L[2] +
+                         (org[2] - g.box_lo[2]);
+  auto stage = [&](int P, double* buf) {  // footprint plane P of the bin
+    for (int idx = tid; idx < plane * V; idx += blockDim.x) {
+      const int t = idx / V, v = idx - t * V;
+      const int op = v / RC, c = v - op * RC;
+      const int q1 = t / F2, q2 = t - q1 * F2;
+      const long long tap = tap0 + ((long long)P * g.L[1] + q1) * g.L[2] + q2;
+      buf[t * VP + v] = H[tap * row_vals + op * r + r0 + c];
+    }
+  };
+  stage(0, sm);
+  __syncthreads();  // poly, plane 0
+
+  const bool has = tid < it.count;
+  const long long pidx = (long long)it.start + (has ? tid : 0);
+  int s[3] = {0, 0, 0};  // the point's cell offset inside the bin (= its footprint offset)
+  double x[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int a = 3 - D; a < 3; ++a) {
+    const double u = u_sorted[((long long)it.win * 3 + a) * n + pidx];
+    const double fl = floor(u);
+    x[a] = 2.0 * (u - fl) - 1.0;
+    s[a] = (int)fl - tab.m + 1 - org[a];
+  }
+  double w1[T1], w2[TAPS];
+  window_taps_estrin<TAPS>(poly, x[2], w2);
+  if (D >= 2) {
+    window_taps_estrin<T1>(poly, x[1], w1);
+  } else {
+#pragma unroll
+    for (int o = 0; o < T1; ++o) w1[o] = 1.0;
+  }
+  double acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.0;
+
+  for (int P = 0; P < F0; ++P) {
+    double* cur = sm + (P & 1) * plane * VP;
+    if (P + 1 < F0) stage(P + 1, sm + ((P + 1) & 1) * plane * VP);
+    const int o0 = P - s[0];
+    if (has && o0 >= 0 && o0 < ((D >= 3) ? TAPS : 1)) {
+      const double wa = (D >= 3) ? window_tap(poly, o0, x[0]) : 1.0;
+      const double* base = cur + (s[1] * F2 + s[2]) * VP;
+      // sum-factorised over o2 with T1 * V independent accumulator chains (ILP for the FP64 pipe)
+      double t[T1][V];
+#pragma unroll
+      for (int o1 = 0; o1 < T1; ++o1)
+#pragma unroll
+        for (int v = 0; v < V; ++v) t[o1][v] = 0.0;
+#pragma unroll
+      for (int o2 = 0; o2 < TAPS; ++o2) {
+#pragma unroll
+        for (int o1 = 0; o1 < T1; ++o1) {
+          const double* hp = base + (o1 * F2 + o2) * VP;
+#pragma unroll
+          for (int v = 0; v < V; ++v) t[o1][v] = fma(w2[o2], hp[v], t[o1][v]);
+        }
+      }
+#pragma unroll
+      for (int o1 = 0; o1 < T1; ++o1) {
+        const double w01 = wa * w1[o1];
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = fma(w01, t[o1][v], acc[v]);
+      }
+    }
+    __syncthreads();  // plane P consumed; plane P+1 staged
+  }
+  if (!has) return;
+  const long long i = perm[(long long)it.win * n + pidx];
+  double* out = part + (((long long)it.win * n + i) * OPS) * r + r0;
+#pragma unroll
+  for (int q = 0; q < OPS; ++q)
+#pragma unroll
+    for (int c = 0; c < RC; ++c) out[(long long)q * r + c] = acc[q * RC + c];
+}
+
+inline size_t interp_bin_smem(int V, int F1, int F2) {
+  return 2 * (size_t)F1 * F2 * ((V + 1) & ~1) * sizeof(double);
+}
+
 template <int D, int T>
-cudaError_t launch_interp_dt(const WinTable* dtab, const WorkItem* items, int n_items, const double* u_sorted,
-                             const int* perm, const double* H, int ops, int r, int r0, int rc, double* part,
-                             long long n, cudaStream_t s) {
-  constexpr int PPT = 2;
+cudaError_t launch_interp_dt(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
+                             int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                             const double* H, int ops, int r, int r0, int rc, double* part, long long n,
+                             cudaStream_t s) {
 #define AKM_CASE(O, R)                                                                                              \
   if (ops == O && rc == R) {                                                                                        \
     if constexpr (O * R >= 8) {                                                                                     \
@@ -308,15 +280,16 @@ cudaError_t launch_interp_dt(const WinTable* dtab, const WorkItem* items, int n_
       }                                                                                                             \
       k_interp_mma<D, T, O, R><<<n_items, 256, smem, s>>>(dtab, items, u_sorted, perm, H, r, r0, part, n);         \
     } else {                                                                                                        \
-      const size_t smem = interp_smem(D, T, O, R);                                                                  \
+      if (n_items_bin <= 0) return cudaSuccess;                                                                     \
+      const size_t smem = interp_bin_smem(O * R, Fb1, Fb2);                                                         \
       static bool attr_set = false;                                                                                 \
       if (!attr_set) {                                                                                              \
-        cudaError_t e = cudaFuncSetAttribute(k_interp<D, T, O, R, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
-                                             (int)smem);                                                            \
+        cudaError_t e = cudaFuncSetAttribute(k_interp_bin<D, T, O, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             200 * 1024);                                                           \
         if (e != cudaSuccess) return e;                                                                             \
         attr_set = true;                                                                                            \
       }                                                                                                             \
-      k_interp<D, T, O, R, PPT><<<n_items, 64, smem, s>>>(dtab, items, u_sorted, perm, H, r, r0, part, n);         \
+      k_interp_bin<D, T, O, R><<<n_items_bin, 128, smem, s>>>(dtab, items_bin, u_sorted, perm, H, r, r0, part, n); \
     }                                                                                                               \
     return cudaGetLastError();                                                                                      \
   }

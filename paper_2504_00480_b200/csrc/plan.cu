@@ -54,6 +54,7 @@ struct Group {  // windows sharing (d, F) -> one spread / interp launch
   std::vector<int> wins;
   int spread_begin = 0, spread_count = 0;  // slice of the concatenated spread work items
   int interp_begin = 0, interp_count = 0;
+  int interp_bin_begin = 0, interp_bin_count = 0;
 };
 
 }  // namespace
@@ -78,18 +79,37 @@ struct akm_plan {
   std::vector<double> c_w, c_w_binned;      // current scale, scale the bins were built for
   WinTable tab{};                           // host copy
   PolyParam poly_param{};                   // window polynomials, passed to kernels by value
-  std::vector<WorkItem> items_spread, items_interp;
+  std::vector<WorkItem> items_spread, items_interp, items_interp_bin;
   std::vector<Group> groups;
   std::vector<long long> occupied, maxbin;
   long long total_taps = 0, szA1 = 0, szA2 = 0, szA3 = 0, szC = 0, szC2 = 0, szTW = 0, szD = 0;
   long long maxA1 = 0, maxA2 = 0, maxA3 = 0, maxC = 0, maxC2 = 0, maxTap = 0;
 
   // device buffers
-  DevBuf dtab, Xc, u_tmp, u_sorted, perm, hist, hist_off, err_flag, items_s, items_i, minmax, r2;
+  DevBuf dtab, Xc, u_tmp, u_sorted, perm, hist, hist_off, err_flag, items_s, items_i, items_ib, minmax, r2;
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
   DevBuf stageV, stageY, stageL, stageS;
   DevBuf krB, krKB, krW, krX, krY, krQ, krPart, krH, krState, krErr, krStage;
   long long r_cap = 0;
+
+  // CUDA graph of the last MVM launch sequence (replayed when called again with the same buffers)
+  struct GraphKey {
+    const void *V, *Y, *dYl, *dYsf;
+    long long ldv, ldy;
+    int r;
+    long long epoch;
+    bool operator==(const GraphKey& o) const {
+      return V == o.V && Y == o.Y && dYl == o.dYl && dYsf == o.dYsf && ldv == o.ldv && ldy == o.ldy && r == o.r &&
+             epoch == o.epoch;
+    }
+  };
+  long long epoch = 0;                 // bumped whenever buffers, items or theta change
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey{};
+  long long glaunches = 0, gspread = 0, ginterp = 0;
+  cudaStream_t own_stream = nullptr;   // used to capture / replay when the caller passes the legacy stream
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  bool use_graphs = true;
 
   // profiling (akm_set_profiling / akm_get_stage_times): a ring of event sets, drained lazily
   static constexpr int kRing = 512;
@@ -126,6 +146,10 @@ struct akm_plan {
   ~akm_plan() {
     for (auto& es : ring)
       for (auto& e : es.e) cudaEventDestroy(e);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (own_stream) cudaStreamDestroy(own_stream);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
   }
 
   akm_status fail(akm_status st, const char* fmt, ...) {
@@ -178,6 +202,7 @@ inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 // Build per-window boxes for the current c_w, histogram the points per cell on the device,
 // choose the bin edge B per window from the histogram, lay the cells out bin-major, scatter.
 static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
+  ++plan->epoch;
   const int P = plan->P, m = plan->m, n_g = plan->n_g;
   const long long n = plan->n;
   WinTable& tab = plan->tab;
@@ -239,13 +264,15 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   std::vector<int> cell_off(std::max<long long>(ncells, 1), 0);
   plan->items_spread.clear();
   plan->items_interp.clear();
+  plan->items_interp_bin.clear();
   plan->occupied.assign(P, 0);
   plan->maxbin.assign(P, 0);
   const long long total_pts = n * P;
   long long ch_s = total_pts / (148 * 2);
   ch_s = std::max(32LL, std::min(4096LL, ch_s));
   const int ch_i = 128;  // interpolation: one cell per work item (64 thr x 2 pts, or 8 warps x 16 pts on DMMA)
-  std::vector<std::vector<WorkItem>> its_s(P), its_i(P);
+  std::vector<std::vector<WorkItem>> its_s(P), its_i(P), its_ib(P);
+  const int ch_ib = 128;  // interpolation, few values per node: one bin per work item, 1 point / thread
   for (int w = 0; w < P; ++w) {
     WinGeom& g = tab.w[w];
     const int* hc = hist.data() + hoff[w];
@@ -330,6 +357,8 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
           plan->maxbin[w] = std::max(plan->maxbin[w], cnt);
           for (long long q = 0; q < cnt; q += ch_s)
             its_s[w].push_back(WorkItem{w, {b0, b1, b2}, (int)(start + q), (int)std::min<long long>(ch_s, cnt - q)});
+          for (long long q = 0; q < cnt; q += ch_ib)
+            its_ib[w].push_back(WorkItem{w, {b0, b1, b2}, (int)(start + q), (int)std::min<long long>(ch_ib, cnt - q)});
         }
     if (pos != n) return plan->fail(AKM_ERR_CUDA, "internal error: histogram of window %d holds %lld of %lld points",
                                     w, pos, n);
@@ -352,10 +381,11 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     grp->wins.push_back(w);
   }
   for (auto& grp : plan->groups) {
-    std::vector<WorkItem> gs, gi;
+    std::vector<WorkItem> gs, gi, gib;
     for (int w : grp.wins) {
       gs.insert(gs.end(), its_s[w].begin(), its_s[w].end());
       gi.insert(gi.end(), its_i[w].begin(), its_i[w].end());
+      gib.insert(gib.end(), its_ib[w].begin(), its_ib[w].end());
     }
     std::stable_sort(gs.begin(), gs.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
     std::stable_sort(gi.begin(), gi.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
@@ -365,6 +395,9 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     grp.interp_count = (int)gi.size();
     plan->items_spread.insert(plan->items_spread.end(), gs.begin(), gs.end());
     plan->items_interp.insert(plan->items_interp.end(), gi.begin(), gi.end());
+    grp.interp_bin_begin = (int)plan->items_interp_bin.size();
+    grp.interp_bin_count = (int)gib.size();
+    plan->items_interp_bin.insert(plan->items_interp_bin.end(), gib.begin(), gib.end());
   }
 
   // workspace layout (per RHS) for grids, spectra, twiddles and multipliers
@@ -416,6 +449,10 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   if (!plan->items_interp.empty())
     AKM_CK(cudaMemcpyAsync(plan->items_i.p, plan->items_interp.data(), sizeof(WorkItem) * plan->items_interp.size(),
                            cudaMemcpyHostToDevice, s));
+  AKM_CK(plan->items_ib.ensure(sizeof(WorkItem) * std::max<size_t>(plan->items_interp_bin.size(), 1)));
+  if (!plan->items_interp_bin.empty())
+    AKM_CK(cudaMemcpyAsync(plan->items_ib.p, plan->items_interp_bin.data(),
+                           sizeof(WorkItem) * plan->items_interp_bin.size(), cudaMemcpyHostToDevice, s));
   // twiddles
   AKM_CK(plan->tw.ensure(sizeof(double2) * std::max<long long>(twc, 1)));
   AKM_CK(launch_twiddles(tab, plan->dtab.as<WinTable>(), plan->tw.as<double2>(), s));
@@ -462,6 +499,7 @@ static akm_status rebuild_tables(akm_plan* plan, cudaStream_t s) {
 
 static akm_status ensure_rhs_workspace(akm_plan* plan, int r) {
   if (r <= plan->r_cap) return AKM_OK;
+  ++plan->epoch;
   const long long R = r;
   AKM_CK(plan->grid.ensure(sizeof(double) * std::max<long long>(plan->total_taps * R, 1)));
   AKM_CK(plan->H.ensure(sizeof(double) * std::max<long long>(plan->total_taps * 2 * R, 1)));
@@ -502,8 +540,8 @@ static bool choose_spread_tile(int M, int Nn, int& MT, int& NT, int& threads) {
 }
 
 // ================================================================== the MVM
-static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r, double* Y, double* dYl,
-                          double* dYsf, long long ldy, cudaStream_t s) {
+static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, int r, double* Y, double* dYl,
+                              double* dYsf, long long ldy, cudaStream_t s) {
   const bool needK = (Y != nullptr) || (dYsf != nullptr);
   const bool needL = dYl != nullptr;
   const int ops = (needK ? 1 : 0) + (needL ? 1 : 0);
@@ -560,7 +598,9 @@ static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r,
     const int rc = interp_rc_for(r - r0);
     for (const Group& grp : plan->groups) {
       AKM_CK(launch_interp(dtab, plan->items_i.as<WorkItem>() + grp.interp_begin, grp.interp_count,
-                           plan->u_sorted.as<double>(), plan->perm.as<int>(), plan->H.as<double>(), grp.d,
+                           plan->items_ib.as<WorkItem>() + grp.interp_bin_begin, grp.interp_bin_count,
+                           grp.d >= 2 ? grp.F : 1, grp.F, plan->u_sorted.as<double>(), plan->perm.as<int>(),
+                           plan->H.as<double>(), grp.d,
                            2 * plan->m, ops, r, r0, rc, plan->part.as<double>(), n, s));
       if (grp.interp_count > 0) {
         ++plan->launches;
@@ -575,6 +615,65 @@ static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r,
                          dYsf, ldy, slotK, slotL, s));
   ++plan->launches;
   if (ev) AKM_CK(cudaEventRecord(ev->e[4], s));
+  return AKM_OK;
+}
+
+// The MVM launch sequence (a memset and ~9 kernels) is captured once into a CUDA graph and
+// replayed while the buffers, items and theta stay the same: the small configurations are
+// launch-latency bound.  The legacy default stream cannot be captured; calls on it run the graph
+// on a plan-owned stream ordered by two events.  Profiling (stage events) uses direct launches.
+static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r, double* Y, double* dYl,
+                          double* dYsf, long long ldy, cudaStream_t s) {
+  if (plan->n == 0) return AKM_OK;
+  if (plan->profiling || !plan->use_graphs) return enqueue_mvm(plan, V, ldv, r, Y, dYl, dYsf, ldy, s);
+  akm_status st = ensure_rhs_workspace(plan, r);
+  if (st != AKM_OK) return st;
+  const akm_plan::GraphKey key{V, Y, dYl, dYsf, ldv, ldy, r, plan->epoch};
+  cudaStream_t cs = s;
+  if (s == nullptr || s == cudaStreamLegacy) {
+    if (!plan->own_stream) {
+      AKM_CK(cudaStreamCreateWithFlags(&plan->own_stream, cudaStreamNonBlocking));
+      AKM_CK(cudaEventCreateWithFlags(&plan->ev_in, cudaEventDisableTiming));
+      AKM_CK(cudaEventCreateWithFlags(&plan->ev_out, cudaEventDisableTiming));
+    }
+    cs = plan->own_stream;
+    AKM_CK(cudaEventRecord(plan->ev_in, s));
+    AKM_CK(cudaStreamWaitEvent(cs, plan->ev_in, 0));
+  }
+  if (!(plan->gexec && plan->gkey == key)) {
+    if (plan->gexec) {
+      cudaGraphExecDestroy(plan->gexec);
+      plan->gexec = nullptr;
+    }
+    const long long l0 = plan->launches, s0 = plan->spread_launches, i0 = plan->interp_launches;
+    cudaGraph_t graph = nullptr;
+    AKM_CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    st = enqueue_mvm(plan, V, ldv, r, Y, dYl, dYsf, ldy, cs);
+    cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+    if (st != AKM_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    AKM_CK(ec);
+    cudaError_t ei = cudaGraphInstantiate(&plan->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    AKM_CK(ei);
+    plan->gkey = key;
+    plan->glaunches = plan->launches - l0;
+    plan->gspread = plan->spread_launches - s0;
+    plan->ginterp = plan->interp_launches - i0;
+    plan->launches = l0;  // counted again below, once per replay
+    plan->spread_launches = s0;
+    plan->interp_launches = i0;
+  }
+  AKM_CK(cudaGraphLaunch(plan->gexec, cs));
+  plan->launches += plan->glaunches;
+  plan->spread_launches += plan->gspread;
+  plan->interp_launches += plan->ginterp;
+  if (cs != s) {
+    AKM_CK(cudaEventRecord(plan->ev_out, cs));
+    AKM_CK(cudaStreamWaitEvent(s, plan->ev_out, 0));
+  }
   return AKM_OK;
 }
 
@@ -839,6 +938,7 @@ akm_status akm_set_theta(akm_plan* plan, double sigma_f, double ell, double sigm
   cudaStream_t s = S(stream);
   AKM_CK(cudaSetDevice(plan->device));
   plan->have_theta = false;
+  ++plan->epoch;  // theta is baked into captured launch sequences
   plan->sigma_f = sigma_f;
   plan->ell = ell;
   plan->sigma_eps = sigma_eps;

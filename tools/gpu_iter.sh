@@ -22,7 +22,7 @@ if [ "${NCU_C4:-0}" = 1 ]; then
 fi
 if [ "${NCU_C2:-0}" = 1 ]; then
   timeout 300 python tools/prof_run.py --config c2 --calls 3 > gpurun_out/plain_c2.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_" -s 20 -c 12 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_" -s ${NCU2_S:-43} -c ${NCU2_N:-9} \
       -o gpurun_out/prof_c2 -f python tools/prof_run.py --config c2 --calls 3 > gpurun_out/ncu_c2.log 2>&1
   tail -2 gpurun_out/ncu_c2.log
 fi
