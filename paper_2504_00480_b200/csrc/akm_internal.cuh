@@ -230,7 +230,7 @@ void kr_summary_offsets(size_t* off_quad, size_t* off_samples, size_t* off_steps
 bool interp_supported(int d, int taps, int ops, int rc);
 int interp_rc_for(int r_remaining);
 cudaError_t launch_interp(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                          int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm, const double* H,
+                          int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm, const double* H,
                           int d, int taps, int ops, int r, int r0, int rc, double* part, long long n, cudaStream_t s);
 cudaError_t launch_epilogue(long long n, int P, int r, int ops, const double* part, const double* V, long long ldv,
                             double sigma_f, double sigma_eps, double* Y, double* dYl, double* dYsf, long long ldy,

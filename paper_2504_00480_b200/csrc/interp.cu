@@ -6,39 +6,39 @@
 namespace akm {
 
 cudaError_t launch_interp_d1_t8(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                              int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 cudaError_t launch_interp_d1_t12(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                              int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 cudaError_t launch_interp_d1_t16(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                              int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 cudaError_t launch_interp_d2_t8(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                              int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 cudaError_t launch_interp_d2_t12(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                              int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 cudaError_t launch_interp_d2_t16(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                              int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 cudaError_t launch_interp_d3_t8(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                              int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 cudaError_t launch_interp_d3_t12(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                              int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 cudaError_t launch_interp_d3_t16(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                              int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 
@@ -57,35 +57,35 @@ int interp_rc_for(int r_remaining) {
 }
 
 cudaError_t launch_interp(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                          int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm, const double* H,
+                          int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm, const double* H,
                           int d, int taps, int ops, int r, int r0, int rc, double* part, long long n, cudaStream_t s) {
   if (n_items <= 0 && n_items_bin <= 0) return cudaSuccess;
   if (d == 1 && taps == 8)
-    return launch_interp_d1_t8(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, u_sorted, perm, H, ops,
+    return launch_interp_d1_t8(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
                                    r, r0, rc, part, n, s);
   if (d == 1 && taps == 12)
-    return launch_interp_d1_t12(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, u_sorted, perm, H, ops,
+    return launch_interp_d1_t12(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
                                    r, r0, rc, part, n, s);
   if (d == 1 && taps == 16)
-    return launch_interp_d1_t16(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, u_sorted, perm, H, ops,
+    return launch_interp_d1_t16(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
                                    r, r0, rc, part, n, s);
   if (d == 2 && taps == 8)
-    return launch_interp_d2_t8(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, u_sorted, perm, H, ops,
+    return launch_interp_d2_t8(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
                                    r, r0, rc, part, n, s);
   if (d == 2 && taps == 12)
-    return launch_interp_d2_t12(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, u_sorted, perm, H, ops,
+    return launch_interp_d2_t12(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
                                    r, r0, rc, part, n, s);
   if (d == 2 && taps == 16)
-    return launch_interp_d2_t16(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, u_sorted, perm, H, ops,
+    return launch_interp_d2_t16(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
                                    r, r0, rc, part, n, s);
   if (d == 3 && taps == 8)
-    return launch_interp_d3_t8(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, u_sorted, perm, H, ops,
+    return launch_interp_d3_t8(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
                                    r, r0, rc, part, n, s);
   if (d == 3 && taps == 12)
-    return launch_interp_d3_t12(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, u_sorted, perm, H, ops,
+    return launch_interp_d3_t12(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
                                    r, r0, rc, part, n, s);
   if (d == 3 && taps == 16)
-    return launch_interp_d3_t16(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, u_sorted, perm, H, ops,
+    return launch_interp_d3_t16(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
                                    r, r0, rc, part, n, s);
   return cudaErrorInvalidValue;
 }

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(256) k_interp_mma(const WinTable* __restrict__
     for (int kq = 0; kq < KQ; ++kq) w2[mt][kq] = has[mt] ? window_tap(poly, kq * 4 + (lane & 3), x[2]) : 0.0;
   }
   __syncwarp();
+  const bool wact = warp * 16 < it.count;  // warp-uniform: this warp holds at least one point
 
   double acc[MT][NT][2];
 #pragma unroll
@@ -108,23 +109,37 @@ __global__ void __launch_bounds__(256) k_interp_mma(const WinTable* __restrict__
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) wa[mt] = (D >= 3) ? window_tap(poly, o0, x0[mt]) : 1.0;
     const double* bbase = cur + (lane & 3) * LDH + (lane >> 2);
+    // rows in groups of G: first all A values of the group (a burst of DMULs), then its DMMAs (a
+    // burst with no scalar FP64 in between -- interleaving them stalls the DMMAs behind DMULs that
+    // other warps' DMMA streams starve).  Warps without points skip the MMAs.
+    constexpr int G = (T1 % 4 == 0) ? 4 : 1;
+    if (wact) {
 #pragma unroll 1
-    for (int o1 = 0; o1 < T1; ++o1) {
-      double w01[MT];
+      for (int g0 = 0; g0 < T1; g0 += G) {
+        double af[G][KQ][MT];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) w01[mt] = wa[mt] * w1s[warp * 16 + mt * 8 + (lane >> 2)][o1];
+        for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
-      for (int kq = 0; kq < KQ; ++kq) {
-        const double* bp = bbase + (o1 * TAPS + kq * 4) * LDH;
-        double b[NT], a[MT];
+          for (int mt = 0; mt < MT; ++mt) {
+            const double w01 = wa[mt] * w1s[warp * 16 + mt * 8 + (lane >> 2)][g0 + gg];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) b[nt] = bp[nt * 8];
+            for (int kq = 0; kq < KQ; ++kq) af[gg][kq][mt] = w01 * w2[mt][kq];
+          }
+        }
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) a[mt] = w01[mt] * w2[mt][kq];
+        for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
+          for (int kq = 0; kq < KQ; ++kq) {
+            const double* bp = bbase + ((g0 + gg) * TAPS + kq * 4) * LDH;
+            double b[NT];
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+            for (int nt = 0; nt < NT; ++nt) b[nt] = bp[nt * 8];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[gg][kq][mt], b[nt]);
+          }
+        }
       }
     }
     __syncthreads();  // buffer `cur` is re-filled two planes later
@@ -225,26 +240,45 @@ __global__ void __launch_bounds__(128) k_interp_bin(const WinTable* __restrict__
     if (has && o0 >= 0 && o0 < ((D >= 3) ? TAPS : 1)) {
       const double wa = (D >= 3) ? window_tap(poly, o0, x[0]) : 1.0;
       const double* base = cur + (s[1] * F2 + s[2]) * VP;
-      // sum-factorised over o2 with T1 * V independent accumulator chains (ILP for the FP64 pipe)
-      double t[T1][V];
+      if constexpr (T1 * V <= 32) {
+        // sum-factorised over o2 with T1 * V independent accumulator chains (ILP for the FP64 pipe)
+        double t[T1][V];
 #pragma unroll
-      for (int o1 = 0; o1 < T1; ++o1)
+        for (int o1 = 0; o1 < T1; ++o1)
 #pragma unroll
-        for (int v = 0; v < V; ++v) t[o1][v] = 0.0;
+          for (int v = 0; v < V; ++v) t[o1][v] = 0.0;
 #pragma unroll
-      for (int o2 = 0; o2 < TAPS; ++o2) {
+        for (int o2 = 0; o2 < TAPS; ++o2) {
+#pragma unroll
+          for (int o1 = 0; o1 < T1; ++o1) {
+            const double* hp = base + (o1 * F2 + o2) * VP;
+#pragma unroll
+            for (int v = 0; v < V; ++v) t[o1][v] = fma(w2[o2], hp[v], t[o1][v]);
+          }
+        }
 #pragma unroll
         for (int o1 = 0; o1 < T1; ++o1) {
-          const double* hp = base + (o1 * F2 + o2) * VP;
+          const double w01 = wa * w1[o1];
 #pragma unroll
-          for (int v = 0; v < V; ++v) t[o1][v] = fma(w2[o2], hp[v], t[o1][v]);
+          for (int v = 0; v < V; ++v) acc[v] = fma(w01, t[o1][v], acc[v]);
         }
-      }
+      } else {
+        // many values per node: V independent chains per row already
+#pragma unroll 2
+        for (int o1 = 0; o1 < T1; ++o1) {
+          const double* rowp = base + o1 * F2 * VP;
+          double t[V];
 #pragma unroll
-      for (int o1 = 0; o1 < T1; ++o1) {
-        const double w01 = wa * w1[o1];
+          for (int v = 0; v < V; ++v) t[v] = 0.0;
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[v] = fma(w01, t[o1][v], acc[v]);
+          for (int o2 = 0; o2 < TAPS; ++o2) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) t[v] = fma(w2[o2], rowp[o2 * VP + v], t[v]);
+          }
+          const double w01 = wa * w1[o1];
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[v] = fma(w01, t[v], acc[v]);
+        }
       }
     }
     __syncthreads();  // plane P consumed; plane P+1 staged
@@ -264,12 +298,12 @@ inline size_t interp_bin_smem(int V, int F1, int F2) {
 
 template <int D, int T>
 cudaError_t launch_interp_dt(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
-                             int n_items_bin, int Fb1, int Fb2, const double* u_sorted, const int* perm,
+                             int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                              const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                              cudaStream_t s) {
 #define AKM_CASE(O, R)                                                                                              \
   if (ops == O && rc == R) {                                                                                        \
-    if constexpr (O * R >= 8) {                                                                                     \
+    if (O * R >= 8 && !sparse) {                                                                                    \
       const size_t smem = interp_mma_smem(D, T, O, R);                                                              \
       static bool attr_set = false;                                                                                 \
       if (!attr_set) {                                                                                              \

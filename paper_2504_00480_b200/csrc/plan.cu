@@ -55,6 +55,7 @@ struct Group {  // windows sharing (d, F) -> one spread / interp launch
   int spread_begin = 0, spread_count = 0;  // slice of the concatenated spread work items
   int interp_begin = 0, interp_count = 0;
   int interp_bin_begin = 0, interp_bin_count = 0;
+  bool sparse = false;  // few points per occupied cell: interpolate per bin (scalar) rather than per cell
 };
 
 }  // namespace
@@ -395,6 +396,9 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     grp.interp_count = (int)gi.size();
     plan->items_spread.insert(plan->items_spread.end(), gs.begin(), gs.end());
     plan->items_interp.insert(plan->items_interp.end(), gi.begin(), gi.end());
+    // per-cell DMMA items pay a whole cell footprint per item: with few points per occupied cell
+    // the per-bin scalar kernel wins (c3: ~16 points per cell; c4/c5: hundreds)
+    grp.sparse = gi.size() > 0 && (double)(n * grp.wins.size()) / (double)gi.size() < 48.0;
     grp.interp_bin_begin = (int)plan->items_interp_bin.size();
     grp.interp_bin_count = (int)gib.size();
     plan->items_interp_bin.insert(plan->items_interp_bin.end(), gib.begin(), gib.end());
@@ -599,7 +603,7 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
     for (const Group& grp : plan->groups) {
       AKM_CK(launch_interp(dtab, plan->items_i.as<WorkItem>() + grp.interp_begin, grp.interp_count,
                            plan->items_ib.as<WorkItem>() + grp.interp_bin_begin, grp.interp_bin_count,
-                           grp.d >= 2 ? grp.F : 1, grp.F, plan->u_sorted.as<double>(), plan->perm.as<int>(),
+                           grp.d >= 2 ? grp.F : 1, grp.F, grp.sparse, plan->u_sorted.as<double>(), plan->perm.as<int>(),
                            plan->H.as<double>(), grp.d,
                            2 * plan->m, ops, r, r0, rc, plan->part.as<double>(), n, s));
       if (grp.interp_count > 0) {
