@@ -211,13 +211,16 @@ template <int MODE>
 static cudaError_t launch_pass(const WinTable& tab, const WinTable* dtab, const void* X, void* Y, const double2* tw,
                                const double* D, int dslot0, int r, int ops, cudaStream_t s) {
   long long cols = 1, total = 0;
-  int Lmax = 1;
+  int Lmax = 1, Kmax = 1;
   for (int w = 0; w < tab.P; ++w) {
     const DftShape sh = dft_shape(tab.w[w], MODE, r, ops);
     cols = std::max(cols, sh.O * sh.I);
     total += sh.O * sh.I;
     Lmax = std::max(Lmax, sh.L);
+    Kmax = std::max(Kmax, sh.K);
   }
+  if (Kmax <= 2)  // singleton axis (d < 3): a copy / scaling, every thread its own column
+    return launch_cols<MODE, 128>((cols + 127) / 128, tab.P, Lmax, dtab, X, Y, tw, D, dslot0, r, ops, s);
   if (total >= 148LL * 4 * 32)
     return launch_cols<MODE, 32>((cols + 31) / 32, tab.P, Lmax, dtab, X, Y, tw, D, dslot0, r, ops, s);
   return launch_cols<MODE, 8>((cols + 7) / 8, tab.P, Lmax, dtab, X, Y, tw, D, dslot0, r, ops, s);

@@ -28,7 +28,11 @@
 
 namespace akm {
 
-constexpr int kSpreadPB = 64;        // points per batch (16 MMA k-steps)
+// points per batch: 64 (16 MMA k-steps) for large register tiles; 32 for small tiles (MB*NB <= 12,
+// the small-RHS footprints), whose CTAs are then capped at 128 registers and half the shared
+// memory so that two CTAs share an SM and one's staging overlaps the other's DMMAs
+__host__ __device__ constexpr int spread_pb(int mb, int nb) { return mb * nb <= 12 ? 32 : 64; }
+__host__ __device__ constexpr int spread_minb(int mb, int nb) { return mb * nb <= 12 ? 2 : 1; }
 constexpr int kSpreadWarps = 8;      // two per SM sub-partition
 constexpr int kSpreadThreads = 32 * kSpreadWarps;
 constexpr int kRing = 4;             // cp.async ring depth (batches)
@@ -48,7 +52,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __host__ __device__ constexpr int spread_ldf(int f) { return (f + 2) & ~1; }  // weight row: even, > f
 
 template <int MB, int NB>
-__global__ void __launch_bounds__(kSpreadThreads, 1) k_spread_mma(const WinTable* __restrict__ tabp,
+__global__ void __launch_bounds__(kSpreadThreads, spread_minb(MB, NB)) k_spread_mma(const WinTable* __restrict__ tabp,
                                                                   const WorkItem* __restrict__ items,
                                                                   const double* __restrict__ u_sorted,
                                                                   const int* __restrict__ perm,
@@ -56,7 +60,7 @@ __global__ void __launch_bounds__(kSpreadThreads, 1) k_spread_mma(const WinTable
                                                                   long long n, int r0, int rc, int r_total,
                                                                   double* __restrict__ grid, int WN,
                                                                   const __grid_constant__ PolyParam pp) {
-  constexpr int PB = kSpreadPB;
+  constexpr int PB = spread_pb(MB, NB);
   constexpr int NT = kSpreadThreads;
   const WinTable& tab = *tabp;
   const WorkItem it = items[blockIdx.x];
@@ -259,13 +263,12 @@ __global__ void __launch_bounds__(kSpreadThreads, 1) k_spread_mma(const WinTable
 // (MB, NB) register tiles of the 8 warps (WM x WN = 8); an 8x8 f64 accumulator tile costs 4
 // registers per thread, MB x NB <= 45 keeps a thread under the 255-register cap
 #define AKM_MMA_TILES(X)                                                                                      \
-  X(9, 5) X(5, 9) X(9, 4) X(4, 9) X(6, 6) X(9, 3) X(3, 9) X(6, 3) X(3, 6) X(3, 7) X(7, 3) X(12, 2) X(2, 12)  \
+  X(9, 5) X(5, 9) X(9, 4) X(4, 9) X(6, 6) X(9, 3) X(3, 9) X(6, 3) X(3, 6) X(3, 7) X(7, 3) X(12, 2) X(2, 12) X(3, 4)  \
   X(6, 2) X(2, 6) X(4, 4) X(3, 3) X(4, 2) X(2, 4) X(3, 2) X(2, 3) X(2, 2) X(1, 6) X(1, 3) X(1, 2)
 
-static size_t spread_smem_for(int lda, int ldb, int Fmax, int rc) {
-  return sizeof(double) * ((size_t)kSpreadPB * (lda + ldb) + 3 * (size_t)kSpreadPB * spread_ldf(Fmax) +
-                           (size_t)kRing * kSpreadPB * (rc + 3)) +
-         sizeof(int) * (size_t)kRing * kSpreadPB;
+static size_t spread_smem_for(int lda, int ldb, int Fmax, int rc, int PB) {
+  return sizeof(double) * ((size_t)PB * (lda + ldb) + 3 * (size_t)PB * spread_ldf(Fmax) + (size_t)kRing * PB * (rc + 3)) +
+         sizeof(int) * (size_t)kRing * PB;
 }
 
 bool spread_mma_choose(int M, int Nn, int Fmax, int rc, int& MB, int& NB, int& WM, int& WN) {
@@ -283,7 +286,7 @@ bool spread_mma_choose(int M, int Nn, int Fmax, int rc, int& MB, int& NB, int& W
       const int wn = kSpreadWarps / wm;
       if (wm * mb < TMt || wn * nb < TNt) continue;
       // panels (and the worst-case scratch) must fit the 227 KB of a CTA
-      if (spread_smem_for(mma_ld(wm * mb * 8), mma_ld(wn * nb * 8), Fmax, rc) > 224 * 1024) continue;
+      if (spread_smem_for(mma_ld(wm * mb * 8), mma_ld(wn * nb * 8), Fmax, rc, spread_pb(mb, nb)) > 224 * 1024) continue;
       // time ~ DMMA slots per sub-partition (incl. padding tiles) + fragment loads per k-step
       const double slots = (double)mb * nb;
       const double score = slots * (1.0 + 0.25 * (double)(mb + nb) / (mb * nb));
@@ -303,7 +306,7 @@ bool spread_mma_choose(int M, int Nn, int Fmax, int rc, int& MB, int& NB, int& W
 size_t spread_mma_smem(int /*PB*/, int M, int Nn, int Fmax, int rc) {
   int MB, NB, WM, WN;
   if (!spread_mma_choose(M, Nn, Fmax, rc, MB, NB, WM, WN)) return 0;
-  return spread_smem_for(mma_ld(WM * MB * 8), mma_ld(WN * NB * 8), Fmax, rc);
+  return spread_smem_for(mma_ld(WM * MB * 8), mma_ld(WN * NB * 8), Fmax, rc, spread_pb(MB, NB));
 }
 
 cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,

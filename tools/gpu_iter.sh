@@ -15,10 +15,11 @@ print('$c', '%.4f ms'%d['ms_per_step'], '%.3e pts/s'%d['value'], {k:round(v,4) f
 PY
 done
 if [ "${NCU_C4:-0}" = 1 ]; then
-  timeout 300 python tools/prof_run.py --config c4 --calls 2 > gpurun_out/plain_c4.log 2>&1 && \
+  NC=${NCU_CFG:-c4}
+  timeout 300 python tools/prof_run.py --config $NC --calls 2 > gpurun_out/plain_$NC.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${NCU_K:-k_spread|k_interp}" -s ${NCU_S:-2} -c ${NCU_N:-2} \
-      -o gpurun_out/prof_c4 -f python tools/prof_run.py --config c4 --calls 2 > gpurun_out/ncu_c4.log 2>&1
-  tail -2 gpurun_out/ncu_c4.log
+      -o gpurun_out/prof_$NC -f python tools/prof_run.py --config $NC --calls 2 > gpurun_out/ncu_$NC.log 2>&1
+  tail -2 gpurun_out/ncu_$NC.log
 fi
 if [ "${NCU_C2:-0}" = 1 ]; then
   timeout 300 python tools/prof_run.py --config c2 --calls 3 > gpurun_out/plain_c2.log 2>&1 && \
