@@ -327,6 +327,10 @@ def main():
     if stages["interp_launches"]:
         cand.append(("interp", stages["interp_ms"], stages["interp_launches"], interp_fl))
     name, st_ms, launches, flops = max(cand, key=lambda c: c[1])
+    try:   # DRAM traffic of that kernel per launch, from the round's committed ncu capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bytes_per_launch"][wl.name][name]
+    except Exception:
+        traffic = None
     per_launch_ms = st_ms / launches
     flops_per_launch = flops * products_per_step / (launches / K)
     achieved = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
@@ -343,7 +347,7 @@ def main():
                 "d2h_bytes_per_step": int(8 * (10 + 2 * wl.r) if objective else V.nbytes * len(wl.ops))},
         "gpu_launches": int(launches_timed),
         "roofline": {"bound": "alu", "kernel": name, "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS, "traffic": traffic,
                      "peak_note": "FP64 FMA: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz; measured DFMA 34.1 / DMMA 37.1 "
                                   "TFLOP/s (profiles/r01_fp64_peaks.txt)",
                      "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": per_launch_ms},
