@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(128) k_interp_bin(const WinTable* __restrict__
                                                     const WorkItem* __restrict__ items,
                                                     const double* __restrict__ u_sorted, const int* __restrict__ perm,
                                                     const double* __restrict__ H, int r, int r0,
-                                                    double* __restrict__ part, long long n) {
+                                                    double* __restrict__ part, long long n, int whole) {
   constexpr int V = OPS * RC;
   constexpr int VP = (V + 1) & ~1;
   constexpr int T1 = (D >= 2) ? TAPS : 1;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(128) k_interp_bin(const WinTable* __restrict__
   const int F0 = g.F[0], F1 = g.F[1], F2 = g.F[2], B = g.B;
   const int plane = F1 * F2;
   __shared__ double poly[TAPS * kPolyLen];
-  extern __shared__ double sm[];  // [2][F1*F2][VP]
+  extern __shared__ double sm[];  // whole ? [F0][F1*F2][VP] : [2][F1*F2][VP]
   const int tid = threadIdx.x;
   for (int idx = tid; idx < TAPS * kPolyLen; idx += blockDim.x) poly[idx] = tab.poly[idx];
 
@@ -204,11 +204,15 @@ __global__ void __launch_bounds__(128) k_interp_bin(const WinTable* __restrict__
       const int op = v / RC, c = v - op * RC;
       const int q1 = t / F2, q2 = t - q1 * F2;
       const long long tap = tap0 + ((long long)P * g.L[1] + q1) * g.L[2] + q2;
-      buf[t * VP + v] = H[tap * row_vals + op * r + r0 + c];
+      cp_async8(buf + t * VP + v, H + tap * row_vals + op * r + r0 + c);
     }
+    cp_async_commit();
   };
-  stage(0, sm);
-  __syncthreads();  // poly, plane 0
+  // the whole bin footprint when it fits (one barrier), else planes double-buffered
+  const int nstage = whole ? F0 : 1;
+  for (int P = 0; P < nstage; ++P) stage(P, sm + P * plane * VP);
+  cp_async_wait<0>();
+  __syncthreads();  // poly, staged planes
 
   const bool has = tid < it.count;
   const long long pidx = (long long)it.start + (has ? tid : 0);
@@ -234,8 +238,8 @@ __global__ void __launch_bounds__(128) k_interp_bin(const WinTable* __restrict__
   for (int v = 0; v < V; ++v) acc[v] = 0.0;
 
   for (int P = 0; P < F0; ++P) {
-    double* cur = sm + (P & 1) * plane * VP;
-    if (P + 1 < F0) stage(P + 1, sm + ((P + 1) & 1) * plane * VP);
+    double* cur = whole ? sm + P * plane * VP : sm + (P & 1) * plane * VP;
+    if (!whole && P + 1 < F0) stage(P + 1, sm + ((P + 1) & 1) * plane * VP);
     const int o0 = P - s[0];
     if (has && o0 >= 0 && o0 < ((D >= 3) ? TAPS : 1)) {
       const double wa = (D >= 3) ? window_tap(poly, o0, x[0]) : 1.0;
@@ -281,7 +285,10 @@ __global__ void __launch_bounds__(128) k_interp_bin(const WinTable* __restrict__
         }
       }
     }
-    __syncthreads();  // plane P consumed; plane P+1 staged
+    if (!whole) {
+      cp_async_wait<0>();
+      __syncthreads();  // plane P consumed; plane P+1 staged
+    }
   }
   if (!has) return;
   const long long i = perm[(long long)it.win * n + pidx];
@@ -292,8 +299,10 @@ __global__ void __launch_bounds__(128) k_interp_bin(const WinTable* __restrict__
     for (int c = 0; c < RC; ++c) out[(long long)q * r + c] = acc[q * RC + c];
 }
 
-inline size_t interp_bin_smem(int V, int F1, int F2) {
-  return 2 * (size_t)F1 * F2 * ((V + 1) & ~1) * sizeof(double);
+inline size_t interp_bin_smem(int V, int F0, int F1, int F2, int& whole) {
+  const size_t planeb = (size_t)F1 * F2 * ((V + 1) & ~1) * sizeof(double);
+  whole = (size_t)F0 * planeb <= 96 * 1024;
+  return whole ? F0 * planeb : 2 * planeb;
 }
 
 template <int D, int T>
@@ -315,7 +324,8 @@ cudaError_t launch_interp_dt(const WinTable* dtab, const WorkItem* items, int n_
       k_interp_mma<D, T, O, R><<<n_items, 256, smem, s>>>(dtab, items, u_sorted, perm, H, r, r0, part, n);         \
     } else {                                                                                                        \
       if (n_items_bin <= 0) return cudaSuccess;                                                                     \
-      const size_t smem = interp_bin_smem(O * R, Fb1, Fb2);                                                         \
+      int whole = 0;                                                                                                \
+      const size_t smem = interp_bin_smem(O * R, D >= 3 ? Fb2 : 1, Fb1, Fb2, whole);                                \
       static bool attr_set = false;                                                                                 \
       if (!attr_set) {                                                                                              \
         cudaError_t e = cudaFuncSetAttribute(k_interp_bin<D, T, O, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -323,7 +333,8 @@ cudaError_t launch_interp_dt(const WinTable* dtab, const WorkItem* items, int n_
         if (e != cudaSuccess) return e;                                                                             \
         attr_set = true;                                                                                            \
       }                                                                                                             \
-      k_interp_bin<D, T, O, R><<<n_items_bin, 128, smem, s>>>(dtab, items_bin, u_sorted, perm, H, r, r0, part, n); \
+      k_interp_bin<D, T, O, R><<<n_items_bin, 128, smem, s>>>(dtab, items_bin, u_sorted, perm, H, r, r0, part, n,  \
+                                                              whole);                                               \
     }                                                                                                               \
     return cudaGetLastError();                                                                                      \
   }
