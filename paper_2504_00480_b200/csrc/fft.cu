@@ -190,6 +190,204 @@ __global__ void __launch_bounds__(kDftThreads) k_dft_axis(const WinTable* __rest
 }
 
 // host: grid for one pass = max over windows of the column tiles; smem = max L
+
+// ---------------------------------------------------------------- fused plane kernels
+// When a (window, l0) plane of the box fits in shared memory (the 3-D configurations), FA+FB and
+// FD+FE run as one kernel per plane with 1024 threads (the intermediate A1 / C2 never leaves
+// shared memory; one or a few outputs per thread) and FC1+FC2 as one kernel per column tile:
+// three launches instead of six for the latency-bound small problems.
+constexpr int kFuseThreads = 1024;
+
+// FA + FB for plane (window blockIdx.y, l0 = blockIdx.x): G[l0] (L1 x L2 x r, real) -> A2[l0]
+__global__ void __launch_bounds__(kFuseThreads) k_plane_fwd(const WinTable* __restrict__ tabp,
+                                                            const double* __restrict__ G, double2* __restrict__ A2,
+                                                            const double2* __restrict__ tw, int r) {
+  const WinGeom& g = tabp->w[blockIdx.y];
+  const int l0 = blockIdx.x;
+  if (l0 >= g.L[0]) return;
+  const int L1 = g.L[1], L2 = g.L[2], K1 = g.K[1], K2 = g.K[2];
+  extern __shared__ double sm_[];
+  double* gs = sm_;                                                           // [L1][L2][r]
+  double2* a1 = reinterpret_cast<double2*>(gs + ((L1 * L2 * r + 1) & ~1));    // [L1][K2][r]
+  double2* T2 = a1 + L1 * K2 * r;                                             // [K2][L2]
+  double2* T1 = T2 + K2 * L2;                                                 // [K1][L1]
+  const double* src = G + (g.tap_off + (long long)l0 * L1 * L2) * r;
+  for (int idx = threadIdx.x; idx < L1 * L2 * r; idx += blockDim.x) gs[idx] = src[idx];
+  for (int idx = threadIdx.x; idx < K2 * L2; idx += blockDim.x) T2[idx] = tw[g.tw_off[2] + idx];
+  for (int idx = threadIdx.x; idx < K1 * L1; idx += blockDim.x) T1[idx] = tw[g.tw_off[1] + idx];
+  __syncthreads();
+  const int KR = K2 * r;
+  for (int idx = threadIdx.x; idx < L1 * KR; idx += blockDim.x) {  // (l1, k2, c)
+    const int l1 = idx / KR, rem = idx - l1 * KR, k2 = rem / r, c = rem - k2 * r;
+    const double* x = gs + (l1 * L2) * r + c;
+    const double2* t = T2 + (long long)k2 * L2;
+    double re[2] = {0.0, 0.0}, im[2] = {0.0, 0.0};
+    int l = 0;
+    for (; l + 2 <= L2; l += 2) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double v = x[(l + q) * r];
+        re[q] = fma(t[l + q].x, v, re[q]);
+        im[q] = fma(t[l + q].y, v, im[q]);
+      }
+    }
+    if (l < L2) {
+      const double v = x[l * r];
+      re[0] = fma(t[l].x, v, re[0]);
+      im[0] = fma(t[l].y, v, im[0]);
+    }
+    a1[idx] = make_double2(re[0] + re[1], im[0] + im[1]);
+  }
+  __syncthreads();
+  double2* dst = A2 + g.a2_off * r + (long long)l0 * K1 * KR;  // A2[l0][k1][k2][c]
+  for (int idx = threadIdx.x; idx < K1 * KR; idx += blockDim.x) {  // (k1, (k2, c))
+    const int k1 = idx / KR, j = idx - k1 * KR;
+    const double2* t = T1 + (long long)k1 * L1;
+    double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    int l = 0;
+    for (; l + 2 <= L1; l += 2) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double2 v = a1[(l + q) * KR + j], tt = t[l + q];
+        acc[q].x = fma(tt.x, v.x, fma(-tt.y, v.y, acc[q].x));
+        acc[q].y = fma(tt.x, v.y, fma(tt.y, v.x, acc[q].y));
+      }
+    }
+    if (l < L1) {
+      const double2 v = a1[l * KR + j], tt = t[l];
+      acc[0].x = fma(tt.x, v.x, fma(-tt.y, v.y, acc[0].x));
+      acc[0].y = fma(tt.x, v.y, fma(tt.y, v.x, acc[0].y));
+    }
+    dst[idx] = make_double2(acc[0].x + acc[1].x, acc[0].y + acc[1].y);
+  }
+}
+
+// FD + FE for plane (window blockIdx.y, (op, l0) = blockIdx.x): C[op][l0] (K1 x K2 x r) -> H
+__global__ void __launch_bounds__(kFuseThreads) k_plane_inv(const WinTable* __restrict__ tabp,
+                                                            const double2* __restrict__ C, double* __restrict__ H,
+                                                            const double2* __restrict__ tw, int r, int ops) {
+  const WinGeom& g = tabp->w[blockIdx.y];
+  const int L0 = g.L[0];
+  if ((int)blockIdx.x >= ops * L0) return;
+  const int op = blockIdx.x / L0, l0 = blockIdx.x - op * L0;
+  const int L1 = g.L[1], L2 = g.L[2], K1 = g.K[1], K2 = g.K[2];
+  const int KR = K2 * r;
+  extern __shared__ double2 smc[];
+  double2* cs = smc;                 // [K1][K2][r]
+  double2* c2 = smc + K1 * KR;       // [L1][K2][r]
+  double2* T1 = c2 + L1 * KR;        // [K1][L1]
+  double2* T2 = T1 + K1 * L1;        // [K2][L2]
+  const double2* src = C + g.c_off * r + ((long long)op * L0 + l0) * K1 * KR;
+  for (int idx = threadIdx.x; idx < K1 * KR; idx += blockDim.x) cs[idx] = src[idx];
+  for (int idx = threadIdx.x; idx < K1 * L1; idx += blockDim.x) T1[idx] = tw[g.tw_off[1] + idx];
+  for (int idx = threadIdx.x; idx < K2 * L2; idx += blockDim.x) T2[idx] = tw[g.tw_off[2] + idx];
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < L1 * KR; idx += blockDim.x) {  // (l1, (k2, c)): sum_k1 conj(T1[k1][l1]) C[k1]
+    const int l1 = idx / KR, j = idx - l1 * KR;
+    double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    int k = 0;
+    for (; k + 2 <= K1; k += 2) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double2 v = cs[(k + q) * KR + j], t = T1[(long long)(k + q) * L1 + l1];
+        acc[q].x = fma(t.x, v.x, fma(t.y, v.y, acc[q].x));
+        acc[q].y = fma(t.x, v.y, fma(-t.y, v.x, acc[q].y));
+      }
+    }
+    if (k < K1) {
+      const double2 v = cs[k * KR + j], t = T1[(long long)k * L1 + l1];
+      acc[0].x = fma(t.x, v.x, fma(t.y, v.y, acc[0].x));
+      acc[0].y = fma(t.x, v.y, fma(-t.y, v.x, acc[0].y));
+    }
+    c2[idx] = make_double2(acc[0].x + acc[1].x, acc[0].y + acc[1].y);
+  }
+  __syncthreads();
+  // H[((l0 L1 + l1) L2 + l2) ops + op][c] = Re sum_k2 alpha conj(T2[k2][l2]) C2[l1][k2][c]
+  const long long hbase = g.tap_off * (long long)ops * r;
+  const int LR = L2 * r;
+  for (int idx = threadIdx.x; idx < L1 * LR; idx += blockDim.x) {
+    const int l1 = idx / LR, rem = idx - l1 * LR, l2 = rem / r, c = rem - l2 * r;
+    const double2* x = c2 + l1 * KR + c;
+    double acc[2] = {0.0, 0.0};
+    for (int k = 0; k < K2; ++k) {
+      const double2 t = T2[(long long)k * L2 + l2], v = x[k * r];
+      const double w = (k == 0) ? 1.0 : 2.0;
+      acc[k & 1] = fma(w, fma(t.x, v.x, t.y * v.y), acc[k & 1]);
+    }
+    const long long tap = ((long long)l0 * L1 + l1) * L2 + l2;
+    H[hbase + (tap * ops + op) * r + c] = acc[0] + acc[1];
+  }
+}
+
+// FC1 + FC2 for a tile of columns (k1, k2, c): A2[l0][col] -> A3 (smem) -> C[op][l0][col]
+template <int COLS>
+__global__ void __launch_bounds__(kDftThreads) k_pencil(const WinTable* __restrict__ tabp, const double2* __restrict__ A2,
+                                                        double2* __restrict__ C, const double2* __restrict__ tw,
+                                                        const double* __restrict__ D, int dslot0, int r, int ops) {
+  const WinGeom& g = tabp->w[blockIdx.y];
+  const int L0 = g.L[0], K0 = g.K[0];
+  const long long I = (long long)g.K[1] * g.K[2] * r;
+  const long long col0 = (long long)blockIdx.x * COLS;
+  if (col0 >= I) return;
+  extern __shared__ double2 smp[];
+  double2* xs = smp;                     // [L0][COLS]
+  double2* a3 = smp + L0 * COLS;         // [ops][K0][COLS]  D_op * A3
+  double2* T0 = a3 + ops * K0 * COLS;    // [K0][L0]
+  const int tid = threadIdx.x;
+  const double2* src = A2 + g.a2_off * r;
+  for (int idx = tid; idx < L0 * COLS; idx += kDftThreads) {
+    const int l = idx / COLS, j = idx - l * COLS;
+    xs[idx] = (col0 + j < I) ? src[(long long)l * I + col0 + j] : make_double2(0.0, 0.0);
+  }
+  for (int idx = tid; idx < K0 * L0; idx += kDftThreads) T0[idx] = tw[g.tw_off[0] + idx];
+  __syncthreads();
+  const long long kk = (long long)g.K[1] * g.K[2], dper = (long long)K0 * kk;
+  for (int idx = tid; idx < K0 * COLS; idx += kDftThreads) {  // forward along l0, then D_op
+    const int k = idx / COLS, j = idx - k * COLS;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int l = 0; l < L0; ++l) {
+      const double2 t = T0[k * L0 + l], v = xs[l * COLS + j];
+      acc.x = fma(t.x, v.x, fma(-t.y, v.y, acc.x));
+      acc.y = fma(t.x, v.y, fma(t.y, v.x, acc.y));
+    }
+    const long long col = col0 + j;
+    for (int op = 0; op < ops; ++op) {
+      const double dd = (col < I) ? D[g.d_off + (dslot0 + op) * dper + (long long)k * kk + col / r] : 0.0;
+      a3[(op * K0 + k) * COLS + j] = make_double2(dd * acc.x, dd * acc.y);
+    }
+  }
+  __syncthreads();
+  double2* dst = C + g.c_off * r;
+  for (int idx = tid; idx < ops * L0 * COLS; idx += kDftThreads) {  // inverse along k0
+    const int j = idx % COLS, ol = idx / COLS, op = ol / L0, l = ol - op * L0;
+    const long long col = col0 + j;
+    if (col >= I) continue;
+    const double2* av = a3 + op * K0 * COLS + j;
+    double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    for (int k = 0; k < K0; ++k) {
+      const double2 t = T0[k * L0 + l], v = av[k * COLS];
+      acc[k & 1].x = fma(t.x, v.x, fma(t.y, v.y, acc[k & 1].x));
+      acc[k & 1].y = fma(t.x, v.y, fma(-t.y, v.x, acc[k & 1].y));
+    }
+    dst[((long long)op * L0 + l) * I + col] = make_double2(acc[0].x + acc[1].x, acc[0].y + acc[1].y);
+  }
+}
+
+static bool planes_fit(const WinTable& tab, int r, size_t& smem_fwd, size_t& smem_inv) {
+  smem_fwd = smem_inv = 0;
+  for (int w = 0; w < tab.P; ++w) {
+    const WinGeom& g = tab.w[w];
+    if (g.d < 3) return false;  // 2-D boxes are single large planes: the generic passes
+    const size_t tws = sizeof(double2) * ((size_t)g.K[1] * g.L[1] + (size_t)g.K[2] * g.L[2]);
+    const size_t fwd = sizeof(double) * (((size_t)g.L[1] * g.L[2] * r + 1) & ~(size_t)1) +
+                       sizeof(double2) * (size_t)g.L[1] * g.K[2] * r + tws;
+    const size_t inv = sizeof(double2) * ((size_t)g.K[1] + g.L[1]) * g.K[2] * r + tws;
+    smem_fwd = std::max(smem_fwd, fwd);
+    smem_inv = std::max(smem_inv, inv);
+  }
+  return smem_fwd <= 200 * 1024 && smem_inv <= 200 * 1024;
+}
+
 template <int MODE, int COLS>
 static cudaError_t launch_cols(long long tiles, int P, int Lmax, const WinTable* dtab, const void* X, void* Y,
                                const double2* tw, const double* D, int dslot0, int r, int ops, cudaStream_t s) {
@@ -228,6 +426,19 @@ static cudaError_t launch_pass(const WinTable& tab, const WinTable* dtab, const 
 
 cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1, double2* A2,
                                const double2* tw, int r, long long /*maxA1*/, long long /*maxA2*/, cudaStream_t s) {
+  size_t sf, si;
+  if (planes_fit(tab, r, sf, si)) {
+    int L0 = 1;
+    for (int w = 0; w < tab.P; ++w) L0 = std::max(L0, tab.w[w].L[0]);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_plane_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    k_plane_fwd<<<dim3(L0, tab.P), kFuseThreads, sf, s>>>(dtab, grid, A2, tw, r);
+    return cudaGetLastError();
+  }
   cudaError_t e = launch_pass<kFA>(tab, dtab, grid, A1, tw, nullptr, 0, r, 1, s);
   if (e != cudaSuccess) return e;
   return launch_pass<kFB>(tab, dtab, A1, A2, tw, nullptr, 0, r, 1, s);
@@ -237,6 +448,30 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
                                         double2* C, double2* C2, const double2* tw, const double* D, int ops,
                                         int dslot0, int r, double* H, long long /*maxA3*/, long long /*maxC*/,
                                         long long /*maxC2*/, long long /*maxTap*/, cudaStream_t s) {
+  size_t sf, si;
+  if (planes_fit(tab, r, sf, si)) {
+    int L0 = 1, K0 = 1;
+    long long I = 1;
+    for (int w = 0; w < tab.P; ++w) {
+      L0 = std::max(L0, tab.w[w].L[0]);
+      K0 = std::max(K0, tab.w[w].K[0]);
+      I = std::max(I, (long long)tab.w[w].K[1] * tab.w[w].K[2] * r);
+    }
+    constexpr int PC = 8;
+    const size_t sp = sizeof(double2) * ((size_t)(L0 + ops * K0) * PC + (size_t)K0 * L0);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_plane_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(k_pencil<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    k_pencil<PC><<<dim3((unsigned)((I + PC - 1) / PC), tab.P), kDftThreads, sp, s>>>(dtab, A2, C, tw, D, dslot0, r,
+                                                                                    ops);
+    k_plane_inv<<<dim3(L0 * ops, tab.P), kFuseThreads, si, s>>>(dtab, C, H, tw, r, ops);
+    return cudaGetLastError();
+  }
   cudaError_t e = launch_pass<kFC1>(tab, dtab, A2, A3, tw, nullptr, 0, r, ops, s);
   if (e == cudaSuccess) e = launch_pass<kFC2>(tab, dtab, A3, C, tw, D, dslot0, r, ops, s);
   if (e == cudaSuccess) e = launch_pass<kFD>(tab, dtab, C, C2, tw, nullptr, 0, r, ops, s);
