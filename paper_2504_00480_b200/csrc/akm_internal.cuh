@@ -129,6 +129,23 @@ __device__ __forceinline__ void window_taps_estrin(const double* __restrict__ c,
   }
 }
 
+// Estrin evaluation of the K taps first, first + stride, ... (shared x powers)
+template <int K>
+__device__ __forceinline__ void window_taps_estrin_strided(const double* __restrict__ c, int first, int stride,
+                                                           double x, double* w) {
+  const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const double* k = c + (first + q * stride) * kPolyLen;
+    const double p0 = fma(k[1], x, k[0]), p1 = fma(k[3], x, k[2]), p2 = fma(k[5], x, k[4]);
+    const double p3 = fma(k[7], x, k[6]), p4 = fma(k[9], x, k[8]), p5 = fma(k[11], x, k[10]);
+    const double p6 = fma(k[13], x, k[12]), p7 = k[14];
+    const double q0 = fma(p1, x2, p0), q1 = fma(p3, x2, p2), q2 = fma(p5, x2, p4), q3 = fma(p7, x2, p6);
+    const double r0 = fma(q1, x4, q0), r1 = fma(q3, x4, q2);
+    w[q] = fma(r1, x8, r0);
+  }
+}
+
 __device__ __forceinline__ double window_tap(const double* __restrict__ c, int o, double x) {
   double v = c[o * kPolyLen + kPolyDeg];
 #pragma unroll

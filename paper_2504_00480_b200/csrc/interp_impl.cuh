@@ -26,7 +26,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int D, int TAPS, int OPS, int RC>
-__global__ void __launch_bounds__(256) k_interp_mma(const WinTable* __restrict__ tabp,
+__global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restrict__ tabp,
                                                     const WorkItem* __restrict__ items,
                                                     const double* __restrict__ u_sorted, const int* __restrict__ perm,
                                                     const double* __restrict__ H, int r, int r0,
@@ -63,9 +63,13 @@ __global__ void __launch_bounds__(256) k_interp_mma(const WinTable* __restrict__
   __syncthreads();  // poly
 
   __shared__ double w1s[8 * MT * 8][T1];  // [point of the CTA][o1]
+  __shared__ double w0s[8 * MT * 8][T0];  // [point of the CTA][o0]
   bool has[MT];
   long long pidx[MT];
-  double x0[MT], w2[MT][KQ];
+  double w2[MT][KQ];
+  // window weights by Estrin (independent chains: next to the other CTA's DMMA stream every
+  // dependent FP64 step costs ~135 clk).  The 4 lanes of a quad share a point: lane&3 takes the
+  // taps {lane&3, +4, +8, ...} of w2 and a quarter of the w0 / w1 taps for the shared tables.
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int q = warp * 16 + mt * 8 + (lane >> 2);
@@ -77,15 +81,26 @@ __global__ void __launch_bounds__(256) k_interp_mma(const WinTable* __restrict__
       const double u = u_sorted[((long long)it.win * 3 + a) * n + pidx[mt]];
       x[a] = 2.0 * (u - floor(u)) - 1.0;
     }
-    x0[mt] = x[0];
-    // the 4 lanes of a quad share a point: lane&3 evaluates taps {lane&3, +4, +8, ...}
+    // lane&3 evaluates the taps {lane&3, +4, +8, ...} of each axis (KQ = TAPS / 4 of them)
+    const int l4 = lane & 3;
+    double wt[KQ];
+    window_taps_estrin_strided<KQ>(poly, l4, 4, x[2], wt);
 #pragma unroll
-    for (int kq = 0; kq < (T1 + 3) / 4; ++kq) {
-      const int o = kq * 4 + (lane & 3);
-      if (o < T1) w1s[q][o] = (D >= 2) ? window_tap(poly, o, x[1]) : 1.0;
+    for (int kq = 0; kq < KQ; ++kq) w2[mt][kq] = has[mt] ? wt[kq] : 0.0;
+    if (D >= 2) {
+      window_taps_estrin_strided<KQ>(poly, l4, 4, x[1], wt);
+#pragma unroll
+      for (int kq = 0; kq < KQ; ++kq) w1s[q][l4 + 4 * kq] = wt[kq];
+    } else if (l4 == 0) {
+      w1s[q][0] = 1.0;
     }
+    if (D >= 3) {
+      window_taps_estrin_strided<KQ>(poly, l4, 4, x[0], wt);
 #pragma unroll
-    for (int kq = 0; kq < KQ; ++kq) w2[mt][kq] = has[mt] ? window_tap(poly, kq * 4 + (lane & 3), x[2]) : 0.0;
+      for (int kq = 0; kq < KQ; ++kq) w0s[q][l4 + 4 * kq] = wt[kq];
+    } else if (l4 == 0) {
+      w0s[q][0] = 1.0;
+    }
   }
   __syncwarp();
   const bool wact = warp * 16 < it.count;  // warp-uniform: this warp holds at least one point
@@ -107,7 +122,7 @@ __global__ void __launch_bounds__(256) k_interp_mma(const WinTable* __restrict__
     __syncthreads();
     double wa[MT];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) wa[mt] = (D >= 3) ? window_tap(poly, o0, x0[mt]) : 1.0;
+    for (int mt = 0; mt < MT; ++mt) wa[mt] = w0s[warp * 16 + mt * 8 + (lane >> 2)][o0];
     const double* bbase = cur + (lane & 3) * LDH + (lane >> 2);
     // rows in groups of G: first all A values of the group (a burst of DMULs), then its DMMAs (a
     // burst with no scalar FP64 in between -- interleaving them stalls the DMMAs behind DMULs that
