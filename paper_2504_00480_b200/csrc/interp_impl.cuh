@@ -49,13 +49,26 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
 
   const int cell0 = it.bin[0], cell1 = it.bin[1], cell2 = it.bin[2];
   const long long row_vals = (long long)OPS * r;
+  const bool contiguous = (RC == r && r0 == 0);  // all V values of a node adjacent in H
+  const long long L1g = g.L[1], L2g = g.L[2], toff = g.tap_off;
   auto stage = [&](int o0, double* buf) {
-    for (int idx = tid; idx < SLAB * V; idx += blockDim.x) {
-      const int t = idx / V, v = idx % V;
-      const int op = v / RC, c = v % RC;
-      const int o1 = t / TAPS, o2 = t % TAPS;
-      const long long tap = ((long long)(cell0 + o0) * g.L[1] + (cell1 + o1)) * g.L[2] + (cell2 + o2);
-      cp_async8(buf + t * LDH + v, H + (g.tap_off + tap) * row_vals + op * r + r0 + c);
+    if (contiguous) {
+      // each footprint row (o0, o1) is one run of TAPS * V consecutive doubles of H: source =
+      // plane base + idx + o1 * (row stride - TAPS * V), two divisions by constants per element
+      const double* base = H + (toff + ((long long)(cell0 + o0) * L1g + cell1) * L2g + cell2) * row_vals;
+      const long long delta = L2g * row_vals - TAPS * V;
+      for (int idx = tid; idx < SLAB * V; idx += blockDim.x) {
+        const int t = idx / V, v = idx - t * V, o1 = t / TAPS;
+        cp_async8(buf + t * LDH + v, base + idx + o1 * delta);
+      }
+    } else {
+      for (int idx = tid; idx < SLAB * V; idx += blockDim.x) {
+        const int t = idx / V, v = idx % V;
+        const int op = v / RC, c = v % RC;
+        const int o1 = t / TAPS, o2 = t % TAPS;
+        const long long tap = ((long long)(cell0 + o0) * L1g + (cell1 + o1)) * L2g + (cell2 + o2);
+        cp_async8(buf + t * LDH + v, H + (toff + tap) * row_vals + op * r + r0 + c);
+      }
     }
     cp_async_commit();
   };
