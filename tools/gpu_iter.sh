@@ -1,12 +1,12 @@
 #!/bin/bash
 # Iteration loop on the GPU box: parity tests, bench lines, optional ncu captures.
-#   TESTS="-k expr" CONFIGS="c2 c4" NCU_C4=1 NCU_C2=1 bash tools/gpu_iter.sh
+#   KEXPR="expr" CONFIGS="c2 c4" NCU_C4=1 NCU_C2=1 bash tools/gpu_iter.sh
 set -u
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo build failed; cat gpurun_out/build.log; exit 1; }
-timeout 1500 python -m pytest tests -m gpu -x -q ${TESTS:-} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 1500 python -m pytest tests -m gpu -x -q ${KEXPR:+-k "$KEXPR"} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
-for c in ${CONFIGS:-c1 c2 c3 c4}; do
+for c in ${CONFIGS-c1 c2 c3 c4}; do
   timeout 600 python bench.py --config $c --steps ${STEPS:-30} --warmup 5 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
   python - <<PY || tail -5 gpurun_out/bench_$c.err
 import json
