@@ -222,6 +222,7 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
                                         double* H, long long maxA3, long long maxC, long long maxC2,
                                         long long maxTap, cudaStream_t s);
 cudaError_t launch_zero(double* p, long long count, cudaStream_t s);
+int fft_launch_count(const WinTable& tab, int r);
 
 // krylov.cu (config-5 objective driver)
 size_t kr_state_bytes();

@@ -479,6 +479,12 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
   return e;
 }
 
+// kernels launched by launch_fft_forward + launch_fft_multiply_inverse (for the launch counters)
+int fft_launch_count(const WinTable& tab, int r) {
+  size_t sf, si;
+  return planes_fit(tab, r, sf, si) ? 3 : 6;
+}
+
 cudaError_t launch_zero(double* p, long long count, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   return cudaMemsetAsync(p, 0, sizeof(double) * count, s);

@@ -594,7 +594,7 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
                                      plan->C.as<double2>(), plan->C2.as<double2>(), plan->tw.as<double2>(),
                                      plan->D.as<double>(), ops, dslot0, r, plan->H.as<double>(), plan->maxA3,
                                      plan->maxC, plan->maxC2, plan->maxTap, s));
-  plan->launches += 6;
+  plan->launches += fft_launch_count(plan->tab, r);
   if (ev) AKM_CK(cudaEventRecord(ev->e[2], s));
   // S6: interpolation
   int r0 = 0;
