@@ -215,12 +215,10 @@ cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const W
 
 // fft.cu
 cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1,
-                               double2* A2, const double2* tw, int r, long long maxA1, long long maxA2,
-                               cudaStream_t s);
+                               double2* A2, const double2* tw, int r, cudaStream_t s);
 cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dtab, const double2* A2, double2* A3,
                                         double2* C, double2* C2, const double2* tw, const double* D, int ops, int dslot0, int r,
-                                        double* H, long long maxA3, long long maxC, long long maxC2,
-                                        long long maxTap, cudaStream_t s);
+                                        double* H, cudaStream_t s);
 cudaError_t launch_zero(double* p, long long count, cudaStream_t s);
 int fft_launch_count(const WinTable& tab, int r);
 
@@ -245,7 +243,6 @@ cudaError_t launch_kr_slq_quad(void* st, int R, const double* part_yx, int* err,
 void kr_summary_offsets(size_t* off_quad, size_t* off_samples, size_t* off_steps, size_t* off_hist, size_t* off_znorm);
 
 // interp.cu
-bool interp_supported(int d, int taps, int ops, int rc);
 int interp_rc_for(int r_remaining);
 cudaError_t launch_interp(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                           int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm, const double* H,

@@ -425,7 +425,7 @@ static cudaError_t launch_pass(const WinTable& tab, const WinTable* dtab, const 
 }
 
 cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1, double2* A2,
-                               const double2* tw, int r, long long /*maxA1*/, long long /*maxA2*/, cudaStream_t s) {
+                               const double2* tw, int r, cudaStream_t s) {
   size_t sf, si;
   if (planes_fit(tab, r, sf, si)) {
     int L0 = 1;
@@ -446,8 +446,7 @@ cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const 
 
 cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dtab, const double2* A2, double2* A3,
                                         double2* C, double2* C2, const double2* tw, const double* D, int ops,
-                                        int dslot0, int r, double* H, long long /*maxA3*/, long long /*maxC*/,
-                                        long long /*maxC2*/, long long /*maxTap*/, cudaStream_t s) {
+                                        int dslot0, int r, double* H, cudaStream_t s) {
   size_t sf, si;
   if (planes_fit(tab, r, sf, si)) {
     int L0 = 1, K0 = 1;

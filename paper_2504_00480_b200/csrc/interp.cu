@@ -42,11 +42,6 @@ cudaError_t launch_interp_d3_t16(const WinTable* dtab, const WorkItem* items, in
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
                               cudaStream_t s);
 
-bool interp_supported(int d, int taps, int ops, int rc) {
-  const bool dt = (d >= 1 && d <= 3) && (taps == 8 || taps == 12 || taps == 16);
-  const bool orc = (ops == 1 || ops == 2) && (rc == 1 || rc == 2 || rc == 4 || rc == 11);
-  return dt && orc;
-}
 
 // Largest instantiated RHS chunk not exceeding r_remaining.
 int interp_rc_for(int r_remaining) {

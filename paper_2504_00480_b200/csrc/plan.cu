@@ -84,7 +84,6 @@ struct akm_plan {
   std::vector<Group> groups;
   std::vector<long long> occupied, maxbin;
   long long total_taps = 0, szA1 = 0, szA2 = 0, szA3 = 0, szC = 0, szC2 = 0, szTW = 0, szD = 0;
-  long long maxA1 = 0, maxA2 = 0, maxA3 = 0, maxC = 0, maxC2 = 0, maxTap = 0;
 
   // device buffers
   DevBuf dtab, Xc, u_tmp, u_sorted, perm, hist, hist_off, err_flag, items_s, items_i, items_ib, minmax, r2;
@@ -406,7 +405,6 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
 
   // workspace layout (per RHS) for grids, spectra, twiddles and multipliers
   long long tap = 0, a1 = 0, a2 = 0, a3 = 0, cc = 0, c2 = 0, twc = 0, dd = 0;
-  plan->maxA1 = plan->maxA2 = plan->maxA3 = plan->maxC = plan->maxC2 = plan->maxTap = 0;
   for (int w = 0; w < P; ++w) {
     WinGeom& g = tab.w[w];
     g.ntap = (long long)g.L[0] * g.L[1] * g.L[2];
@@ -427,12 +425,6 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     }
     g.d_off = dd;
     dd += 2 * s3;
-    plan->maxA1 = std::max(plan->maxA1, s1);
-    plan->maxA2 = std::max(plan->maxA2, s2);
-    plan->maxA3 = std::max(plan->maxA3, s3);
-    plan->maxC = std::max(plan->maxC, s2);
-    plan->maxC2 = std::max(plan->maxC2, s1);
-    plan->maxTap = std::max(plan->maxTap, g.ntap);
   }
   plan->total_taps = tap;
   plan->szA1 = a1; plan->szA2 = a2; plan->szA3 = a3; plan->szC = cc; plan->szC2 = c2; plan->szTW = twc; plan->szD = dd;
@@ -589,11 +581,10 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
   if (ev) AKM_CK(cudaEventRecord(ev->e[1], s));
   // S3-S5: DFT, multiply, inverse DFT
   AKM_CK(launch_fft_forward(plan->tab, dtab, plan->grid.as<double>(), plan->A1.as<double2>(), plan->A2.as<double2>(),
-                            plan->tw.as<double2>(), r, plan->maxA1, plan->maxA2, s));
+                            plan->tw.as<double2>(), r, s));
   AKM_CK(launch_fft_multiply_inverse(plan->tab, dtab, plan->A2.as<double2>(), plan->A3.as<double2>(),
                                      plan->C.as<double2>(), plan->C2.as<double2>(), plan->tw.as<double2>(),
-                                     plan->D.as<double>(), ops, dslot0, r, plan->H.as<double>(), plan->maxA3,
-                                     plan->maxC, plan->maxC2, plan->maxTap, s));
+                                     plan->D.as<double>(), ops, dslot0, r, plan->H.as<double>(), s));
   plan->launches += fft_launch_count(plan->tab, r);
   if (ev) AKM_CK(cudaEventRecord(ev->e[2], s));
   // S6: interpolation
