@@ -212,6 +212,13 @@ cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const W
                               int r_total, double* grid, int MB, int NB, int WM, int WN, int PB, size_t smem,
                               cudaStream_t s);
 
+// spread_v5.cu (one warp per SM sub-partition, fragments formed on the fly)
+bool spread_v5_choose(int M, int Nn, int& MB, int& NB, int& WN);
+size_t spread_v5_smem(int Fmax, int rc, int MB, int NB, int WN);
+cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
+                             const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
+                             int r0, int rc, int r_total, double* grid, int MB, int NB, int WN, size_t smem,
+                             cudaStream_t s);
 
 // fft.cu
 cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1,

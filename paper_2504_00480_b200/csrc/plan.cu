@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -558,6 +559,25 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
     int M = 1;
     for (int t = 0; t < d - 1; ++t) M *= F;
     int r0 = 0;
+    // one-warp-per-SMSP kernel (spread_v5.cu) for 3-D windows with enough work items to fill the
+    // GPU at one CTA per SM; AKM_SPREAD_V5=0/1 forces either kernel (A/B measurement)
+    static const int v5_env = getenv("AKM_SPREAD_V5") ? atoi(getenv("AKM_SPREAD_V5")) : -1;
+    const bool v5 = v5_env >= 0 ? v5_env != 0 : (d == 3 && grp.spread_count >= 2 * 148);
+    while (v5 && r0 < r) {
+      int rc = std::min(12, r - r0), MB = 0, NB = 0, WN = 0;
+      while (rc > 1 && !(spread_v5_choose(M, F * rc, MB, NB, WN) && spread_v5_smem(F, rc, MB, NB, WN) <= 220 * 1024)) --rc;
+      if (rc < r - r0 && rc > (r - r0 + 1) / 2) rc = (r - r0 + 1) / 2;
+      if (!spread_v5_choose(M, F * rc, MB, NB, WN))
+        return plan->fail(AKM_ERR_UNSUPPORTED, "no spread tile for footprint %d x %d", M, F * rc);
+      AKM_CK(launch_spread_v5(dtab, plan->poly_param, plan->items_s.as<WorkItem>() + grp.spread_begin,
+                              grp.spread_count, plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc,
+                              r, plan->grid.as<double>(), MB, NB, WN, spread_v5_smem(F, rc, MB, NB, WN), s));
+      if (grp.spread_count > 0) {
+        ++plan->launches;
+        ++plan->spread_launches;
+      }
+      r0 += rc;
+    }
     while (r0 < r) {
       // largest RHS chunk (<= 12) whose footprint accumulator fits the 8 warps' DMMA tiles and whose
       // panels fit shared memory; split the rest evenly
