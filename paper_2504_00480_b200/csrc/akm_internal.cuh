@@ -220,6 +220,12 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
                              int r0, int rc, int r_total, double* grid, int MB, int NB, int WN, size_t smem,
                              cudaStream_t s);
 
+// interp_t.cu (3-D windows, many values per node: GEMM over (o0, o1) with N = (o2, v))
+bool interp_t_supported(int d, int taps, int ops, int rc);
+cudaError_t launch_interp_t(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
+                            const double* u_sorted, const int* perm, const double* H, int taps, int ops, int r, int r0,
+                            int rc, double* part, long long n, cudaStream_t s);
+
 // fft.cu
 cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1,
                                double2* A2, const double2* tw, int r, cudaStream_t s);
