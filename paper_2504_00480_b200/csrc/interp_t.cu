@@ -24,7 +24,8 @@ template <int N>
 __device__ __forceinline__ void it_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 constexpr int kItWarps = 4;  // two CTAs per SM: one's barriers and epilogue hide under the other's MMAs
-constexpr int kItRing = 3;  // o0-plane ring slots (two planes in flight)
+constexpr int kItPS = 1;              // o0-planes per pipeline step (one CTA barrier per step)
+constexpr int kItRing = 3 * kItPS;    // ring slots: steps s (computing), s+1, s+2 (in flight)
 
 template <int TAPS, int V, int MT, int WN>
 struct ItShape {
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(32 * kItWarps, 2) k_interp_t(const WinTable* _
   const int wm = warp / WN, wn = warp % WN, j4 = lane & 3;
 
   extern __shared__ double sm[];
-  double* ring = sm;                                       // [kItRing][TAPS][LDB]; later T [PPC][LDT]
+  double* ring = sm;  // [kItRing][TAPS][LDB]; later T [PPC][LDT]
   double* w0s = sm + (S::ring_bytes > S::t_bytes ? S::ring_bytes : S::t_bytes) / sizeof(double);  // [PPC][TAPS]
   double* w2s = w0s + PPC * TAPS;                          // [PPC][TAPS]
 
@@ -71,25 +72,45 @@ __global__ void __launch_bounds__(32 * kItWarps, 2) k_interp_t(const WinTable* _
   const int cell0 = it.bin[0], cell1 = it.bin[1], cell2 = it.bin[2];
   // staging of footprint plane o0 into ring slot slot_of(o0): footprint row o1 by warp
   // o1 % kItWarps, consecutive lanes on consecutive columns (contiguous H: a row (o0, o1) is one
-  // run of N doubles; otherwise a gather per element)
+  // run of N doubles of H; otherwise a gather per element)
   int plane_ctr = 0;  // planes staged in earlier passes
   auto slot_of = [&](int o0) { return (plane_ctr + o0) % kItRing; };
+  // contiguous H: the warp's rows (o1 = warp + kItWarps * i) start at fixed offsets from the
+  // footprint origin; a plane step adds L1 * L2 nodes.  Unrolled, each copy is one cp.async with
+  // an immediate offset.
+  static_assert(TAPS % kItWarps == 0, "rows per warp");
+  constexpr int RPW = TAPS / kItWarps, CPL = (N + 31) / 32;
+  const double* src0 = H + (toff + ((long long)cell0 * L1g + cell1 + warp) * L2g + cell2) * row_vals + lane;
+  const long long plane_stride = L1g * L2g * row_vals, row_stride = kItWarps * L2g * row_vals;
   auto stage = [&](int o0) {
     double* buf = ring + slot_of(o0) * TAPS * LDB;
+    if (contiguous) {
+      const double* src = src0 + o0 * plane_stride;
+      double* dst = buf + warp * LDB + lane;
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+#pragma unroll
+        for (int j = 0; j < CPL; ++j)
+          if (j * 32 + 32 <= N || j * 32 + lane < N) it_cp8(dst + j * 32, src + j * 32);
+        src += row_stride;
+        dst += kItWarps * LDB;
+      }
+      return;
+    }
     const long long tap_row = toff + ((long long)(cell0 + o0) * L1g + cell1) * L2g + cell2;
     for (int o1 = warp; o1 < TAPS; o1 += kItWarps) {
       const long long trow = tap_row + o1 * L2g;
       double* dst = buf + o1 * LDB;
-      if (contiguous) {
-        const double* src = H + trow * row_vals;
-        for (int col = lane; col < N; col += 32) it_cp8(dst + col, src + col);
-      } else {
-        for (int col = lane; col < N; col += 32) {
-          const int o2 = col / V, v = col - o2 * V, op = v / RC, c = v - op * RC;
-          it_cp8(dst + col, H + (trow + o2) * row_vals + op * r + r0 + c);
-        }
+      for (int col = lane; col < N; col += 32) {
+        const int o2 = col / V, v = col - o2 * V, op = v / RC, c = v - op * RC;
+        it_cp8(dst + col, H + (trow + o2) * row_vals + op * r + r0 + c);
       }
     }
+  };
+  auto stage_step = [&](int st) {  // planes st*kItPS .. +kItPS-1 as one cp.async group
+#pragma unroll
+    for (int k = 0; k < kItPS; ++k)
+      if (st * kItPS + k < TAPS) stage(st * kItPS + k);
     it_commit();
   };
 
@@ -101,8 +122,9 @@ __global__ void __launch_bounds__(32 * kItWarps, 2) k_interp_t(const WinTable* _
 
   for (int pbase = 0; pbase < it.count; pbase += PPC) {
     const int cnt = min(PPC, it.count - pbase);
-    // stage the first planes while the weights are evaluated
-    for (int o0 = 0; o0 < kItRing - 1; ++o0) stage(o0);
+    // stage the first two steps while the weights are evaluated
+    stage_step(0);
+    stage_step(1);
 
     // weights: the quad of lanes sharing a point row takes taps {j4, j4+4, j4+8, ...} of each axis
     double w1r[MT][KQ];
@@ -139,28 +161,31 @@ __global__ void __launch_bounds__(32 * kItWarps, 2) k_interp_t(const WinTable* _
       for (int nt = 0; nt < NTW; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 
     const int boff = j4 * LDB + wn * NTW * 8 + (lane >> 2);
-    for (int o0 = 0; o0 < TAPS; ++o0) {
-      if (o0 + 1 < TAPS) it_wait<kItRing - 2>();
+    constexpr int NSTEP = (TAPS + kItPS - 1) / kItPS;
+    for (int st = 0; st < NSTEP; ++st) {
+      if (st + 1 < NSTEP) it_wait<1>();
       else it_wait<0>();
-      __syncthreads();  // plane o0 visible to all; plane o0-1's slot free; w0s written
-      if (o0 + kItRing - 1 < TAPS) stage(o0 + kItRing - 1);
-      else it_commit();  // keep the group count uniform
+      __syncthreads();  // step st visible to all; step st-1's slots free; w0s written
+      stage_step(st + 2);
       if (!wact) continue;
-      const double* bp = ring + slot_of(o0) * TAPS * LDB + boff;
-      double w0c[MT];
+#pragma unroll 1
+      for (int o0 = st * kItPS; o0 < min(TAPS, st * kItPS + kItPS); ++o0) {
+        const double* bp = ring + slot_of(o0) * TAPS * LDB + boff;
+        double w0c[MT];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) w0c[mt] = w0s[((wm * MT + mt) * 8 + (lane >> 2)) * TAPS + o0];
+        for (int mt = 0; mt < MT; ++mt) w0c[mt] = w0s[((wm * MT + mt) * 8 + (lane >> 2)) * TAPS + o0];
 #pragma unroll
-      for (int k = 0; k < KQ; ++k) {
-        double af[MT];
+        for (int k = 0; k < KQ; ++k) {
+          double af[MT];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) af[mt] = w0c[mt] * w1r[mt][k];
-        const double* bk = bp + 4 * k * LDB;
+          for (int mt = 0; mt < MT; ++mt) af[mt] = w0c[mt] * w1r[mt][k];
+          const double* bk = bp + 4 * k * LDB;
 #pragma unroll
-        for (int nt = 0; nt < NTW; ++nt) {
-          const double b = bk[nt * 8];
+          for (int nt = 0; nt < NTW; ++nt) {
+            const double b = bk[nt * 8];
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], b);
+            for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], b);
+          }
         }
       }
     }
