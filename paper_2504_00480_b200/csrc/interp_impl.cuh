@@ -53,13 +53,19 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
   const long long L1g = g.L[1], L2g = g.L[2], toff = g.tap_off;
   auto stage = [&](int o0, double* buf) {
     if (contiguous) {
-      // each footprint row (o0, o1) is one run of TAPS * V consecutive doubles of H: source =
-      // plane base + idx + o1 * (row stride - TAPS * V), two divisions by constants per element
-      const double* base = H + (toff + ((long long)(cell0 + o0) * L1g + cell1) * L2g + cell2) * row_vals;
-      const long long delta = L2g * row_vals - TAPS * V;
-      for (int idx = tid; idx < SLAB * V; idx += blockDim.x) {
-        const int t = idx / V, v = idx - t * V, o1 = t / TAPS;
-        cp_async8(buf + t * LDH + v, base + idx + o1 * delta);
+      // each footprint row (o0, o1) is one run of TAPS * V consecutive doubles of H, copied by
+      // warp o1 % 8 with consecutive lanes on consecutive doubles (immediate source offsets)
+      constexpr int RUN = TAPS * V, CPL = (RUN + 31) / 32;
+      const int lane = tid & 31;
+      const double* base = H + (toff + ((long long)(cell0 + o0) * L1g + cell1) * L2g + cell2) * row_vals + lane;
+      for (int o1 = tid >> 5; o1 < T1; o1 += 8) {
+        const double* src = base + o1 * L2g * row_vals;
+        double* dst = buf + o1 * TAPS * LDH;
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+          const int col = lane + 32 * j, o2 = col / V;
+          if (j * 32 + 32 <= RUN || col < RUN) cp_async8(dst + o2 * LDH + (col - o2 * V), src + 32 * j);
+        }
       }
     } else {
       for (int idx = tid; idx < SLAB * V; idx += blockDim.x) {
