@@ -33,13 +33,19 @@ __device__ __forceinline__ void v5_cp4(void* dst, const void* src) {
                : "memory");
 }
 __device__ __forceinline__ void v5_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void v5_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void v5_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void v5_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 __host__ __device__ constexpr int v5_ldw(int fmax) { return ((fmax + 1 + 7) / 16) * 16 + 8; }  // 8 mod 16, > fmax
 }  // namespace
 
-template <int MB, int NB, int OCC>
-__global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* __restrict__ tabp,
+template <int MB, int NB, bool WS>
+__global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_v5(const WinTable* __restrict__ tabp,
                                                              const WorkItem* __restrict__ items,
                                                              const double* __restrict__ u_sorted,
                                                              const int* __restrict__ perm, const double* __restrict__ V,
@@ -58,6 +64,9 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
   const int VS = PB * rc + 1;  // ring slot of RHS values + one zero
   const int M = g.F[0] * F1, Nn = g.F[2] * rc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // WS: warps 0-3 run the MMAs, warps 4-7 ("helpers") the weights and the input ring; otherwise
+  // the same 4 warps do both, phase after phase
+  const int ltid = WS ? (tid & (NT - 1)) : tid, lwarp = WS ? (warp & (kV5Warps - 1)) : warp;
   const int taps = 2 * tab.m;
   const int nbatch = (it.count + PB - 1) / PB;
   const float inv_rc = 1.0f / rc;
@@ -73,9 +82,10 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
   int org[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) org[a] = g.box_lo[a] + it.bin[a] * g.B;
-  for (int idx = tid; idx < 2 * 3 * PB * LDW; idx += NT) Wb[idx] = 0.0;
-  for (int s = tid; s < kV5Ring; s += NT) Vring[s * VS + PB * rc] = 0.0;
-  for (int idx = tid; idx < 16 * kV5LdC; idx += NT) {
+  constexpr int NALL = WS ? 2 * NT : NT;
+  for (int idx = tid; idx < 2 * 3 * PB * LDW; idx += NALL) Wb[idx] = 0.0;
+  for (int s = tid; s < kV5Ring; s += NALL) Vring[s * VS + PB * rc] = 0.0;
+  for (int idx = tid; idx < 16 * kV5LdC; idx += NALL) {
     const int k = idx / kV5LdC, q = idx - k * kV5LdC;
     Cs[idx] = (k < kPolyLen && q < taps) ? pp.c[q * kPolyLen + k] : 0.0;
   }
@@ -85,12 +95,12 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
   auto issue_perm = [&](int b) {
     if (b >= nbatch) return;
     const int q0 = b * PB, pb = min(PB, it.count - q0);
-    if (tid < pb) v5_cp4(Pring + (b % kV5Ring) * PB + tid, perm + ptbase + q0 + tid);
+    if (ltid < pb) v5_cp4(Pring + (b % kV5Ring) * PB + ltid, perm + ptbase + q0 + ltid);
   };
   auto issue_u = [&](int b) {
     if (b >= nbatch) return;
     const int q0 = b * PB, pb = min(PB, it.count - q0);
-    for (int j = tid; j < 3 * PB; j += NT) {
+    for (int j = ltid; j < 3 * PB; j += NT) {
       const int a = j / PB, p = j - a * PB;
       if (a >= 3 - d && p < pb) v5_cp8(Uring + ((b % kV5Ring) * 3 + a) * PB + p, ubase + (long long)a * n + q0 + p);
     }
@@ -100,7 +110,7 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
     const int q0 = b * PB, pb = min(PB, it.count - q0);
     double* Vs = Vring + (b % kV5Ring) * VS;
     const int* pr = Pring + (b % kV5Ring) * PB;
-    for (int j = tid; j < PB * rc; j += NT) {
+    for (int j = ltid; j < PB * rc; j += NT) {
       const int p = fdiv(j, inv_rc), c = j - p * rc;
       if (p < pb) v5_cp8(Vs + j, V + (long long)pr[p] * ldv + r0 + c);
       else Vs[j] = 0.0;
@@ -123,7 +133,7 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
     int s0[NTL];
 #pragma unroll
     for (int t = 0; t < NTL; ++t) {
-      const int R = (warp * 3 + t0 + t) * 8 + (lane >> 2), a = R / PB, p = R - a * PB;
+      const int R = (lwarp * 3 + t0 + t) * 8 + (lane >> 2), a = R / PB, p = R - a * PB;
       const bool real = p < pb && a >= 3 - d;
       const double u = real ? U[a * PB + p] : 0.5;
       const double fl = floor(u);
@@ -148,7 +158,7 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
     }
 #pragma unroll
     for (int t = 0; t < NTL; ++t) {
-      const int R = (warp * 3 + t0 + t) * 8 + (lane >> 2), a = R / PB, p = R - a * PB;
+      const int R = (lwarp * 3 + t0 + t) * 8 + (lane >> 2), a = R / PB, p = R - a * PB;
       const bool live = p < pb, real = live && a >= 3 - d;
       double* wrow = W + (a * PB + p) * LDW;
       const int Fa = g.F[a], s = s0[t];
@@ -167,7 +177,9 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
     }
   };
   auto wgemm = [&](int b) {
-    if constexpr (MB * NB >= 45) {
+    if constexpr (WS) {  // helpers hold no accumulators: all three tiles interleaved
+      wtiles(b, 0, std::integral_constant<int, 3>{});
+    } else if constexpr (MB * NB >= 45) {
 #pragma unroll 1
       for (int t = 0; t < 3; ++t) wtiles(b, t, std::integral_constant<int, 1>{});
     } else if constexpr (MB * NB >= 36) {
@@ -178,17 +190,46 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
     }
   };
 
-  // prologue: perm 0..3, u 0..2, then V 0..2 and the weights of batch 0
-  for (int b = 0; b < 4; ++b) issue_perm(b);
-  for (int b = 0; b < 3; ++b) issue_u(b);
-  v5_commit();
-  v5_wait_all();
-  __syncthreads();
-  for (int b = 0; b < 3; ++b) issue_v(b);
-  v5_commit();
-  wgemm(0);
-  v5_wait_all();
-  __syncthreads();
+  if constexpr (WS) {
+    __syncthreads();  // initialised tables
+    if (warp >= kV5Warps) {
+      // helpers: per batch b, wait until the MMA warps released W[b&1] (batch b-2), evaluate the
+      // weights of b, issue the loads of later batches, then hand W[b&1] and V(b) over
+      for (int b = 0; b < 4; ++b) issue_perm(b);
+      for (int b = 0; b < 3; ++b) issue_u(b);
+      v5_commit();
+      v5_wait_all();
+      v5_bar_sync(5, NT);
+      for (int b = 0; b < 3; ++b) issue_v(b);
+      v5_commit();
+      for (int b = 0; b < nbatch; ++b) {
+        if (b >= 2) v5_bar_sync(3 + (b & 1), 2 * NT);  // FREE: batch b-2 consumed
+        v5_wait_all();
+        v5_bar_sync(5, NT);  // every helper's copies visible to all helpers
+        wgemm(b);
+        issue_perm(b + 4);
+        issue_u(b + 3);
+        issue_v(b + 3);
+        v5_commit();
+        v5_bar_arrive(1 + (b & 1), 2 * NT);  // READY: W(b), V(b)
+      }
+      for (int b = max(nbatch, 2); b < nbatch + 2; ++b) v5_bar_sync(3 + (b & 1), 2 * NT);
+      v5_wait_all();
+      return;
+    }
+  } else {
+    // prologue: perm 0..3, u 0..2, then V 0..2 and the weights of batch 0
+    for (int b = 0; b < 4; ++b) issue_perm(b);
+    for (int b = 0; b < 3; ++b) issue_u(b);
+    v5_commit();
+    v5_wait_all();
+    __syncthreads();
+    for (int b = 0; b < 3; ++b) issue_v(b);
+    v5_commit();
+    wgemm(0);
+    v5_wait_all();
+    __syncthreads();
+  }
 
   // fragment coordinates (invalid rows / columns point at the zero weight slot)
   unsigned ai[MB], bi[NB];  // (w0 row | w1 row << 16), (w2 row | rhs << 16)
@@ -212,6 +253,7 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
     for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   for (int b = 0; b < nbatch; ++b) {
+    if constexpr (WS) v5_bar_sync(1 + (b & 1), 2 * NT);  // READY
     const double* W0 = Wb + (b & 1) * 3 * PB * LDW;
     const double* W1 = W0 + PB * LDW;
     const double* W2 = W1 + PB * LDW;
@@ -234,13 +276,17 @@ __global__ void __launch_bounds__(kV5Threads, OCC) k_spread_v5(const WinTable* _
 #pragma unroll
         for (int j = 0; j < NB; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    if (b + 1 < nbatch) wgemm(b + 1);  // the next batch's weights (its coordinates have landed)
-    v5_wait_all();                     // V(b+1..), u(b+2..), perm(b+3..) issued earlier
-    __syncthreads();
-    issue_perm(b + 4);
-    issue_u(b + 3);
-    issue_v(b + 3);
-    v5_commit();
+    if constexpr (WS) {
+      v5_bar_arrive(3 + (b & 1), 2 * NT);  // FREE
+    } else {
+      if (b + 1 < nbatch) wgemm(b + 1);  // the next batch's weights (its coordinates have landed)
+      v5_wait_all();                     // V(b+1..), u(b+2..), perm(b+3..) issued earlier
+      __syncthreads();
+      issue_perm(b + 4);
+      issue_u(b + 3);
+      issue_v(b + 3);
+      v5_commit();
+    }
   }
 
   // flush
@@ -309,9 +355,13 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
                              int r0, int rc, int r_total, double* grid, int MB, int NB, int WN, size_t smem,
                              cudaStream_t s) {
   if (n_items <= 0) return cudaSuccess;
-  static const int occ = (getenv("AKM_V5_OCC") && atoi(getenv("AKM_V5_OCC")) == 2) ? 2 : 1;
+  // warp-specialised variant for small register tiles (few RHS, e.g. c2: the helpers' latency-bound
+  // weight and ring work overlaps the MMAs); with big tiles the helpers' scalar FP64 on the same
+  // SM sub-partitions slows the DMMA stream more than it hides
+  static const int ws_env = getenv("AKM_V5_WS") ? atoi(getenv("AKM_V5_WS")) : -1;
+  const bool ws = ws_env >= 0 ? ws_env != 0 : MB * NB <= 24;
 #define AKM_CASE1(a, b, o)                                                                                     \
-  if (MB == a && NB == b && occ == o) {                                                                         \
+  if (MB == a && NB == b && ws == o) {                                                                          \
     static bool attr_set = false;                                                                               \
     if (!attr_set) {                                                                                            \
       cudaError_t e = cudaFuncSetAttribute(k_spread_v5<a, b, o>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
@@ -319,11 +369,12 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
       if (e != cudaSuccess) return e;                                                                           \
       attr_set = true;                                                                                          \
     }                                                                                                           \
-    k_spread_v5<a, b, o><<<n_items, kV5Threads, smem, s>>>(dtab, items, u_sorted, perm, V, ldv, n, r0, rc,      \
+    k_spread_v5<a, b, o><<<n_items, o ? 2 * kV5Threads : kV5Threads, smem, s>>>(dtab, items, u_sorted, perm, V, \
+                                                                                ldv, n, r0, rc,                \
                                                            r_total, grid, WN, pp);                              \
     return cudaGetLastError();                                                                                  \
   }
-#define AKM_CASE(a, b) AKM_CASE1(a, b, 1) AKM_CASE1(a, b, 2)
+#define AKM_CASE(a, b) AKM_CASE1(a, b, true) AKM_CASE1(a, b, false)
   AKM_V5_TILES(AKM_CASE)
 #undef AKM_CASE
 #undef AKM_CASE1
