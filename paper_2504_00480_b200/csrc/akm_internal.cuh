@@ -221,10 +221,10 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
                              cudaStream_t s);
 
 // interp_t.cu (3-D windows, many values per node: GEMM over (o0, o1) with N = (o2, v))
-bool interp_t_supported(int d, int taps, int ops, int rc);
+bool interp_t_supported(int d, int taps, int fp, int ops, int rc);
 cudaError_t launch_interp_t(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
-                            const double* u_sorted, const int* perm, const double* H, int taps, int ops, int r, int r0,
-                            int rc, double* part, long long n, cudaStream_t s);
+                            const double* u_sorted, const int* perm, const double* H, int taps, int fp, int ops, int r,
+                            int r0, int rc, double* part, long long n, cudaStream_t s);
 
 // fft.cu
 cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1,

@@ -390,6 +390,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     }
     std::stable_sort(gs.begin(), gs.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
     std::stable_sort(gi.begin(), gi.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
+    std::stable_sort(gib.begin(), gib.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
     grp.spread_begin = (int)plan->items_spread.size();
     grp.spread_count = (int)gs.size();
     grp.interp_begin = (int)plan->items_interp.size();
@@ -612,14 +613,15 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
   while (r0 < r) {
     const int rc = interp_rc_for(r - r0);
     for (const Group& grp : plan->groups) {
-      // 3-D windows with dense cells and many values per node: GEMM over (o0, o1) (interp_t.cu);
+      // 3-D windows: per-bin GEMM over the footprint rows (o0, o1), N = (o2, v) (interp_t.cu);
       // AKM_INTERP_T=0 selects the per-plane kernel (A/B measurement)
       static const bool it_off = getenv("AKM_INTERP_T") && atoi(getenv("AKM_INTERP_T")) == 0;
-      if (!it_off && !grp.sparse && interp_t_supported(grp.d, 2 * plan->m, ops, rc)) {
-        AKM_CK(launch_interp_t(dtab, plan->poly_param, plan->items_i.as<WorkItem>() + grp.interp_begin,
-                               grp.interp_count, plan->u_sorted.as<double>(), plan->perm.as<int>(),
-                               plan->H.as<double>(), 2 * plan->m, ops, r, r0, rc, plan->part.as<double>(), n, s));
-        if (grp.interp_count > 0) {
+      if (!it_off && interp_t_supported(grp.d, 2 * plan->m, grp.F, ops, rc)) {
+        AKM_CK(launch_interp_t(dtab, plan->poly_param, plan->items_ib.as<WorkItem>() + grp.interp_bin_begin,
+                               grp.interp_bin_count, plan->u_sorted.as<double>(), plan->perm.as<int>(),
+                               plan->H.as<double>(), 2 * plan->m, grp.F, ops, r, r0, rc, plan->part.as<double>(), n,
+                               s));
+        if (grp.interp_bin_count > 0) {
           ++plan->launches;
           ++plan->interp_launches;
         }
