@@ -13,7 +13,7 @@ timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch exit $?"
 timeout 300 python tools/prof_run.py --config c2 --calls 3 > gpurun_out/plain_c2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_" -s 43 -c 9 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spread|k_plane|k_pencil|k_dft|k_interp|k_epilogue" -s 6 -c 6 \
     -o gpurun_out/prof_c2 -f python tools/prof_run.py --config c2 --calls 3 > gpurun_out/ncu_c2.log 2>&1; echo "ncu c2 exit $?"
 timeout 300 python tools/prof_run.py --config c4 --calls 2 > gpurun_out/plain_c4.log 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_spread|k_interp" -s 2 -c 2 \

@@ -37,7 +37,7 @@ with open(os.path.join(P, f"{R}_launches_c2_summary.txt"), "w") as out:
     for k in order:
         v = d[k]
         out.write(f"{k:45s} {len(v):8d} {sum(v) / len(v) / 1e3:9.2f}\n")
-    mvm = [k for k in order if any(s in k for s in ("k_spread", "k_dft", "k_interp", "k_epilogue"))]
+    mvm = [k for k in order if any(s in k for s in ("k_spread", "k_dft", "k_plane", "k_pencil", "k_interp", "k_epilogue"))]
     tot = sum(sum(d[k]) / len(d[k]) for k in mvm)
     out.write("\nper-MVM-step share (mean launch time of each kernel, one launch each per step):\n")
     for k in mvm:
@@ -57,7 +57,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"]
-CMD = {"c2": "ncu --set full --clock-control none --import-source on -k regex:k_ -s 43 -c 9 "
+CMD = {"c2": "ncu --set full --clock-control none --import-source on "
+             "-k regex:'k_spread|k_plane|k_pencil|k_dft|k_interp|k_epilogue' -s 6 -c 6 "
              "python tools/prof_run.py --config c2 --calls 3",
        "c4": "ncu --set full --clock-control none --import-source on -k regex:'k_spread|k_interp' -s 2 -c 2 "
              "python tools/prof_run.py --config c4 --calls 2"}
