@@ -39,11 +39,20 @@ __global__ void k_col2_partial(long long n, int R, const double* __restrict__ A,
   }
 }
 
+// sum over the nblk partials of the 2R column sums; one warp per output, lanes over blocks in a
+// fixed order and a fixed butterfly (deterministic)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 __device__ void col2_final(const double* __restrict__ part, int nblk, int R, double* out /* [R][2] */) {
-  for (int idx = threadIdx.x; idx < 2 * R; idx += blockDim.x) {
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int idx = threadIdx.x >> 5; idx < 2 * R; idx += nw) {
     double acc = 0.0;
-    for (int b = 0; b < nblk; ++b) acc += part[(long long)b * 2 * R + idx];
-    out[idx] = acc;
+    for (int b = lane; b < nblk; b += 32) acc += part[(long long)b * 2 * R + idx];
+    acc = warp_sum(acc);
+    if (lane == 0) out[idx] = acc;
   }
 }
 
@@ -209,12 +218,15 @@ __global__ void k_kr_proj_partial(long long n, int R, int nq, const double* __re
   }
 }
 
+// one warp per output h[j][c] (fixed order, as col2_final)
 __global__ void k_kr_proj_final(const double* __restrict__ part, int nblk, int nq, int R, double* __restrict__ h) {
-  for (int idx = threadIdx.x; idx < nq * R; idx += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[(long long)b * nq * R + idx];
-    h[idx] = s;
-  }
+  const int lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (idx >= nq * R) return;
+  double s = 0.0;
+  for (int b = lane; b < nblk; b += 32) s += part[(long long)b * nq * R + idx];
+  s = warp_sum(s);
+  if (lane == 0) h[idx] = s;
 }
 
 // W[:, c] -= sum_j Q_j[:, c] h[j][c] for probes that continue
@@ -382,7 +394,7 @@ cudaError_t launch_kr_col2(long long n, int R, const double* A, const double* B,
 int kr_blocks() { return kKrBlocks; }
 
 cudaError_t launch_kr_init(void* st, const double* part, int R, double c, cudaStream_t s) {
-  k_kr_init<<<1, 64, 0, s>>>((KrylovState*)st, part, kKrBlocks, R, c);
+  k_kr_init<<<1, 256, 0, s>>>((KrylovState*)st, part, kKrBlocks, R, c);
   return cudaGetLastError();
 }
 
@@ -405,7 +417,7 @@ cudaError_t launch_kr_start(long long n, int R, const void* st, double* B, doubl
 }
 
 cudaError_t launch_kr_after_dots(void* st, const double* part, int R, int cg_iters, int lanczos_steps, cudaStream_t s) {
-  k_kr_after_dots<<<1, 64, 0, s>>>((KrylovState*)st, part, kKrBlocks, R, cg_iters, lanczos_steps);
+  k_kr_after_dots<<<1, 256, 0, s>>>((KrylovState*)st, part, kKrBlocks, R, cg_iters, lanczos_steps);
   return cudaGetLastError();
 }
 
@@ -418,16 +430,23 @@ cudaError_t launch_kr_update(long long n, int R, const void* st, const double* B
 cudaError_t launch_kr_reorth(long long n, int R, int nq, const void* st, const double* Q, long long slab, double* W,
                              double* part, double* h, cudaStream_t s) {
   const int chunks = (nq + kProjJC - 1) / kProjJC;
+  static bool attr_set = false;  // R up to kKrMaxR needs more than the default 48 KB
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_kr_proj_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(double) * kProjJC * 32 * kKrMaxR));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
   k_kr_proj_partial<<<dim3(kKrBlocks, chunks), 32 * R, sizeof(double) * kProjJC * 32 * R, s>>>(n, R, nq, Q, slab, W,
                                                                                                   part);
-  k_kr_proj_final<<<1, 256, 0, s>>>(part, kKrBlocks, nq, R, h);
+  k_kr_proj_final<<<(nq * R + 7) / 8, 256, 0, s>>>(part, kKrBlocks, nq, R, h);
   k_kr_orth_update<<<grid_for(n * R), 256, sizeof(double) * nq * R, s>>>(n, R, nq, (const KrylovState*)st, Q, slab, h,
                                                                          W);
   return cudaGetLastError();
 }
 
 cudaError_t launch_kr_after_norms(void* st, const double* part, int R, cudaStream_t s) {
-  k_kr_after_norms<<<1, 64, 0, s>>>((KrylovState*)st, part, kKrBlocks, R);
+  k_kr_after_norms<<<1, 256, 0, s>>>((KrylovState*)st, part, kKrBlocks, R);
   return cudaGetLastError();
 }
 

@@ -129,3 +129,16 @@ def test_objective_full_size_c5_invariants(akm):
     assert np.std(g["samples"]) <= 0.05 * abs(np.mean(g["samples"]))   # Hutchinson spread is small here
     # 50 CG iterations do not converge at this theta (cond ~1e7): the residual is only finite
     assert 0.0 < g["cg_relres"] < 1e3 and math.isfinite(g["Z"])
+
+
+def test_objective_max_probes_matches_oracle(akm):
+    """n_z = AKM_MAX_PROBES (R = 32 columns per block): the widest reorthogonalisation shapes."""
+    assert akm.AKM_MAX_PROBES == 31
+    wl, X, y, Z = _inputs(1500, 31, seed=4)
+    theta = (0.5, 0.5, 1.0)
+    g = _gpu(akm, wl, X, theta, y, Z, 12, 12)
+    o = _oracle(wl, X, theta, y, Z, 12, 12)
+    assert g["steps"] == o["steps"] == [12] * 31
+    for a, b in zip(g["samples"], o["samples"]):
+        assert a == pytest.approx(b, rel=1e-8)
+    assert g["quad"] == pytest.approx(o["quad"], rel=1e-6)
