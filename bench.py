@@ -114,45 +114,68 @@ class ClockSampler:
 
 
 def algorithmic_counts(wl, info, r, ops):
-    """FP64 flops of spreading / interpolation and minimal bytes of one step."""
+    """FP64 flops of spreading / interpolation and minimal bytes of one step.
+    Cross products (extra n_src): the method spreads the sources and interpolates at the targets."""
     n, W = wl.n, len(wl.windows)
+    n_s = wl.extra.get("n_src", n)
+    n_i = n - n_s if "n_src" in wl.extra else n
     d = [len(w) for w in wl.windows]
     taps = [(2 * wl.m) ** dw for dw in d]
     n_ops = len({"K" if o in ("K", "dsf") else o for o in ops})      # distinct operators interpolated
-    spread_flops = sum(2.0 * n * r * t for t in taps)
-    interp_flops = sum(2.0 * n * r * t * n_ops for t in taps)
+    spread_flops = sum(2.0 * n_s * r * t for t in taps)
+    interp_flops = sum(2.0 * n_i * r * t * n_ops for t in taps)
     ntap = [int(np.prod(b)) for b in info["box"]]
     grid_bytes = sum(8.0 * nt * r * (2 + 2 * n_ops) for nt in ntap)
-    bytes_ = 2 * 8.0 * n * sum(d) + 8.0 * n * r * (1 + len(ops)) + grid_bytes
+    bytes_ = 8.0 * (n_s + n_i) * sum(d) + 8.0 * n_s * r + 8.0 * n_i * r * len(ops) + grid_bytes
     return spread_flops, interp_flops, bytes_
+
+
+def _oracle_inputs(wl):
+    """(X, V, theta, candidate rows) for the CPU oracle legs.  Cross workloads: the dense products
+    on the union with the targets' V rows zero are exactly the cross product at the target rows
+    (tests/test_oracle_cross.py), so the targets' rows are sampled."""
+    X = workloads.make_X(wl)
+    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    if "n_src" in wl.extra:
+        n_s = wl.extra["n_src"]
+        V = np.vstack([workloads.make_V(wl, n=n_s), np.zeros((wl.n - n_s, wl.r))])
+        rows_all = n_s + workloads.make_rows(wl, wl.n - n_s, n=wl.n - n_s)
+    else:
+        V = workloads.make_V(wl)
+        rows_all = workloads.make_rows(wl, wl.n)
+    return X, V, theta, rows_all
+
+
+def _metric(wl):
+    if "n_src" in wl.extra:
+        return "cross K_{*X} V throughput (n_target*r*windows pts/s)"
+    return "batched K-hat V throughput (n*r*windows pts/s)"
 
 
 def run_reference(args, wl):
     """The reference arm: the CPU float64 dense oracle timed as it stands on bounded row samples."""
     from oracle import dense_apply
-    X = workloads.make_X(wl)
-    V = workloads.make_V(wl)
-    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
-    rows_all = workloads.make_rows(wl, wl.n)
+    X, V, theta, rows_all = _oracle_inputs(wl)
+    n_rows = rows_all.shape[0]
     # calibrate the sample so that each step is ~1-3 s of CPU work
     t0 = time.perf_counter()
     dense_apply(X, wl.windows, wl.family, theta, V, rows=rows_all[:64], ops=wl.ops)
     per_row = (time.perf_counter() - t0) / 64
-    rows_per_step = int(min(wl.n, max(64, 2.0 / max(per_row, 1e-9))))
+    rows_per_step = int(min(n_rows, max(64, 2.0 / max(per_row, 1e-9))))
     times = []
     for s in range(args.warmup + args.steps):
-        rows = rows_all[(s * rows_per_step) % max(1, wl.n - rows_per_step + 1):][:rows_per_step]
+        rows = rows_all[(s * rows_per_step) % max(1, n_rows - rows_per_step + 1):][:rows_per_step]
         t0 = time.perf_counter()
         dense_apply(X, wl.windows, wl.family, theta, V, rows=rows, ops=wl.ops)
         if s >= args.warmup:
             times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
-    full_equiv = t * wl.n / rows_per_step
+    full_equiv = t * n_rows / rows_per_step
     value = wl.units / full_equiv
     cores = os.cpu_count()
-    sample = f"{rows_per_step} of {wl.n} rows per step (dense direct sums, all {wl.n} columns), extrapolated x{wl.n / rows_per_step:.1f}"
+    sample = f"{rows_per_step} of {n_rows} rows per step (dense direct sums, all {wl.n} columns), extrapolated x{n_rows / rows_per_step:.1f}"
     line = {
-        "impl": "reference", "metric": "batched K-hat V throughput (n*r*windows pts/s)", "value": value,
+        "impl": "reference", "metric": _metric(wl), "value": value,
         "unit": "pts/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_equiv * 1e3,
         "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(wl),
@@ -163,7 +186,8 @@ def run_reference(args, wl):
 
 
 def config_dict(wl):
-    return {"workload": wl.name, "description": wl.description, "n": wl.n, "r": wl.r, "windows": len(wl.windows),
+    extra = {"n_src": wl.extra["n_src"], "n_target": wl.n - wl.extra["n_src"]} if "n_src" in wl.extra else {}
+    return {"workload": wl.name, "description": wl.description, "n": wl.n, **extra, "r": wl.r, "windows": len(wl.windows),
             "d": [len(w) for w in wl.windows], "family": "gaussian" if wl.family == 0 else "matern12",
             "N": wl.N, "sigma_over": wl.sigma_over, "m": wl.m, "ops": list(wl.ops),
             "l2": "256 MiB written between timed steps (L2 flush)"}
@@ -171,20 +195,18 @@ def config_dict(wl):
 
 def cpu_baseline(wl, budget_s=10.0):
     from oracle import dense_apply
-    X = workloads.make_X(wl)
-    V = workloads.make_V(wl)
-    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
-    rows_all = workloads.make_rows(wl, wl.n)
+    X, V, theta, rows_all = _oracle_inputs(wl)
     t0 = time.perf_counter()
     dense_apply(X, wl.windows, wl.family, theta, V, rows=rows_all[:32], ops=wl.ops)
     per_row = max((time.perf_counter() - t0) / 32, 1e-9)
-    nrows = int(min(wl.n, max(32, budget_s / per_row)))
+    nrows = int(min(rows_all.shape[0], max(32, budget_s / per_row)))
     t0 = time.perf_counter()
     dense_apply(X, wl.windows, wl.family, theta, V, rows=rows_all[:nrows], ops=wl.ops)
     t = time.perf_counter() - t0
     value = nrows * wl.r * len(wl.windows) / t
     return {"value": value, "unit": "pts/s", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"{nrows} seeded rows of {wl.n} (all columns) of the dense float64 products {list(wl.ops)}; "
+            "sample": f"{nrows} seeded rows of {rows_all.shape[0]} (all {wl.n} columns) of the dense float64 products "
+                      f"{list(wl.ops)}; "
                       f"{t:.1f} s"}
 
 
@@ -221,10 +243,14 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     X = workloads.make_X(wl)
-    V = workloads.make_V(wl, seed=D.rank_seed(2000 + wl.index, rank))  # independent RHS block per rank
+    cross = "n_src" in wl.extra              # f2: K_{*X} V from the first n_src rows to the rest
+    n_src = wl.extra.get("n_src", wl.n)
+    V = workloads.make_V(wl, n=n_src, seed=D.rank_seed(2000 + wl.index, rank))  # independent RHS block per rank
     Xd = torch.from_numpy(X).to(dev)
     Vd = torch.from_numpy(V).to(dev)
     outs = {op: torch.empty_like(Vd) for op in wl.ops}
+    if cross:
+        outs = {"K": torch.empty((wl.n - n_src, wl.r), dtype=torch.float64, device=dev)}
     stream = torch.cuda.current_stream(dev)
 
     plan = akm.Plan(local)
@@ -243,6 +269,11 @@ def main():
 
         def step():
             last["out"] = plan.objective_diag(yd, Zd, cg, lz)
+    elif cross:
+        products_per_step = 1
+
+        def step():
+            plan.cross_mvm(n_src, Vd, outs["K"])
     else:
         products_per_step = 1
 
@@ -292,13 +323,16 @@ def main():
 
     # ---------------- e2e: same call with pinned host V and outputs
     Vh = torch.from_numpy(V).pin_memory()
-    Oh = {op: torch.empty(V.shape, dtype=torch.float64).pin_memory() for op in wl.ops}
+    Oh = {op: torch.empty(tuple(outs[op].shape) if cross else V.shape, dtype=torch.float64).pin_memory()
+          for op in wl.ops}
     if objective:
         yh, Zh = Vh[:, 0].contiguous().pin_memory(), Vh[:, 1:].contiguous().pin_memory()
 
     def e2e_step():
         if objective:   # host y, Z in; the objective's terms come back to the host
             plan.objective_diag(yh, Zh, cg, lz, stream=stream.cuda_stream)
+        elif cross:
+            plan.cross_mvm(n_src, Vh, Oh["K"], stream=stream.cuda_stream)
         else:
             plan.mvm_multi(Vh, Y=Oh.get("K"), dY_ell=Oh.get("dell"), dY_sf=Oh.get("dsf"), stream=stream.cuda_stream)
 
@@ -339,12 +373,13 @@ def main():
     clocks = sampler.summary(tail)
 
     line = {
-        "metric": "batched K-hat V throughput (n*r*windows pts/s)",
+        "metric": _metric(wl),
         "value": value, "unit": "pts/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": config_dict(wl),
         "e2e": {"value": e2e_value, "unit": "pts/s", "h2d_bytes_per_step": int(V.nbytes),
-                "d2h_bytes_per_step": int(8 * (10 + 2 * wl.r) if objective else V.nbytes * len(wl.ops))},
+                "d2h_bytes_per_step": int(8 * (10 + 2 * wl.r) if objective else
+                                          sum(o.numel() * 8 for o in Oh.values()))},
         "gpu_launches": int(launches_timed),
         "roofline": {"bound": "alu", "kernel": name, "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS, "traffic": traffic,

@@ -117,6 +117,18 @@ akm_status akm_kernel_deriv_mvm(akm_plan* plan, int32_t which, const double* V, 
 akm_status akm_kernel_mvm_multi(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y,
                                 double* dY_ell, double* dY_sf, int64_t ldy, void* stream);
 
+/* Cross product for prediction (posterior mean / variance use K_{*X} V,
+ * P:947):  Yt = sigma_f^2 sum_w K_w(X_t, X_s) V  (no noise term).
+ * The points of the last akm_set_points are read as [sources X_s = rows 0 .. n_src-1; targets
+ * X_t = rows n_src .. n-1]: both sets are centred, scaled and binned together (the scaled ball of
+ * reading R2 holds the union), so every source-target difference stays inside the torus window.
+ * V: n_src x r (ld ldv >= r); Yt: (n - n_src) x r (ld ldy >= r); row-major float64, device or host
+ * memory (host buffers are staged).  0 <= n_src <= n, else INVALID_ARG; n_src == n is a no-op;
+ * n_src == 0 gives Yt = 0.  Cost: one product on the union with V zero-padded (the targets' rows
+ * of that product are exactly the cross product, since their V rows are zero). */
+akm_status akm_kernel_cross_mvm(akm_plan* plan, int64_t n_src, const double* V, int64_t ldv, int32_t r,
+                                double* Yt, int64_t ldy, void* stream);
+
 /* Plan description (scale factors, grid boxes, bin sizes, workspace). */
 akm_status akm_get_info(const akm_plan* plan, akm_info* out);
 

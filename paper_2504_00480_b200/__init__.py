@@ -31,7 +31,8 @@ AKM_MAX_WINDOWS = 32
 # names exported by include/akm.h (checked by tests/test_abi_cpu.py)
 ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm", "akm_kernel_deriv_mvm",
                "akm_kernel_mvm_multi", "akm_get_info", "akm_set_scale_override", "akm_last_error", "akm_destroy",
-               "akm_version", "akm_set_profiling", "akm_get_stage_times", "akm_objective_diag")
+               "akm_version", "akm_set_profiling", "akm_get_stage_times", "akm_objective_diag",
+               "akm_kernel_cross_mvm")
 AKM_MAX_PROBES = 31
 
 
@@ -89,6 +90,8 @@ def _load():
     lib.akm_kernel_deriv_mvm.restype = st
     lib.akm_kernel_mvm_multi.argtypes = [P, P, i64, i32, P, P, P, i64, P]
     lib.akm_kernel_mvm_multi.restype = st
+    lib.akm_kernel_cross_mvm.argtypes = [P, i64, P, i64, i32, P, i64, P]
+    lib.akm_kernel_cross_mvm.restype = st
     lib.akm_get_info.argtypes = [P, ctypes.POINTER(akm_info)]
     lib.akm_get_info.restype = st
     lib.akm_set_scale_override.argtypes = [P, P]
@@ -129,6 +132,8 @@ def _ptr_ld(a, name):
                 raise TypeError(f"{name} must be float64")
             if a.dim() == 1:
                 a = a.unsqueeze(1)
+            if a.dim() == 2 and a.numel() == 0:  # empty blocks carry no strides (torch reports 0)
+                return ctypes.c_void_p(a.data_ptr()), max(1, a.shape[1]), a.shape[0], a.shape[1], a.is_cuda, a
             if a.dim() != 2 or (a.stride(1) != 1 and a.shape[1] > 1):
                 raise ValueError(f"{name} must be 2-D with unit column stride")
             ld = a.stride(0) if a.shape[0] > 1 else a.shape[1]
@@ -222,6 +227,15 @@ def akm_kernel_mvm_multi(plan, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
                                            _stream(stream, kv, *[o[5] for o in outs])))
 
 
+def akm_kernel_cross_mvm(plan, n_src, V, Yt, stream=None):
+    """Yt = sigma_f^2 sum_w K_w(X_t, X_s) V; the plan's points are [X_s (n_src rows); X_t]."""
+    pv, ldv, nv, r, _, kv = _ptr_ld(V, "V")
+    py, ldy, _, ry, _, ky = _ptr_ld(Yt, "Yt")
+    if nv != n_src or (Yt is not None and ry != r):
+        raise ValueError(f"V must have n_src = {n_src} rows and Yt the same number of columns ({r})")
+    _check(plan, _lib.akm_kernel_cross_mvm(plan, int(n_src), pv, ldv, r, py, ldy, _stream(stream, kv, ky)))
+
+
 def akm_get_info(plan) -> dict:
     info = akm_info()
     _check(plan, _lib.akm_get_info(plan, ctypes.byref(info)))
@@ -310,6 +324,10 @@ class Plan:
     def mvm_multi(self, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
         akm_kernel_mvm_multi(self.handle, V, Y, dY_ell, dY_sf, stream)
         return Y, dY_ell, dY_sf
+
+    def cross_mvm(self, n_src, V, Yt, stream=None):
+        akm_kernel_cross_mvm(self.handle, n_src, V, Yt, stream)
+        return Yt
 
     def objective_diag(self, y, Z, cg_iters=50, lanczos_steps=30, stream=None):
         return akm_objective_diag(self.handle, y, Z, cg_iters, lanczos_steps, stream)

@@ -90,6 +90,7 @@ struct akm_plan {
   DevBuf dtab, Xc, u_tmp, u_sorted, perm, hist, hist_off, err_flag, items_s, items_i, items_ib, minmax, r2;
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
   DevBuf stageV, stageY, stageL, stageS;
+  DevBuf crossV, crossY;  // akm_kernel_cross_mvm: zero-padded V and the union's product
   DevBuf krB, krKB, krW, krX, krY, krQ, krPart, krH, krState, krErr, krStage;
   long long r_cap = 0;
 
@@ -1028,6 +1029,39 @@ akm_status akm_kernel_deriv_mvm(akm_plan* plan, int32_t which, const double* V, 
 akm_status akm_kernel_mvm_multi(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y, double* dY_ell,
                                 double* dY_sf, int64_t ldy, void* stream) {
   return mvm_entry(plan, V, ldv, r, Y, dY_ell, dY_sf, nullptr, ldy, S(stream));
+}
+
+akm_status akm_kernel_cross_mvm(akm_plan* plan, int64_t n_src, const double* V, int64_t ldv, int32_t r, double* Yt,
+                                int64_t ldy, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points || !plan->have_theta)
+    return plan->fail(AKM_ERR_STATE, "kernel_cross_mvm called before set_points and set_theta");
+  const long long n = plan->n;
+  if (n_src < 0 || n_src > n) return plan->fail(AKM_ERR_INVALID_ARG, "n_src = %lld outside [0, n = %lld]", (long long)n_src, n);
+  if (r < 1 || ldv < r || ldy < r) return plan->fail(AKM_ERR_INVALID_ARG, "bad r/ldv/ldy (r=%d ldv=%lld ldy=%lld)", r, (long long)ldv, (long long)ldy);
+  const long long n_t = n - n_src;
+  if (n_t == 0) return AKM_OK;
+  if (!Yt) return plan->fail(AKM_ERR_INVALID_ARG, "Yt is NULL");
+  if (n_src > 0 && !V) return plan->fail(AKM_ERR_INVALID_ARG, "V is NULL");
+  cudaStream_t s = S(stream);
+  AKM_CK(cudaSetDevice(plan->device));
+  AKM_CK(plan->crossV.ensure(sizeof(double) * n * r));
+  AKM_CK(plan->crossY.ensure(sizeof(double) * n * r));
+  double* Vu = plan->crossV.as<double>();
+  double* Yu = plan->crossY.as<double>();
+  // V into the sources' rows, zeros into the targets' rows
+  if (n_src > 0)
+    AKM_CK(cudaMemcpy2DAsync(Vu, sizeof(double) * r, V, sizeof(double) * ldv, sizeof(double) * r, n_src,
+                             cudaMemcpyDefault, s));
+  AKM_CK(cudaMemsetAsync(Vu + n_src * r, 0, sizeof(double) * n_t * r, s));
+  akm_status st = run_mvm(plan, Vu, r, r, Yu, nullptr, nullptr, r, s);
+  if (st != AKM_OK) return st;
+  // the targets' rows: sigma_f^2 S + sigma_eps^2 * 0
+  AKM_CK(cudaMemcpy2DAsync(Yt, sizeof(double) * ldy, Yu + n_src * r, sizeof(double) * r, sizeof(double) * r, n_t,
+                           cudaMemcpyDefault, s));
+  if (!is_device_ptr(Yt)) AKM_CK(cudaStreamSynchronize(s));
+  return AKM_OK;
 }
 
 akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,

@@ -1,0 +1,118 @@
+"""GPU parity of the cross product akm_kernel_cross_mvm (K_{*X} V for prediction)
+against the dense oracle (oracle/cross.py), through the C ABI.
+
+Gate: relative Frobenius error over the n_t x r block <= 1e-6 (Gaussian) / 1e-3 (Matern), as for
+the square products (BASELINE.json north_star; reading R8), full rows at small sizes and
+seeded row samples of the x4 workload at full size.
+"""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import dense_apply
+from oracle.cross import dense_cross
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def akm():
+    import __graft_entry__
+    __graft_entry__.build_library()
+    import paper_2504_00480_b200 as mod
+    return mod
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def gpu_cross(akm, X, n_src, windows, family, theta, V, N=32, m=6, host=False):
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(np.ascontiguousarray(X)).to(dev), windows, family, N, 2.0, m, 1.0 / 16)
+    plan.set_theta(*theta)
+    V = np.ascontiguousarray(V if V.ndim == 2 else V[:, None])
+    n_t = X.shape[0] - n_src
+    if host:
+        Yt = np.full((n_t, V.shape[1]), np.nan)
+        plan.cross_mvm(n_src, V, Yt)
+    else:
+        Yt = torch.full((n_t, V.shape[1]), float("nan"), dtype=torch.float64, device=dev)
+        plan.cross_mvm(n_src, torch.from_numpy(V).to(dev), Yt)
+        torch.cuda.synchronize()
+        Yt = Yt.cpu().numpy()
+    plan.close()
+    return Yt
+
+
+@pytest.mark.parametrize("n_src,n_t,r", [(4000, 1000, 1), (3000, 2500, 3), (2500, 37, 11)])
+def test_cross_gaussian_d3_matches_oracle(akm, n_src, n_t, r):
+    wl = workloads.CONFIGS["c2"]
+    X = workloads.make_X(wl, n=n_src + n_t)
+    V = workloads.make_V(wl, n=n_src, r=r)
+    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    got = gpu_cross(akm, X, n_src, wl.windows, wl.family, theta, V)
+    want = dense_cross(X[:n_src], X[n_src:], wl.windows, wl.family, theta, V)
+    assert rel(got, want) <= 1e-6
+
+
+def test_cross_matern_d2_matches_oracle(akm):
+    wl = workloads.CONFIGS["c3"]
+    X = workloads.make_X(wl, n=3000)
+    V = workloads.make_V(wl, n=2400, r=11)
+    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    got = gpu_cross(akm, X, 2400, wl.windows, wl.family, theta, V, N=128, m=8)
+    want = dense_cross(X[:2400], X[2400:], wl.windows, wl.family, theta, V)
+    assert rel(got, want) <= 1e-3
+
+
+def test_cross_host_buffers_and_edges(akm):
+    wl = workloads.CONFIGS["c1"]
+    X = workloads.make_X(wl, n=1500)
+    V = workloads.make_V(wl, n=1000, r=2)
+    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    dev_out = gpu_cross(akm, X, 1000, wl.windows, wl.family, theta, V)
+    host_out = gpu_cross(akm, X, 1000, wl.windows, wl.family, theta, V, host=True)
+    np.testing.assert_allclose(host_out, dev_out, rtol=1e-13, atol=1e-13)
+    assert rel(dev_out, dense_cross(X[:1000], X[1000:], wl.windows, wl.family, theta, V)) <= 1e-6
+    # no sources: the product is exactly zero
+    z = gpu_cross(akm, X, 0, wl.windows, wl.family, theta, np.zeros((0, 2)))
+    assert z.shape == (1500, 2) and np.all(z == 0.0)
+
+
+def test_cross_argument_errors(akm):
+    wl = workloads.CONFIGS["c1"]
+    X = workloads.make_X(wl, n=200)
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    V = torch.zeros((100, 1), dtype=torch.float64, device=dev)
+    Y = torch.zeros((100, 1), dtype=torch.float64, device=dev)
+    with pytest.raises(akm.AkmError):   # before set_points / set_theta
+        plan.cross_mvm(100, V, Y)
+    plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family, wl.N, 2.0, wl.m, 1.0 / 16)
+    plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    with pytest.raises(ValueError):     # V rows != n_src
+        plan.cross_mvm(101, V, Y)
+    st = akm._lib.akm_kernel_cross_mvm(plan.handle, 201, None, 1, 1, None, 1, None)
+    assert st == akm.AKM_ERR_INVALID_ARG
+    # n_src == n: nothing to compute, OK
+    assert akm._lib.akm_kernel_cross_mvm(plan.handle, 200, V.data_ptr(), 1, 1, None, 1, None) == akm.AKM_OK
+    plan.close()
+
+
+def test_cross_full_size_x4_row_sample(akm):
+    """x4 at full size (1e6 sources -> 1e5 targets, r = 11): seeded target rows vs the oracle."""
+    wl = workloads.CONFIGS["x4"]
+    n_src = wl.extra["n_src"]
+    X = workloads.make_X(wl)
+    V = workloads.make_V(wl, n=n_src)
+    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    got = gpu_cross(akm, X, n_src, wl.windows, wl.family, theta, V)
+    rows = workloads.make_rows(wl, 64, n=wl.n - n_src)
+    # the C dense oracle on the union with zero-padded V (equal to dense_cross by
+    # tests/test_oracle_cross.py), row-sampled at the targets
+    Vu = np.vstack([V, np.zeros((wl.n - n_src, wl.r))])
+    want = dense_apply(X, wl.windows, wl.family, theta, Vu, rows=n_src + rows, ops=("K",))["K"]
+    assert rel(got[rows], want) <= 1e-6

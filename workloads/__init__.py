@@ -55,8 +55,9 @@ class Workload:
 
     @property
     def units(self) -> int:
-        """n * r * windows: the unit the throughput metric counts (BASELINE.json metric)."""
-        return self.n * self.r * len(self.windows)
+        """n * r * windows: the unit the throughput metric counts (BASELINE.json metric); for a
+        cross-product workload (extra n_src) the TARGET points count: (n - n_src) * r * windows."""
+        return (self.n - self.extra.get("n_src", 0)) * self.r * len(self.windows)
 
 
 def _consecutive(start_count: int, size: int, count: int):
@@ -80,6 +81,13 @@ CONFIGS = {
                    ("K",), "normal_minmax", "normal_plus_rademacher",
                    "one Z~ evaluation: n=5e5 p=9, 3 Gaussian windows, 50 CG + 30 Lanczos, r=11 (theta per reading R10)",
                    extra={"cg_iters": 50, "lanczos_steps": 30, "n_z": 10}),
+    # SURVEY.md 8(f) f2 (not a BASELINE.json config): prediction at c4 scale -- K_{*X} V from
+    # 1e6 training points to 1e5 test points drawn with them (rows n_src.. of one c4-style X)
+    "x4": Workload("x4", 6, 1100000, 12, _consecutive(0, 3, 4), GAUSSIAN, 1.0, 0.3, 0.01, 11, 32, 2.0, 6, 1.0 / 16,
+                   ("K",), "normal_minmax", "normal_plus_rademacher",
+                   "cross K_{*X} V: 1e6 training -> 1e5 test points, p=12 N(0,1) min-max, 4 Gaussian windows of 3, "
+                   "r=11, N=32, m=6",
+                   extra={"n_src": 1000000}),
 }
 
 
