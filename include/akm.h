@@ -190,6 +190,21 @@ akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, 
                               void* stream);
 
 /* Library version string. */
+/* Gradient of the objective Z~ (eq. (div)) with M = diag(Khat) = c I,
+ * c = sigma_f^2 P + sigma_eps^2 (reading R11):
+ *   grad[k] = dZ~/dtheta_k ~= 1/2 ( -alpha^T dKhat_k alpha + tr(M^{-1} dM_k)
+ *             + (1/n_z) sum_i z_i^T (M^{-1} Khat)^{-1} d(M^{-1} Khat)_k z_i ),  theta = (sigma_f, ell, sigma_eps),
+ * where (M^{-1} Khat)^{-1} d(M^{-1} Khat)_k = Khat^{-1} dKhat_k - (dc_k / c) I and, Khat being
+ * symmetric, z^T Khat^{-1} dKhat_k z = (Khat^{-1} z)^T (dKhat_k z).  alpha = Khat^{-1} y and
+ * Khat^{-1} z_i come from cg_iters iterations of PCG (x0 = 0, M = c I) run on the n x (1 + n_z) block
+ * [y | Z] through the NFFT product; then one fused derivative product (dKhat/dell, dKhat/dsigma_f)
+ * on [alpha | Z] and column dot products on the device; the three sums are combined on the host.
+ * y: n; Z: n x n_z row-major (ld ldz >= n_z); device or host.  grad: host double[3] (output).
+ * cg_relres: optional host double[cg_iters] (column 0 relative residual per iteration, -1 if not
+ * run).  1 <= n_z <= AKM_MAX_PROBES, 0 <= cg_iters <= 1024.  Products: cg_iters + 1. */
+akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                             int32_t cg_iters, double* grad, double* cg_relres, void* stream);
+
 const char* akm_version(void);
 
 #ifdef __cplusplus

@@ -171,3 +171,32 @@ def objective_diag(apply_K, y, Z, diagM, cg_iters, lanczos_steps):
     Zt = 0.5 * (quad + logdetM + slq + n * math.log(2.0 * math.pi))
     return {"Z": Zt, "quad": quad, "logdetM": logdetM, "slq": slq, "samples": samples, "x": x,
             "cg_hist": cg_hist, "steps": [len(a) for a in alpha], "alpha": alpha, "beta": beta}
+
+
+def gradient_diag(apply_K, apply_dK, y, Z, c, dc, cg_iters):
+    """eq. (div) with M = c I (reading R11), for theta = (sigma_f, ell, sigma_eps):
+
+        dZ~/dtheta_j ~= 1/2 ( -alpha^T dKhat_j alpha + tr(M^{-1} dM_j)
+                              + (1/n_z) sum_i z_i^T (M^{-1} Khat)^{-1} d(M^{-1} Khat)_j z_i ).
+
+    With M = c I:  tr(M^{-1} dM_j) = n dc_j / c  and
+    (M^{-1} Khat)^{-1} d(M^{-1} Khat)_j = Khat^{-1} dKhat_j - (dc_j / c) I, so the probe term is
+    z_i^T w_i' - (dc_j / c) z_i^T z_i with w_i' = Khat^{-1} dKhat_j z_i; by symmetry of Khat,
+    z_i^T Khat^{-1} dKhat_j z_i = (Khat^{-1} z_i)^T (dKhat_j z_i).  alpha = Khat^{-1} y and
+    Khat^{-1} z_i come from fixed-iteration PCG (``pcg``, M^{-1} = 1/c) from x0 = 0.
+
+    apply_K(B) -> Khat B; apply_dK(B) -> dict j -> dKhat_j B for j in ("sf", "ell", "se").
+    dc: dict j -> dc/dtheta_j.  Returns dict j -> gradient component, plus the solves."""
+    y = np.asarray(y, dtype=np.float64)
+    Z = np.asarray(Z, dtype=np.float64)
+    n, n_z = Z.shape
+    minv = np.full(n, 1.0 / c)
+    alpha, _ = pcg(apply_K, y, cg_iters, minv)
+    W = np.stack([pcg(apply_K, Z[:, i], cg_iters, minv)[0] for i in range(n_z)], axis=1)
+    D = apply_dK(np.column_stack([alpha, Z]))
+    grad = {}
+    for j, Dj in D.items():
+        quad = -float(alpha @ Dj[:, 0])
+        probes = np.mean([float(W[:, i] @ Dj[:, 1 + i]) - dc[j] / c * float(Z[:, i] @ Z[:, i]) for i in range(n_z)])
+        grad[j] = 0.5 * (quad + n * dc[j] / c + probes)
+    return {"grad": grad, "alpha": alpha, "W": W}

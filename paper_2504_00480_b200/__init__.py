@@ -32,7 +32,7 @@ AKM_MAX_WINDOWS = 32
 ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm", "akm_kernel_deriv_mvm",
                "akm_kernel_mvm_multi", "akm_get_info", "akm_set_scale_override", "akm_last_error", "akm_destroy",
                "akm_version", "akm_set_profiling", "akm_get_stage_times", "akm_objective_diag",
-               "akm_kernel_cross_mvm")
+               "akm_kernel_cross_mvm", "akm_gradient_diag")
 AKM_MAX_PROBES = 31
 
 
@@ -92,6 +92,8 @@ def _load():
     lib.akm_kernel_mvm_multi.restype = st
     lib.akm_kernel_cross_mvm.argtypes = [P, i64, P, i64, i32, P, i64, P]
     lib.akm_kernel_cross_mvm.restype = st
+    lib.akm_gradient_diag.argtypes = [P, P, P, i64, i32, i32, P, P, P]
+    lib.akm_gradient_diag.restype = st
     lib.akm_get_info.argtypes = [P, ctypes.POINTER(akm_info)]
     lib.akm_get_info.restype = st
     lib.akm_set_scale_override.argtypes = [P, P]
@@ -282,6 +284,17 @@ def akm_objective_diag(plan, y, Z, cg_iters=50, lanczos_steps=30, stream=None) -
             "cg_relres": out.cg_relres, "cg_hist": [h for h in hist[:cg_iters]]}
 
 
+def akm_gradient_diag(plan, y, Z, cg_iters=50, stream=None) -> dict:
+    """eq. (div) with M = diag(Khat): block PCG on [y | Z], one fused derivative product (include/akm.h)."""
+    py, _, n, _, _, ky = _ptr_ld(y, "y")
+    pz, ldz, _, n_z, _, kz = _ptr_ld(Z, "Z")
+    grad = (ctypes.c_double * 3)()
+    hist = (ctypes.c_double * max(int(cg_iters), 1))()
+    _check(plan, _lib.akm_gradient_diag(plan, py, pz, ldz, n_z, int(cg_iters), grad, hist, _stream(stream, ky, kz)))
+    return {"grad": {"sf": grad[0], "ell": grad[1], "se": grad[2]}, "cg_hist": [h for h in hist[:cg_iters]],
+            "products": int(cg_iters) + 1}
+
+
 # ---------------------------------------------------------------- convenience wrapper
 class Plan:
     """RAII wrapper: ``Plan(device).set_points(...).set_theta(...)`` then ``mvm`` / ``deriv_mvm`` / ``mvm_multi``."""
@@ -328,6 +341,9 @@ class Plan:
     def cross_mvm(self, n_src, V, Yt, stream=None):
         akm_kernel_cross_mvm(self.handle, n_src, V, Yt, stream)
         return Yt
+
+    def gradient_diag(self, y, Z, cg_iters=50, stream=None):
+        return akm_gradient_diag(self.handle, y, Z, cg_iters, stream)
 
     def objective_diag(self, y, Z, cg_iters=50, lanczos_steps=30, stream=None):
         return akm_objective_diag(self.handle, y, Z, cg_iters, lanczos_steps, stream)

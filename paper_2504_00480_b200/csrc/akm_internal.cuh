@@ -237,6 +237,19 @@ int fft_launch_count(const WinTable& tab, int r);
 
 // krylov.cu (config-5 objective driver)
 size_t kr_state_bytes();
+// block PCG for the gradient (krylov.cu)
+size_t bcg_state_bytes();
+cudaError_t launch_bcg_init(void* st, const double* part, int R, double c, cudaStream_t s);
+cudaError_t launch_bcg_start(long long n, int R, const void* st, const double* B, double* Rr, double* P, double* X,
+                             cudaStream_t s);
+cudaError_t launch_bcg_after_dots(void* st, const double* part, int R, cudaStream_t s);
+cudaError_t launch_bcg_update(long long n, int R, const void* st, const double* P, const double* KP, double* Rr,
+                              double* X, cudaStream_t s);
+cudaError_t launch_bcg_after_norms(void* st, const double* part, int R, int t, cudaStream_t s);
+cudaError_t launch_bcg_dir(long long n, int R, const void* st, const double* Rr, double* P, cudaStream_t s);
+cudaError_t launch_bcg_grad_rhs(long long n, int R, const double* X, const double* B, double* B2, cudaStream_t s);
+cudaError_t launch_bcg_store(void* st, const double* part, int R, int slot, cudaStream_t s);
+void bcg_offsets(size_t* off_hist, size_t* off_out, size_t* off_bnorm);
 int kr_blocks();
 cudaError_t launch_kr_col2(long long n, int R, const double* A, const double* B, double* part, cudaStream_t s);
 cudaError_t launch_kr_load(long long n, int R, const double* y, const double* Z, long long ldz, double* B,

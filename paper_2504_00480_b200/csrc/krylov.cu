@@ -466,6 +466,145 @@ cudaError_t launch_kr_slq_quad(void* st, int R, const double* part_yx, int* err,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- gradient
+// eq. (div) needs alpha = Khat^{-1} y and Khat^{-1} z_i: fixed-iteration PCG with
+// M = c I from x0 = 0 on every column of the n x R block [y | Z] at once (one block product per
+// iteration; the columns are independent recurrences with their own scalars).
+struct BcgState {
+  double c;
+  double rz[kKrMaxR], a[kKrMaxR], beta[kKrMaxR];
+  double bnorm[kKrMaxR];                  // ||b_c|| (relative residuals)
+  double sums[2 * kKrMaxR];
+  double hist[kKrMaxIters];               // column 0 relative residual per iteration
+  double out[3][2 * kKrMaxR];             // the gradient dot products (col2 finals)
+};
+
+size_t bcg_state_bytes() { return sizeof(BcgState); }
+
+__global__ void k_bcg_init(BcgState* st, const double* __restrict__ part, int nblk, int R, double c) {
+  col2_final(part, nblk, R, st->sums);
+  __syncthreads();
+  if (threadIdx.x == 0) st->c = c;
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    st->rz[i] = st->sums[2 * i + 1] / c;
+    st->bnorm[i] = sqrt(st->sums[2 * i + 1]);
+    st->a[i] = st->beta[i] = 0.0;
+  }
+  for (int t = threadIdx.x; t < kKrMaxIters; t += blockDim.x) st->hist[t] = -1.0;
+}
+
+// R (residual) = B, P = B / c, X = 0
+__global__ void k_bcg_start(long long n, int R, const BcgState* __restrict__ st, const double* __restrict__ B,
+                            double* __restrict__ Rr, double* __restrict__ P, double* __restrict__ X) {
+  const double invc = 1.0 / st->c;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * R; e += (long long)gridDim.x * blockDim.x) {
+    const double b = B[e];
+    Rr[e] = b;
+    P[e] = b * invc;
+    X[e] = 0.0;
+  }
+}
+
+// a_c = rz_c / (p_c^T Khat p_c) for live columns (rz_c > 0)
+__global__ void k_bcg_after_dots(BcgState* st, const double* __restrict__ part, int nblk, int R) {
+  col2_final(part, nblk, R, st->sums);
+  __syncthreads();
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    const double pkp = st->sums[2 * i];
+    st->a[i] = (st->rz[i] > 0.0 && pkp != 0.0) ? st->rz[i] / pkp : 0.0;
+  }
+}
+
+// X += a P;  R -= a KP
+__global__ void k_bcg_update(long long n, int R, const BcgState* __restrict__ st, const double* __restrict__ P,
+                             const double* __restrict__ KP, double* __restrict__ Rr, double* __restrict__ X) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * R; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e - (e / R) * R);
+    const double a = st->a[c];
+    X[e] = fma(a, P[e], X[e]);
+    Rr[e] = fma(-a, KP[e], Rr[e]);
+  }
+}
+
+// rz_new = ||r||^2 / c, beta = rz_new / rz; column 0 relative residual into the history
+__global__ void k_bcg_after_norms(BcgState* st, const double* __restrict__ part, int nblk, int R, int t) {
+  col2_final(part, nblk, R, st->sums);
+  __syncthreads();
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    if (!(st->rz[i] > 0.0)) {
+      st->beta[i] = 0.0;
+      continue;
+    }
+    const double rr = st->sums[2 * i + 1], rz_new = rr / st->c;
+    st->beta[i] = rz_new / st->rz[i];
+    st->rz[i] = rz_new;
+    if (i == 0) st->hist[t] = sqrt(rr) / st->bnorm[0];
+  }
+}
+
+// P = R / c + beta P
+__global__ void k_bcg_dir(long long n, int R, const BcgState* __restrict__ st, const double* __restrict__ Rr,
+                          double* __restrict__ P) {
+  const double invc = 1.0 / st->c;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * R; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e - (e / R) * R);
+    P[e] = fma(st->beta[c], P[e], Rr[e] * invc);
+  }
+}
+
+// B2 = [alpha | Z]: column 0 from X, the probe columns from B (the original block)
+__global__ void k_bcg_grad_rhs(long long n, int R, const double* __restrict__ X, const double* __restrict__ B,
+                               double* __restrict__ B2) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * R; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e - (e / R) * R);
+    B2[e] = (c == 0) ? X[e] : B[e];
+  }
+}
+
+__global__ void k_bcg_store(BcgState* st, const double* __restrict__ part, int nblk, int R, int slot) {
+  col2_final(part, nblk, R, st->out[slot]);
+}
+
+cudaError_t launch_bcg_init(void* st, const double* part, int R, double c, cudaStream_t s) {
+  k_bcg_init<<<1, 256, 0, s>>>((BcgState*)st, part, kKrBlocks, R, c);
+  return cudaGetLastError();
+}
+cudaError_t launch_bcg_start(long long n, int R, const void* st, const double* B, double* Rr, double* P, double* X,
+                             cudaStream_t s) {
+  k_bcg_start<<<grid_for(n * R), 256, 0, s>>>(n, R, (const BcgState*)st, B, Rr, P, X);
+  return cudaGetLastError();
+}
+cudaError_t launch_bcg_after_dots(void* st, const double* part, int R, cudaStream_t s) {
+  k_bcg_after_dots<<<1, 256, 0, s>>>((BcgState*)st, part, kKrBlocks, R);
+  return cudaGetLastError();
+}
+cudaError_t launch_bcg_update(long long n, int R, const void* st, const double* P, const double* KP, double* Rr,
+                              double* X, cudaStream_t s) {
+  k_bcg_update<<<grid_for(n * R), 256, 0, s>>>(n, R, (const BcgState*)st, P, KP, Rr, X);
+  return cudaGetLastError();
+}
+cudaError_t launch_bcg_after_norms(void* st, const double* part, int R, int t, cudaStream_t s) {
+  k_bcg_after_norms<<<1, 256, 0, s>>>((BcgState*)st, part, kKrBlocks, R, t);
+  return cudaGetLastError();
+}
+cudaError_t launch_bcg_dir(long long n, int R, const void* st, const double* Rr, double* P, cudaStream_t s) {
+  k_bcg_dir<<<grid_for(n * R), 256, 0, s>>>(n, R, (const BcgState*)st, Rr, P);
+  return cudaGetLastError();
+}
+cudaError_t launch_bcg_grad_rhs(long long n, int R, const double* X, const double* B, double* B2, cudaStream_t s) {
+  k_bcg_grad_rhs<<<grid_for(n * R), 256, 0, s>>>(n, R, X, B, B2);
+  return cudaGetLastError();
+}
+cudaError_t launch_bcg_store(void* st, const double* part, int R, int slot, cudaStream_t s) {
+  k_bcg_store<<<1, 256, 0, s>>>((BcgState*)st, part, kKrBlocks, R, slot);
+  return cudaGetLastError();
+}
+void bcg_offsets(size_t* off_hist, size_t* off_out, size_t* off_bnorm) {
+  *off_hist = offsetof(BcgState, hist);
+  *off_out = offsetof(BcgState, out);
+  *off_bnorm = offsetof(BcgState, bnorm);
+}
+
 // host-readable summary (offsets into KrylovState)
 void kr_summary_offsets(size_t* off_quad, size_t* off_samples, size_t* off_steps, size_t* off_hist, size_t* off_znorm) {
   *off_quad = offsetof(KrylovState, quad);

@@ -91,6 +91,7 @@ struct akm_plan {
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
   DevBuf stageV, stageY, stageL, stageS;
   DevBuf crossV, crossY;  // akm_kernel_cross_mvm: zero-padded V and the union's product
+  DevBuf gX, gP, gB2, gD1, gD2, gState;  // akm_gradient_diag: block PCG and derivative products
   DevBuf krB, krKB, krW, krX, krY, krQ, krPart, krH, krState, krErr, krStage;
   long long r_cap = 0;
 
@@ -1188,6 +1189,117 @@ akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, 
   if (cg_relres)
     for (int t = 0; t < cg_iters; ++t) cg_relres[t] = hist[t];
   if (errf) return plan->fail(AKM_ERR_NONFINITE, "SLQ: tridiagonal eigensolve failed or non-positive Ritz value (flags %d)", errf);
+  return AKM_OK;
+}
+
+akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                             int32_t cg_iters, double* grad, double* cg_relres, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points || !plan->have_theta)
+    return plan->fail(AKM_ERR_STATE, "gradient_diag called before set_points and set_theta");
+  if (!grad) return plan->fail(AKM_ERR_INVALID_ARG, "grad is NULL");
+  if (n_z < 1 || n_z > AKM_MAX_PROBES) return plan->fail(AKM_ERR_INVALID_ARG, "n_z must be in [1, %d]", AKM_MAX_PROBES);
+  if (ldz < n_z) return plan->fail(AKM_ERR_INVALID_ARG, "ldz < n_z");
+  if (cg_iters < 0 || cg_iters > kKrMaxIters) return plan->fail(AKM_ERR_INVALID_ARG, "cg_iters must be in [0, %d]", kKrMaxIters);
+  const long long n = plan->n;
+  if (n < 1) return plan->fail(AKM_ERR_INVALID_ARG, "gradient needs n >= 1");
+  if (!y || !Z) return plan->fail(AKM_ERR_INVALID_ARG, "y or Z is NULL");
+  cudaStream_t s = S(stream);
+  AKM_CK(cudaSetDevice(plan->device));
+  const int R = 1 + n_z;
+  const long long blk = n * R;
+  const double* yd = y;
+  const double* Zd = Z;
+  long long ldzd = ldz;
+  const bool y_dev = is_device_ptr(y), z_dev = is_device_ptr(Z);
+  if (!y_dev || !z_dev) {
+    AKM_CK(plan->krStage.ensure(sizeof(double) * (size_t)(n + n * n_z)));
+    double* st = plan->krStage.as<double>();
+    if (!y_dev) {
+      AKM_CK(cudaMemcpyAsync(st, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      yd = st;
+    }
+    if (!z_dev) {
+      AKM_CK(cudaMemcpy2DAsync(st + n, sizeof(double) * n_z, Z, sizeof(double) * ldz, sizeof(double) * n_z, n,
+                               cudaMemcpyHostToDevice, s));
+      Zd = st + n;
+      ldzd = n_z;
+    }
+  }
+  const int nblk = kr_blocks();
+  AKM_CK(plan->krB.ensure(sizeof(double) * blk));
+  AKM_CK(plan->krKB.ensure(sizeof(double) * blk));
+  AKM_CK(plan->krW.ensure(sizeof(double) * blk));
+  AKM_CK(plan->krY.ensure(sizeof(double) * n));
+  AKM_CK(plan->gX.ensure(sizeof(double) * blk));
+  AKM_CK(plan->gP.ensure(sizeof(double) * blk));
+  AKM_CK(plan->gB2.ensure(sizeof(double) * blk));
+  AKM_CK(plan->gD1.ensure(sizeof(double) * blk));
+  AKM_CK(plan->gD2.ensure(sizeof(double) * blk));
+  AKM_CK(plan->krPart.ensure(sizeof(double) * (size_t)nblk * 2 * R));
+  AKM_CK(plan->gState.ensure(bcg_state_bytes()));
+  double* B = plan->krB.as<double>();
+  double* KP = plan->krKB.as<double>();
+  double* Rr = plan->krW.as<double>();
+  double* X = plan->gX.as<double>();
+  double* P = plan->gP.as<double>();
+  double* part = plan->krPart.as<double>();
+  void* st = plan->gState.p;
+  // M = diag(Khat) = c I (reading R11); dc/dsigma_f = 2 sigma_f P, dc/dsigma_eps = 2 sigma_eps
+  const double c = plan->sigma_f * plan->sigma_f * plan->P + plan->sigma_eps * plan->sigma_eps;
+  AKM_CK(launch_kr_load(n, R, yd, Zd, ldzd, B, plan->krY.as<double>(), s));
+  AKM_CK(launch_kr_col2(n, R, B, B, part, s));
+  AKM_CK(launch_bcg_init(st, part, R, c, s));
+  AKM_CK(launch_bcg_start(n, R, st, B, Rr, P, X, s));
+  plan->launches += 5;
+  for (int t = 0; t < cg_iters; ++t) {
+    akm_status stt = run_mvm(plan, P, R, R, KP, nullptr, nullptr, R, s);
+    if (stt != AKM_OK) return stt;
+    AKM_CK(launch_kr_col2(n, R, P, KP, part, s));
+    AKM_CK(launch_bcg_after_dots(st, part, R, s));
+    AKM_CK(launch_bcg_update(n, R, st, P, KP, Rr, X, s));
+    AKM_CK(launch_kr_col2(n, R, Rr, Rr, part, s));
+    AKM_CK(launch_bcg_after_norms(st, part, R, t, s));
+    AKM_CK(launch_bcg_dir(n, R, st, Rr, P, s));
+    plan->launches += 6;
+  }
+  // one fused derivative product on [alpha | Z]
+  double* B2 = plan->gB2.as<double>();
+  double* D1 = plan->gD1.as<double>();
+  double* D2 = plan->gD2.as<double>();
+  AKM_CK(launch_bcg_grad_rhs(n, R, X, B, B2, s));
+  akm_status stt = run_mvm(plan, B2, R, R, nullptr, D1, D2, R, s);
+  if (stt != AKM_OK) return stt;
+  const double* Ds[3] = {D1, D2, B2};  // ell, sigma_f, sigma_eps (dKhat/dsigma_eps = 2 sigma_eps I)
+  for (int j = 0; j < 3; ++j) {
+    AKM_CK(launch_kr_col2(n, R, X, Ds[j], part, s));
+    AKM_CK(launch_bcg_store(st, part, R, j, s));
+  }
+  plan->launches += 7;
+  size_t o_hist, o_out, o_bn;
+  bcg_offsets(&o_hist, &o_out, &o_bn);
+  std::vector<double> outv(3 * 2 * kKrMaxR), bn(R), hist(std::max(cg_iters, 1));
+  const char* base = static_cast<const char*>(st);
+  AKM_CK(cudaMemcpyAsync(outv.data(), base + o_out, sizeof(double) * outv.size(), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaMemcpyAsync(bn.data(), base + o_bn, sizeof(double) * R, cudaMemcpyDeviceToHost, s));
+  if (cg_iters > 0)
+    AKM_CK(cudaMemcpyAsync(hist.data(), base + o_hist, sizeof(double) * cg_iters, cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaStreamSynchronize(s));
+  // eq. (div): 1/2 (-alpha^T dK alpha + n dc/c + (1/n_z) sum_i [(Khat^{-1} z_i)^T dK z_i - dc/c ||z_i||^2])
+  const double sf = plan->sigma_f, se = plan->sigma_eps;
+  const double scale[3] = {1.0, 1.0, 2.0 * se};          // dK applied: D1, D2 as computed; 2 se * B2
+  const double dc[3] = {0.0, 2.0 * sf * plan->P, 2.0 * se};
+  const int slot_of_param[3] = {1, 0, 2};                  // grad order (sigma_f, ell, sigma_eps)
+  for (int k = 0; k < 3; ++k) {
+    const int j = slot_of_param[k];
+    const double* o = outv.data() + j * 2 * kKrMaxR;
+    double probes = 0.0;
+    for (int i = 1; i < R; ++i) probes += scale[j] * o[2 * i] - dc[j] / c * bn[i] * bn[i];
+    grad[k] = 0.5 * (-scale[j] * o[0] + (double)n * dc[j] / c + probes / n_z);
+  }
+  if (cg_relres)
+    for (int t = 0; t < cg_iters; ++t) cg_relres[t] = hist[t];
   return AKM_OK;
 }
 
