@@ -269,6 +269,14 @@ def main():
 
         def step():
             last["out"] = plan.objective_diag(yd, Zd, cg, lz)
+    elif "grad_cg_iters" in wl.extra:        # g5: one gradient of Z~ per step (f1)
+        gcg = wl.extra["grad_cg_iters"]
+        yd, Zd = Vd[:, 0].contiguous(), Vd[:, 1:].contiguous()
+        products_per_step = gcg + 1
+        last = {}
+
+        def step():
+            last["out"] = plan.gradient_diag(yd, Zd, gcg)
     elif cross:
         products_per_step = 1
 
@@ -325,12 +333,15 @@ def main():
     Vh = torch.from_numpy(V).pin_memory()
     Oh = {op: torch.empty(tuple(outs[op].shape) if cross else V.shape, dtype=torch.float64).pin_memory()
           for op in wl.ops}
-    if objective:
+    gradient = "grad_cg_iters" in wl.extra
+    if objective or gradient:
         yh, Zh = Vh[:, 0].contiguous().pin_memory(), Vh[:, 1:].contiguous().pin_memory()
 
     def e2e_step():
         if objective:   # host y, Z in; the objective's terms come back to the host
             plan.objective_diag(yh, Zh, cg, lz, stream=stream.cuda_stream)
+        elif gradient:  # host y, Z in; the three components come back to the host
+            plan.gradient_diag(yh, Zh, gcg, stream=stream.cuda_stream)
         elif cross:
             plan.cross_mvm(n_src, Vh, Oh["K"], stream=stream.cuda_stream)
         else:
@@ -378,7 +389,7 @@ def main():
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": config_dict(wl),
         "e2e": {"value": e2e_value, "unit": "pts/s", "h2d_bytes_per_step": int(V.nbytes),
-                "d2h_bytes_per_step": int(8 * (10 + 2 * wl.r) if objective else
+                "d2h_bytes_per_step": int(8 * (10 + 2 * wl.r) if objective else 8 * (3 + gcg) if gradient else
                                           sum(o.numel() * 8 for o in Oh.values()))},
         "gpu_launches": int(launches_timed),
         "roofline": {"bound": "alu", "kernel": name, "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
@@ -401,6 +412,9 @@ def main():
         line["objective"] = {"Z": o["Z"], "quad": o["quad"], "logdetM": o["logdetM"], "slq": o["slq"],
                              "cg_relres": o["cg_relres"], "steps": o["steps"], "ms_per_evaluation": ms_per_step,
                              "ms_per_product": ms_per_step / products_per_step}
+    if gradient:
+        line["gradient"] = {"grad": last["out"]["grad"], "cg_relres_last": last["out"]["cg_hist"][-1],
+                            "ms_per_evaluation": ms_per_step, "ms_per_product": ms_per_step / products_per_step}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl)
     plan.close()

@@ -88,6 +88,13 @@ CONFIGS = {
                    "cross K_{*X} V: 1e6 training -> 1e5 test points, p=12 N(0,1) min-max, 4 Gaussian windows of 3, "
                    "r=11, N=32, m=6",
                    extra={"n_src": 1000000}),
+    # SURVEY.md 8(f) f1 (not a BASELINE.json config): one gradient of Z~ at c5's sizes -- 50 block
+    # PCG iterations on [y | Z] (r = 11) and one fused derivative product (dKhat/dell, dKhat/dsigma_f)
+    "g5": Workload("g5", 5, 500000, 9, _consecutive(0, 3, 3), GAUSSIAN, 1.0, 0.5, 0.05, 11, 32, 2.0, 6, 1.0 / 16,
+                   ("K",), "normal_minmax", "normal_plus_rademacher",
+                   "one gradient of Z~: n=5e5 p=9, 3 Gaussian windows, 50 block-PCG iterations at r=11 + one "
+                   "dKhat/dell, dKhat/dsigma_f product (theta per reading R10)",
+                   extra={"grad_cg_iters": 50, "n_z": 10}),
 }
 
 
