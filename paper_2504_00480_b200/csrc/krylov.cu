@@ -200,7 +200,23 @@ __global__ void k_kr_proj_partial(long long n, int R, int nq, const double* __re
   double acc[kProjJC];
 #pragma unroll
   for (int jj = 0; jj < kProjJC; ++jj) acc[jj] = 0.0;
-  for (long long k = (long long)blockIdx.x * 32 + slot; k < n; k += (long long)gridDim.x * 32) {
+  // two rows per iteration: 2 kProjJC independent loads in flight per thread (the kernel is
+  // latency-bound at the occupancy its registers allow)
+  const long long stride = (long long)gridDim.x * 32;
+  long long k = (long long)blockIdx.x * 32 + slot;
+  for (; k + stride < n; k += 2 * stride) {
+    const long long e0 = k * R + c, e1 = e0 + stride * R;
+    const double w0 = W[e0], w1 = W[e1];
+    double q0[kProjJC], q1[kProjJC];
+#pragma unroll
+    for (int jj = 0; jj < kProjJC; ++jj) {
+      q0[jj] = jj < jn ? Q[(long long)(j0 + jj) * slab + e0] : 0.0;
+      q1[jj] = jj < jn ? Q[(long long)(j0 + jj) * slab + e1] : 0.0;
+    }
+#pragma unroll
+    for (int jj = 0; jj < kProjJC; ++jj) acc[jj] = fma(q1[jj], w1, fma(q0[jj], w0, acc[jj]));
+  }
+  for (; k < n; k += stride) {
     const long long e = k * R + c;
     const double w = W[e];
 #pragma unroll
