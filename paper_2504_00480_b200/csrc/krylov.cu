@@ -193,8 +193,8 @@ __global__ void k_kr_update(long long n, int R, const KrylovState* __restrict__ 
 constexpr int kProjJC = 8;
 __global__ void k_kr_proj_partial(long long n, int R, int nq, const double* __restrict__ Q, long long slab,
                                   const double* __restrict__ W, double* __restrict__ part) {
-  extern __shared__ double sm[];  // [JC][32][R]
-  const int t = threadIdx.x, c = t % R, slot = t / R;
+  extern __shared__ double sm[];  // [JC][S][R], S = blockDim.x / R row slots
+  const int t = threadIdx.x, c = t % R, slot = t / R, S = blockDim.x / R;
   const int j0 = blockIdx.y * kProjJC;
   const int jn = min(kProjJC, nq - j0);
   double acc[kProjJC];
@@ -202,8 +202,8 @@ __global__ void k_kr_proj_partial(long long n, int R, int nq, const double* __re
   for (int jj = 0; jj < kProjJC; ++jj) acc[jj] = 0.0;
   // two rows per iteration: 2 kProjJC independent loads in flight per thread (the kernel is
   // latency-bound at the occupancy its registers allow)
-  const long long stride = (long long)gridDim.x * 32;
-  long long k = (long long)blockIdx.x * 32 + slot;
+  const long long stride = (long long)gridDim.x * S;
+  long long k = (long long)blockIdx.x * S + slot;
   for (; k + stride < n; k += 2 * stride) {
     const long long e0 = k * R + c, e1 = e0 + stride * R;
     const double w0 = W[e0], w1 = W[e1];
@@ -224,12 +224,12 @@ __global__ void k_kr_proj_partial(long long n, int R, int nq, const double* __re
       if (jj < jn) acc[jj] = fma(Q[(long long)(j0 + jj) * slab + e], w, acc[jj]);
   }
 #pragma unroll
-  for (int jj = 0; jj < kProjJC; ++jj) sm[(jj * 32 + slot) * R + c] = acc[jj];
+  for (int jj = 0; jj < kProjJC; ++jj) sm[(jj * S + slot) * R + c] = acc[jj];
   __syncthreads();
   for (int idx = t; idx < jn * R; idx += blockDim.x) {
     const int jj = idx / R, cc = idx % R;
     double s = 0.0;
-    for (int q = 0; q < 32; ++q) s += sm[(jj * 32 + q) * R + cc];
+    for (int q = 0; q < S; ++q) s += sm[(jj * S + q) * R + cc];
     part[((long long)blockIdx.x * nq + j0 + jj) * R + cc] = s;
   }
 }
@@ -453,7 +453,8 @@ cudaError_t launch_kr_reorth(long long n, int R, int nq, const void* st, const d
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_kr_proj_partial<<<dim3(kKrBlocks, chunks), 32 * R, sizeof(double) * kProjJC * 32 * R, s>>>(n, R, nq, Q, slab, W,
+  const int slots = R <= 16 ? 32 : 16;  // block <= 512 threads: the registers of 2 rows in flight fit
+  k_kr_proj_partial<<<dim3(kKrBlocks, chunks), slots * R, sizeof(double) * kProjJC * slots * R, s>>>(n, R, nq, Q, slab, W,
                                                                                                   part);
   k_kr_proj_final<<<(nq * R + 7) / 8, 256, 0, s>>>(part, kKrBlocks, nq, R, h);
   k_kr_orth_update<<<grid_for(n * R), 256, sizeof(double) * nq * R, s>>>(n, R, nq, (const KrylovState*)st, Q, slab, h,
