@@ -124,8 +124,9 @@ akm_status akm_kernel_mvm_multi(akm_plan* plan, const double* V, int64_t ldv, in
  * reading R2 holds the union), so every source-target difference stays inside the torus window.
  * V: n_src x r (ld ldv >= r); Yt: (n - n_src) x r (ld ldy >= r); row-major float64, device or host
  * memory (host buffers are staged).  0 <= n_src <= n, else INVALID_ARG; n_src == n is a no-op;
- * n_src == 0 gives Yt = 0.  Cost: one product on the union with V zero-padded (the targets' rows
- * of that product are exactly the cross product, since their V rows are zero). */
+ * n_src == 0 gives Yt = 0.  The first call with a given n_src re-sorts the points so that every
+ * bin holds its sources, then its targets; the product then spreads only the sources and
+ * interpolates only at the targets (the square products keep working on the same plan). */
 akm_status akm_kernel_cross_mvm(akm_plan* plan, int64_t n_src, const double* V, int64_t ldv, int32_t r,
                                 double* Yt, int64_t ldy, void* stream);
 

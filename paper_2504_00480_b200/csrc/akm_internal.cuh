@@ -192,10 +192,10 @@ cudaError_t launch_window_radius(const double* X, long long n, long long ldx, co
                                  const WinTable* dtab, double* r2_dev, cudaStream_t s);
 cudaError_t launch_scale_and_key(const double* X, long long n, long long ldx, const WinTable& tab,
                                  const WinTable* dtab, double* u_tmp, int* key, int* hist, const long long* hist_off,
-                                 int* err_flag, cudaStream_t s);
+                                 int* err_flag, long long n_split, cudaStream_t s);
 cudaError_t launch_scatter(long long n, const WinTable& tab, const WinTable* dtab, const double* u_tmp,
                            const int* key, int* cursor, const long long* hist_off, double* u_sorted, int* perm,
-                           cudaStream_t s);
+                           long long n_split, cudaStream_t s);
 cudaError_t launch_kernel_samples(int family, int d, int N, double ell_eff, int deriv, double* out, cudaStream_t s);
 cudaError_t launch_cos_dft_axis(int d, int N, int axis, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_multiplier(const WinTable& tab, const WinTable* dtab, int win, const double* bK, const double* bL,
@@ -273,6 +273,8 @@ int interp_rc_for(int r_remaining);
 cudaError_t launch_interp(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                           int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm, const double* H,
                           int d, int taps, int ops, int r, int r0, int rc, double* part, long long n, cudaStream_t s);
+cudaError_t launch_epilogue_cross(long long n, long long n_src, int P, int r, int ops, int slotK, const double* part,
+                                  double sigma_f, double* Yt, long long ldy, cudaStream_t s);
 cudaError_t launch_epilogue(long long n, int P, int r, int ops, const double* part, const double* V, long long ldv,
                             double sigma_f, double sigma_eps, double* Y, double* dYl, double* dYsf, long long ldy,
                             int slotK, int slotL, cudaStream_t s);

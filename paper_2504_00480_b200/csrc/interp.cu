@@ -120,6 +120,33 @@ cudaError_t launch_epilogue(long long n, int P, int r, int ops, const double* pa
   return cudaGetLastError();
 }
 
+// cross product (akm_kernel_cross_mvm): Yt[i - n_src][c] = sigma_f^2 sum_w S^w[i][c] for the target
+// rows i >= n_src (no noise term: a target is not a training point), windows in a fixed order
+__global__ void k_epilogue_cross(long long n, long long n_src, int P, int r, int ops, int slotK,
+                                 const double* __restrict__ part, double sigma_f, double* __restrict__ Yt,
+                                 long long ldy) {
+  const long long total = (n - n_src) * r;
+  const double sf2 = sigma_f * sigma_f;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long t = idx / r, i = n_src + t;
+    const int c = (int)(idx - t * r);
+    double sK = 0.0;
+    for (int w = 0; w < P; ++w) sK += part[(((long long)w * n + i) * ops + slotK) * r + c];
+    Yt[t * ldy + c] = sf2 * sK;
+  }
+}
+
+cudaError_t launch_epilogue_cross(long long n, long long n_src, int P, int r, int ops, int slotK, const double* part,
+                                  double sigma_f, double* Yt, long long ldy, cudaStream_t s) {
+  const long long total = (n - n_src) * r;
+  if (total <= 0) return cudaSuccess;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_epilogue_cross<<<(int)blocks, 256, 0, s>>>(n, n_src, P, r, ops, slotK, part, sigma_f, Yt, ldy);
+  return cudaGetLastError();
+}
+
 __global__ void k_scaled_copy(long long n, int r, double alpha, const double* __restrict__ V, long long ldv,
                               double* __restrict__ Y, long long ldy) {
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n * r;

@@ -50,13 +50,17 @@ struct DevBuf {
   T* as() const { return static_cast<T*>(p); }
 };
 
-struct Group {  // windows sharing (d, F) -> one spread / interp launch
-  int d = 0, F = 0;
-  std::vector<int> wins;
-  int spread_begin = 0, spread_count = 0;  // slice of the concatenated spread work items
+struct ItemSlice {  // a group's slice of the concatenated work items of one item set
+  int spread_begin = 0, spread_count = 0;
   int interp_begin = 0, interp_count = 0;
   int interp_bin_begin = 0, interp_bin_count = 0;
   bool sparse = false;  // few points per occupied cell: interpolate per bin (scalar) rather than per cell
+};
+
+struct Group {  // windows sharing (d, F) -> one spread / interp launch
+  int d = 0, F = 0;
+  std::vector<int> wins;
+  ItemSlice sl[2];  // item set 0: square product; 1: cross product (sources -> targets)
 };
 
 }  // namespace
@@ -81,13 +85,15 @@ struct akm_plan {
   std::vector<double> c_w, c_w_binned;      // current scale, scale the bins were built for
   WinTable tab{};                           // host copy
   PolyParam poly_param{};                   // window polynomials, passed to kernels by value
-  std::vector<WorkItem> items_spread, items_interp, items_interp_bin;
+  std::vector<WorkItem> items_spread[2], items_interp[2], items_interp_bin[2];  // [item set]
   std::vector<Group> groups;
   std::vector<long long> occupied, maxbin;
   long long total_taps = 0, szA1 = 0, szA2 = 0, szA3 = 0, szC = 0, szC2 = 0, szTW = 0, szD = 0;
 
   // device buffers
-  DevBuf dtab, Xc, u_tmp, u_sorted, perm, hist, hist_off, err_flag, items_s, items_i, items_ib, minmax, r2;
+  DevBuf dtab, Xc, u_tmp, u_sorted, perm, hist, hist_off, err_flag, minmax, r2;
+  DevBuf items_s[2], items_i[2], items_ib[2];  // [item set]
+  long long n_split = 0;  // rows >= n_split are class 1 (cross-product targets); n = no targets
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
   DevBuf stageV, stageY, stageL, stageS;
   DevBuf crossV, crossY;  // akm_kernel_cross_mvm: zero-padded V and the union's product
@@ -101,9 +107,10 @@ struct akm_plan {
     long long ldv, ldy;
     int r;
     long long epoch;
+    int set;
     bool operator==(const GraphKey& o) const {
       return V == o.V && Y == o.Y && dYl == o.dYl && dYsf == o.dYsf && ldv == o.ldv && ldy == o.ldy && r == o.r &&
-             epoch == o.epoch;
+             epoch == o.epoch && set == o.set;
     }
   };
   long long epoch = 0;                 // bumped whenever buffers, items or theta change
@@ -239,7 +246,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
       g.L[a] = g.ncell[a] + 2 * m - 1;
       g.K[a] = (a == 2) ? plan->N / 2 + 1 : plan->N + 1;
     }
-    hoff[w + 1] = hoff[w] + (long long)g.ncell[0] * g.ncell[1] * g.ncell[2];
+    hoff[w + 1] = hoff[w] + 2LL * g.ncell[0] * g.ncell[1] * g.ncell[2];  // (cell, class) slots
   }
   const long long ncells = hoff[P];
   AKM_CK(plan->hist.ensure(sizeof(int) * std::max<long long>(ncells, 1)));
@@ -255,7 +262,8 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   AKM_CK(cudaMemsetAsync(plan->err_flag.p, 0, sizeof(int), s));
   const int nf = (int)plan->feat_used.size();
   AKM_CK(launch_scale_and_key(plan->Xc.as<double>(), n, nf, tab, plan->dtab.as<WinTable>(), plan->u_tmp.as<double>(),
-                              nullptr, plan->hist.as<int>(), plan->hist_off.as<long long>(), plan->err_flag.as<int>(), s));
+                              nullptr, plan->hist.as<int>(), plan->hist_off.as<long long>(), plan->err_flag.as<int>(),
+                              plan->n_split, s));
   std::vector<int> hist(std::max<long long>(ncells, 1));
   int errf = 0;
   AKM_CK(cudaMemcpyAsync(hist.data(), plan->hist.p, sizeof(int) * std::max<long long>(ncells, 1), cudaMemcpyDeviceToHost, s));
@@ -265,16 +273,22 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
 
   // choose B per window (cost model in FMA-equivalents per RHS)
   std::vector<int> cell_off(std::max<long long>(ncells, 1), 0);
-  plan->items_spread.clear();
-  plan->items_interp.clear();
-  plan->items_interp_bin.clear();
+  for (int set = 0; set < 2; ++set) {
+    plan->items_spread[set].clear();
+    plan->items_interp[set].clear();
+    plan->items_interp_bin[set].clear();
+  }
   plan->occupied.assign(P, 0);
   plan->maxbin.assign(P, 0);
   const long long total_pts = n * P;
   long long ch_s = total_pts / (148 * 2);
   ch_s = std::max(32LL, std::min(4096LL, ch_s));
   const int ch_i = 128;  // interpolation: one cell per work item (64 thr x 2 pts, or 8 warps x 16 pts on DMMA)
-  std::vector<std::vector<WorkItem>> its_s(P), its_i(P), its_ib(P);
+  // item set 0: the square product over all points; set 1: the cross product (spread the class-0
+  // sources, interpolate at the class-1 targets; akm_kernel_cross_mvm)
+  std::vector<std::vector<WorkItem>> its_s[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
+  std::vector<std::vector<WorkItem>> its_i[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
+  std::vector<std::vector<WorkItem>> its_ib[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
   const int ch_ib = 128;  // interpolation, few values per node: one bin per work item, 1 point / thread
   for (int w = 0; w < P; ++w) {
     WinGeom& g = tab.w[w];
@@ -302,7 +316,8 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
       for (int c0 = 0; c0 < g.ncell[0]; ++c0)
         for (int c1 = 0; c1 < g.ncell[1]; ++c1)
           for (int c2 = 0; c2 < g.ncell[2]; ++c2) {
-            const int v = hc[((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2];
+            const long long ci = ((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2;
+            const int v = hc[2 * ci] + hc[2 * ci + 1];
             if (!v) continue;
             const int b0 = (3 - d > 0) ? 0 : c0 / B, b1 = (3 - d > 1) ? 0 : c1 / B, b2 = c2 / B;
             bc[((size_t)b0 * nb[1] + b1) * nb[2] + b2] += v;
@@ -335,33 +350,45 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
                           "window %d: grid box of %d nodes exceeds the oversampled grid (n_g = %d); "
                           "increase N or sigma_over, or decrease m", w, g.L[a], n_g);
     }
-    // cell offsets in bin-major order and work items
+    // cell offsets in bin-major order (inside a bin: the class-0 points cell by cell, then the
+    // class-1 points cell by cell) and work items
     long long pos = 0;
     const int Bd0 = (3 - d > 0) ? 1 : B, Bd1 = (3 - d > 1) ? 1 : B, Bd2 = B;
     for (int b0 = 0; b0 < g.nbin[0]; ++b0)
       for (int b1 = 0; b1 < g.nbin[1]; ++b1)
         for (int b2 = 0; b2 < g.nbin[2]; ++b2) {
           const long long start = pos;
-          for (int s0 = 0; s0 < Bd0; ++s0)
-            for (int s1 = 0; s1 < Bd1; ++s1)
-              for (int s2 = 0; s2 < Bd2; ++s2) {
-                const int c0 = b0 * Bd0 + s0, c1 = b1 * Bd1 + s1, c2 = b2 * Bd2 + s2;
-                if (c0 >= g.ncell[0] || c1 >= g.ncell[1] || c2 >= g.ncell[2]) continue;
-                const long long ci = ((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2;
-                cell_off[hoff[w] + ci] = (int)pos;
-                const int cc = hc[ci];
-                for (int q = 0; q < cc; q += ch_i)
-                  its_i[w].push_back(WorkItem{w, {c0, c1, c2}, (int)(pos + q), std::min(ch_i, cc - q)});
-                pos += cc;
-              }
+          long long cls_start[2] = {pos, pos};
+          for (int cls = 0; cls < 2; ++cls) {
+            cls_start[cls] = pos;
+            for (int s0 = 0; s0 < Bd0; ++s0)
+              for (int s1 = 0; s1 < Bd1; ++s1)
+                for (int s2 = 0; s2 < Bd2; ++s2) {
+                  const int c0 = b0 * Bd0 + s0, c1 = b1 * Bd1 + s1, c2 = b2 * Bd2 + s2;
+                  if (c0 >= g.ncell[0] || c1 >= g.ncell[1] || c2 >= g.ncell[2]) continue;
+                  const long long ci = ((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2;
+                  cell_off[hoff[w] + 2 * ci + cls] = (int)pos;
+                  const int cc = hc[2 * ci + cls];
+                  for (int q = 0; q < cc; q += ch_i) {
+                    const WorkItem wi{w, {c0, c1, c2}, (int)(pos + q), std::min(ch_i, cc - q)};
+                    its_i[0][w].push_back(wi);
+                    if (cls == 1) its_i[1][w].push_back(wi);
+                  }
+                  pos += cc;
+                }
+          }
           const long long cnt = pos - start;
           if (!cnt) continue;
           plan->occupied[w] += 1;
           plan->maxbin[w] = std::max(plan->maxbin[w], cnt);
-          for (long long q = 0; q < cnt; q += ch_s)
-            its_s[w].push_back(WorkItem{w, {b0, b1, b2}, (int)(start + q), (int)std::min<long long>(ch_s, cnt - q)});
-          for (long long q = 0; q < cnt; q += ch_ib)
-            its_ib[w].push_back(WorkItem{w, {b0, b1, b2}, (int)(start + q), (int)std::min<long long>(ch_ib, cnt - q)});
+          auto chunk = [&](std::vector<WorkItem>& out, long long a, long long e, long long ch) {
+            for (long long q = a; q < e; q += ch)
+              out.push_back(WorkItem{w, {b0, b1, b2}, (int)q, (int)std::min<long long>(ch, e - q)});
+          };
+          chunk(its_s[0][w], start, pos, ch_s);
+          chunk(its_ib[0][w], start, pos, ch_ib);
+          chunk(its_s[1][w], cls_start[0], cls_start[1], ch_s);  // sources
+          chunk(its_ib[1][w], cls_start[1], pos, ch_ib);         // targets
         }
     if (pos != n) return plan->fail(AKM_ERR_CUDA, "internal error: histogram of window %d holds %lld of %lld points",
                                     w, pos, n);
@@ -384,27 +411,33 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     grp->wins.push_back(w);
   }
   for (auto& grp : plan->groups) {
-    std::vector<WorkItem> gs, gi, gib;
-    for (int w : grp.wins) {
-      gs.insert(gs.end(), its_s[w].begin(), its_s[w].end());
-      gi.insert(gi.end(), its_i[w].begin(), its_i[w].end());
-      gib.insert(gib.end(), its_ib[w].begin(), its_ib[w].end());
+    for (int set = 0; set < 2; ++set) {
+      std::vector<WorkItem> gs, gi, gib;
+      for (int w : grp.wins) {
+        gs.insert(gs.end(), its_s[set][w].begin(), its_s[set][w].end());
+        gi.insert(gi.end(), its_i[set][w].begin(), its_i[set][w].end());
+        gib.insert(gib.end(), its_ib[set][w].begin(), its_ib[set][w].end());
+      }
+      auto larger_first = [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; };
+      std::stable_sort(gs.begin(), gs.end(), larger_first);
+      std::stable_sort(gi.begin(), gi.end(), larger_first);
+      std::stable_sort(gib.begin(), gib.end(), larger_first);
+      ItemSlice& sl = grp.sl[set];
+      sl.spread_begin = (int)plan->items_spread[set].size();
+      sl.spread_count = (int)gs.size();
+      sl.interp_begin = (int)plan->items_interp[set].size();
+      sl.interp_count = (int)gi.size();
+      plan->items_spread[set].insert(plan->items_spread[set].end(), gs.begin(), gs.end());
+      plan->items_interp[set].insert(plan->items_interp[set].end(), gi.begin(), gi.end());
+      // per-cell DMMA items pay a whole cell footprint per item: with few points per occupied cell
+      // the per-bin scalar kernel wins (c3: ~16 points per cell; c4/c5: hundreds)
+      long long pts = 0;
+      for (const WorkItem& it : gi) pts += it.count;
+      sl.sparse = gi.size() > 0 && (double)pts / (double)gi.size() < 48.0;
+      sl.interp_bin_begin = (int)plan->items_interp_bin[set].size();
+      sl.interp_bin_count = (int)gib.size();
+      plan->items_interp_bin[set].insert(plan->items_interp_bin[set].end(), gib.begin(), gib.end());
     }
-    std::stable_sort(gs.begin(), gs.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
-    std::stable_sort(gi.begin(), gi.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
-    std::stable_sort(gib.begin(), gib.end(), [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; });
-    grp.spread_begin = (int)plan->items_spread.size();
-    grp.spread_count = (int)gs.size();
-    grp.interp_begin = (int)plan->items_interp.size();
-    grp.interp_count = (int)gi.size();
-    plan->items_spread.insert(plan->items_spread.end(), gs.begin(), gs.end());
-    plan->items_interp.insert(plan->items_interp.end(), gi.begin(), gi.end());
-    // per-cell DMMA items pay a whole cell footprint per item: with few points per occupied cell
-    // the per-bin scalar kernel wins (c3: ~16 points per cell; c4/c5: hundreds)
-    grp.sparse = gi.size() > 0 && (double)(n * grp.wins.size()) / (double)gi.size() < 48.0;
-    grp.interp_bin_begin = (int)plan->items_interp_bin.size();
-    grp.interp_bin_count = (int)gib.size();
-    plan->items_interp_bin.insert(plan->items_interp_bin.end(), gib.begin(), gib.end());
   }
 
   // workspace layout (per RHS) for grids, spectra, twiddles and multipliers
@@ -440,19 +473,19 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   AKM_CK(plan->dtab.ensure(sizeof(WinTable)));
   AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
   AKM_CK(launch_scatter(n, tab, plan->dtab.as<WinTable>(), plan->u_tmp.as<double>(), nullptr, plan->hist.as<int>(),
-                        plan->hist_off.as<long long>(), plan->u_sorted.as<double>(), plan->perm.as<int>(), s));
-  AKM_CK(plan->items_s.ensure(sizeof(WorkItem) * std::max<size_t>(plan->items_spread.size(), 1)));
-  AKM_CK(plan->items_i.ensure(sizeof(WorkItem) * std::max<size_t>(plan->items_interp.size(), 1)));
-  if (!plan->items_spread.empty())
-    AKM_CK(cudaMemcpyAsync(plan->items_s.p, plan->items_spread.data(), sizeof(WorkItem) * plan->items_spread.size(),
-                           cudaMemcpyHostToDevice, s));
-  if (!plan->items_interp.empty())
-    AKM_CK(cudaMemcpyAsync(plan->items_i.p, plan->items_interp.data(), sizeof(WorkItem) * plan->items_interp.size(),
-                           cudaMemcpyHostToDevice, s));
-  AKM_CK(plan->items_ib.ensure(sizeof(WorkItem) * std::max<size_t>(plan->items_interp_bin.size(), 1)));
-  if (!plan->items_interp_bin.empty())
-    AKM_CK(cudaMemcpyAsync(plan->items_ib.p, plan->items_interp_bin.data(),
-                           sizeof(WorkItem) * plan->items_interp_bin.size(), cudaMemcpyHostToDevice, s));
+                        plan->hist_off.as<long long>(), plan->u_sorted.as<double>(), plan->perm.as<int>(), plan->n_split,
+                        s));
+  for (int set = 0; set < 2; ++set) {
+    const std::vector<WorkItem>* lists[3] = {&plan->items_spread[set], &plan->items_interp[set],
+                                             &plan->items_interp_bin[set]};
+    DevBuf* bufs[3] = {&plan->items_s[set], &plan->items_i[set], &plan->items_ib[set]};
+    for (int k = 0; k < 3; ++k) {
+      AKM_CK(bufs[k]->ensure(sizeof(WorkItem) * std::max<size_t>(lists[k]->size(), 1)));
+      if (!lists[k]->empty())
+        AKM_CK(cudaMemcpyAsync(bufs[k]->p, lists[k]->data(), sizeof(WorkItem) * lists[k]->size(),
+                               cudaMemcpyHostToDevice, s));
+    }
+  }
   // twiddles
   AKM_CK(plan->tw.ensure(sizeof(double2) * std::max<long long>(twc, 1)));
   AKM_CK(launch_twiddles(tab, plan->dtab.as<WinTable>(), plan->tw.as<double2>(), s));
@@ -540,8 +573,10 @@ static bool choose_spread_tile(int M, int Nn, int& MT, int& NT, int& threads) {
 }
 
 // ================================================================== the MVM
+// set 0: the square products over all n points (Y: n x r).  set 1: the cross product (Y: the
+// (n - n_split) x r target rows; V holds the n_split source rows; only Y = K_{*X} V).
 static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, int r, double* Y, double* dYl,
-                              double* dYsf, long long ldy, cudaStream_t s) {
+                              double* dYsf, long long ldy, cudaStream_t s, int set = 0) {
   const bool needK = (Y != nullptr) || (dYsf != nullptr);
   const bool needL = dYl != nullptr;
   const int ops = (needK ? 1 : 0) + (needL ? 1 : 0);
@@ -565,17 +600,17 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
     // one-warp-per-SMSP kernel (spread_v5.cu) for 3-D windows with enough work items to fill the
     // GPU at one CTA per SM; AKM_SPREAD_V5=0/1 forces either kernel (A/B measurement)
     static const int v5_env = getenv("AKM_SPREAD_V5") ? atoi(getenv("AKM_SPREAD_V5")) : -1;
-    const bool v5 = v5_env >= 0 ? v5_env != 0 : (d == 3 && grp.spread_count >= 2 * 148);
+    const bool v5 = v5_env >= 0 ? v5_env != 0 : (d == 3 && grp.sl[set].spread_count >= 2 * 148);
     while (v5 && r0 < r) {
       int rc = std::min(12, r - r0), MB = 0, NB = 0, WN = 0;
       while (rc > 1 && !(spread_v5_choose(M, F * rc, MB, NB, WN) && spread_v5_smem(F, rc, MB, NB, WN) <= 220 * 1024)) --rc;
       if (rc < r - r0 && rc > (r - r0 + 1) / 2) rc = (r - r0 + 1) / 2;
       if (!spread_v5_choose(M, F * rc, MB, NB, WN))
         return plan->fail(AKM_ERR_UNSUPPORTED, "no spread tile for footprint %d x %d", M, F * rc);
-      AKM_CK(launch_spread_v5(dtab, plan->poly_param, plan->items_s.as<WorkItem>() + grp.spread_begin,
-                              grp.spread_count, plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc,
+      AKM_CK(launch_spread_v5(dtab, plan->poly_param, plan->items_s[set].as<WorkItem>() + grp.sl[set].spread_begin,
+                              grp.sl[set].spread_count, plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc,
                               r, plan->grid.as<double>(), MB, NB, WN, spread_v5_smem(F, rc, MB, NB, WN), s));
-      if (grp.spread_count > 0) {
+      if (grp.sl[set].spread_count > 0) {
         ++plan->launches;
         ++plan->spread_launches;
       }
@@ -591,10 +626,10 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
         return plan->fail(AKM_ERR_UNSUPPORTED, "no spread tile for footprint %d x %d", M, F * rc);
       const int PB = 0;  // fixed inside the kernel (kSpreadPB)
       const size_t smem = spread_mma_smem(PB, M, F * rc, F, rc);
-      AKM_CK(launch_spread_mma(dtab, plan->poly_param, plan->items_s.as<WorkItem>() + grp.spread_begin, grp.spread_count,
+      AKM_CK(launch_spread_mma(dtab, plan->poly_param, plan->items_s[set].as<WorkItem>() + grp.sl[set].spread_begin, grp.sl[set].spread_count,
                                plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc, r,
                                plan->grid.as<double>(), MB, NB, WM, WN, PB, smem, s));
-      if (grp.spread_count > 0) {
+      if (grp.sl[set].spread_count > 0) {
         ++plan->launches;
         ++plan->spread_launches;
       }
@@ -619,22 +654,22 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
       // AKM_INTERP_T=0 selects the per-plane kernel (A/B measurement)
       static const bool it_off = getenv("AKM_INTERP_T") && atoi(getenv("AKM_INTERP_T")) == 0;
       if (!it_off && interp_t_supported(grp.d, 2 * plan->m, grp.F, ops, rc)) {
-        AKM_CK(launch_interp_t(dtab, plan->poly_param, plan->items_ib.as<WorkItem>() + grp.interp_bin_begin,
-                               grp.interp_bin_count, plan->u_sorted.as<double>(), plan->perm.as<int>(),
+        AKM_CK(launch_interp_t(dtab, plan->poly_param, plan->items_ib[set].as<WorkItem>() + grp.sl[set].interp_bin_begin,
+                               grp.sl[set].interp_bin_count, plan->u_sorted.as<double>(), plan->perm.as<int>(),
                                plan->H.as<double>(), 2 * plan->m, grp.F, ops, r, r0, rc, plan->part.as<double>(), n,
                                s));
-        if (grp.interp_bin_count > 0) {
+        if (grp.sl[set].interp_bin_count > 0) {
           ++plan->launches;
           ++plan->interp_launches;
         }
         continue;
       }
-      AKM_CK(launch_interp(dtab, plan->items_i.as<WorkItem>() + grp.interp_begin, grp.interp_count,
-                           plan->items_ib.as<WorkItem>() + grp.interp_bin_begin, grp.interp_bin_count,
-                           grp.d >= 2 ? grp.F : 1, grp.F, grp.sparse, plan->u_sorted.as<double>(), plan->perm.as<int>(),
+      AKM_CK(launch_interp(dtab, plan->items_i[set].as<WorkItem>() + grp.sl[set].interp_begin, grp.sl[set].interp_count,
+                           plan->items_ib[set].as<WorkItem>() + grp.sl[set].interp_bin_begin, grp.sl[set].interp_bin_count,
+                           grp.d >= 2 ? grp.F : 1, grp.F, grp.sl[set].sparse, plan->u_sorted.as<double>(), plan->perm.as<int>(),
                            plan->H.as<double>(), grp.d,
                            2 * plan->m, ops, r, r0, rc, plan->part.as<double>(), n, s));
-      if (grp.interp_count > 0) {
+      if (grp.sl[set].interp_count > 0) {
         ++plan->launches;
         ++plan->interp_launches;
       }
@@ -643,8 +678,13 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
   }
   if (ev) AKM_CK(cudaEventRecord(ev->e[3], s));
   // S7: epilogue
-  AKM_CK(launch_epilogue(n, plan->P, r, ops, plan->part.as<double>(), V, ldv, plan->sigma_f, plan->sigma_eps, Y, dYl,
-                         dYsf, ldy, slotK, slotL, s));
+  if (set == 0) {
+    AKM_CK(launch_epilogue(n, plan->P, r, ops, plan->part.as<double>(), V, ldv, plan->sigma_f, plan->sigma_eps, Y, dYl,
+                           dYsf, ldy, slotK, slotL, s));
+  } else {
+    AKM_CK(launch_epilogue_cross(n, plan->n_split, plan->P, r, ops, slotK, plan->part.as<double>(), plan->sigma_f, Y,
+                                 ldy, s));
+  }
   ++plan->launches;
   if (ev) AKM_CK(cudaEventRecord(ev->e[4], s));
   return AKM_OK;
@@ -655,12 +695,12 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
 // launch-latency bound.  The legacy default stream cannot be captured; calls on it run the graph
 // on a plan-owned stream ordered by two events.  Profiling (stage events) uses direct launches.
 static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r, double* Y, double* dYl,
-                          double* dYsf, long long ldy, cudaStream_t s) {
+                          double* dYsf, long long ldy, cudaStream_t s, int set = 0) {
   if (plan->n == 0) return AKM_OK;
-  if (plan->profiling || !plan->use_graphs) return enqueue_mvm(plan, V, ldv, r, Y, dYl, dYsf, ldy, s);
+  if (plan->profiling || !plan->use_graphs) return enqueue_mvm(plan, V, ldv, r, Y, dYl, dYsf, ldy, s, set);
   akm_status st = ensure_rhs_workspace(plan, r);
   if (st != AKM_OK) return st;
-  const akm_plan::GraphKey key{V, Y, dYl, dYsf, ldv, ldy, r, plan->epoch};
+  const akm_plan::GraphKey key{V, Y, dYl, dYsf, ldv, ldy, r, plan->epoch, set};
   cudaStream_t cs = s;
   if (s == nullptr || s == cudaStreamLegacy) {
     if (!plan->own_stream) {
@@ -680,7 +720,7 @@ static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r,
     const long long l0 = plan->launches, s0 = plan->spread_launches, i0 = plan->interp_launches;
     cudaGraph_t graph = nullptr;
     AKM_CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    st = enqueue_mvm(plan, V, ldv, r, Y, dYl, dYsf, ldy, cs);
+    st = enqueue_mvm(plan, V, ldv, r, Y, dYl, dYsf, ldy, cs, set);
     cudaError_t ec = cudaStreamEndCapture(cs, &graph);
     if (st != AKM_OK) {
       if (graph) cudaGraphDestroy(graph);
@@ -848,6 +888,7 @@ akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p,
   }
   AKM_CK(cudaSetDevice(plan->device));
   plan->n = n;
+  plan->n_split = n;  // no cross-product targets until akm_kernel_cross_mvm asks for a split
   plan->p = p;
   plan->P = P;
   plan->family = family;
@@ -1047,21 +1088,45 @@ akm_status akm_kernel_cross_mvm(akm_plan* plan, int64_t n_src, const double* V, 
   if (n_src > 0 && !V) return plan->fail(AKM_ERR_INVALID_ARG, "V is NULL");
   cudaStream_t s = S(stream);
   AKM_CK(cudaSetDevice(plan->device));
-  AKM_CK(plan->crossV.ensure(sizeof(double) * n * r));
-  AKM_CK(plan->crossY.ensure(sizeof(double) * n * r));
-  double* Vu = plan->crossV.as<double>();
-  double* Yu = plan->crossY.as<double>();
-  // V into the sources' rows, zeros into the targets' rows
-  if (n_src > 0)
-    AKM_CK(cudaMemcpy2DAsync(Vu, sizeof(double) * r, V, sizeof(double) * ldv, sizeof(double) * r, n_src,
-                             cudaMemcpyDefault, s));
-  AKM_CK(cudaMemsetAsync(Vu + n_src * r, 0, sizeof(double) * n_t * r, s));
-  akm_status st = run_mvm(plan, Vu, r, r, Yu, nullptr, nullptr, r, s);
+  if (plan->n_split != n_src) {
+    // re-sort so that every bin holds its sources first and its targets after them; the spreading
+    // then reads only sources and the interpolation visits only targets (item set 1)
+    plan->n_split = n_src;
+    akm_status st = rebuild_bins(plan, s);
+    if (st != AKM_OK) return st;
+  }
+  const double* Vd = V;
+  long long ldvd = ldv;
+  if (n_src > 0 && !is_device_ptr(V)) {
+    AKM_CK(plan->crossV.ensure(sizeof(double) * n_src * r));
+    AKM_CK(cudaMemcpy2DAsync(plan->crossV.p, sizeof(double) * r, V, sizeof(double) * ldv, sizeof(double) * r, n_src,
+                             cudaMemcpyHostToDevice, s));
+    Vd = plan->crossV.as<double>();
+    ldvd = r;
+  }
+  if (n_src == 0) {  // nothing to spread: the product is zero
+    if (is_device_ptr(Yt)) {
+      AKM_CK(cudaMemset2DAsync(Yt, sizeof(double) * ldy, 0, sizeof(double) * r, n_t, s));
+    } else {
+      for (long long i = 0; i < n_t; ++i) std::memset(Yt + i * ldy, 0, sizeof(double) * r);
+    }
+    return AKM_OK;
+  }
+  const bool y_dev = is_device_ptr(Yt);
+  double* Yd = Yt;
+  long long ldyd = ldy;
+  if (!y_dev) {
+    AKM_CK(plan->crossY.ensure(sizeof(double) * n_t * r));
+    Yd = plan->crossY.as<double>();
+    ldyd = r;
+  }
+  akm_status st = run_mvm(plan, Vd, ldvd, r, Yd, nullptr, nullptr, ldyd, s, /*set=*/1);
   if (st != AKM_OK) return st;
-  // the targets' rows: sigma_f^2 S + sigma_eps^2 * 0
-  AKM_CK(cudaMemcpy2DAsync(Yt, sizeof(double) * ldy, Yu + n_src * r, sizeof(double) * r, sizeof(double) * r, n_t,
-                           cudaMemcpyDefault, s));
-  if (!is_device_ptr(Yt)) AKM_CK(cudaStreamSynchronize(s));
+  if (!y_dev) {
+    AKM_CK(cudaMemcpy2DAsync(Yt, sizeof(double) * ldy, Yd, sizeof(double) * r, sizeof(double) * r, n_t,
+                             cudaMemcpyDeviceToHost, s));
+    AKM_CK(cudaStreamSynchronize(s));
+  }
   return AKM_OK;
 }
 
@@ -1352,12 +1417,13 @@ akm_status akm_get_info(const akm_plan* plan, akm_info* out) {
     out->occupied_bins[w] = plan->occupied.empty() ? 0 : plan->occupied[w];
     out->max_bin_points[w] = plan->maxbin.empty() ? 0 : plan->maxbin[w];
   }
-  out->work_items_spread = (int64_t)plan->items_spread.size();
-  out->work_items_interp = (int64_t)plan->items_interp.size();
+  out->work_items_spread = (int64_t)plan->items_spread[0].size();
+  out->work_items_interp = (int64_t)plan->items_interp[0].size();
   long long ws = 0;
   const DevBuf* bufs[] = {&plan->Xc, &plan->u_tmp, &plan->u_sorted, &plan->perm, &plan->hist, &plan->grid, &plan->H,
                           &plan->A1, &plan->A2, &plan->A3, &plan->C, &plan->C2, &plan->tw, &plan->D, &plan->part,
-                          &plan->items_s, &plan->items_i};
+                          &plan->items_s[0], &plan->items_i[0], &plan->items_ib[0], &plan->items_s[1],
+                          &plan->items_i[1], &plan->items_ib[1]};
   for (const DevBuf* b : bufs) ws += (long long)b->bytes;
   out->workspace_bytes = ws;
   return AKM_OK;

@@ -116,9 +116,11 @@ __device__ __forceinline__ long long cell_linear(const WinGeom& g, const int c[3
   return ((long long)c[0] * g.ncell[1] + c[1]) * g.ncell[2] + c[2];
 }
 
+// Histogram key = (cell, class): class 1 marks the rows i >= n_split (the targets of a cross
+// product, akm_kernel_cross_mvm), so the two classes can be laid out apart inside every bin.
 __global__ void k_scale_and_key(const double* __restrict__ X, long long n, long long ldx, const WinTable* __restrict__ tabp,
                                 double* __restrict__ u_tmp, int* __restrict__ hist,
-                                const long long* __restrict__ hist_off, int* __restrict__ err_flag) {
+                                const long long* __restrict__ hist_off, int* __restrict__ err_flag, long long n_split) {
   const WinTable& tab = *tabp;
   const int w = blockIdx.y;
   const WinGeom& g = tab.w[w];
@@ -137,23 +139,25 @@ __global__ void k_scale_and_key(const double* __restrict__ X, long long n, long 
       atomicOr(err_flag, 1);
       continue;
     }
-    atomicAdd(hist + hist_off[w] + cell_linear(g, c), 1);
+    atomicAdd(hist + hist_off[w] + 2 * cell_linear(g, c) + (i >= n_split ? 1 : 0), 1);
   }
 }
 
 cudaError_t launch_scale_and_key(const double* X, long long n, long long ldx, const WinTable& tab, const WinTable* dtab, double* u_tmp,
-                                 int* /*key*/, int* hist, const long long* hist_off, int* err_flag, cudaStream_t s) {
+                                 int* /*key*/, int* hist, const long long* hist_off, int* err_flag, long long n_split,
+                                 cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   long long blocks = (n + 255) / 256;
   if (blocks > 4736) blocks = 4736;
-  k_scale_and_key<<<dim3((unsigned)blocks, tab.P), 256, 0, s>>>(X, n, ldx, dtab, u_tmp, hist, hist_off, err_flag);
+  k_scale_and_key<<<dim3((unsigned)blocks, tab.P), 256, 0, s>>>(X, n, ldx, dtab, u_tmp, hist, hist_off, err_flag, n_split);
   return cudaGetLastError();
 }
 
-// cursor[hist_off[w] + cell] holds the (window-relative) sorted position of the cell's next point.
+// cursor[hist_off[w] + 2 cell + class] holds the (window-relative) sorted position of the next
+// point of that cell and class.
 __global__ void k_scatter(long long n, const WinTable* __restrict__ tabp, const double* __restrict__ u_tmp, int* __restrict__ cursor,
                           const long long* __restrict__ hist_off, double* __restrict__ u_sorted,
-                          int* __restrict__ perm) {
+                          int* __restrict__ perm, long long n_split) {
   const WinTable& tab = *tabp;
   const int w = blockIdx.y;
   const WinGeom& g = tab.w[w];
@@ -165,18 +169,18 @@ __global__ void k_scatter(long long n, const WinTable* __restrict__ tabp, const 
       u[a] = u_tmp[((long long)w * 3 + a) * n + i];
       c[a] = (int)floor(u[a]) - (g.box_lo[a] + m - 1);
     }
-    const int pos = atomicAdd(cursor + hist_off[w] + cell_linear(g, c), 1);
+    const int pos = atomicAdd(cursor + hist_off[w] + 2 * cell_linear(g, c) + (i >= n_split ? 1 : 0), 1);
     perm[(long long)w * n + pos] = (int)i;
     for (int a = 3 - g.d; a < 3; ++a) u_sorted[((long long)w * 3 + a) * n + pos] = u[a];
   }
 }
 
 cudaError_t launch_scatter(long long n, const WinTable& tab, const WinTable* dtab, const double* u_tmp, const int* /*key*/, int* cursor,
-                           const long long* hist_off, double* u_sorted, int* perm, cudaStream_t s) {
+                           const long long* hist_off, double* u_sorted, int* perm, long long n_split, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   long long blocks = (n + 255) / 256;
   if (blocks > 4736) blocks = 4736;
-  k_scatter<<<dim3((unsigned)blocks, tab.P), 256, 0, s>>>(n, dtab, u_tmp, cursor, hist_off, u_sorted, perm);
+  k_scatter<<<dim3((unsigned)blocks, tab.P), 256, 0, s>>>(n, dtab, u_tmp, cursor, hist_off, u_sorted, perm, n_split);
   return cudaGetLastError();
 }
 

@@ -116,3 +116,33 @@ def test_cross_full_size_x4_row_sample(akm):
     Vu = np.vstack([V, np.zeros((wl.n - n_src, wl.r))])
     want = dense_apply(X, wl.windows, wl.family, theta, Vu, rows=n_src + rows, ops=("K",))["K"]
     assert rel(got[rows], want) <= 1e-6
+
+
+def test_square_products_unchanged_after_a_cross_split(akm):
+    """A cross call re-sorts the plan's points (sources, then targets, inside every bin); the square
+    products on the same plan must stay within the same tolerance, before and after."""
+    wl = workloads.CONFIGS["c2"]
+    X = workloads.make_X(wl, n=4000)
+    V = workloads.make_V(wl, n=4000, r=2)
+    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family, wl.N, 2.0, wl.m, 1.0 / 16)
+    plan.set_theta(*theta)
+    Vd = torch.from_numpy(V).to(dev)
+    Y0 = torch.empty_like(Vd)
+    plan.mvm(Vd, Y0)
+    Yt = torch.empty((1000, 2), dtype=torch.float64, device=dev)
+    plan.cross_mvm(3000, Vd[:3000].contiguous(), Yt)
+    Y1 = torch.empty_like(Vd)
+    plan.mvm(Vd, Y1)
+    torch.cuda.synchronize()
+    want = dense_apply(X, wl.windows, wl.family, theta, V, ops=("K",))["K"]
+    assert rel(Y0.cpu().numpy(), want) <= 1e-6 and rel(Y1.cpu().numpy(), want) <= 1e-6
+    assert rel(Yt.cpu().numpy(), dense_cross(X[:3000], X[3000:], wl.windows, wl.family, theta, V[:3000])) <= 1e-6
+    # a different split, then the first again
+    plan.cross_mvm(2000, Vd[:2000].contiguous(), torch.empty((2000, 2), dtype=torch.float64, device=dev))
+    plan.cross_mvm(3000, Vd[:3000].contiguous(), Yt)
+    torch.cuda.synchronize()
+    assert rel(Yt.cpu().numpy(), dense_cross(X[:3000], X[3000:], wl.windows, wl.family, theta, V[:3000])) <= 1e-6
+    plan.close()
