@@ -208,7 +208,7 @@ inline size_t interp_mma_smem(int D, int TAPS, int OPS, int RC) {
 // offset inside the bin.  Points are sorted by cell inside a bin, so the lanes of a warp mostly
 // read the same addresses (broadcasts).  FP64 FMAs per point and value: (2m)^d + (2m)^(d-1).
 template <int D, int TAPS, int OPS, int RC>
-__global__ void __launch_bounds__(128, (OPS * RC == 2) ? 6 : 1) k_interp_bin(const WinTable* __restrict__ tabp,
+__global__ void __launch_bounds__(128, (OPS * RC == 2) ? 6 : ((OPS * RC >= 8 && OPS * RC <= 12) ? 4 : 1)) k_interp_bin(const WinTable* __restrict__ tabp,
                                                     const WorkItem* __restrict__ items,
                                                     const double* __restrict__ u_sorted, const int* __restrict__ perm,
                                                     const double* __restrict__ H, int r, int r0,
