@@ -289,7 +289,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   std::vector<std::vector<WorkItem>> its_s[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
   std::vector<std::vector<WorkItem>> its_i[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
   std::vector<std::vector<WorkItem>> its_ib[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
-  const int ch_ib = 128;  // interpolation, few values per node: one bin per work item, 1 point / thread
+  const int ch_ib = 128;  // per-bin interpolation items: up to 128 points of one bin
   for (int w = 0; w < P; ++w) {
     WinGeom& g = tab.w[w];
     const int* hc = hist.data() + hoff[w];
