@@ -146,3 +146,17 @@ def test_square_products_unchanged_after_a_cross_split(akm):
     torch.cuda.synchronize()
     assert rel(Yt.cpu().numpy(), dense_cross(X[:3000], X[3000:], wl.windows, wl.family, theta, V[:3000])) <= 1e-6
     plan.close()
+
+
+@pytest.mark.parametrize("family", [0, 1])
+def test_cross_mixed_window_dims(akm, family):
+    """windows of 1, 2 and 3 features in one plan (three groups, three kernel paths)."""
+    rng = np.random.default_rng(41)
+    X = rng.random((2600, 6))
+    windows = [(0,), (1, 2), (3, 4, 5)]
+    theta = (1.1, 0.7 if family == 1 else 0.25, 0.2)
+    V = rng.standard_normal((2000, 3))
+    N, m = (128, 8) if family == 1 else (32, 6)   # Matern: the method needs N = 128 for 1e-3 (cf. test_gpu_parity)
+    got = gpu_cross(akm, X, 2000, windows, family, theta, V, N=N, m=m)
+    want = dense_cross(X[:2000], X[2000:], windows, family, theta, V)
+    assert rel(got, want) <= (1e-3 if family == 1 else 1e-6)
