@@ -26,6 +26,8 @@
 // output straight from global memory and was latency-bound: profiles/r01_launches_c2_summary.txt.)
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "akm_internal.cuh"
 
 namespace akm {
@@ -187,6 +189,124 @@ __global__ void __launch_bounds__(kDftThreads) k_dft_axis(const WinTable* __rest
       static_cast<double2*>(Yv)[ybase + o * sh.yo + (long long)k * sh.yk + i] = make_double2(re, im);
     }
   }
+}
+
+// ---------------------------------------------------------------- DMMA passes (kFB, kFD)
+// The complex axis-1 passes of the generic path as FP64 tensor-core GEMMs (large 2-D boxes, c3):
+// Y_o[k][i] = sum_l M[k][l] X_o[l][i] with M = T (kFB) or M[k][l] = conj(T[l][k]) (kFD), computed
+// as the real product C (2K x I) = A (2K x 2L) B (2L x I): A is the 2x2 real block form of M
+// (rows 2k + q: component q of the output; columns 2l + p: component p of the input), B's row
+// 2l + p holds component p of X[l][i].  A CTA owns 16 complex rows x 32 columns (2x2 warps of
+// 2x2 DMMA tiles: many CTAs for latency hiding); the K loop stages 8 complex l per step.
+constexpr int kMmaK = 8;  // complex l per staged step (16 real k)
+constexpr int kMmaT = 2;  // DMMA tiles per warp along each of m and n (2 x 2 warps per CTA)
+constexpr int kMmaRows = 2 * kMmaT * 8, kMmaCols = 2 * kMmaT * 8;  // real rows / columns per CTA
+template <int MODE>
+__global__ void __launch_bounds__(128) k_dft_mma(const WinTable* __restrict__ tabp, const double2* __restrict__ X,
+                                                 double2* __restrict__ Y, const double2* __restrict__ tw, int r,
+                                                 int ops, int ktiles) {
+  constexpr int CK = kMmaRows / 2;  // complex rows per CTA
+  const WinGeom& g = tabp->w[blockIdx.z];
+  const DftShape sh = dft_shape(g, MODE, r, ops);
+  const int o = blockIdx.y / ktiles, kt = blockIdx.y - o * ktiles;
+  const long long i0 = (long long)blockIdx.x * kMmaCols;
+  const int k0 = kt * CK;
+  if (o >= sh.O || i0 >= sh.I || k0 >= sh.K) return;
+  const long long xbase = (MODE == kFB ? g.a1_off : g.c_off) * r + (long long)o * sh.xo;
+  const long long ybase = (MODE == kFB ? g.a2_off : g.c2_off) * r + (long long)o * sh.yo;
+  const double2* T = tw + g.tw_off[1];
+  const int Lt = g.L[1];
+  __shared__ double2 Xs[kMmaK][kMmaCols];
+  __shared__ double2 Ms[CK][kMmaK + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wm = warp >> 1, wn = warp & 1;
+  double acc[kMmaT][kMmaT][2];
+#pragma unroll
+  for (int a = 0; a < kMmaT; ++a)
+#pragma unroll
+    for (int b = 0; b < kMmaT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int l0 = 0; l0 < sh.L; l0 += kMmaK) {
+    for (int idx = tid; idx < kMmaK * kMmaCols; idx += 128) {
+      const int l = idx / kMmaCols, j = idx - l * kMmaCols;
+      const long long i = i0 + j;
+      Xs[l][j] = (l0 + l < sh.L && i < sh.I) ? X[xbase + (long long)(l0 + l) * sh.xl + i] : make_double2(0.0, 0.0);
+    }
+    for (int idx = tid; idx < CK * kMmaK; idx += 128) {
+      const int k = idx / kMmaK, l = idx - k * kMmaK;
+      double2 m = make_double2(0.0, 0.0);
+      if (k0 + k < sh.K && l0 + l < sh.L) {
+        if (MODE == kFB) {
+          m = T[(long long)(k0 + k) * Lt + l0 + l];
+        } else {
+          const double2 t = T[(long long)(l0 + l) * Lt + k0 + k];
+          m = make_double2(t.x, -t.y);
+        }
+      }
+      Ms[k][l] = m;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int kr = ks * 4 + (lane & 3), ll = kr >> 1, p = kr & 1;
+      double af[kMmaT], bf[kMmaT];
+#pragma unroll
+      for (int mt = 0; mt < kMmaT; ++mt) {
+        const int row = (wm * kMmaT + mt) * 8 + (lane >> 2), q = row & 1;
+        const double2 m = Ms[row >> 1][ll];
+        af[mt] = (q == 0) ? (p == 0 ? m.x : -m.y) : (p == 0 ? m.y : m.x);
+      }
+#pragma unroll
+      for (int nt = 0; nt < kMmaT; ++nt) {
+        const double2 x = Xs[ll][(wn * kMmaT + nt) * 8 + (lane >> 2)];
+        bf[nt] = p == 0 ? x.x : x.y;
+      }
+#pragma unroll
+      for (int mt = 0; mt < kMmaT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < kMmaT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+    }
+    __syncthreads();
+  }
+  // rows 2k (real) and 2k + 1 (imaginary) sit in lanes l and l ^ 4
+#pragma unroll
+  for (int mt = 0; mt < kMmaT; ++mt) {
+    const int row = (wm * kMmaT + mt) * 8 + (lane >> 2), k = k0 + (row >> 1);
+#pragma unroll
+    for (int nt = 0; nt < kMmaT; ++nt) {
+      const double im0 = __shfl_xor_sync(0xffffffffu, acc[mt][nt][0], 4);
+      const double im1 = __shfl_xor_sync(0xffffffffu, acc[mt][nt][1], 4);
+      if ((row & 1) || k >= sh.K) continue;
+      const long long i = i0 + (wn * kMmaT + nt) * 8 + 2 * (lane & 3);
+      if (i < sh.I) Y[ybase + (long long)k * sh.yk + i] = make_double2(acc[mt][nt][0], im0);
+      if (i + 1 < sh.I) Y[ybase + (long long)k * sh.yk + i + 1] = make_double2(acc[mt][nt][1], im1);
+    }
+  }
+}
+
+template <int MODE>
+static cudaError_t launch_dft_mma(const WinTable& tab, const WinTable* dtab, const double2* X, double2* Y,
+                                  const double2* tw, int r, int ops, cudaStream_t s) {
+  long long itiles = 1, O = 1;
+  int ktiles = 1;
+  for (int w = 0; w < tab.P; ++w) {
+    const DftShape sh = dft_shape(tab.w[w], MODE, r, ops);
+    itiles = std::max(itiles, (sh.I + kMmaCols - 1) / kMmaCols);
+    O = std::max(O, sh.O);
+    ktiles = std::max(ktiles, (sh.K + kMmaRows / 2 - 1) / (kMmaRows / 2));
+  }
+  k_dft_mma<MODE><<<dim3((unsigned)itiles, (unsigned)(O * ktiles), tab.P), 128, 0, s>>>(dtab, X, Y, tw, r, ops,
+                                                                                        ktiles);
+  return cudaGetLastError();
+}
+
+// the DMMA passes pay off for long axes (the 2-D c3 boxes); short ones stay scalar
+static bool use_dft_mma(const WinTable& tab, int mode, int r, int ops) {
+  static const int env = getenv("AKM_DFT_MMA") ? atoi(getenv("AKM_DFT_MMA")) : -1;
+  if (env >= 0) return env != 0;
+  for (int w = 0; w < tab.P; ++w) {
+    const DftShape sh = dft_shape(tab.w[w], mode, r, ops);
+    if (sh.L < 64 || sh.K < 64) return false;
+  }
+  return true;
 }
 
 // host: grid for one pass = max over windows of the column tiles; smem = max L
@@ -441,6 +561,7 @@ cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const 
   }
   cudaError_t e = launch_pass<kFA>(tab, dtab, grid, A1, tw, nullptr, 0, r, 1, s);
   if (e != cudaSuccess) return e;
+  if (use_dft_mma(tab, kFB, r, 1)) return launch_dft_mma<kFB>(tab, dtab, A1, A2, tw, r, 1, s);
   return launch_pass<kFB>(tab, dtab, A1, A2, tw, nullptr, 0, r, 1, s);
 }
 
@@ -473,7 +594,10 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
   }
   cudaError_t e = launch_pass<kFC1>(tab, dtab, A2, A3, tw, nullptr, 0, r, ops, s);
   if (e == cudaSuccess) e = launch_pass<kFC2>(tab, dtab, A3, C, tw, D, dslot0, r, ops, s);
-  if (e == cudaSuccess) e = launch_pass<kFD>(tab, dtab, C, C2, tw, nullptr, 0, r, ops, s);
+  if (e == cudaSuccess) {
+    if (use_dft_mma(tab, kFD, r, ops)) e = launch_dft_mma<kFD>(tab, dtab, C, C2, tw, r, ops, s);
+    else e = launch_pass<kFD>(tab, dtab, C, C2, tw, nullptr, 0, r, ops, s);
+  }
   if (e == cudaSuccess) e = launch_pass<kFE>(tab, dtab, C2, H, tw, nullptr, 0, r, ops, s);
   return e;
 }
