@@ -298,6 +298,144 @@ static cudaError_t launch_dft_mma(const WinTable& tab, const WinTable* dtab, con
   return cudaGetLastError();
 }
 
+// The real-side axis-2 passes (kFA: real grid -> half spectrum; kFE: half spectrum -> real H with
+// the Hermitian weights) as FP64 tensor-core GEMMs over the columns (o, c):
+//   kFA:  C[2k + q][(o, c)] = sum_l  {Re, Im} T[k][l] * x[o][l][c]
+//   kFE:  C[l][(o, c)]      = sum_{k, p} w_k {Re, Im} T[k][l] * {Re, Im} X[o][k][c]   (w_0 = 1, else 2)
+// A CTA owns 32 real rows x 32 columns (2x2 warps of 2x2 DMMA tiles); K is staged 8 (complex for kFE) at a time.
+template <int MODE>
+__global__ void __launch_bounds__(128) k_dft_mma_r(const WinTable* __restrict__ tabp, const void* __restrict__ Xv,
+                                                   void* __restrict__ Yv, const double2* __restrict__ tw, int r,
+                                                   int ops) {
+  const WinGeom& g = tabp->w[blockIdx.z];
+  const DftShape sh = dft_shape(g, MODE, r, ops);
+  const long long ncol = sh.O * sh.I, c0 = (long long)blockIdx.x * 32;
+  const int rows = (MODE == kFA) ? 2 * sh.K : sh.K;  // real output rows
+  const int row0 = blockIdx.y * 32;
+  if (c0 >= ncol || row0 >= rows) return;
+  const double2* T = tw + g.tw_off[2];
+  const int Lt = g.L[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wm = warp >> 1, wn = warp & 1;
+  __shared__ double2 Xs[8][33];  // kFA: .x only (real input), [l][col]; kFE: [k][col]
+  __shared__ double2 Ms[32][9];  // kFA: [k (16 used)][l]; kFE: [l][k]
+  double acc[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const long long xbase = (MODE == kFA) ? g.tap_off * r : g.c2_off * r;
+  for (int l0 = 0; l0 < sh.L; l0 += 8) {  // sh.L: kFA nodes l2, kFE frequencies k2
+    for (int idx = tid; idx < 8 * 32; idx += 128) {
+      const int l = idx >> 5, j = idx & 31;
+      const long long col = c0 + j;
+      double2 v = make_double2(0.0, 0.0);
+      if (l0 + l < sh.L && col < ncol) {
+        const long long o = col / sh.I, c = col - o * sh.I;
+        const long long off = xbase + o * sh.xo + (long long)(l0 + l) * sh.xl + c;
+        if (MODE == kFA) v.x = static_cast<const double*>(Xv)[off];
+        else v = static_cast<const double2*>(Xv)[off];
+      }
+      Xs[l][j] = v;
+    }
+    for (int idx = tid; idx < 32 * 8; idx += 128) {
+      const int a = idx >> 3, b = idx & 7;  // kFA: a = k (row/2), b = l; kFE: a = l (row), b = k
+      double2 m = make_double2(0.0, 0.0);
+      if (MODE == kFA) {
+        const int k = row0 / 2 + a;
+        if (a < 16 && k < sh.K && l0 + b < sh.L) m = T[(long long)k * Lt + l0 + b];
+      } else {
+        const int l = row0 + a, k = l0 + b;
+        if (l < sh.K && k < sh.L) {
+          const double2 t = T[(long long)k * Lt + l];
+          const double w = (k == 0) ? 1.0 : 2.0;
+          m = make_double2(w * t.x, w * t.y);
+        }
+      }
+      Ms[a][b] = m;
+    }
+    __syncthreads();
+    constexpr int KS = (MODE == kFA) ? 2 : 4;  // k-steps of 4 real k per staged chunk
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int kr = ks * 4 + (lane & 3);
+      double af[2], bf[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int row = (wm * 2 + mt) * 8 + (lane >> 2);
+        if (MODE == kFA) {
+          const double2 m = Ms[row >> 1][kr];
+          af[mt] = (row & 1) ? m.y : m.x;
+        } else {
+          const double2 m = Ms[row][kr >> 1];
+          af[mt] = (kr & 1) ? m.y : m.x;
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int col = (wn * 2 + nt) * 8 + (lane >> 2);
+        if (MODE == kFA) {
+          bf[nt] = Xs[kr][col].x;
+        } else {
+          const double2 x = Xs[kr >> 1][col];
+          bf[nt] = (kr & 1) ? x.y : x.x;
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int row = row0 + (wm * 2 + mt) * 8 + (lane >> 2);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const long long colb = c0 + (wn * 2 + nt) * 8 + 2 * (lane & 3);
+      if (MODE == kFA) {
+        const double im0 = __shfl_xor_sync(0xffffffffu, acc[mt][nt][0], 4);
+        const double im1 = __shfl_xor_sync(0xffffffffu, acc[mt][nt][1], 4);
+        const int k = row >> 1;
+        if ((row & 1) || k >= sh.K) continue;
+        double2* Y = static_cast<double2*>(Yv) + g.a1_off * r;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const long long col = colb + h;
+          if (col >= ncol) continue;
+          const long long o = col / sh.I, c = col - o * sh.I;
+          Y[o * sh.yo + (long long)k * sh.yk + c] = make_double2(h ? acc[mt][nt][1] : acc[mt][nt][0], h ? im1 : im0);
+        }
+      } else {
+        if (row >= sh.K) continue;
+        double* H = static_cast<double*>(Yv) + g.tap_off * (long long)ops * r;
+        const long long lines = (long long)g.L[0] * g.L[1];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const long long col = colb + h;
+          if (col >= ncol) continue;
+          const long long o = col / sh.I, c = col - o * sh.I, op = o / lines, line = o - op * lines;
+          H[((line * g.L[2] + row) * ops + op) * r + c] = acc[mt][nt][h];
+        }
+      }
+    }
+  }
+}
+
+template <int MODE>
+static cudaError_t launch_dft_mma_r(const WinTable& tab, const WinTable* dtab, const void* X, void* Y,
+                                    const double2* tw, int r, int ops, cudaStream_t s) {
+  long long ctiles = 1;
+  int rtiles = 1;
+  for (int w = 0; w < tab.P; ++w) {
+    const DftShape sh = dft_shape(tab.w[w], MODE, r, ops);
+    ctiles = std::max(ctiles, (sh.O * sh.I + 31) / 32);
+    rtiles = std::max(rtiles, ((MODE == kFA ? 2 * sh.K : sh.K) + 31) / 32);
+  }
+  k_dft_mma_r<MODE><<<dim3((unsigned)ctiles, (unsigned)rtiles, tab.P), 128, 0, s>>>(dtab, X, Y, tw, r, ops);
+  return cudaGetLastError();
+}
+
 // the DMMA passes pay off for long axes (the 2-D c3 boxes); short ones stay scalar
 static bool use_dft_mma(const WinTable& tab, int mode, int r, int ops) {
   static const int env = getenv("AKM_DFT_MMA") ? atoi(getenv("AKM_DFT_MMA")) : -1;
@@ -559,7 +697,8 @@ cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const 
     k_plane_fwd<<<dim3(L0, tab.P), kFuseThreads, sf, s>>>(dtab, grid, A2, tw, r);
     return cudaGetLastError();
   }
-  cudaError_t e = launch_pass<kFA>(tab, dtab, grid, A1, tw, nullptr, 0, r, 1, s);
+  cudaError_t e = use_dft_mma(tab, kFA, r, 1) ? launch_dft_mma_r<kFA>(tab, dtab, grid, A1, tw, r, 1, s)
+                                               : launch_pass<kFA>(tab, dtab, grid, A1, tw, nullptr, 0, r, 1, s);
   if (e != cudaSuccess) return e;
   if (use_dft_mma(tab, kFB, r, 1)) return launch_dft_mma<kFB>(tab, dtab, A1, A2, tw, r, 1, s);
   return launch_pass<kFB>(tab, dtab, A1, A2, tw, nullptr, 0, r, 1, s);
@@ -598,7 +737,10 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
     if (use_dft_mma(tab, kFD, r, ops)) e = launch_dft_mma<kFD>(tab, dtab, C, C2, tw, r, ops, s);
     else e = launch_pass<kFD>(tab, dtab, C, C2, tw, nullptr, 0, r, ops, s);
   }
-  if (e == cudaSuccess) e = launch_pass<kFE>(tab, dtab, C2, H, tw, nullptr, 0, r, ops, s);
+  if (e == cudaSuccess) {
+    if (use_dft_mma(tab, kFE, r, ops)) e = launch_dft_mma_r<kFE>(tab, dtab, C2, H, tw, r, ops, s);
+    else e = launch_pass<kFE>(tab, dtab, C2, H, tw, nullptr, 0, r, ops, s);
+  }
   return e;
 }
 
