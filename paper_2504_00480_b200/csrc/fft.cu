@@ -201,10 +201,13 @@ __global__ void __launch_bounds__(kDftThreads) k_dft_axis(const WinTable* __rest
 constexpr int kMmaK = 8;  // complex l per staged step (16 real k)
 constexpr int kMmaT = 2;  // DMMA tiles per warp along each of m and n (2 x 2 warps per CTA)
 constexpr int kMmaRows = 2 * kMmaT * 8, kMmaCols = 2 * kMmaT * 8;  // real rows / columns per CTA
-template <int MODE>
+// FUSED_D (kFD, every window without an axis 0): the input is A2 itself times the multiplier
+// D_op[k0 = 0][k1][k2] (the FC1 copy and the FC2 multiply folded into the load).
+template <int MODE, bool FUSED_D = false>
 __global__ void __launch_bounds__(128) k_dft_mma(const WinTable* __restrict__ tabp, const double2* __restrict__ X,
                                                  double2* __restrict__ Y, const double2* __restrict__ tw, int r,
-                                                 int ops, int ktiles) {
+                                                 int ops, int ktiles, const double* __restrict__ D = nullptr,
+                                                 int dslot0 = 0) {
   constexpr int CK = kMmaRows / 2;  // complex rows per CTA
   const WinGeom& g = tabp->w[blockIdx.z];
   const DftShape sh = dft_shape(g, MODE, r, ops);
@@ -212,7 +215,8 @@ __global__ void __launch_bounds__(128) k_dft_mma(const WinTable* __restrict__ ta
   const long long i0 = (long long)blockIdx.x * kMmaCols;
   const int k0 = kt * CK;
   if (o >= sh.O || i0 >= sh.I || k0 >= sh.K) return;
-  const long long xbase = (MODE == kFB ? g.a1_off : g.c_off) * r + (long long)o * sh.xo;
+  const long long xbase = FUSED_D ? g.a2_off * r : (MODE == kFB ? g.a1_off : g.c_off) * r + (long long)o * sh.xo;
+  const long long dbase = g.d_off + (long long)(dslot0 + o) * g.K[0] * g.K[1] * g.K[2];  // FUSED_D: o = op
   const long long ybase = (MODE == kFB ? g.a2_off : g.c2_off) * r + (long long)o * sh.yo;
   const double2* T = tw + g.tw_off[1];
   const int Lt = g.L[1];
@@ -228,7 +232,16 @@ __global__ void __launch_bounds__(128) k_dft_mma(const WinTable* __restrict__ ta
     for (int idx = tid; idx < kMmaK * kMmaCols; idx += 128) {
       const int l = idx / kMmaCols, j = idx - l * kMmaCols;
       const long long i = i0 + j;
-      Xs[l][j] = (l0 + l < sh.L && i < sh.I) ? X[xbase + (long long)(l0 + l) * sh.xl + i] : make_double2(0.0, 0.0);
+      double2 v = make_double2(0.0, 0.0);
+      if (l0 + l < sh.L && i < sh.I) {
+        v = X[xbase + (long long)(l0 + l) * sh.xl + i];
+        if (FUSED_D) {  // D_op[k1 = l][k2 = i / r]
+          const double dd = D[dbase + (long long)(l0 + l) * g.K[2] + i / r];
+          v.x *= dd;
+          v.y *= dd;
+        }
+      }
+      Xs[l][j] = v;
     }
     for (int idx = tid; idx < CK * kMmaK; idx += 128) {
       const int k = idx / kMmaK, l = idx - k * kMmaK;
@@ -282,9 +295,10 @@ __global__ void __launch_bounds__(128) k_dft_mma(const WinTable* __restrict__ ta
   }
 }
 
-template <int MODE>
+template <int MODE, bool FUSED_D = false>
 static cudaError_t launch_dft_mma(const WinTable& tab, const WinTable* dtab, const double2* X, double2* Y,
-                                  const double2* tw, int r, int ops, cudaStream_t s) {
+                                  const double2* tw, int r, int ops, cudaStream_t s, const double* D = nullptr,
+                                  int dslot0 = 0) {
   long long itiles = 1, O = 1;
   int ktiles = 1;
   for (int w = 0; w < tab.P; ++w) {
@@ -293,8 +307,8 @@ static cudaError_t launch_dft_mma(const WinTable& tab, const WinTable* dtab, con
     O = std::max(O, sh.O);
     ktiles = std::max(ktiles, (sh.K + kMmaRows / 2 - 1) / (kMmaRows / 2));
   }
-  k_dft_mma<MODE><<<dim3((unsigned)itiles, (unsigned)(O * ktiles), tab.P), 128, 0, s>>>(dtab, X, Y, tw, r, ops,
-                                                                                        ktiles);
+  k_dft_mma<MODE, FUSED_D><<<dim3((unsigned)itiles, (unsigned)(O * ktiles), tab.P), 128, 0, s>>>(
+      dtab, X, Y, tw, r, ops, ktiles, D, dslot0);
   return cudaGetLastError();
 }
 
@@ -434,6 +448,12 @@ static cudaError_t launch_dft_mma_r(const WinTable& tab, const WinTable* dtab, c
   }
   k_dft_mma_r<MODE><<<dim3((unsigned)ctiles, (unsigned)rtiles, tab.P), 128, 0, s>>>(dtab, X, Y, tw, r, ops);
   return cudaGetLastError();
+}
+
+static bool no_axis0(const WinTable& tab) {
+  for (int w = 0; w < tab.P; ++w)
+    if (tab.w[w].L[0] != 1 || tab.w[w].K[0] != 1) return false;
+  return true;
 }
 
 // the DMMA passes pay off for long axes (the 2-D c3 boxes); short ones stay scalar
@@ -731,11 +751,17 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
     k_plane_inv<<<dim3(L0 * ops, tab.P), kFuseThreads, si, s>>>(dtab, C, H, tw, r, ops);
     return cudaGetLastError();
   }
-  cudaError_t e = launch_pass<kFC1>(tab, dtab, A2, A3, tw, nullptr, 0, r, ops, s);
-  if (e == cudaSuccess) e = launch_pass<kFC2>(tab, dtab, A3, C, tw, D, dslot0, r, ops, s);
-  if (e == cudaSuccess) {
-    if (use_dft_mma(tab, kFD, r, ops)) e = launch_dft_mma<kFD>(tab, dtab, C, C2, tw, r, ops, s);
-    else e = launch_pass<kFD>(tab, dtab, C, C2, tw, nullptr, 0, r, ops, s);
+  cudaError_t e = cudaSuccess;
+  if (use_dft_mma(tab, kFD, r, ops) && no_axis0(tab)) {
+    // no axis 0: FC1 is a copy and FC2 a multiply; both fold into the FD load
+    e = launch_dft_mma<kFD, true>(tab, dtab, A2, C2, tw, r, ops, s, D, dslot0);
+  } else {
+    e = launch_pass<kFC1>(tab, dtab, A2, A3, tw, nullptr, 0, r, ops, s);
+    if (e == cudaSuccess) e = launch_pass<kFC2>(tab, dtab, A3, C, tw, D, dslot0, r, ops, s);
+    if (e == cudaSuccess) {
+      if (use_dft_mma(tab, kFD, r, ops)) e = launch_dft_mma<kFD>(tab, dtab, C, C2, tw, r, ops, s);
+      else e = launch_pass<kFD>(tab, dtab, C, C2, tw, nullptr, 0, r, ops, s);
+    }
   }
   if (e == cudaSuccess) {
     if (use_dft_mma(tab, kFE, r, ops)) e = launch_dft_mma_r<kFE>(tab, dtab, C2, H, tw, r, ops, s);
@@ -747,7 +773,8 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
 // kernels launched by launch_fft_forward + launch_fft_multiply_inverse (for the launch counters)
 int fft_launch_count(const WinTable& tab, int r) {
   size_t sf, si;
-  return planes_fit(tab, r, sf, si) ? 3 : 6;
+  if (planes_fit(tab, r, sf, si)) return 3;
+  return use_dft_mma(tab, kFD, r, 1) && no_axis0(tab) ? 4 : 6;
 }
 
 cudaError_t launch_zero(double* p, long long count, cudaStream_t s) {
