@@ -206,6 +206,15 @@ bool is_pinned_host(const void* ptr) {
 
 inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Row-block copies: one linear copy when both sides are contiguous (a 2-D copy of a million
+// 88-byte rows runs row by row on the copy engine), else the strided 2-D copy.
+cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                      cudaMemcpyKind kind, cudaStream_t s) {
+  if (rows == 0 || width == 0) return cudaSuccess;
+  if (dpitch == width && spitch == width) return cudaMemcpyAsync(dst, src, width * rows, kind, s);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, s);
+}
+
 }  // namespace
 
 // ================================================================== geometry / binning
@@ -774,7 +783,7 @@ static akm_status mvm_entry(akm_plan* plan, const double* V, long long ldv, int 
   long long ldvd = ldv;
   if (!v_dev) {
     AKM_CK(plan->stageV.ensure(sizeof(double) * n * r));
-    AKM_CK(cudaMemcpy2DAsync(plan->stageV.p, sizeof(double) * r, V, sizeof(double) * ldv, sizeof(double) * r, n,
+    AKM_CK(copy_rows(plan->stageV.p, sizeof(double) * r, V, sizeof(double) * ldv, sizeof(double) * r, n,
                              cudaMemcpyHostToDevice, s));
     Vd = plan->stageV.as<double>();
     ldvd = r;
@@ -812,7 +821,7 @@ static akm_status mvm_entry(akm_plan* plan, const double* V, long long ldv, int 
   if (staged) {
     for (int k = 0; k < 4; ++k) {
       if (!outs[k]) continue;
-      AKM_CK(cudaMemcpy2DAsync(outs[k], sizeof(double) * ldy, od[k], sizeof(double) * r, sizeof(double) * r, n,
+      AKM_CK(copy_rows(outs[k], sizeof(double) * ldy, od[k], sizeof(double) * r, sizeof(double) * r, n,
                                out_dev[k] ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     }
   }
@@ -1099,7 +1108,7 @@ akm_status akm_kernel_cross_mvm(akm_plan* plan, int64_t n_src, const double* V, 
   long long ldvd = ldv;
   if (n_src > 0 && !is_device_ptr(V)) {
     AKM_CK(plan->crossV.ensure(sizeof(double) * n_src * r));
-    AKM_CK(cudaMemcpy2DAsync(plan->crossV.p, sizeof(double) * r, V, sizeof(double) * ldv, sizeof(double) * r, n_src,
+    AKM_CK(copy_rows(plan->crossV.p, sizeof(double) * r, V, sizeof(double) * ldv, sizeof(double) * r, n_src,
                              cudaMemcpyHostToDevice, s));
     Vd = plan->crossV.as<double>();
     ldvd = r;
@@ -1123,7 +1132,7 @@ akm_status akm_kernel_cross_mvm(akm_plan* plan, int64_t n_src, const double* V, 
   akm_status st = run_mvm(plan, Vd, ldvd, r, Yd, nullptr, nullptr, ldyd, s, /*set=*/1);
   if (st != AKM_OK) return st;
   if (!y_dev) {
-    AKM_CK(cudaMemcpy2DAsync(Yt, sizeof(double) * ldy, Yd, sizeof(double) * r, sizeof(double) * r, n_t,
+    AKM_CK(copy_rows(Yt, sizeof(double) * ldy, Yd, sizeof(double) * r, sizeof(double) * r, n_t,
                              cudaMemcpyDeviceToHost, s));
     AKM_CK(cudaStreamSynchronize(s));
   }
@@ -1164,7 +1173,7 @@ akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, 
       yd = st;
     }
     if (!z_dev) {
-      AKM_CK(cudaMemcpy2DAsync(st + n, sizeof(double) * n_z, Z, sizeof(double) * ldz, sizeof(double) * n_z, n,
+      AKM_CK(copy_rows(st + n, sizeof(double) * n_z, Z, sizeof(double) * ldz, sizeof(double) * n_z, n,
                                cudaMemcpyHostToDevice, s));
       Zd = st + n;
       ldzd = n_z;
@@ -1286,7 +1295,7 @@ akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, i
       yd = st;
     }
     if (!z_dev) {
-      AKM_CK(cudaMemcpy2DAsync(st + n, sizeof(double) * n_z, Z, sizeof(double) * ldz, sizeof(double) * n_z, n,
+      AKM_CK(copy_rows(st + n, sizeof(double) * n_z, Z, sizeof(double) * ldz, sizeof(double) * n_z, n,
                                cudaMemcpyHostToDevice, s));
       Zd = st + n;
       ldzd = n_z;
