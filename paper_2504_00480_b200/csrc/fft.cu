@@ -736,18 +736,28 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
       K0 = std::max(K0, tab.w[w].K[0]);
       I = std::max(I, (long long)tab.w[w].K[1] * tab.w[w].K[2] * r);
     }
-    constexpr int PC = 8;
-    const size_t sp = sizeof(double2) * ((size_t)(L0 + ops * K0) * PC + (size_t)K0 * L0);
+    // columns per pencil CTA: 4 for few columns (r = 1: more CTAs against latency), else 8
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(k_plane_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(k_pencil<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      e = cudaFuncSetAttribute(k_pencil<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(k_pencil<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    k_pencil<PC><<<dim3((unsigned)((I + PC - 1) / PC), tab.P), kDftThreads, sp, s>>>(dtab, A2, C, tw, D, dslot0, r,
-                                                                                    ops);
+    if (I < 2048) {
+      constexpr int PC = 4;
+      const size_t sp = sizeof(double2) * ((size_t)(L0 + ops * K0) * PC + (size_t)K0 * L0);
+      k_pencil<PC><<<dim3((unsigned)((I + PC - 1) / PC), tab.P), kDftThreads, sp, s>>>(dtab, A2, C, tw, D, dslot0, r,
+                                                                                      ops);
+    } else {
+      constexpr int PC = 8;
+      const size_t sp = sizeof(double2) * ((size_t)(L0 + ops * K0) * PC + (size_t)K0 * L0);
+      k_pencil<PC><<<dim3((unsigned)((I + PC - 1) / PC), tab.P), kDftThreads, sp, s>>>(dtab, A2, C, tw, D, dslot0, r,
+                                                                                      ops);
+    }
     k_plane_inv<<<dim3(L0 * ops, tab.P), kFuseThreads, si, s>>>(dtab, C, H, tw, r, ops);
     return cudaGetLastError();
   }
