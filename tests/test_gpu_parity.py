@@ -384,3 +384,26 @@ def test_large_r_chunking_vs_ndft(akm):
     nd = F.additive_fastsum(X, [(0, 1, 2)], 0, th, V, 32, 1.0 / 16, ops=("K", "dell"))
     for op in ("K", "dell"):
         assert rel(out[op], nd[op]) <= 1e-9
+
+
+def test_window_error_decreases_with_m(akm):
+    """SURVEY.md §4 tier 3: against the exact truncated-Fourier operator (eq. 3.3), the GPU error is
+    the NFFT window error of eq. (A.3), which must fall as the window half-width m grows."""
+    wl, X, V = _wl_inputs("c1", n=1500, r=2)
+    nd = F.additive_fastsum(X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.eps_B, ops=("K",))
+    errs = []
+    for m in (4, 6, 8):              # the built window supports (2m taps: 8, 12, 16)
+        out, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, m, wl.eps_B, ("K",))
+        errs.append(rel(out["K"], nd["K"]))
+    assert all(b < a for a, b in zip(errs, errs[1:])), errs
+    assert errs[-1] <= 1e-9
+
+
+def test_run_to_run_agreement(akm):
+    """Spreading accumulates footprints with float64 atomics, so bits may differ between runs (reading
+    R13); the outputs agree to rounding."""
+    wl, X, V = _wl_inputs("c2", n=4000, r=3)
+    a, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B, ("K", "dell"))
+    b, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B, ("K", "dell"))
+    for op in ("K", "dell"):
+        assert rel(a[op], b[op]) <= 1e-13
