@@ -1,14 +1,18 @@
-// spread_v5.cu -- adjoint NFFT gridding, one warp per SM sub-partition (experimental variant of
-// spread_mma.cu, selected with AKM_SPREAD_V5=1 for A/B measurement).
+// spread_v5.cu -- adjoint NFFT gridding (NFFT step 1 transposed, App. A), the kernel
+// for 3-D windows with enough work items to fill the GPU (plan.cu; k_spread_mma otherwise).
 //
 // Same GEMM as spread_mma.cu (C[(o0,o1),(o2,c)] = sum_p (w0 w1)[p] (w2 v)[p] on DMMA), but:
-//   * 4 warps per CTA and one CTA per SM: every SM sub-partition has exactly one warp, so the
-//     scalar FP64 work of a warp (its fragment products, its share of the window weights) is never
-//     starved by another warp's DMMA stream (tools/microbench/dmma_occupancy.cu);
-//   * fragments are formed on the fly (A = W0 * W1, B = W2 * V: one DMUL each) from the per-point
-//     weight rows, so there are no operand panels to build and no staging phase for them;
-//   * the weights of batch b+1 are evaluated right after the MMAs of batch b (double-buffered), raw
-//     inputs stream through a 5-deep cp.async ring.
+//   * 4 MMA warps per CTA and one CTA per SM: every SM sub-partition has exactly one MMA warp, so
+//     each can hold up to 9 x 5 DMMA accumulator tiles (tools/microbench/dmma_occupancy.cu: one warp
+//     per sub-partition keeps the DMMA pipe busy);
+//   * fragments are formed on the fly (A = W0 * W1, B = W2 * V: one independent DMUL each) from
+//     the per-point weight rows, so there are no operand panels and no staging phase for them;
+//   * the window weights of a batch are a small DMMA product (powers of x times the polynomial
+//     coefficients), evaluated for batch b+1 right after the MMAs of batch b (double-buffered);
+//     raw inputs stream through a 5-deep cp.async ring;
+//   * with small register tiles (few RHS) a warp-specialised variant adds 4 helper warps that run
+//     the weights and the ring while the MMA warps stream (named-barrier handshake per batch).
+// AKM_SPREAD_V5=0/1 and AKM_V5_WS=0/1 force the kernel choices (A/B measurements).
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
