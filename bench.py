@@ -130,6 +130,28 @@ def algorithmic_counts(wl, info, r, ops):
     return spread_flops, interp_flops, bytes_
 
 
+def stage_bytes(wl, info, r, ops):
+    """Algorithmic HBM bytes per MVM of each stage (BJ north_star: HBM GB/s of spreading, DFT and
+    interpolation): what the stage must read and write at least, with every grid in HBM.
+      spread: coordinates (d doubles per point-window) + permutation (int32) + V rows + grid write;
+      fft:    grid read + H write (one grid per interpolated operator);
+      interp: H read + coordinates + permutation + per-window partial outputs;
+      epilogue: partials read + V (noise term) + outputs."""
+    n, W = wl.n, len(wl.windows)
+    n_s = wl.extra.get("n_src", n)
+    n_i = n - n_s if "n_src" in wl.extra else n
+    d = [len(w) for w in wl.windows]
+    n_ops = len({"K" if o in ("K", "dsf") else o for o in ops})
+    ntap = [int(np.prod(b)) for b in info["box"]]
+    grid = sum(8.0 * nt * r for nt in ntap)
+    return {
+        "spread": 8.0 * n_s * sum(d) + 4.0 * n_s * W + 8.0 * n_s * r + grid,
+        "fft": grid + grid * n_ops,
+        "interp": grid * n_ops + 8.0 * n_i * sum(d) + 4.0 * n_i * W + 8.0 * n_i * r * n_ops * W,
+        "epilogue": 8.0 * n_i * r * n_ops * W + 8.0 * n_i * r + 8.0 * n_i * r * len(ops),
+    }
+
+
 def _oracle_inputs(wl):
     """(X, V, theta, candidate rows) for the CPU oracle legs.  Cross workloads: the dense products
     on the union with the targets' V rows zero are exactly the cross product at the target rows
@@ -381,6 +403,24 @@ def main():
     achieved = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
     peaks = _peaks()
     stage_total = stages["spread_ms"] + stages["fft_ms"] + stages["interp_ms"] + stages["epilogue_ms"]
+    # per-stage HBM rate (algorithmic bytes / stage time) and, where the round's ncu capture has
+    # this workload, the measured DRAM bytes of the stage's dominant kernel per launch
+    sb = stage_bytes(wl, info, wl.r, wl.ops)
+    try:
+        measured = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bytes_per_launch"].get(wl.name, {})
+    except Exception:
+        measured = {}
+    hbm_stages = {}
+    for k in ("spread", "fft", "interp", "epilogue"):
+        t = stages[k + "_ms"] / (K * products_per_step) * 1e-3  # seconds per MVM
+        if t <= 0:
+            continue
+        e = {"algorithmic_bytes": sb[k], "gbs": sb[k] / t / 1e9, "frac": sb[k] / t / 1e9 / peaks.get("hbm_gbs", 6650.0)}
+        if k in measured and stages.get(k + "_launches"):
+            per_mvm = measured[k] * stages[k + "_launches"] / (K * products_per_step)
+            e["dram_bytes_ncu"] = per_mvm
+            e["dram_gbs_ncu"] = per_mvm / t / 1e9
+        hbm_stages[k] = e
     clocks = sampler.summary(tail)
 
     line = {
@@ -401,6 +441,7 @@ def main():
         "stage_share": {k: stages[k + "_ms"] / stage_total for k in ("spread", "fft", "interp", "epilogue")},
         "hbm": {"algorithmic_bytes_per_step": alg_bytes, "achieved_gbs": alg_bytes / (ms_per_step * 1e-3) / 1e9,
                 "peak_gbs": peaks.get("hbm_gbs"), "frac": alg_bytes / (ms_per_step * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)},
+        "hbm_stages": hbm_stages,
         "set_theta_ms": set_theta_ms,
         "products_per_step": products_per_step,
         "plan": {"bin": info["bin"], "box": info["box"], "c_w": info["c_w"], "work_items_spread": info["work_items_spread"],
