@@ -184,17 +184,21 @@ __global__ void __launch_bounds__(kSpreadThreads, spread_minb(MB, NB)) k_spread_
       const double* W1 = Ws + PB * LDF;
       const double* W2 = Ws + 2 * PB * LDF;
       const int F0 = g.F[0], F2 = g.F[2];
-      for (int job = tid; job < PB * F0; job += NT) {
-        const int o0 = job / PB, p = job - o0 * PB;
-        const double w0 = W0[p * LDF + o0];
-        const double* w1 = W1 + p * LDF;
-        double* dst = As + p * lda + o0 * F1;
-        if ((F1 & 1) == 0) {
-          for (int o = 0; o < F1; o += 2) {
-            const double2 t = *reinterpret_cast<const double2*>(w1 + o);
-            *reinterpret_cast<double2*>(dst + o) = make_double2(w0 * t.x, w0 * t.y);
-          }
-        } else {
+      if ((F1 & 1) == 0) {  // one job per (point, o0, pair of o1): enough jobs when F0 = 1 (d = 2)
+        const int H1 = F1 >> 1;
+        for (int job = tid; job < PB * F0 * H1; job += NT) {
+          const int po = job / H1, h = job - po * H1;
+          const int o0 = po / PB, p = po - o0 * PB;
+          const double w0 = W0[p * LDF + o0];
+          const double2 t = *reinterpret_cast<const double2*>(W1 + p * LDF + 2 * h);
+          *reinterpret_cast<double2*>(As + p * lda + o0 * F1 + 2 * h) = make_double2(w0 * t.x, w0 * t.y);
+        }
+      } else {
+        for (int job = tid; job < PB * F0; job += NT) {
+          const int o0 = job / PB, p = job - o0 * PB;
+          const double w0 = W0[p * LDF + o0];
+          const double* w1 = W1 + p * LDF;
+          double* dst = As + p * lda + o0 * F1;
           for (int o = 0; o < F1; ++o) dst[o] = w0 * w1[o];
         }
       }
