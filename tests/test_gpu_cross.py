@@ -160,3 +160,27 @@ def test_cross_mixed_window_dims(akm, family):
     got = gpu_cross(akm, X, 2000, windows, family, theta, V, N=N, m=m)
     want = dense_cross(X[:2000], X[2000:], windows, family, theta, V)
     assert rel(got, want) <= (1e-3 if family == 1 else 1e-6)
+
+
+def test_cross_strided_blocks(akm):
+    """V and Yt as column slices of wider row-major blocks (ld > r), device and host."""
+    wl = workloads.CONFIGS["c2"]
+    X = workloads.make_X(wl, n=3000)
+    theta = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    Vw = workloads.make_V(wl, n=2200, r=5)
+    want = dense_cross(X[:2200], X[2200:], wl.windows, wl.family, theta, Vw[:, 1:4])
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family, wl.N, 2.0, wl.m, 1.0 / 16)
+    plan.set_theta(*theta)
+    Vd = torch.from_numpy(Vw).to(dev)
+    Yw = torch.full((800, 7), float("nan"), dtype=torch.float64, device=dev)
+    plan.cross_mvm(2200, Vd[:, 1:4], Yw[:, 2:5])
+    torch.cuda.synchronize()
+    Yh = Yw.cpu().numpy()
+    assert rel(Yh[:, 2:5], want) <= 1e-6
+    assert np.isnan(Yh[:, :2]).all() and np.isnan(Yh[:, 5:]).all()   # untouched columns
+    Yhost = np.full((800, 6), np.nan)
+    plan.cross_mvm(2200, Vw[:, 1:4], Yhost[:, 1:4])
+    assert rel(Yhost[:, 1:4], want) <= 1e-6 and np.isnan(Yhost[:, 0]).all() and np.isnan(Yhost[:, 4:]).all()
+    plan.close()
