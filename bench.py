@@ -183,7 +183,9 @@ def run_reference(args, wl):
     t0 = time.perf_counter()
     dense_apply(X, wl.windows, wl.family, theta, V, rows=rows_all[:64], ops=wl.ops)
     per_row = (time.perf_counter() - t0) / 64
-    rows_per_step = int(min(n_rows, max(64, 2.0 / max(per_row, 1e-9))))
+    # each step ~2 s of CPU work, and the whole --warmup + --steps run within ~2 minutes
+    step_budget = min(2.0, 120.0 / max(1, args.warmup + args.steps))
+    rows_per_step = int(min(n_rows, max(64, step_budget / max(per_row, 1e-9))))
     times = []
     for s in range(args.warmup + args.steps):
         rows = rows_all[(s * rows_per_step) % max(1, n_rows - rows_per_step + 1):][:rows_per_step]
