@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_
   }
 }
 
-#define AKM_V5_TILES(X) X(9, 5) X(5, 9) X(9, 4) X(4, 9) X(6, 6) X(6, 3) X(3, 6) X(3, 4) X(6, 2) X(3, 2) X(2, 2) X(1, 2)
+#define AKM_V5_TILES(X) X(9, 5) X(5, 9) X(9, 4) X(4, 9) X(6, 6) X(6, 3) X(3, 6) X(3, 7) X(3, 4) X(6, 2) X(3, 2) X(2, 2) X(1, 2)
 
 bool spread_v5_choose(int M, int Nn, int& MB, int& NB, int& WN) {
   static const int cand[][2] = {
@@ -363,7 +363,7 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
   // weight and ring work overlaps the MMAs); with big tiles the helpers' scalar FP64 on the same
   // SM sub-partitions slows the DMMA stream more than it hides
   static const int ws_env = getenv("AKM_V5_WS") ? atoi(getenv("AKM_V5_WS")) : -1;
-  const bool ws = ws_env >= 0 ? ws_env != 0 : MB * NB <= 24;
+  const bool ws = ws_env >= 0 ? ws_env != 0 : MB * NB <= 12;
 #define AKM_CASE1(a, b, o)                                                                                     \
   if (MB == a && NB == b && ws == o) {                                                                          \
     static bool attr_set = false;                                                                               \
