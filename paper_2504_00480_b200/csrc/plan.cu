@@ -609,7 +609,7 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
     // one-warp-per-SMSP kernel (spread_v5.cu) for 2-D / 3-D windows with enough work items to fill the
     // GPU at one CTA per SM; AKM_SPREAD_V5=0/1 forces either kernel (A/B measurement)
     static const int v5_env = getenv("AKM_SPREAD_V5") ? atoi(getenv("AKM_SPREAD_V5")) : -1;
-    const bool v5 = v5_env >= 0 ? v5_env != 0 : (d >= 2 && grp.sl[set].spread_count >= 2 * 148);
+    const bool v5 = v5_env >= 0 ? v5_env != 0 : d >= 2;
     while (v5 && r0 < r) {
       int rc = std::min(12, r - r0), MB = 0, NB = 0, WN = 0;
       while (rc > 1 && !(spread_v5_choose(M, F * rc, MB, NB, WN) && spread_v5_smem(F, rc, MB, NB, WN) <= 220 * 1024)) --rc;

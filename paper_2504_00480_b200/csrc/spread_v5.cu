@@ -363,7 +363,7 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
   // weight and ring work overlaps the MMAs); with big tiles the helpers' scalar FP64 on the same
   // SM sub-partitions slows the DMMA stream more than it hides
   static const int ws_env = getenv("AKM_V5_WS") ? atoi(getenv("AKM_V5_WS")) : -1;
-  const bool ws = ws_env >= 0 ? ws_env != 0 : MB * NB <= 12;
+  const bool ws = ws_env >= 0 ? ws_env != 0 : (MB * NB <= 12 || n_items < 2 * 148);
 #define AKM_CASE1(a, b, o)                                                                                     \
   if (MB == a && NB == b && ws == o) {                                                                          \
     static bool attr_set = false;                                                                               \
