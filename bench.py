@@ -12,7 +12,7 @@ One "step" is one pass of the hot path: a single
            FP64 FMA peak (the path is FP64-ALU bound)
   cpu_baseline: the float64 dense oracle (oracle/dense.c) on a bounded row sample, rank 0, N = 1
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
 Under torchrun (N > 1) every rank runs its own independent RHS block of the same workload
 (weak scaling, no data-path collective) and rank 0 prints the max-over-ranks
 timing.
@@ -239,7 +239,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(workloads.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-launches", action="store_true", help="short run for ncu launch lists")

@@ -190,6 +190,14 @@ akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, 
                               int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,
                               void* stream);
 
+/* Test hook: the window polynomials the kernels evaluate.  For tap o in [0, 2m) of a
+ * point with fractional grid position t = u - floor(u), the Kaiser-Bessel weight (App. A,
+ * P:1240-1247) phi((t + m - 1 - o) / n_g) is replaced by sum_k coef[o*(degree+1) + k] x^k with
+ * x = 2t - 1 (the degree-14 Chebyshev interpolant on t in [0, 1], built in akm_set_points).
+ * coef: host array of at least 16 * 15 doubles (output); *taps = 2m, *degree = 14.
+ * Errors: INVALID_ARG (NULL), STATE (before akm_set_points). */
+akm_status akm_get_window_poly(const akm_plan* plan, double* coef, int32_t* taps, int32_t* degree);
+
 /* Library version string. */
 /* Gradient of the objective Z~ (eq. (div)) with M = diag(Khat) = c I,
  * c = sigma_f^2 P + sigma_eps^2 (reading R11):

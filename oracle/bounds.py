@@ -4,10 +4,13 @@ Used as pins: the oracle's Fourier coefficients (eq. 3.2) and truncated series m
 stay below these bounds, and the NFFT oracle below eq. (A.3).
 
 * ``delta_m``     Lemma 4.2
-* ``delta_derm``  Lemma 4.3, ell < 1/2
 * ``thm44``       Theorem 4.4: ||kappa~^m_ERR||_inf <= 8 / (pi^2 ell (m - 2 sqrt 3))
 * ``thm45``       Theorem 4.5: 32/(3 ell^4 pi^4 (m-2sqrt3)^3) + 8/(ell^2 pi^2 (m-2sqrt3))
 * ``nfft_bound``  eq. (A.3), per unit ||b||_1, d = 1
+
+Lemma 4.3's delta^derm is not carried: it bounds nothing on the product path and
+the only check available for it (dominance of a sampled periodisation gap, which it exceeds by
+20-1500x) cannot tell a transcription error from the bound itself (Weak 1).
 * ``periodized``  kappa~(r) = sum_{z in Z^d} kappa(r + z) (Def. 4.1), truncated image sum
 """
 from __future__ import annotations
@@ -26,12 +29,6 @@ def delta_m(ell):
     a = 1.0 + 2.0 * S3 * ell
     return (3.0 * math.exp(-1.0 / (2.0 * S3 * ell)) * a + 3.0 * math.exp(-1.0 / (S3 * ell)) * a * a
             + math.exp(-3.0 / (2.0 * S3 * ell)) * a ** 3)
-
-
-def delta_derm(ell):
-    e = math.exp(-1.0 / (2.0 * S3 * ell))
-    return (3.0 / ell**2 * (1.0 + e * (1.0 + 2.0 * S3 * ell)) ** 2 * (1.0 + e * (1.0 + 2.0 * S3 * ell + 12.0 * ell**2))
-            - 3.0 / ell**2)
 
 
 def thm44(m, ell):

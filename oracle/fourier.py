@@ -90,6 +90,8 @@ def ndft_adjoint(xs, V, N):
     d = xs.shape[1]
     V = np.asarray(V, dtype=np.float64).reshape(xs.shape[0], -1)
     E = _exp_table(xs, N, -1.0)
+    if d == 2:  # the same sum as one matrix product per column: a[c] = (E_0 diag(V[:, c]))^T E_1
+        return np.stack([(E[0] * V[:, c:c + 1]).T @ E[1] for c in range(V.shape[1])])
     sub = "abc"[:d]
     expr = "jr," + ",".join("j" + s for s in sub) + "->r" + sub
     return np.einsum(expr, V, *E, optimize=True)
@@ -106,11 +108,13 @@ def ndft_forward(xs, fhat):
     return np.einsum(expr, fhat, *E, optimize=True)
 
 
-def trunc_fastsum(xs, V, b):
-    """eq. (3.3) with the real part (reading R5): h_i = Re sum_{k in I_N} b_k a_k e^{2 pi i k.x_i}."""
+def trunc_fastsum(xs, V, b, rows=None):
+    """eq. (3.3) with the real part (reading R5): h_i = Re sum_{k in I_N} b_k a_k e^{2 pi i k.x_i}.
+    ``rows`` evaluates the outer sum at those points only (the inner sums a_k run over all points)."""
     N = b.shape[0]
     a = ndft_adjoint(xs, V, N)
-    return np.real(ndft_forward(xs, b[None, ...] * a))
+    xo = xs if rows is None else np.atleast_2d(xs)[rows]
+    return np.real(ndft_forward(xo, b[None, ...] * a))
 
 
 # ----------------------------------------------------------------------------- App. A: window
@@ -245,16 +249,20 @@ def window_scaling(Xw, family, ell, N, eps_B):
 
 
 def additive_fastsum(X, windows, family, theta, V, N, eps_B=1.0 / 16, method="ndft", sigma=2.0, m=6,
-                     ops=("K", "dell", "dsf", "dse"), scales=None):
+                     ops=("K", "dell", "dsf", "dse"), scales=None, rows=None):
     """Truncated-Fourier (method='ndft', eq. 3.3) or NFFT (method='nfft', App. A) additive operator.
 
     Y = sigma_f^2 sum_w h_w + sigma_eps^2 V;  dY_ell = sigma_f^2 sum_w (1/c_w) h_w[b(kappa_der at ell/c_w)];
-    dY_sf = 2 sigma_f sum_w h_w;  dY_se = 2 sigma_eps V.  ``scales`` optionally fixes c_w (list)."""
+    dY_sf = 2 sigma_f sum_w h_w;  dY_se = 2 sigma_eps V.  ``scales`` optionally fixes c_w (list).
+    ``rows`` (method 'ndft' only) returns the outputs at those rows only."""
     X = np.asarray(X, dtype=np.float64)
     V = np.asarray(V, dtype=np.float64).reshape(X.shape[0], -1)
     sf, ell, se = theta
-    S = np.zeros_like(V)
-    SD = np.zeros_like(V)
+    if rows is not None and method != "ndft":
+        raise ValueError("rows= needs method='ndft'")
+    Vo = V if rows is None else V[rows]
+    S = np.zeros_like(Vo)
+    SD = np.zeros_like(Vo)
     for wi, win in enumerate(windows):
         Xw = X[:, list(win)]
         d = Xw.shape[1]
@@ -268,7 +276,7 @@ def additive_fastsum(X, windows, family, theta, V, N, eps_B=1.0 / 16, method="nd
                 continue
             b = fourier_coefficients(kernel_samples(family, ell_eff, N, d, deriv))
             if method == "ndft":
-                h = trunc_fastsum(xs, V, b)
+                h = trunc_fastsum(xs, V, b, rows)
             else:
                 h = nfft_fastsum(xs, V, b, sigma, m)
             if deriv:
@@ -277,11 +285,11 @@ def additive_fastsum(X, windows, family, theta, V, N, eps_B=1.0 / 16, method="nd
                 S += h
     out = {}
     if "K" in ops:
-        out["K"] = sf * sf * S + se * se * V
+        out["K"] = sf * sf * S + se * se * Vo
     if "dell" in ops:
         out["dell"] = sf * sf * SD
     if "dsf" in ops:
         out["dsf"] = 2.0 * sf * S
     if "dse" in ops:
-        out["dse"] = 2.0 * se * V
+        out["dse"] = 2.0 * se * Vo
     return out

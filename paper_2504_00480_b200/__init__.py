@@ -32,7 +32,7 @@ AKM_MAX_WINDOWS = 32
 ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm", "akm_kernel_deriv_mvm",
                "akm_kernel_mvm_multi", "akm_get_info", "akm_set_scale_override", "akm_last_error", "akm_destroy",
                "akm_version", "akm_set_profiling", "akm_get_stage_times", "akm_objective_diag",
-               "akm_kernel_cross_mvm", "akm_gradient_diag")
+               "akm_kernel_cross_mvm", "akm_gradient_diag", "akm_get_window_poly")
 AKM_MAX_PROBES = 31
 
 
@@ -108,6 +108,8 @@ def _load():
     lib.akm_get_stage_times.restype = st
     lib.akm_objective_diag.argtypes = [P, P, P, i64, i32, i32, i32, ctypes.POINTER(akm_objective_out), P, P]
     lib.akm_objective_diag.restype = st
+    lib.akm_get_window_poly.argtypes = [P, P, P, P]
+    lib.akm_get_window_poly.restype = st
     lib.akm_version.argtypes = []
     lib.akm_version.restype = ctypes.c_char_p
     return lib
@@ -165,6 +167,39 @@ def _stream(stream, *tensors):
     return ctypes.c_void_p(0)
 
 
+# rows n of the last successful akm_set_points per plan handle: the C side reads and writes exactly
+# n rows of every block (n - n_src target rows for the cross product), so mismatched tensors are
+# rejected here before any pointer crosses the ABI
+_ROWS = {}
+
+
+def _expect_rows(plan, name, rows, want=None):
+    if want is None:
+        want = _ROWS.get(getattr(plan, "value", plan))
+    if want is not None and rows != want:
+        raise ValueError(f"{name} has {rows} rows; the plan expects {want}")
+
+
+def _vector(a, name):
+    """A 1-D float64 vector (or n x 1 block) made contiguous: the C ABI reads n consecutive doubles."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.dim() == 2 and a.shape[1] == 1:
+                a = a[:, 0]
+            if a.dim() != 1:
+                raise ValueError(f"{name} must be a vector")
+            return a.contiguous()
+    except ImportError:  # pragma: no cover
+        pass
+    arr = np.asarray(a)
+    if arr.ndim == 2 and arr.shape[1] == 1:
+        arr = arr[:, 0]
+    if arr.ndim != 1:
+        raise ValueError(f"{name} must be a vector")
+    return np.ascontiguousarray(arr)
+
+
 def _check(plan, status):
     if status != AKM_OK:
         msg = _lib.akm_last_error(plan).decode() if plan else ""
@@ -185,6 +220,7 @@ def akm_create(device: int = 0):
 
 
 def akm_destroy(plan) -> None:
+    _ROWS.pop(getattr(plan, "value", plan), None)
     _lib.akm_destroy(plan)
 
 
@@ -199,28 +235,40 @@ def akm_set_points(plan, X, windows, family, N, sigma_over, m, eps_B, stream=Non
     st = _lib.akm_set_points(plan, px, n, p, ldx, feat.ctypes.data_as(ctypes.c_void_p),
                              lens.ctypes.data_as(ctypes.c_void_p), len(windows), int(family), int(N),
                              float(sigma_over), int(m), float(eps_B), _stream(stream, keep))
+    _ROWS.pop(getattr(plan, "value", plan), None)
     _check(plan, st)
+    _ROWS[getattr(plan, "value", plan)] = n
 
 
 def akm_set_theta(plan, sigma_f, ell, sigma_eps, stream=None):
     _check(plan, _lib.akm_set_theta(plan, float(sigma_f), float(ell), float(sigma_eps), _stream(stream)))
 
 
-def akm_kernel_mvm(plan, V, Y, stream=None):
+def _same_block(plan, V, outs):
+    """Marshal V and the outputs of a square product: every block n x r with the plan's n."""
     pv, ldv, n, r, _, kv = _ptr_ld(V, "V")
-    py, ldy, _, _, _, ky = _ptr_ld(Y, "Y")
+    _expect_rows(plan, "V", n)
+    res = []
+    for name, o in outs:
+        m = _ptr_ld(o, name)
+        if o is not None and (m[2] != n or m[3] != r):
+            raise ValueError(f"{name} must be {n} x {r} like V (got {m[2]} x {m[3]})")
+        res.append(m)
+    return (pv, ldv, n, r, kv), res
+
+
+def akm_kernel_mvm(plan, V, Y, stream=None):
+    (pv, ldv, n, r, kv), [(py, ldy, _, _, _, ky)] = _same_block(plan, V, [("Y", Y)])
     _check(plan, _lib.akm_kernel_mvm(plan, pv, ldv, r, py, ldy, _stream(stream, kv, ky)))
 
 
 def akm_kernel_deriv_mvm(plan, which, V, dY, stream=None):
-    pv, ldv, n, r, _, kv = _ptr_ld(V, "V")
-    py, ldy, _, _, _, ky = _ptr_ld(dY, "dY")
+    (pv, ldv, n, r, kv), [(py, ldy, _, _, _, ky)] = _same_block(plan, V, [("dY", dY)])
     _check(plan, _lib.akm_kernel_deriv_mvm(plan, int(which), pv, ldv, r, py, ldy, _stream(stream, kv, ky)))
 
 
 def akm_kernel_mvm_multi(plan, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
-    pv, ldv, n, r, _, kv = _ptr_ld(V, "V")
-    outs = [_ptr_ld(o, "out") for o in (Y, dY_ell, dY_sf)]
+    (pv, ldv, n, r, kv), outs = _same_block(plan, V, [("Y", Y), ("dY_ell", dY_ell), ("dY_sf", dY_sf)])
     lds = {o[1] for o in outs if o[0] is not None}
     if len(lds) > 1:
         raise ValueError("all outputs of akm_kernel_mvm_multi must share one leading dimension")
@@ -235,6 +283,9 @@ def akm_kernel_cross_mvm(plan, n_src, V, Yt, stream=None):
     py, ldy, _, ry, _, ky = _ptr_ld(Yt, "Yt")
     if nv != n_src or (Yt is not None and ry != r):
         raise ValueError(f"V must have n_src = {n_src} rows and Yt the same number of columns ({r})")
+    n_all = _ROWS.get(getattr(plan, "value", plan))
+    if n_all is not None and Yt is not None:
+        _expect_rows(plan, "Yt", _ptr_ld(Yt, "Yt")[2], n_all - int(n_src))
     _check(plan, _lib.akm_kernel_cross_mvm(plan, int(n_src), pv, ldv, r, py, ldy, _stream(stream, kv, ky)))
 
 
@@ -261,6 +312,15 @@ def akm_set_scale_override(plan, c_w=None):
         _check(plan, _lib.akm_set_scale_override(plan, arr.ctypes.data_as(ctypes.c_void_p)))
 
 
+def akm_get_window_poly(plan):
+    """(coefficients (2m, degree + 1), taps, degree) of the window polynomials the kernels evaluate."""
+    coef = np.zeros(16 * 15, dtype=np.float64)
+    taps, deg = ctypes.c_int32(), ctypes.c_int32()
+    _check(plan, _lib.akm_get_window_poly(plan, coef.ctypes.data_as(ctypes.c_void_p), ctypes.byref(taps),
+                                          ctypes.byref(deg)))
+    return coef[:taps.value * (deg.value + 1)].reshape(taps.value, deg.value + 1), taps.value, deg.value
+
+
 def akm_set_profiling(plan, enable: bool):
     _check(plan, _lib.akm_set_profiling(plan, 1 if enable else 0))
 
@@ -273,8 +333,11 @@ def akm_get_stage_times(plan, reset: bool = False) -> dict:
 
 def akm_objective_diag(plan, y, Z, cg_iters=50, lanczos_steps=30, stream=None) -> dict:
     """eq. (1.4) with M = diag(Khat): CG + SLQ, every Krylov step one block product (include/akm.h)."""
+    y = _vector(y, "y")
     py, _, n, _, _, ky = _ptr_ld(y, "y")
-    pz, ldz, _, n_z, _, kz = _ptr_ld(Z, "Z")
+    pz, ldz, nz_rows, n_z, _, kz = _ptr_ld(Z, "Z")
+    _expect_rows(plan, "y", n)
+    _expect_rows(plan, "Z", nz_rows)
     out = akm_objective_out()
     hist = (ctypes.c_double * max(int(cg_iters), 1))()
     _check(plan, _lib.akm_objective_diag(plan, py, pz, ldz, n_z, int(cg_iters), int(lanczos_steps), ctypes.byref(out),
@@ -286,8 +349,11 @@ def akm_objective_diag(plan, y, Z, cg_iters=50, lanczos_steps=30, stream=None) -
 
 def akm_gradient_diag(plan, y, Z, cg_iters=50, stream=None) -> dict:
     """eq. (div) with M = diag(Khat): block PCG on [y | Z], one fused derivative product (include/akm.h)."""
+    y = _vector(y, "y")
     py, _, n, _, _, ky = _ptr_ld(y, "y")
-    pz, ldz, _, n_z, _, kz = _ptr_ld(Z, "Z")
+    pz, ldz, nz_rows, n_z, _, kz = _ptr_ld(Z, "Z")
+    _expect_rows(plan, "y", n)
+    _expect_rows(plan, "Z", nz_rows)
     grad = (ctypes.c_double * 3)()
     hist = (ctypes.c_double * max(int(cg_iters), 1))()
     _check(plan, _lib.akm_gradient_diag(plan, py, pz, ldz, n_z, int(cg_iters), grad, hist, _stream(stream, ky, kz)))
@@ -350,6 +416,9 @@ class Plan:
 
     def info(self):
         return akm_get_info(self.handle)
+
+    def window_poly(self):
+        return akm_get_window_poly(self.handle)
 
     def set_profiling(self, enable=True):
         akm_set_profiling(self.handle, enable)

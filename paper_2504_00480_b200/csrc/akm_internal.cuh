@@ -15,6 +15,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace akm {
@@ -176,6 +177,20 @@ __host__ __device__ inline double bessel_i0(double x) {
     if (term < 1e-17 * sum) break;
   }
   return sum;
+}
+
+// Opt-ins to more than 48 KB of dynamic shared memory (cudaFuncSetAttribute) hold per device: each
+// launch site keeps one bit per device.  Two threads racing on the first launch both set
+// the attribute, which is idempotent.
+inline bool optin_done(const std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  return (mask.load(std::memory_order_acquire) >> (dev & 63)) & 1ull;
+}
+inline void optin_mark(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  mask.fetch_or(1ull << (dev & 63), std::memory_order_release);
 }
 
 }  // namespace akm

@@ -670,12 +670,12 @@ template <int MODE, int COLS>
 static cudaError_t launch_cols(long long tiles, int P, int Lmax, const WinTable* dtab, const void* X, void* Y,
                                const double2* tw, const double* D, int dslot0, int r, int ops, cudaStream_t s) {
   const size_t smem = sizeof(double2) * (size_t)Lmax * COLS;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};
+  if (!optin_done(attr_set)) {
     cudaError_t e = cudaFuncSetAttribute(k_dft_axis<MODE, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          200 * 1024);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    optin_mark(attr_set);
   }
   k_dft_axis<MODE, COLS><<<dim3((unsigned)tiles, P), kDftThreads, smem, s>>>(dtab, X, Y, tw, D, dslot0, r, ops);
   return cudaGetLastError();
@@ -708,11 +708,11 @@ cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const 
   if (planes_fit(tab, r, sf, si)) {
     int L0 = 1;
     for (int w = 0; w < tab.P; ++w) L0 = std::max(L0, tab.w[w].L[0]);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (!optin_done(attr)) {
       cudaError_t e = cudaFuncSetAttribute(k_plane_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
-      attr = true;
+      optin_mark(attr);
     }
     k_plane_fwd<<<dim3(L0, tab.P), kFuseThreads, sf, s>>>(dtab, grid, A2, tw, r);
     return cudaGetLastError();
@@ -737,15 +737,15 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
       I = std::max(I, (long long)tab.w[w].K[1] * tab.w[w].K[2] * r);
     }
     // columns per pencil CTA: 4 for few columns (r = 1: more CTAs against latency), else 8
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (!optin_done(attr)) {
       cudaError_t e = cudaFuncSetAttribute(k_plane_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute(k_pencil<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute(k_pencil<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
-      attr = true;
+      optin_mark(attr);
     }
     if (I < 2048) {
       constexpr int PC = 4;

@@ -348,24 +348,24 @@ cudaError_t launch_interp_dt(const WinTable* dtab, const WorkItem* items, int n_
   if (ops == O && rc == R) {                                                                                        \
     if (O * R >= 8 && !sparse) {                                                                                    \
       const size_t smem = interp_mma_smem(D, T, O, R);                                                              \
-      static bool attr_set = false;                                                                                 \
-      if (!attr_set) {                                                                                              \
+      static std::atomic<unsigned long long> attr_set{0};                                                                                 \
+      if (!optin_done(attr_set)) {                                                                                              \
         cudaError_t e = cudaFuncSetAttribute(k_interp_mma<D, T, O, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                              (int)smem);                                                            \
         if (e != cudaSuccess) return e;                                                                             \
-        attr_set = true;                                                                                            \
+        optin_mark(attr_set);                                                                                            \
       }                                                                                                             \
       k_interp_mma<D, T, O, R><<<n_items, 256, smem, s>>>(dtab, items, u_sorted, perm, H, r, r0, part, n);         \
     } else {                                                                                                        \
       if (n_items_bin <= 0) return cudaSuccess;                                                                     \
       int whole = 0;                                                                                                \
       const size_t smem = interp_bin_smem(O * R, D >= 3 ? Fb2 : 1, Fb1, Fb2, whole);                                \
-      static bool attr_set = false;                                                                                 \
-      if (!attr_set) {                                                                                              \
+      static std::atomic<unsigned long long> attr_set{0};                                                                                 \
+      if (!optin_done(attr_set)) {                                                                                              \
         cudaError_t e = cudaFuncSetAttribute(k_interp_bin<D, T, O, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                              200 * 1024);                                                           \
         if (e != cudaSuccess) return e;                                                                             \
-        attr_set = true;                                                                                            \
+        optin_mark(attr_set);                                                                                            \
       }                                                                                                             \
       k_interp_bin<D, T, O, R><<<n_items_bin, 128, smem, s>>>(dtab, items_bin, u_sorted, perm, H, r, r0, part, n,  \
                                                               whole);                                               \

@@ -288,12 +288,12 @@ cudaError_t launch_interp_t(const WinTable* dtab, const PolyParam& pp, const Wor
 #define AKM_IT_CASE(T, F, O, R, M, W)                                                                          \
   if (taps == T && fp == F && ops == O && rc == R) {                                                           \
     constexpr size_t smem = ItShape<F, O * R, M, W>::smem;                                                     \
-    static bool attr_set = false;                                                                              \
-    if (!attr_set) {                                                                                           \
+    static std::atomic<unsigned long long> attr_set{0};                                                                              \
+    if (!optin_done(attr_set)) {                                                                                           \
       cudaError_t e = cudaFuncSetAttribute(k_interp_t<T, F, O, R, M, W>,                                       \
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
       if (e != cudaSuccess) return e;                                                                          \
-      attr_set = true;                                                                                         \
+      optin_mark(attr_set);                                                                                         \
     }                                                                                                          \
     k_interp_t<T, F, O, R, M, W><<<n_items, 32 * kItWarps, smem, s>>>(dtab, items, u_sorted, perm, H, r, r0,   \
                                                                       part, n, pp);                            \

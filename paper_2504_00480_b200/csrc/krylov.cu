@@ -315,7 +315,9 @@ __global__ void k_kr_advance(KrylovState* st, int R) {
 
 // ---------------------------------------------------------------- SLQ quadrature
 // Symmetric tridiagonal eigenproblem by implicit QL with Wilkinson-type shifts, tracking only the
-// first row of the eigenvector matrix (tau_j); one thread per probe.
+// first row of the eigenvector matrix (tau_j); one thread per probe.  This is the textbook implicit
+// QL iteration (EISPACK tql2, Bowdler, Martin, Reinsch and Wilkinson 1968; the same loop as the
+// widely reprinted "tqli" routine), restated here with the eigenvector update reduced to row 0.
 __device__ bool tridiag_eig_first_row(int k, double* d, double* e, double* z) {
   for (int i = 0; i < k; ++i) z[i] = (i == 0) ? 1.0 : 0.0;
   e[k - 1] = 0.0;
@@ -446,12 +448,12 @@ cudaError_t launch_kr_update(long long n, int R, const void* st, const double* B
 cudaError_t launch_kr_reorth(long long n, int R, int nq, const void* st, const double* Q, long long slab, double* W,
                              double* part, double* h, cudaStream_t s) {
   const int chunks = (nq + kProjJC - 1) / kProjJC;
-  static bool attr_set = false;  // R up to kKrMaxR needs more than the default 48 KB
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};  // R up to kKrMaxR needs more than the default 48 KB
+  if (!optin_done(attr_set)) {
     cudaError_t e = cudaFuncSetAttribute(k_kr_proj_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(sizeof(double) * kProjJC * 32 * kKrMaxR));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    optin_mark(attr_set);
   }
   const int slots = R <= 16 ? 32 : 16;  // block <= 512 threads: the registers of 2 rows in flight fit
   k_kr_proj_partial<<<dim3(kKrBlocks, chunks), slots * R, sizeof(double) * kProjJC * slots * R, s>>>(n, R, nq, Q, slab, W,

@@ -312,10 +312,11 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
       if (Fd > 20000) continue;
       bool fits = true;
       for (int a = 3 - d; a < 3; ++a) fits = fits && ((g.ncell[a] + B - 1) / B) * B + 2 * m - 1 <= n_g;
-      {
+      {  // both spreading kernels must have a tile for this footprint (enqueue_mvm picks by d)
         int MB_, NB_, WM_, WN_, Mr = 1;
         for (int t = 0; t < d - 1; ++t) Mr *= F;
         fits = fits && spread_mma_choose(Mr, F, F, 1, MB_, NB_, WM_, WN_);
+        if (d >= 2) fits = fits && spread_v5_choose(Mr, F, MB_, NB_, WN_);
       }
       if (!fits) continue;
       int nb[3];
@@ -606,8 +607,8 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
     int M = 1;
     for (int t = 0; t < d - 1; ++t) M *= F;
     int r0 = 0;
-    // one-warp-per-SMSP kernel (spread_v5.cu) for 2-D / 3-D windows with enough work items to fill the
-    // GPU at one CTA per SM; AKM_SPREAD_V5=0/1 forces either kernel (A/B measurement)
+    // one-warp-per-SMSP kernel (spread_v5.cu) for every 2-D / 3-D window group, k_spread_mma for 1-D
+    // windows; AKM_SPREAD_V5=0/1 forces either kernel (A/B measurement)
     static const int v5_env = getenv("AKM_SPREAD_V5") ? atoi(getenv("AKM_SPREAD_V5")) : -1;
     const bool v5 = v5_env >= 0 ? v5_env != 0 : d >= 2;
     while (v5 && r0 < r) {
@@ -1374,6 +1375,15 @@ akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, i
   }
   if (cg_relres)
     for (int t = 0; t < cg_iters; ++t) cg_relres[t] = hist[t];
+  return AKM_OK;
+}
+
+akm_status akm_get_window_poly(const akm_plan* plan, double* coef, int32_t* taps, int32_t* degree) {
+  if (!plan || !coef || !taps || !degree) return AKM_ERR_INVALID_ARG;
+  if (!plan->have_points) return AKM_ERR_STATE;
+  *taps = 2 * plan->m;
+  *degree = kPolyDeg;
+  std::memcpy(coef, plan->poly_param.c, sizeof(double) * 2 * plan->m * kPolyLen);
   return AKM_OK;
 }
 

@@ -320,12 +320,12 @@ cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const W
   if (n_items <= 0) return cudaSuccess;
 #define AKM_CASE(a, b)                                                                                         \
   if (MB == a && NB == b) {                                                                                    \
-    static bool attr_set = false;                                                                              \
-    if (!attr_set) {                                                                                           \
+    static std::atomic<unsigned long long> attr_set{0};                                                                              \
+    if (!optin_done(attr_set)) {                                                                                           \
       cudaError_t e = cudaFuncSetAttribute(k_spread_mma<a, b>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                            227 * 1024);                                                        \
       if (e != cudaSuccess) return e;                                                                          \
-      attr_set = true;                                                                                         \
+      optin_mark(attr_set);                                                                                         \
     }                                                                                                          \
     k_spread_mma<a, b><<<n_items, kSpreadThreads, smem, s>>>(dtab, items, u_sorted, perm, V, ldv, n, r0, rc,   \
                                                              r_total, grid, WN, pp);                           \

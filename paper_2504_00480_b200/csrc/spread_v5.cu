@@ -1,5 +1,6 @@
 // spread_v5.cu -- adjoint NFFT gridding (NFFT step 1 transposed, App. A), the kernel
-// for 3-D windows with enough work items to fill the GPU (plan.cu; k_spread_mma otherwise).
+// for every 2-D and 3-D window group (plan.cu; k_spread_mma serves 1-D windows, or all windows
+// under AKM_SPREAD_V5=0).
 //
 // Same GEMM as spread_mma.cu (C[(o0,o1),(o2,c)] = sum_p (w0 w1)[p] (w2 v)[p] on DMMA), but:
 //   * 4 MMA warps per CTA and one CTA per SM: every SM sub-partition has exactly one MMA warp, so
@@ -360,18 +361,19 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
                              cudaStream_t s) {
   if (n_items <= 0) return cudaSuccess;
   // warp-specialised variant for small register tiles (few RHS, e.g. c2: the helpers' latency-bound
-  // weight and ring work overlaps the MMAs); with big tiles the helpers' scalar FP64 on the same
+  // weight and ring work overlaps the MMAs) and for launches with fewer than 2 x 148 work items
+  // (c1: nothing to hide behind); with big tiles and many items the helpers' scalar FP64 on the same
   // SM sub-partitions slows the DMMA stream more than it hides
   static const int ws_env = getenv("AKM_V5_WS") ? atoi(getenv("AKM_V5_WS")) : -1;
   const bool ws = ws_env >= 0 ? ws_env != 0 : (MB * NB <= 12 || n_items < 2 * 148);
 #define AKM_CASE1(a, b, o)                                                                                     \
   if (MB == a && NB == b && ws == o) {                                                                          \
-    static bool attr_set = false;                                                                               \
-    if (!attr_set) {                                                                                            \
+    static std::atomic<unsigned long long> attr_set{0};                                                                               \
+    if (!optin_done(attr_set)) {                                                                                            \
       cudaError_t e = cudaFuncSetAttribute(k_spread_v5<a, b, o>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                            227 * 1024);                                                         \
       if (e != cudaSuccess) return e;                                                                           \
-      attr_set = true;                                                                                          \
+      optin_mark(attr_set);                                                                                          \
     }                                                                                                           \
     k_spread_v5<a, b, o><<<n_items, o ? 2 * kV5Threads : kV5Threads, smem, s>>>(dtab, items, u_sorted, perm, V, \
                                                                                 ldv, n, r0, rc,                \

@@ -90,3 +90,40 @@ def test_objective_struct_matches_header_fields(lib):
             flat += [v.strip().split("[")[0] for v in m.group(2).split(",")]
     assert flat == [f[0] for f in akm.akm_objective_out._fields_]
     assert "#define AKM_MAX_PROBES %d" % akm.AKM_MAX_PROBES in text
+
+
+def test_binding_rejects_mismatched_row_counts(lib):
+    """The C side reads / writes exactly the plan's n rows (n - n_src for the cross product); the
+    binding rejects blocks of another height before any pointer crosses the ABI."""
+    import numpy as np
+    _, akm = lib
+    fake = ctypes.c_void_p(0xABC0)
+    akm._ROWS[fake.value] = 10
+    try:
+        for call in (lambda: akm.akm_kernel_mvm(fake, np.zeros((9, 2)), np.zeros((9, 2))),
+                     lambda: akm.akm_kernel_mvm(fake, np.zeros((10, 2)), np.zeros((9, 2))),
+                     lambda: akm.akm_kernel_mvm_multi(fake, np.zeros((10, 2)), Y=np.zeros((10, 1))),
+                     lambda: akm.akm_kernel_deriv_mvm(fake, 0, np.zeros((11, 1)), np.zeros((11, 1))),
+                     lambda: akm.akm_kernel_cross_mvm(fake, 4, np.zeros((4, 1)), np.zeros((5, 1))),
+                     lambda: akm.akm_objective_diag(fake, np.zeros(9), np.zeros((9, 2))),
+                     lambda: akm.akm_gradient_diag(fake, np.zeros(10), np.zeros((8, 2)))):
+            with pytest.raises(ValueError):
+                call()
+    finally:
+        akm._ROWS.pop(fake.value, None)
+
+
+def test_binding_makes_strided_vectors_contiguous(lib):
+    """A strided column (e.g. V[:, 0]) passed as y is copied to contiguous memory: the C ABI reads n
+    consecutive doubles."""
+    import numpy as np
+    _, akm = lib
+    V = np.arange(30.0).reshape(10, 3)
+    y = akm._vector(V[:, 1], "y")
+    assert y.flags["C_CONTIGUOUS"] and np.array_equal(y, V[:, 1])
+    torch = pytest.importorskip("torch")
+    t = torch.arange(30.0, dtype=torch.float64).reshape(10, 3)
+    yt = akm._vector(t[:, 2], "y")
+    assert yt.is_contiguous() and torch.equal(yt, t[:, 2])
+    with pytest.raises(ValueError):
+        akm._vector(np.zeros((4, 2)), "y")
