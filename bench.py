@@ -13,9 +13,10 @@ One "step" is one pass of the hot path: a single
   cpu_baseline: the float64 dense oracle (oracle/dense.c) on a bounded row sample, rank 0, N = 1
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
-Under torchrun (N > 1) every rank runs its own independent RHS block of the same workload
-(weak scaling, no data-path collective) and rank 0 prints the max-over-ranks
-timing.
+Under torchrun (N > 1) the square products (c1-c4) are point-sharded: each rank owns a row block of
+the same problem and every product does one NCCL all-reduce of the grids (strong scaling,
+"scaling": "strong"); the Krylov drivers (c5, g5) and the cross product (x4) run one independent
+replica per rank (weak scaling).  Rank 0 prints the max-over-ranks timing.
 """
 from __future__ import annotations
 
@@ -113,10 +114,11 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def algorithmic_counts(wl, info, r, ops):
-    """FP64 flops of spreading / interpolation and minimal bytes of one step.
+def algorithmic_counts(wl, info, r, ops, n_local=None):
+    """FP64 flops of spreading / interpolation and minimal bytes of one step on this
+    rank (n_local: its rows under point sharding).
     Cross products (extra n_src): the method spreads the sources and interpolates at the targets."""
-    n, W = wl.n, len(wl.windows)
+    n, W = (wl.n if n_local is None else n_local), len(wl.windows)
     n_s = wl.extra.get("n_src", n)
     n_i = n - n_s if "n_src" in wl.extra else n
     d = [len(w) for w in wl.windows]
@@ -130,14 +132,14 @@ def algorithmic_counts(wl, info, r, ops):
     return spread_flops, interp_flops, bytes_
 
 
-def stage_bytes(wl, info, r, ops):
+def stage_bytes(wl, info, r, ops, n_local=None):
     """Algorithmic HBM bytes per MVM of each stage (BJ north_star: HBM GB/s of spreading, DFT and
     interpolation): what the stage must read and write at least, with every grid in HBM.
       spread: coordinates (d doubles per point-window) + permutation (int32) + V rows + grid write;
       fft:    grid read + H write (one grid per interpolated operator);
       interp: H read + coordinates + permutation + per-window partial outputs;
       epilogue: partials read + V (noise term) + outputs."""
-    n, W = wl.n, len(wl.windows)
+    n, W = (wl.n if n_local is None else n_local), len(wl.windows)
     n_s = wl.extra.get("n_src", n)
     n_i = n - n_s if "n_src" in wl.extra else n
     d = [len(w) for w in wl.windows]
@@ -209,12 +211,12 @@ def run_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(wl):
+def config_dict(wl, parallelism="1 GPU"):
     extra = {"n_src": wl.extra["n_src"], "n_target": wl.n - wl.extra["n_src"]} if "n_src" in wl.extra else {}
     return {"workload": wl.name, "description": wl.description, "n": wl.n, **extra, "r": wl.r, "windows": len(wl.windows),
             "d": [len(w) for w in wl.windows], "family": "gaussian" if wl.family == 0 else "matern12",
             "N": wl.N, "sigma_over": wl.sigma_over, "m": wl.m, "ops": list(wl.ops),
-            "l2": "256 MiB written between timed steps (L2 flush)"}
+            "l2": "256 MiB written between timed steps (L2 flush)", "parallelism": parallelism}
 
 
 def cpu_baseline(wl, budget_s=10.0):
@@ -259,32 +261,57 @@ def main():
     import paper_2504_00480_b200 as akm
     from paper_2504_00480_b200 import dist as D   # host-side N > 1 logic only (no kernels)
 
+    # AKM_BENCH_DEVICE / AKM_BENCH_BACKEND: exercise the N > 1 code path on a single GPU (every rank on
+    # one device over gloo; a plumbing check only, never a timing)
+    if os.environ.get("AKM_BENCH_DEVICE"):
+        local = int(os.environ["AKM_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("AKM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     X = workloads.make_X(wl)
     cross = "n_src" in wl.extra              # f2: K_{*X} V from the first n_src rows to the rest
     n_src = wl.extra.get("n_src", wl.n)
-    V = workloads.make_V(wl, n=n_src, seed=D.rank_seed(2000 + wl.index, rank))  # independent RHS block per rank
-    Xd = torch.from_numpy(X).to(dev)
+    objective = "cg_iters" in wl.extra          # c5: one Z~ evaluation per step (S8)
+    gradient = "grad_cg_iters" in wl.extra      # g5: one gradient of Z~ per step (f1)
+    # N > 1: the square products are point-sharded (each rank owns a row block of the SAME problem,
+    # one grid all-reduce per product: strong scaling); the Krylov drivers and the cross
+    # product run as independent replicas (weak scaling)
+    sharded = world > 1 and not (objective or gradient or cross)
+    if sharded:
+        row0, row1 = D.row_partition(wl.n, world, rank)
+        V = workloads.make_V(wl)[row0:row1]
+        Xd = torch.from_numpy(np.ascontiguousarray(X[row0:row1])).to(dev)
+    else:
+        row0, row1 = 0, wl.n
+        V = workloads.make_V(wl, n=n_src, seed=D.rank_seed(2000 + wl.index, rank))  # independent RHS block per rank
+        Xd = torch.from_numpy(X).to(dev)
+    V = np.ascontiguousarray(V)
     Vd = torch.from_numpy(V).to(dev)
     outs = {op: torch.empty_like(Vd) for op in wl.ops}
     if cross:
         outs = {"K": torch.empty((wl.n - n_src, wl.r), dtype=torch.float64, device=dev)}
     stream = torch.cuda.current_stream(dev)
 
-    plan = akm.Plan(local)
-    plan.set_points(Xd, wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
     t0 = time.perf_counter()
-    plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    if sharded:
+        sp = D.ShardedPlan(Xd, wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B, device=dev)
+        sp.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+        plan = sp.backend
+    else:
+        plan = akm.Plan(local)
+        plan.set_points(Xd, wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+        plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
     set_theta_ms = (time.perf_counter() - t0) * 1e3
     info = plan.info()
 
-    objective = "cg_iters" in wl.extra          # c5: one Z~ evaluation per step (S8)
     if objective:
         cg, lz = wl.extra["cg_iters"], wl.extra["lanczos_steps"]
         yd, Zd = Vd[:, 0].contiguous(), Vd[:, 1:].contiguous()
@@ -293,7 +320,7 @@ def main():
 
         def step():
             last["out"] = plan.objective_diag(yd, Zd, cg, lz)
-    elif "grad_cg_iters" in wl.extra:        # g5: one gradient of Z~ per step (f1)
+    elif gradient:
         gcg = wl.extra["grad_cg_iters"]
         yd, Zd = Vd[:, 0].contiguous(), Vd[:, 1:].contiguous()
         products_per_step = gcg + 1
@@ -306,6 +333,11 @@ def main():
 
         def step():
             plan.cross_mvm(n_src, Vd, outs["K"])
+    elif sharded:
+        products_per_step = 1
+
+        def step():
+            sp.mvm_multi(Vd, Y=outs.get("K"), dY_ell=outs.get("dell"), dY_sf=outs.get("dsf"))
     else:
         products_per_step = 1
 
@@ -340,7 +372,10 @@ def main():
     launches_timed = plan.stage_times(reset=True)["kernel_launches"]
     total_ms = D.max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(starts, ends)), dev)
     ms_per_step = total_ms / K
-    value = D.weak_throughput(wl.units * products_per_step, world, ms_per_step)
+    if sharded:
+        value = D.strong_throughput(wl.units * products_per_step, ms_per_step)
+    else:
+        value = D.weak_throughput(wl.units * products_per_step, world, ms_per_step)
 
     # ---------------- per-stage device times: a separate pass of the same steps with the library's
     # stage events on the launching stream (direct launches; the timed region above replays the
@@ -357,7 +392,6 @@ def main():
     Vh = torch.from_numpy(V).pin_memory()
     Oh = {op: torch.empty(tuple(outs[op].shape) if cross else V.shape, dtype=torch.float64).pin_memory()
           for op in wl.ops}
-    gradient = "grad_cg_iters" in wl.extra
     if objective or gradient:
         yh, Zh = Vh[:, 0].contiguous().pin_memory(), Vh[:, 1:].contiguous().pin_memory()
 
@@ -368,6 +402,11 @@ def main():
             plan.gradient_diag(yh, Zh, gcg, stream=stream.cuda_stream)
         elif cross:
             plan.cross_mvm(n_src, Vh, Oh["K"], stream=stream.cuda_stream)
+        elif sharded:   # the caller's copies around the sharded product (its entry points take device memory)
+            Vd.copy_(Vh, non_blocking=True)
+            sp.mvm_multi(Vd, Y=outs.get("K"), dY_ell=outs.get("dell"), dY_sf=outs.get("dsf"))
+            for op in wl.ops:
+                Oh[op].copy_(outs[op], non_blocking=True)
         else:
             plan.mvm_multi(Vh, Y=Oh.get("K"), dY_ell=Oh.get("dell"), dY_sf=Oh.get("dsf"), stream=stream.cuda_stream)
 
@@ -385,10 +424,13 @@ def main():
         e_e[i].record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = D.max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(e_s, e_e)), dev)
-    e2e_value = D.weak_throughput(wl.units * products_per_step, world, e2e_ms / K)
+    if sharded:
+        e2e_value = D.strong_throughput(wl.units * products_per_step, e2e_ms / K)
+    else:
+        e2e_value = D.weak_throughput(wl.units * products_per_step, world, e2e_ms / K)
 
     # ---------------- roofline of the dominant kernel
-    spread_fl, interp_fl, alg_bytes = algorithmic_counts(wl, info, wl.r, wl.ops)
+    spread_fl, interp_fl, alg_bytes = algorithmic_counts(wl, info, wl.r, wl.ops, n_local=row1 - row0)
     alg_bytes *= products_per_step
     cand = []
     if stages["spread_launches"]:
@@ -407,7 +449,7 @@ def main():
     stage_total = stages["spread_ms"] + stages["fft_ms"] + stages["interp_ms"] + stages["epilogue_ms"]
     # per-stage HBM rate (algorithmic bytes / stage time) and, where the round's ncu capture has
     # this workload, the measured DRAM bytes of the stage's dominant kernel per launch
-    sb = stage_bytes(wl, info, wl.r, wl.ops)
+    sb = stage_bytes(wl, info, wl.r, wl.ops, n_local=row1 - row0)
     try:
         measured = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bytes_per_launch"].get(wl.name, {})
     except Exception:
@@ -428,8 +470,11 @@ def main():
     line = {
         "metric": _metric(wl),
         "value": value, "unit": "pts/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": config_dict(wl),
+        "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": config_dict(wl, f"point-sharded rows x{world} (one grid all-reduce per product)" if sharded else
+                              f"independent replicas x{world}" if world > 1 else "1 GPU"),
         "e2e": {"value": e2e_value, "unit": "pts/s", "h2d_bytes_per_step": int(V.nbytes),
                 "d2h_bytes_per_step": int(8 * (10 + 2 * wl.r) if objective else 8 * (3 + gcg) if gradient else
                                           sum(o.numel() * 8 for o in Oh.values()))},
@@ -439,7 +484,7 @@ def main():
                      "peak_note": "FP64 FMA: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz; measured DFMA 34.1 / DMMA 37.1 "
                                   "TFLOP/s (profiles/r01_fp64_peaks.txt)",
                      "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": per_launch_ms},
-        "stages_ms_per_step": {k: stages[k + "_ms"] / K for k in ("spread", "fft", "interp", "epilogue")},
+        "stages_ms_per_step": {k: stages[k + "_ms"] / K for k in ("spread", "fft", "interp", "epilogue", "exchange")},
         "stage_share": {k: stages[k + "_ms"] / stage_total for k in ("spread", "fft", "interp", "epilogue")},
         "hbm": {"algorithmic_bytes_per_step": alg_bytes, "achieved_gbs": alg_bytes / (ms_per_step * 1e-3) / 1e9,
                 "peak_gbs": peaks.get("hbm_gbs"), "frac": alg_bytes / (ms_per_step * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)},

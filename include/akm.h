@@ -151,6 +151,7 @@ void akm_destroy(akm_plan* plan);
  * launches issued by MVM calls (always counted).  reset != 0 clears the accumulators. */
 typedef struct {
   double spread_ms, fft_ms, interp_ms, epilogue_ms;
+  double exchange_ms; /* point-sharded products: akm_spread_grid end -> akm_mvm_from_grid start (the caller's grid all-reduce) */
   int64_t calls;
   int64_t kernel_launches;
   int64_t spread_launches, interp_launches;
@@ -189,6 +190,52 @@ typedef struct {
 akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
                               int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,
                               void* stream);
+
+/* ------------------------------------------------------------------ point sharding
+ * The product is a sum over points (eq. 3.3: a_k = sum_j v_j e^{-2 pi i k.x_j}), so G
+ * processes that each hold a disjoint row block of X and V can each spread their own points onto
+ * the SAME oversampled grids, sum the grids (one all-reduce, done by the caller, e.g. NCCL), and
+ * each run the DFT / multiply / inverse DFT on the summed grids and interpolate at their own points.
+ * For the grids to coincide every shard must use the union's window frame:
+ *   1. akm_set_points(local rows);  akm_get_bounds -> all-reduce MIN(lo), MAX(hi) over the shards;
+ *   2. akm_set_bounds(global lo, hi) -> this shard's radius about the union's centers;
+ *      all-reduce MAX(radius);  akm_set_radius(global radius);
+ *   3. akm_set_theta on every shard; every shard must end with the same bin edges (akm_get_info .bin):
+ *      otherwise pin them with akm_set_bin_override and call akm_set_theta again;
+ *   4. per product: akm_spread_grid(local V, grid) -> all-reduce SUM(grid) -> akm_mvm_from_grid.
+ * Each shard needs n >= 1.  These calls take DEVICE pointers only. */
+
+/* Bounding box of this plan's points per window and padded axis: lo, hi host arrays of 3P doubles
+ * ([w*3 + a]; the leading 3 - d_w axes are singletons and read 0).  n == 0 gives +inf / -inf.
+ * Errors: INVALID_ARG, STATE (before set_points). */
+akm_status akm_get_bounds(const akm_plan* plan, double* lo, double* hi);
+
+/* Replace the bounding box by the union's (lo, hi as in akm_get_bounds; must contain this plan's
+ * points), move the window centers to its midpoints (reading R2) and return in radius_local (host,
+ * P doubles) the max distance of this plan's points from them.  Invalidates theta.  Synchronises. */
+akm_status akm_set_bounds(akm_plan* plan, const double* lo, const double* hi, double* radius_local, void* stream);
+
+/* Set the radius R_w used by the scale rule (reading R2) to the union's (host, P doubles, each >= this
+ * plan's own radius, else INVALID_ARG).  Invalidates theta. */
+akm_status akm_set_radius(akm_plan* plan, const double* radius);
+
+/* Force the bin edge B of every window (host, P entries in {1,2,3,4,6,8}) instead of the cost model's
+ * choice, or restore the choice (bins == NULL).  A forced B that does not fit the grid box makes the
+ * next akm_set_theta fail with UNSUPPORTED.  Invalidates theta. */
+akm_status akm_set_bin_override(akm_plan* plan, const int32_t* bins);
+
+/* Number of doubles of the grids of one product with r right-hand sides (after set_theta). */
+akm_status akm_grid_size(const akm_plan* plan, int32_t r, int64_t* count);
+
+/* S2 only: zero `grid` (device, akm_grid_size doubles, caller-owned) and spread this plan's points
+ * with weights V (device, n x r, ld ldv >= r) onto it (adjoint NFFT, App. A). */
+akm_status akm_spread_grid(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* grid, void* stream);
+
+/* S3-S7 from a complete (summed) grid: DFT, multiply by the multipliers, inverse DFT, interpolation at
+ * this plan's points and the epilogue of akm_kernel_mvm_multi (V, the same local block, gives the
+ * noise term).  Outputs as in akm_kernel_mvm_multi, device memory. */
+akm_status akm_mvm_from_grid(akm_plan* plan, const double* grid, const double* V, int64_t ldv, int32_t r, double* Y,
+                             double* dY_ell, double* dY_sf, int64_t ldy, void* stream);
 
 /* Test hook: the window polynomials the kernels evaluate.  For tap o in [0, 2m) of a
  * point with fractional grid position t = u - floor(u), the Kaiser-Bessel weight (App. A,

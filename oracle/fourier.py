@@ -90,11 +90,25 @@ def ndft_adjoint(xs, V, N):
     d = xs.shape[1]
     V = np.asarray(V, dtype=np.float64).reshape(xs.shape[0], -1)
     E = _exp_table(xs, N, -1.0)
-    if d == 2:  # the same sum as one matrix product per column: a[c] = (E_0 diag(V[:, c]))^T E_1
-        return np.stack([(E[0] * V[:, c:c + 1]).T @ E[1] for c in range(V.shape[1])])
-    sub = "abc"[:d]
-    expr = "jr," + ",".join("j" + s for s in sub) + "->r" + sub
-    return np.einsum(expr, V, *E, optimize=True)
+    if d == 1:
+        return (E[0].T @ V.astype(np.complex128)).T
+    # the same sums as matrix products: with R[j, (b, c)] = prod_{t >= 1} E_t[j, k_t] (the row-wise outer
+    # product of the other axes), a[col][a, (b, c)] = sum_j E_0[j, a] V[j, col] R[j, (b, c)]
+    out = np.zeros((V.shape[1], N ** d), dtype=np.complex128)
+    for j0 in range(0, xs.shape[0], 8192):
+        j1 = min(xs.shape[0], j0 + 8192)
+        R = _rowwise_outer([Et[j0:j1] for Et in E[1:]])
+        for c in range(V.shape[1]):
+            out[c] += ((E[0][j0:j1] * V[j0:j1, c:c + 1]).T @ R).ravel()
+    return out.reshape((V.shape[1],) + (N,) * d)
+
+
+def _rowwise_outer(mats):
+    """R[j, (k_1, ..., k_q)] = prod_t mats[t][j, k_t] (row-major flattening)."""
+    R = mats[0]
+    for M in mats[1:]:
+        R = (R[:, :, None] * M[:, None, :]).reshape(R.shape[0], -1)
+    return R
 
 
 def ndft_forward(xs, fhat):
@@ -103,9 +117,18 @@ def ndft_forward(xs, fhat):
     d = xs.shape[1]
     N = fhat.shape[1]
     E = _exp_table(xs, N, +1.0)
-    sub = "abc"[:d]
-    expr = "r" + sub + "," + ",".join("i" + s for s in sub) + "->ir"
-    return np.einsum(expr, fhat, *E, optimize=True)
+    if d == 1:
+        return E[0] @ fhat.T
+    # f[i, col] = sum_a E_0[i, a] sum_{(b, c)} fhat[col, a, (b, c)] R[i, (b, c)] (R as in ndft_adjoint)
+    r = fhat.shape[0]
+    F2 = fhat.reshape(r, N, -1)
+    out = np.zeros((xs.shape[0], r), dtype=np.complex128)
+    for i0 in range(0, xs.shape[0], 8192):
+        i1 = min(xs.shape[0], i0 + 8192)
+        R = _rowwise_outer([Et[i0:i1] for Et in E[1:]])
+        for c in range(r):
+            out[i0:i1, c] = np.sum((E[0][i0:i1] @ F2[c]) * R, axis=1)
+    return out
 
 
 def trunc_fastsum(xs, V, b, rows=None):

@@ -32,7 +32,9 @@ AKM_MAX_WINDOWS = 32
 ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm", "akm_kernel_deriv_mvm",
                "akm_kernel_mvm_multi", "akm_get_info", "akm_set_scale_override", "akm_last_error", "akm_destroy",
                "akm_version", "akm_set_profiling", "akm_get_stage_times", "akm_objective_diag",
-               "akm_kernel_cross_mvm", "akm_gradient_diag", "akm_get_window_poly")
+               "akm_kernel_cross_mvm", "akm_gradient_diag", "akm_get_window_poly",
+               "akm_get_bounds", "akm_set_bounds", "akm_set_radius", "akm_set_bin_override", "akm_grid_size",
+               "akm_spread_grid", "akm_mvm_from_grid")
 AKM_MAX_PROBES = 31
 
 
@@ -59,7 +61,7 @@ class akm_info(ctypes.Structure):
 
 class akm_stage_times(ctypes.Structure):
     _fields_ = [("spread_ms", ctypes.c_double), ("fft_ms", ctypes.c_double), ("interp_ms", ctypes.c_double),
-                ("epilogue_ms", ctypes.c_double), ("calls", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("epilogue_ms", ctypes.c_double), ("exchange_ms", ctypes.c_double), ("calls", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("spread_launches", ctypes.c_int64), ("interp_launches", ctypes.c_int64)]
 
 
@@ -110,6 +112,20 @@ def _load():
     lib.akm_objective_diag.restype = st
     lib.akm_get_window_poly.argtypes = [P, P, P, P]
     lib.akm_get_window_poly.restype = st
+    lib.akm_get_bounds.argtypes = [P, P, P]
+    lib.akm_get_bounds.restype = st
+    lib.akm_set_bounds.argtypes = [P, P, P, P, P]
+    lib.akm_set_bounds.restype = st
+    lib.akm_set_radius.argtypes = [P, P]
+    lib.akm_set_radius.restype = st
+    lib.akm_set_bin_override.argtypes = [P, P]
+    lib.akm_set_bin_override.restype = st
+    lib.akm_grid_size.argtypes = [P, i32, ctypes.POINTER(i64)]
+    lib.akm_grid_size.restype = st
+    lib.akm_spread_grid.argtypes = [P, P, i64, i32, P, P]
+    lib.akm_spread_grid.restype = st
+    lib.akm_mvm_from_grid.argtypes = [P, P, P, i64, i32, P, P, P, i64, P]
+    lib.akm_mvm_from_grid.restype = st
     lib.akm_version.argtypes = []
     lib.akm_version.restype = ctypes.c_char_p
     return lib
@@ -321,6 +337,63 @@ def akm_get_window_poly(plan):
     return coef[:taps.value * (deg.value + 1)].reshape(taps.value, deg.value + 1), taps.value, deg.value
 
 
+def akm_get_bounds(plan):
+    """(lo, hi) of this plan's points per window and padded axis, arrays of shape (P, 3)."""
+    P = akm_get_info(plan)["P"]
+    lo, hi = np.zeros(3 * P), np.zeros(3 * P)
+    _check(plan, _lib.akm_get_bounds(plan, lo.ctypes.data_as(ctypes.c_void_p), hi.ctypes.data_as(ctypes.c_void_p)))
+    return lo.reshape(P, 3), hi.reshape(P, 3)
+
+
+def akm_set_bounds(plan, lo, hi, stream=None):
+    """Adopt the union's bounding box; returns this plan's radius per window about the new centers."""
+    lo = np.ascontiguousarray(lo, dtype=np.float64).reshape(-1)
+    hi = np.ascontiguousarray(hi, dtype=np.float64).reshape(-1)
+    rad = np.zeros(lo.size // 3)
+    _check(plan, _lib.akm_set_bounds(plan, lo.ctypes.data_as(ctypes.c_void_p), hi.ctypes.data_as(ctypes.c_void_p),
+                                     rad.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
+    return rad
+
+
+def akm_set_radius(plan, radius):
+    rad = np.ascontiguousarray(radius, dtype=np.float64)
+    _check(plan, _lib.akm_set_radius(plan, rad.ctypes.data_as(ctypes.c_void_p)))
+
+
+def akm_set_bin_override(plan, bins=None):
+    if bins is None:
+        _check(plan, _lib.akm_set_bin_override(plan, None))
+    else:
+        b = np.ascontiguousarray(bins, dtype=np.int32)
+        _check(plan, _lib.akm_set_bin_override(plan, b.ctypes.data_as(ctypes.c_void_p)))
+
+
+def akm_grid_size(plan, r) -> int:
+    c = ctypes.c_int64()
+    _check(plan, _lib.akm_grid_size(plan, int(r), ctypes.byref(c)))
+    return c.value
+
+
+def akm_spread_grid(plan, V, grid, stream=None):
+    pv, ldv, n, r, _, kv = _ptr_ld(V, "V")
+    _expect_rows(plan, "V", n)
+    if grid.numel() < akm_grid_size(plan, r):
+        raise ValueError("grid is smaller than akm_grid_size(r)")
+    _check(plan, _lib.akm_spread_grid(plan, pv, ldv, r, ctypes.c_void_p(grid.data_ptr()), _stream(stream, kv, grid)))
+
+
+def akm_mvm_from_grid(plan, grid, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
+    (pv, ldv, n, r, kv), outs = _same_block(plan, V, [("Y", Y), ("dY_ell", dY_ell), ("dY_sf", dY_sf)])
+    lds = {o[1] for o in outs if o[0] is not None}
+    if len(lds) > 1:
+        raise ValueError("all outputs must share one leading dimension")
+    ldy = lds.pop() if lds else r
+    if grid.numel() < akm_grid_size(plan, r):
+        raise ValueError("grid is smaller than akm_grid_size(r)")
+    _check(plan, _lib.akm_mvm_from_grid(plan, ctypes.c_void_p(grid.data_ptr()), pv, ldv, r, outs[0][0], outs[1][0],
+                                        outs[2][0], ldy, _stream(stream, kv, grid)))
+
+
 def akm_set_profiling(plan, enable: bool):
     _check(plan, _lib.akm_set_profiling(plan, 1 if enable else 0))
 
@@ -419,6 +492,32 @@ class Plan:
 
     def window_poly(self):
         return akm_get_window_poly(self.handle)
+
+    # point sharding (include/akm.h; paper_2504_00480_b200.dist.ShardedPlan drives these)
+    def bounds(self):
+        return akm_get_bounds(self.handle)
+
+    def set_bounds(self, lo, hi, stream=None):
+        return akm_set_bounds(self.handle, lo, hi, stream)
+
+    def set_radius(self, radius):
+        akm_set_radius(self.handle, radius)
+        return self
+
+    def set_bin_override(self, bins=None):
+        akm_set_bin_override(self.handle, bins)
+        return self
+
+    def grid_size(self, r):
+        return akm_grid_size(self.handle, r)
+
+    def spread_grid(self, V, grid, stream=None):
+        akm_spread_grid(self.handle, V, grid, stream)
+        return grid
+
+    def mvm_from_grid(self, grid, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
+        akm_mvm_from_grid(self.handle, grid, V, Y, dY_ell, dY_sf, stream)
+        return Y, dY_ell, dY_sf
 
     def set_profiling(self, enable=True):
         akm_set_profiling(self.handle, enable)

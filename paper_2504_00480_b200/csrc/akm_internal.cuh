@@ -96,8 +96,9 @@ __device__ __forceinline__ double kb_window(double delta, double m, double beta)
 // position t = u - floor(u), the weight phi(t + m - 1 - o) is an entire function of t on [0, 1]
 // (sinh(beta q)/q is analytic in q^2 = m^2 - delta^2).  It is replaced by its degree-kPolyDeg
 // Chebyshev interpolant on [0, 1], stored as monomial coefficients in x = 2t - 1 (Horner).
-// Measured max error <= 1e-14 * phi(0) for m in {4,6,8}, sigma in [1.25, 2] (tests/ and
-// tools/ check it against the exact window).
+// Max error <= 2e-14 * phi(0) for m in {4,6,8}, sigma in {1.25, 2} (measured 1.2e-14 at m = 8,
+// sigma = 2: rounding of the monomial form), checked against the exact sinh form by
+// tests/test_gpu_parity.py::test_window_polynomials_vs_exact_kaiser_bessel via akm_get_window_poly.
 
 // Evaluate the 2m tap weights of one axis at x = 2 frac(u) - 1 from coefficients c[o*kPolyLen + k].
 template <int TAPS>

@@ -81,7 +81,9 @@ struct akm_plan {
 
   // per-window host data
   std::vector<double> lo, hi;               // [w*3 + a] bounding box (padded axes)
-  std::vector<double> radius;               // R_w
+  std::vector<double> radius;               // R_w (global after akm_set_radius)
+  std::vector<double> radius_local;         // R_w of this plan's own points about the current centers
+  std::vector<int> bin_override;            // empty = cost-model choice of B per window (rebuild_bins)
   std::vector<double> c_w, c_w_binned;      // current scale, scale the bins were built for
   WinTable tab{};                           // host copy
   PolyParam poly_param{};                   // window polynomials, passed to kernels by value
@@ -122,20 +124,24 @@ struct akm_plan {
   bool use_graphs = true;
 
   // profiling (akm_set_profiling / akm_get_stage_times): a ring of event sets, drained lazily
+  // e[0] spread start, e[1] spread end, e[5] finish start (== e[1] unless the grids were exchanged
+  // between akm_spread_grid and akm_mvm_from_grid), e[2] DFT end, e[3] interpolation end, e[4] end
   static constexpr int kRing = 512;
-  struct EvSet { cudaEvent_t e[5]; bool pending = false; };
+  struct EvSet { cudaEvent_t e[6]; bool pending = false; };
   bool profiling = false;
   std::vector<EvSet> ring;
   int ring_pos = 0;
-  double stage_ms[4] = {0, 0, 0, 0};
+  EvSet* split_ev = nullptr;  // set by akm_spread_grid, consumed by akm_mvm_from_grid
+  double stage_ms[5] = {0, 0, 0, 0, 0};  // spread, fft, interp, epilogue, exchange
   long long prof_calls = 0, launches = 0, spread_launches = 0, interp_launches = 0;
 
   void drain(EvSet& es) {
     if (!es.pending) return;
     cudaEventSynchronize(es.e[4]);
-    for (int k = 0; k < 4; ++k) {
+    const int from[5] = {0, 5, 2, 3, 1}, to[5] = {1, 2, 3, 4, 5};
+    for (int k = 0; k < 5; ++k) {
       float ms = 0.f;
-      if (cudaEventElapsedTime(&ms, es.e[k], es.e[k + 1]) == cudaSuccess) stage_ms[k] += ms;
+      if (cudaEventElapsedTime(&ms, es.e[from[k]], es.e[to[k]]) == cudaSuccess) stage_ms[k] += ms;
       else cudaGetLastError();
     }
     es.pending = false;
@@ -305,7 +311,9 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     const int d = g.d;
     int bestB = 1;
     double bestCost = 1e300;
+    const bool forced = !plan->bin_override.empty();
     for (int B : {1, 2, 3, 4, 6, 8}) {
+      if (forced && B != plan->bin_override[w]) continue;
       const int F = B + 2 * m - 1;
       double Fd = 1;
       for (int t = 0; t < d; ++t) Fd *= F;
@@ -344,6 +352,9 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
         bestB = B;
       }
     }
+    if (forced && bestCost >= 1e300)
+      return plan->fail(AKM_ERR_UNSUPPORTED, "window %d: forced bin edge %d does not fit the grid box", w,
+                        plan->bin_override[w]);
     // finalize geometry for bestB
     const int B = bestB;
     g.B = B;
@@ -585,23 +596,16 @@ static bool choose_spread_tile(int M, int Nn, int& MT, int& NT, int& threads) {
 // ================================================================== the MVM
 // set 0: the square products over all n points (Y: n x r).  set 1: the cross product (Y: the
 // (n - n_split) x r target rows; V holds the n_split source rows; only Y = K_{*X} V).
-static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, int r, double* Y, double* dYl,
-                              double* dYsf, long long ldy, cudaStream_t s, int set = 0) {
-  const bool needK = (Y != nullptr) || (dYsf != nullptr);
-  const bool needL = dYl != nullptr;
-  const int ops = (needK ? 1 : 0) + (needL ? 1 : 0);
-  const int slotK = needK ? 0 : -1;
-  const int slotL = needL ? (needK ? 1 : 0) : -1;
-  const int dslot0 = needK ? 0 : 1;
+// The product is split at the grids: enqueue_spread (S2: zero + adjoint NFFT of the plan's points
+// into `grid`, total_taps x r doubles) and enqueue_finish (S3-S7 from a complete grid).  The
+// single-GPU product runs both on the plan's own grid; the point-sharded product (akm_spread_grid /
+// akm_mvm_from_grid) sums the ranks' grids in between.
+static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv, int r, double* grid, cudaStream_t s,
+                                 int set) {
   const long long n = plan->n;
-  if (n == 0) return AKM_OK;
-  akm_status st = ensure_rhs_workspace(plan, r);
-  if (st != AKM_OK) return st;
   const WinTable* dtab = plan->dtab.as<WinTable>();
-  akm_plan::EvSet* ev = plan->profiling ? plan->next_set() : nullptr;
-  if (ev) AKM_CK(cudaEventRecord(ev->e[0], s));
-  // S2: spread
-  AKM_CK(launch_zero(plan->grid.as<double>(), plan->total_taps * r, s));
+  AKM_CK(launch_zero(grid, plan->total_taps * r, s));
+  if (n == 0) return AKM_OK;
   for (const Group& grp : plan->groups) {
     const int F = grp.F, d = grp.d;
     int M = 1;
@@ -619,7 +623,7 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
         return plan->fail(AKM_ERR_UNSUPPORTED, "no spread tile for footprint %d x %d", M, F * rc);
       AKM_CK(launch_spread_v5(dtab, plan->poly_param, plan->items_s[set].as<WorkItem>() + grp.sl[set].spread_begin,
                               grp.sl[set].spread_count, plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc,
-                              r, plan->grid.as<double>(), MB, NB, WN, spread_v5_smem(F, rc, MB, NB, WN), s));
+                              r, grid, MB, NB, WN, spread_v5_smem(F, rc, MB, NB, WN), s));
       if (grp.sl[set].spread_count > 0) {
         ++plan->launches;
         ++plan->spread_launches;
@@ -638,7 +642,7 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
       const size_t smem = spread_mma_smem(PB, M, F * rc, F, rc);
       AKM_CK(launch_spread_mma(dtab, plan->poly_param, plan->items_s[set].as<WorkItem>() + grp.sl[set].spread_begin, grp.sl[set].spread_count,
                                plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc, r,
-                               plan->grid.as<double>(), MB, NB, WM, WN, PB, smem, s));
+                               grid, MB, NB, WM, WN, PB, smem, s));
       if (grp.sl[set].spread_count > 0) {
         ++plan->launches;
         ++plan->spread_launches;
@@ -646,15 +650,34 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
       r0 += rc;
     }
   }
-  if (ev) AKM_CK(cudaEventRecord(ev->e[1], s));
+  return AKM_OK;
+}
+
+static akm_status enqueue_finish(akm_plan* plan, const double* grid, const double* V, long long ldv, int r, double* Y,
+                                 double* dYl, double* dYsf, long long ldy, cudaStream_t s, int set,
+                                 akm_plan::EvSet* ev) {
+  const bool needK = (Y != nullptr) || (dYsf != nullptr);
+  const bool needL = dYl != nullptr;
+  const int ops = (needK ? 1 : 0) + (needL ? 1 : 0);
+  const int slotK = needK ? 0 : -1;
+  const int slotL = needL ? (needK ? 1 : 0) : -1;
+  const int dslot0 = needK ? 0 : 1;
+  const long long n = plan->n;
+  const WinTable* dtab = plan->dtab.as<WinTable>();
+  if (ev) AKM_CK(cudaEventRecord(ev->e[5], s));
   // S3-S5: DFT, multiply, inverse DFT
-  AKM_CK(launch_fft_forward(plan->tab, dtab, plan->grid.as<double>(), plan->A1.as<double2>(), plan->A2.as<double2>(),
+  AKM_CK(launch_fft_forward(plan->tab, dtab, grid, plan->A1.as<double2>(), plan->A2.as<double2>(),
                             plan->tw.as<double2>(), r, s));
   AKM_CK(launch_fft_multiply_inverse(plan->tab, dtab, plan->A2.as<double2>(), plan->A3.as<double2>(),
                                      plan->C.as<double2>(), plan->C2.as<double2>(), plan->tw.as<double2>(),
                                      plan->D.as<double>(), ops, dslot0, r, plan->H.as<double>(), s));
   plan->launches += fft_launch_count(plan->tab, r);
   if (ev) AKM_CK(cudaEventRecord(ev->e[2], s));
+  if (n == 0) {
+    if (ev) AKM_CK(cudaEventRecord(ev->e[3], s));
+    if (ev) AKM_CK(cudaEventRecord(ev->e[4], s));
+    return AKM_OK;
+  }
   // S6: interpolation
   int r0 = 0;
   while (r0 < r) {
@@ -698,6 +721,19 @@ static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, in
   ++plan->launches;
   if (ev) AKM_CK(cudaEventRecord(ev->e[4], s));
   return AKM_OK;
+}
+
+static akm_status enqueue_mvm(akm_plan* plan, const double* V, long long ldv, int r, double* Y, double* dYl,
+                              double* dYsf, long long ldy, cudaStream_t s, int set = 0) {
+  if (plan->n == 0) return AKM_OK;
+  akm_status st = ensure_rhs_workspace(plan, r);
+  if (st != AKM_OK) return st;
+  akm_plan::EvSet* ev = plan->profiling ? plan->next_set() : nullptr;
+  if (ev) AKM_CK(cudaEventRecord(ev->e[0], s));
+  st = enqueue_spread(plan, V, ldv, r, plan->grid.as<double>(), s, set);
+  if (st != AKM_OK) return st;
+  if (ev) AKM_CK(cudaEventRecord(ev->e[1], s));
+  return enqueue_finish(plan, plan->grid.as<double>(), V, ldv, r, Y, dYl, dYsf, ldy, s, set, ev);
 }
 
 // The MVM launch sequence (a memset and ~9 kernels) is captured once into a CUDA graph and
@@ -984,6 +1020,8 @@ akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p,
     AKM_CK(cudaStreamSynchronize(s));
     for (int w = 0; w < P; ++w) plan->radius[w] = std::sqrt(r2[w]);
   }
+  plan->radius_local = plan->radius;
+  plan->bin_override.clear();
   plan->c_w.assign(P, 0.0);
   plan->c_w_binned.assign(P, -1.0);
   plan->r_cap = 0;
@@ -1378,6 +1416,141 @@ akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, i
   return AKM_OK;
 }
 
+// ---------------------------------------------------------------- point sharding
+akm_status akm_get_bounds(const akm_plan* plan, double* lo, double* hi) {
+  if (!plan || !lo || !hi) return AKM_ERR_INVALID_ARG;
+  if (!plan->have_points) return AKM_ERR_STATE;
+  for (int w = 0; w < plan->P; ++w)
+    for (int a = 0; a < 3; ++a) {
+      const bool real = a >= 3 - plan->tab.w[w].d;
+      lo[w * 3 + a] = !real ? 0.0 : plan->n > 0 ? plan->lo[w * 3 + a] : HUGE_VAL;
+      hi[w * 3 + a] = !real ? 0.0 : plan->n > 0 ? plan->hi[w * 3 + a] : -HUGE_VAL;
+    }
+  return AKM_OK;
+}
+
+akm_status akm_set_bounds(akm_plan* plan, const double* lo, const double* hi, double* radius_local, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points) return plan->fail(AKM_ERR_STATE, "set_bounds before set_points");
+  if (!lo || !hi || !radius_local) return plan->fail(AKM_ERR_INVALID_ARG, "null bounds / radius array");
+  cudaStream_t s = S(stream);
+  AKM_CK(cudaSetDevice(plan->device));
+  WinTable& tab = plan->tab;
+  for (int w = 0; w < plan->P; ++w)
+    for (int a = 3 - tab.w[w].d; a < 3; ++a) {
+      const int k = w * 3 + a;
+      if (!std::isfinite(lo[k]) || !std::isfinite(hi[k]) || lo[k] > hi[k])
+        return plan->fail(AKM_ERR_INVALID_ARG, "window %d axis %d: bounds [%g, %g] are not a finite interval", w, a,
+                          lo[k], hi[k]);
+      if (plan->n > 0 && (lo[k] > plan->lo[k] || hi[k] < plan->hi[k]))
+        return plan->fail(AKM_ERR_INVALID_ARG, "window %d axis %d: bounds [%g, %g] do not contain this plan's points",
+                          w, a, lo[k], hi[k]);
+    }
+  for (int w = 0; w < plan->P; ++w)
+    for (int a = 3 - tab.w[w].d; a < 3; ++a) {
+      const int k = w * 3 + a;
+      plan->lo[k] = lo[k];
+      plan->hi[k] = hi[k];
+      tab.w[w].center[a] = 0.5 * (lo[k] + hi[k]);  // bounding-box midpoint of the union (reading R2)
+    }
+  std::vector<double> r2(plan->P, 0.0);
+  if (plan->n > 0) {
+    AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
+    AKM_CK(launch_window_radius(plan->Xc.as<double>(), plan->n, (long long)plan->feat_used.size(), tab,
+                                plan->dtab.as<WinTable>(), plan->r2.as<double>(), s));
+    AKM_CK(cudaMemcpyAsync(r2.data(), plan->r2.p, sizeof(double) * plan->P, cudaMemcpyDeviceToHost, s));
+    AKM_CK(cudaStreamSynchronize(s));
+  }
+  for (int w = 0; w < plan->P; ++w) radius_local[w] = plan->radius[w] = plan->radius_local[w] = std::sqrt(r2[w]);
+  plan->c_w_binned.assign(plan->P, -1.0);
+  plan->have_theta = false;
+  return AKM_OK;
+}
+
+akm_status akm_set_radius(akm_plan* plan, const double* radius) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points) return plan->fail(AKM_ERR_STATE, "set_radius before set_points");
+  if (!radius) return plan->fail(AKM_ERR_INVALID_ARG, "radius is NULL");
+  for (int w = 0; w < plan->P; ++w)
+    if (!std::isfinite(radius[w]) || radius[w] < plan->radius_local[w])
+      return plan->fail(AKM_ERR_INVALID_ARG, "radius[%d] = %g is below this plan's own radius %g", w, radius[w],
+                        plan->radius_local[w]);
+  plan->radius.assign(radius, radius + plan->P);
+  plan->c_w_binned.assign(plan->P, -1.0);
+  plan->have_theta = false;
+  return AKM_OK;
+}
+
+akm_status akm_set_bin_override(akm_plan* plan, const int32_t* bins) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points) return plan->fail(AKM_ERR_STATE, "set_bin_override before set_points");
+  if (!bins) {
+    plan->bin_override.clear();
+  } else {
+    for (int w = 0; w < plan->P; ++w)
+      if (bins[w] != 1 && bins[w] != 2 && bins[w] != 3 && bins[w] != 4 && bins[w] != 6 && bins[w] != 8)
+        return plan->fail(AKM_ERR_INVALID_ARG, "bin edge %d of window %d not in {1,2,3,4,6,8}", bins[w], w);
+    plan->bin_override.assign(bins, bins + plan->P);
+  }
+  plan->c_w_binned.assign(plan->P, -1.0);
+  plan->have_theta = false;
+  return AKM_OK;
+}
+
+akm_status akm_grid_size(const akm_plan* plan, int32_t r, int64_t* count) {
+  if (!plan || !count || r < 1) return AKM_ERR_INVALID_ARG;
+  if (!plan->have_points || !plan->have_theta) return AKM_ERR_STATE;
+  *count = (int64_t)plan->total_taps * r;
+  return AKM_OK;
+}
+
+akm_status akm_spread_grid(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* grid, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points || !plan->have_theta) return plan->fail(AKM_ERR_STATE, "spread_grid before set_points / set_theta");
+  if (r < 1 || ldv < r) return plan->fail(AKM_ERR_INVALID_ARG, "bad r/ldv (r=%d ldv=%lld)", r, (long long)ldv);
+  if (plan->n == 0) return plan->fail(AKM_ERR_INVALID_ARG, "spread_grid needs n >= 1 on this plan");
+  if (!is_device_ptr(V) || !is_device_ptr(grid)) return plan->fail(AKM_ERR_INVALID_ARG, "V and grid must be device memory");
+  if (plan->n_split != plan->n) return plan->fail(AKM_ERR_STATE, "spread_grid on a plan sorted for a cross product");
+  cudaStream_t s = S(stream);
+  AKM_CK(cudaSetDevice(plan->device));
+  akm_status st = ensure_rhs_workspace(plan, r);
+  if (st != AKM_OK) return st;
+  akm_plan::EvSet* ev = plan->profiling ? plan->next_set() : nullptr;
+  if (ev) AKM_CK(cudaEventRecord(ev->e[0], s));
+  st = enqueue_spread(plan, V, ldv, r, grid, s, 0);
+  if (st != AKM_OK) return st;
+  if (ev) AKM_CK(cudaEventRecord(ev->e[1], s));
+  plan->split_ev = ev;
+  return AKM_OK;
+}
+
+akm_status akm_mvm_from_grid(akm_plan* plan, const double* grid, const double* V, int64_t ldv, int32_t r, double* Y,
+                             double* dY_ell, double* dY_sf, int64_t ldy, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points || !plan->have_theta) return plan->fail(AKM_ERR_STATE, "mvm_from_grid before set_points / set_theta");
+  if (r < 1 || ldv < r || ldy < r) return plan->fail(AKM_ERR_INVALID_ARG, "bad r/ldv/ldy (r=%d ldv=%lld ldy=%lld)", r,
+                                                   (long long)ldv, (long long)ldy);
+  if (!Y && !dY_ell && !dY_sf) return plan->fail(AKM_ERR_INVALID_ARG, "no output requested");
+  if (plan->n == 0) return plan->fail(AKM_ERR_INVALID_ARG, "mvm_from_grid needs n >= 1 on this plan");
+  const double* outs[3] = {Y, dY_ell, dY_sf};
+  for (const double* o : outs)
+    if (o && !is_device_ptr(o)) return plan->fail(AKM_ERR_INVALID_ARG, "outputs must be device memory");
+  if (!is_device_ptr(V) || !is_device_ptr(grid)) return plan->fail(AKM_ERR_INVALID_ARG, "V and grid must be device memory");
+  if (plan->n_split != plan->n) return plan->fail(AKM_ERR_STATE, "mvm_from_grid on a plan sorted for a cross product");
+  cudaStream_t s = S(stream);
+  AKM_CK(cudaSetDevice(plan->device));
+  akm_status st = ensure_rhs_workspace(plan, r);
+  if (st != AKM_OK) return st;
+  akm_plan::EvSet* ev = plan->profiling ? plan->split_ev : nullptr;
+  plan->split_ev = nullptr;
+  return enqueue_finish(plan, grid, V, ldv, r, Y, dY_ell, dY_sf, ldy, s, 0, ev);
+}
+
 akm_status akm_get_window_poly(const akm_plan* plan, double* coef, int32_t* taps, int32_t* degree) {
   if (!plan || !coef || !taps || !degree) return AKM_ERR_INVALID_ARG;
   if (!plan->have_points) return AKM_ERR_STATE;
@@ -1401,6 +1574,7 @@ akm_status akm_get_stage_times(akm_plan* plan, akm_stage_times* out, int32_t res
   out->fft_ms = plan->stage_ms[1];
   out->interp_ms = plan->stage_ms[2];
   out->epilogue_ms = plan->stage_ms[3];
+  out->exchange_ms = plan->stage_ms[4];
   out->calls = plan->prof_calls;
   out->kernel_launches = plan->launches;
   out->spread_launches = plan->spread_launches;

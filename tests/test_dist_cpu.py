@@ -74,3 +74,165 @@ def test_partition_and_seed_properties():
     assert D.max_over_ranks(3.5) == 3.5            # no process group: identity
     with pytest.raises(ValueError):
         D.column_partition(4, 2, 2)
+
+
+# ---------------------------------------------------------------- point-sharded product (§8(e) item 1)
+class OracleShardBackend:
+    """Test stand-in for the library behind ShardedPlan, built from the oracle's primitives: the
+    'grid' of a shard is its inner sums a_k of eq. (3.3) per window (exact NDFT, real/imag pairs), so
+    the sum over shards is the union's a_k exactly and the driver's frame agreement and all-reduce
+    composition can be checked on CPU against the single-process oracle."""
+
+    def __init__(self):
+        from oracle import fourier as F
+        self.F = F
+
+    def set_points(self, X, windows, family, N, sigma_over, m, eps_B):
+        self.X, self.windows, self.family, self.N, self.eps_B = np.asarray(X), windows, family, N, eps_B
+        self.P = len(windows)
+        self.lo = np.zeros((self.P, 3))
+        self.hi = np.zeros((self.P, 3))
+        for w, win in enumerate(windows):
+            d = len(win)
+            self.lo[w, 3 - d:] = self.X[:, list(win)].min(axis=0)
+            self.hi[w, 3 - d:] = self.X[:, list(win)].max(axis=0)
+
+    def bounds(self):
+        return self.lo.copy(), self.hi.copy()
+
+    def set_bounds(self, lo, hi):
+        self.lo, self.hi = np.asarray(lo).reshape(self.P, 3), np.asarray(hi).reshape(self.P, 3)
+        self.center = [0.5 * (self.lo[w, 3 - len(win):] + self.hi[w, 3 - len(win):]) for w, win in enumerate(self.windows)]
+        self.R = np.array([np.sqrt(((self.X[:, list(win)] - self.center[w]) ** 2).sum(1)).max()
+                           for w, win in enumerate(self.windows)])
+        return self.R.copy()
+
+    def set_radius(self, R):
+        self.R = np.asarray(R, dtype=np.float64)
+
+    def set_theta(self, sf, ell, se):
+        F = self.F
+        self.theta = (sf, ell, se)
+        rho = 0.25 - self.eps_B / 2.0
+        self.c, self.b = [], []
+        for w, win in enumerate(self.windows):
+            c = self.R[w] / rho if self.R[w] > 0 else 1.0
+            if self.family == F.GAUSSIAN:
+                c = max(c, ell * np.sqrt(2.0 * np.pi * self.N))
+            self.c.append(c)
+            d = len(win)
+            self.b.append([F.fourier_coefficients(F.kernel_samples(self.family, ell / c, self.N, d, der))
+                           for der in (False, True)])
+
+    def info(self):
+        return {"bin": [1] * self.P}
+
+    def set_bin_override(self, bins):
+        pass
+
+    def _xs(self, w):
+        return (self.X[:, list(self.windows[w])] - self.center[w]) / self.c[w]
+
+    def grid_size(self, r):
+        return sum(2 * self.N ** len(win) * r for win in self.windows)
+
+    def spread_grid(self, V, grid):
+        parts = []
+        for w in range(self.P):
+            a = self.F.ndft_adjoint(self._xs(w), V.numpy(), self.N)
+            parts += [a.real.ravel(), a.imag.ravel()]
+        grid.copy_(torch.from_numpy(np.concatenate(parts)))
+
+    def mvm_from_grid(self, grid, V, Y, dY_ell, dY_sf):
+        g = grid.numpy()
+        Vn = V.numpy()
+        r = Vn.shape[1]
+        S, SD = np.zeros_like(Vn), np.zeros_like(Vn)
+        off = 0
+        for w, win in enumerate(self.windows):
+            shape = (r,) + (self.N,) * len(win)
+            size = int(np.prod(shape))
+            a = g[off:off + size].reshape(shape) + 1j * g[off + size:off + 2 * size].reshape(shape)
+            off += 2 * size
+            xs = self._xs(w)
+            S += np.real(self.F.ndft_forward(xs, self.b[w][0][None] * a))
+            SD += np.real(self.F.ndft_forward(xs, self.b[w][1][None] * a)) / self.c[w]
+        sf, ell, se = self.theta
+        if Y is not None:
+            Y.copy_(torch.from_numpy(sf * sf * S + se * se * Vn))
+        if dY_ell is not None:
+            dY_ell.copy_(torch.from_numpy(sf * sf * SD))
+        if dY_sf is not None:
+            dY_sf.copy_(torch.from_numpy(2.0 * sf * S))
+
+
+def _shard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = {}
+        for name, n, r in (("c2", 900, 2), ("c3", 700, 3)):
+            wl = workloads.CONFIGS[name]
+            X = workloads.make_X(wl, n=n)
+            V = workloads.make_V(wl, n=n, r=r)
+            a, b = D.row_partition(n, world, rank)
+            sp = D.ShardedPlan(X[a:b], wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B,
+                               backend=OracleShardBackend())
+            sp.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+            Vl = torch.from_numpy(np.ascontiguousarray(V[a:b]))
+            Y, dY = torch.empty_like(Vl), torch.empty_like(Vl)
+            sp.mvm_multi(Vl, Y=Y, dY_ell=dY)
+            out[name] = (a, b, Y.numpy(), dY.numpy())
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_point_sharded_product():
+    """world_size 2: each rank holds half the rows; the frame agreement (bounds MIN/MAX, radius MAX),
+    one grid all-reduce and the per-rank finish reproduce the single-process truncated-Fourier product
+    (eq. 3.3 on the union, scaling reading R2) to rounding, and the dense float64 oracle to the method
+    tolerance."""
+    from oracle import dense_apply
+    from oracle import fourier as F
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(k, world, port, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for name, n, r in (("c2", 900, 2), ("c3", 700, 3)):
+        wl = workloads.CONFIGS[name]
+        X = workloads.make_X(wl, n=n)
+        V = workloads.make_V(wl, n=n, r=r)
+        Y = np.zeros((n, r))
+        dY = np.zeros((n, r))
+        for k in range(world):
+            a, b, y, dy = res[k][name]
+            assert (a, b) == D.row_partition(n, world, k)
+            Y[a:b], dY[a:b] = y, dy
+        th = (wl.sigma_f, wl.ell, wl.sigma_eps)
+        nd = F.additive_fastsum(X, wl.windows, wl.family, th, V, wl.N, wl.eps_B, ops=("K", "dell"))
+        assert np.linalg.norm(Y - nd["K"]) <= 1e-12 * np.linalg.norm(nd["K"])
+        assert np.linalg.norm(dY - nd["dell"]) <= 1e-12 * np.linalg.norm(nd["dell"])
+        de = dense_apply(X, wl.windows, wl.family, th, V, ops=("K",))
+        tol = 1e-6 if wl.family == 0 else 1e-3
+        assert np.linalg.norm(Y - de["K"]) <= tol * np.linalg.norm(de["K"])
+
+
+def test_row_partition():
+    for n in (2, 7, 1000):
+        for world in (1, 2, 8):
+            if n < world:
+                with pytest.raises(ValueError):
+                    D.row_partition(n, world, 0)
+                continue
+            parts = [D.row_partition(n, world, k) for k in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n and all(b > a for a, b in parts)
+    assert D.strong_throughput(1e6, 2.0) == pytest.approx(5e8)

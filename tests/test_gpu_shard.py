@@ -1,0 +1,188 @@
+"""GPU parity of the point-sharded product through the C ABI.
+
+The split entry points (akm_get_bounds / akm_set_bounds / akm_set_radius, akm_spread_grid,
+akm_mvm_from_grid) let G shards of the rows each spread onto the same grids; summing the grids and
+finishing on every shard must reproduce the single-plan product.  Two checks:
+  * one process, two plans on cuda:0, grids summed by a device add (the library calls alone);
+  * the ShardedPlan driver at world_size 2 over gloo, both ranks on cuda:0 (host-mediated all-reduce,
+    no rank's kernels wait on another's: the NCCL/NVLink path differs only in the transport).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import workloads
+from oracle import dense_apply
+from oracle import fourier as F
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def akm():
+    import __graft_entry__
+    __graft_entry__.build_library()
+    import paper_2504_00480_b200 as mod
+    return mod
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def _single(akm, X, wl, V, ops):
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+    plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    Vd = torch.from_numpy(V).to(dev)
+    outs = {op: torch.empty_like(Vd) for op in ops}
+    plan.mvm_multi(Vd, Y=outs.get("K"), dY_ell=outs.get("dell"), dY_sf=outs.get("dsf"))
+    torch.cuda.synchronize()
+    info = plan.info()
+    plan.close()
+    return {k: v.cpu().numpy() for k, v in outs.items()}, info
+
+
+@pytest.mark.parametrize("name,n,r,shards", [("c2", 6000, 2, 2), ("c4", 20000, 11, 3), ("c3", 8000, 3, 2),
+                                              ("c1", 2000, 1, 4)])
+def test_two_plans_sum_grids(akm, name, n, r, shards):
+    wl = workloads.CONFIGS[name]
+    X = workloads.make_X(wl, n=n)
+    V = workloads.make_V(wl, n=n, r=r)
+    ops = ("K", "dell", "dsf")
+    dev = torch.device("cuda:0")
+    plans, parts = [], []
+    for k in range(shards):
+        a = k * n // shards
+        b = (k + 1) * n // shards
+        p = akm.Plan(0)
+        p.set_points(torch.from_numpy(np.ascontiguousarray(X[a:b])).to(dev), wl.windows, wl.family, wl.N,
+                     wl.sigma_over, wl.m, wl.eps_B)
+        plans.append(p)
+        parts.append((a, b))
+    bounds = [p.bounds() for p in plans]
+    lo = np.min([b[0] for b in bounds], axis=0)
+    hi = np.max([b[1] for b in bounds], axis=0)
+    rad = np.max([p.set_bounds(lo, hi) for p in plans], axis=0)
+    for p in plans:
+        p.set_radius(rad)
+        p.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    bins = [p.info()["bin"] for p in plans]
+    if any(b != bins[0] for b in bins):
+        for p in plans:
+            p.set_bin_override(bins[0])
+            p.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    size = plans[0].grid_size(r)
+    assert all(p.grid_size(r) == size for p in plans)
+    total = torch.zeros(size, dtype=torch.float64, device=dev)
+    Vs = [torch.from_numpy(np.ascontiguousarray(V[a:b])).to(dev) for a, b in parts]
+    for p, Vl in zip(plans, Vs):
+        g = torch.empty(size, dtype=torch.float64, device=dev)
+        p.spread_grid(Vl, g)
+        total += g
+    got = {op: np.zeros((n, r)) for op in ops}
+    for p, Vl, (a, b) in zip(plans, Vs, parts):
+        o = {op: torch.empty_like(Vl) for op in ops}
+        p.mvm_from_grid(total, Vl, Y=o["K"], dY_ell=o["dell"], dY_sf=o["dsf"])
+        torch.cuda.synchronize()
+        for op in ops:
+            got[op][a:b] = o[op].cpu().numpy()
+    single, info = _single(akm, X, wl, V, ops)
+    for p in plans:
+        assert p.info()["c_w"] == pytest.approx(info["c_w"], rel=1e-15)
+        p.close()
+    for op in ops:
+        assert rel(got[op], single[op]) <= 1e-12, (op, rel(got[op], single[op]))
+    nd = F.additive_fastsum(X, wl.windows, wl.family, (wl.sigma_f, wl.ell, wl.sigma_eps), V, wl.N, wl.eps_B,
+                            ops=ops, m=wl.m)
+    tol = 1e-9 if wl.m == 6 else 1e-11
+    for op in ops:
+        assert rel(got[op], nd[op]) <= tol, (op, rel(got[op], nd[op]))
+
+
+def test_shard_calls_validate(akm):
+    wl = workloads.CONFIGS["c2"]
+    X = workloads.make_X(wl, n=500)
+    p = akm.Plan(0)
+    p.set_points(X, wl.windows, wl.family)
+    lo, hi = p.bounds()
+    with pytest.raises(akm.AkmError):            # bounds must contain the plan's points
+        p.set_bounds(lo + 0.01, hi)
+    rad = p.set_bounds(lo - 0.1, hi + 0.1)
+    with pytest.raises(akm.AkmError):            # radius below the plan's own
+        p.set_radius(rad * 0.5)
+    with pytest.raises(akm.AkmError):            # grid calls need theta
+        p.grid_size(1)
+    p.set_radius(rad * 1.5)
+    p.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    assert p.info()["radius"] == pytest.approx(list(rad * 1.5))
+    with pytest.raises(akm.AkmError):
+        p.set_bin_override([5, 1, 1])
+    p.set_bin_override([2, 2, 2])
+    p.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    assert p.info()["bin"] == [2, 2, 2]
+    p.close()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2504_00480_b200 import dist as D
+        wl = workloads.CONFIGS["c2"]
+        n, r = 5000, 2
+        X = workloads.make_X(wl, n=n)
+        V = workloads.make_V(wl, n=n, r=r)
+        a, b = D.row_partition(n, world, rank)
+        dev = torch.device("cuda:0")
+        sp = D.ShardedPlan(torch.from_numpy(np.ascontiguousarray(X[a:b])).to(dev), wl.windows, wl.family, wl.N,
+                           wl.sigma_over, wl.m, wl.eps_B, device=dev, comm_device=torch.device("cpu"))
+        sp.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+        Vl = torch.from_numpy(np.ascontiguousarray(V[a:b])).to(dev)
+        Y, dY = torch.empty_like(Vl), torch.empty_like(Vl)
+        sp.mvm_multi(Vl, Y=Y, dY_ell=dY)
+        torch.cuda.synchronize()
+        q.put((rank, a, b, Y.cpu().numpy(), dY.cpu().numpy()))
+        sp.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_plan_gloo_world2(akm):
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(k, world, port, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    wl = workloads.CONFIGS["c2"]
+    n, r = 5000, 2
+    X = workloads.make_X(wl, n=n)
+    V = workloads.make_V(wl, n=n, r=r)
+    Y, dY = np.zeros((n, r)), np.zeros((n, r))
+    for _, a, b, y, dy in res:
+        Y[a:b], dY[a:b] = y, dy
+    single, _ = _single(akm, X, wl, V, ("K", "dell"))
+    assert rel(Y, single["K"]) <= 1e-12 and rel(dY, single["dell"]) <= 1e-12
+    de = dense_apply(X, wl.windows, wl.family, (wl.sigma_f, wl.ell, wl.sigma_eps), V, ops=("K", "dell"))
+    assert rel(Y, de["K"]) <= 1e-6 and rel(dY, de["dell"]) <= 1e-6
