@@ -237,6 +237,21 @@ akm_status akm_spread_grid(akm_plan* plan, const double* V, int64_t ldv, int32_t
 akm_status akm_mvm_from_grid(akm_plan* plan, const double* grid, const double* V, int64_t ldv, int32_t r, double* Y,
                              double* dY_ell, double* dY_sf, int64_t ldy, void* stream);
 
+/* Boundary-regularised kernel kappa_R (eq. 3.1 "a smooth or at least continuous
+ * periodic function kappa_R"; "It is possible to smoothen the inner or outer boundaries",
+ * P:155).  With p > 0 the b_k of eq. (3.2) are taken from the samples of
+ *   kappa_R(r) = T_I(r) (r <= eps_I) | kappa(r) | T_B(r) (1/2 - eps_B < r <= 1/2) | kappa(1/2) (r > 1/2),
+ * r = ||x~|| in every window's scaled coordinates, T_I / T_B the two-point Taylor interpolants of
+ * degree 2p - 1 (kappa's derivatives 0..p-1 at +-eps_I; at 1/2 - eps_B and a flat kappa(1/2) at 1/2;
+ * eps_B is set_points'), and the products add the near-field correction
+ * sum_{||x~_i - x~_j|| < eps_I} (kappa - T_I)(||x~_i - x~_j||) v_j (and the same for kappa^der), so
+ * they still approximate the plain kernel sums -- with the Matern cusp removed from the truncated
+ * Fourier series.  p = 0 (default after set_points) is the paper's implementation (no smoothing).
+ * eps_I in [0, 1/4), 0 <= p <= 8; eps_I = 0 keeps only the outer part.  Invalidates theta.  The
+ * near-field correction is built for the square products (akm_kernel_mvm*, the Krylov drivers);
+ * akm_kernel_cross_mvm and akm_mvm_from_grid return UNSUPPORTED while eps_I > 0. */
+akm_status akm_set_regularization(akm_plan* plan, double eps_I, int32_t p);
+
 /* Test hook: the window polynomials the kernels evaluate.  For tap o in [0, 2m) of a
  * point with fractional grid position t = u - floor(u), the Kaiser-Bessel weight (App. A,
  * P:1240-1247) phi((t + m - 1 - o) / n_g) is replaced by sum_k coef[o*(degree+1) + k] x^k with

@@ -34,7 +34,7 @@ ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm"
                "akm_version", "akm_set_profiling", "akm_get_stage_times", "akm_objective_diag",
                "akm_kernel_cross_mvm", "akm_gradient_diag", "akm_get_window_poly",
                "akm_get_bounds", "akm_set_bounds", "akm_set_radius", "akm_set_bin_override", "akm_grid_size",
-               "akm_spread_grid", "akm_mvm_from_grid")
+               "akm_spread_grid", "akm_mvm_from_grid", "akm_set_regularization")
 AKM_MAX_PROBES = 31
 
 
@@ -126,6 +126,8 @@ def _load():
     lib.akm_spread_grid.restype = st
     lib.akm_mvm_from_grid.argtypes = [P, P, P, i64, i32, P, P, P, i64, P]
     lib.akm_mvm_from_grid.restype = st
+    lib.akm_set_regularization.argtypes = [P, d, i32]
+    lib.akm_set_regularization.restype = st
     lib.akm_version.argtypes = []
     lib.akm_version.restype = ctypes.c_char_p
     return lib
@@ -394,6 +396,11 @@ def akm_mvm_from_grid(plan, grid, V, Y=None, dY_ell=None, dY_sf=None, stream=Non
                                         outs[2][0], ldy, _stream(stream, kv, grid)))
 
 
+def akm_set_regularization(plan, eps_I=0.0, p=0):
+    """kappa_R with inner (eps_I, near-field corrected) and outer (eps_B) smoothing of order p (include/akm.h)."""
+    _check(plan, _lib.akm_set_regularization(plan, float(eps_I), int(p)))
+
+
 def akm_set_profiling(plan, enable: bool):
     _check(plan, _lib.akm_set_profiling(plan, 1 if enable else 0))
 
@@ -459,6 +466,10 @@ class Plan:
 
     def set_theta(self, sigma_f, ell, sigma_eps, stream=None):
         akm_set_theta(self.handle, sigma_f, ell, sigma_eps, stream)
+        return self
+
+    def set_regularization(self, eps_I=0.0, p=0):
+        akm_set_regularization(self.handle, eps_I, p)
         return self
 
     def set_scale_override(self, c_w=None):

@@ -28,6 +28,8 @@ constexpr double kPi = 3.14159265358979323846;
 constexpr int kKrMaxR = 32;               // Krylov driver: 1 CG column + <= 31 probes
 constexpr int kKrMaxSteps = 64;           // Lanczos steps
 constexpr int kKrMaxIters = 1024;         // CG iterations
+constexpr int kRegMaxP = 8;               // regularisation order p (regularize.cu)
+constexpr int kRegStride = 3 * kRegMaxP;  // per (window, operator): T_I (p) then T_B (2p) coefficients
 
 // Per-window geometry passed (by value, inside WinTable) to kernels.
 struct WinGeom {
@@ -52,6 +54,7 @@ struct WinGeom {
   long long c2_off;     // [op][L0][L1][K2]
   long long tw_off[3];  // offsets of twiddle tables (complex) for each padded axis: [K][L]
   long long d_off;      // offset of this window's multiplier tables [op][K0][K1][K2] (real)
+  int bt_off;           // offset of this window's bin-start table (nbin0*nbin1*nbin2 + 1 entries)
 };
 
 // Window polynomial coefficients passed BY VALUE as a __grid_constant__ kernel parameter: with
@@ -218,6 +221,16 @@ cudaError_t launch_multiplier(const WinTable& tab, const WinTable* dtab, int win
                               int ops_mask, double inv_c, double sigma_over, double* D, cudaStream_t s);
 cudaError_t launch_twiddles(const WinTable& tab, const WinTable* dtab, double2* tw, cudaStream_t s);
 cudaError_t launch_window_poly(int m, double beta, double* coef, cudaStream_t s);
+
+// regularize.cu
+cudaError_t launch_reg_coef(int family, double ell_eff, double eps_I, double eps_B, int p, double* coef, cudaStream_t s);
+cudaError_t launch_kernel_samples_reg(int family, int d, int N, double ell_eff, int deriv, double eps_I, double eps_B,
+                                      int p, const double* coef, double* out, cudaStream_t s);
+cudaError_t launch_near_field(const WinTable* dtab, const WorkItem* items, int n_items, const int* bin_start,
+                              const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
+                              int r, int ops, int slotK, int slotL, int family, double ell, double eps_I, int p,
+                              const double* coef, double* part, cudaStream_t s);
+int near_field_launches(int r);
 
 // spread_mma.cu
 bool spread_mma_choose(int M, int Nn, int Fmax, int rc, int& MB, int& NB, int& WM, int& WN);

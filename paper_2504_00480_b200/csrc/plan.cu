@@ -84,6 +84,9 @@ struct akm_plan {
   std::vector<double> radius;               // R_w (global after akm_set_radius)
   std::vector<double> radius_local;         // R_w of this plan's own points about the current centers
   std::vector<int> bin_override;            // empty = cost-model choice of B per window (rebuild_bins)
+  int reg_p = 0;                            // kappa_R regularisation (akm_set_regularization; 0 = off)
+  double reg_eps_I = 0.0;
+  bool near_field() const { return reg_p > 0 && reg_eps_I > 0.0; }
   std::vector<double> c_w, c_w_binned;      // current scale, scale the bins were built for
   WinTable tab{};                           // host copy
   PolyParam poly_param{};                   // window polynomials, passed to kernels by value
@@ -97,6 +100,7 @@ struct akm_plan {
   DevBuf items_s[2], items_i[2], items_ib[2];  // [item set]
   long long n_split = 0;  // rows >= n_split are class 1 (cross-product targets); n = no targets
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
+  DevBuf reg_coef, bin_start;  // regularisation polynomials [w][op][kRegStride]; per-window bin start tables
   DevBuf stageV, stageY, stageL, stageS;
   DevBuf crossV, crossY;  // akm_kernel_cross_mvm: zero-padded V and the union's product
   DevBuf gX, gP, gB2, gD1, gD2, gState;  // akm_gradient_diag: block PCG and derivative products
@@ -305,6 +309,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   std::vector<std::vector<WorkItem>> its_i[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
   std::vector<std::vector<WorkItem>> its_ib[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
   const int ch_ib = 128;  // per-bin interpolation items: up to 128 points of one bin
+  std::vector<int> bstart;  // per window: sorted start of every bin (bin-major order), then n
   for (int w = 0; w < P; ++w) {
     WinGeom& g = tab.w[w];
     const int* hc = hist.data() + hoff[w];
@@ -375,10 +380,12 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     // class-1 points cell by cell) and work items
     long long pos = 0;
     const int Bd0 = (3 - d > 0) ? 1 : B, Bd1 = (3 - d > 1) ? 1 : B, Bd2 = B;
+    g.bt_off = (int)bstart.size();
     for (int b0 = 0; b0 < g.nbin[0]; ++b0)
       for (int b1 = 0; b1 < g.nbin[1]; ++b1)
         for (int b2 = 0; b2 < g.nbin[2]; ++b2) {
           const long long start = pos;
+          bstart.push_back((int)pos);
           long long cls_start[2] = {pos, pos};
           for (int cls = 0; cls < 2; ++cls) {
             cls_start[cls] = pos;
@@ -413,6 +420,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
         }
     if (pos != n) return plan->fail(AKM_ERR_CUDA, "internal error: histogram of window %d holds %lld of %lld points",
                                     w, pos, n);
+    bstart.push_back((int)n);
   }
   // groups of windows with equal (d, F); work items concatenated group by group,
   // larger chunks first inside a group (better tail behaviour)
@@ -507,6 +515,8 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
                                cudaMemcpyHostToDevice, s));
     }
   }
+  AKM_CK(plan->bin_start.ensure(sizeof(int) * bstart.size()));
+  AKM_CK(cudaMemcpyAsync(plan->bin_start.p, bstart.data(), sizeof(int) * bstart.size(), cudaMemcpyHostToDevice, s));
   // twiddles
   AKM_CK(plan->tw.ensure(sizeof(double2) * std::max<long long>(twc, 1)));
   AKM_CK(launch_twiddles(tab, plan->dtab.as<WinTable>(), plan->tw.as<double2>(), s));
@@ -529,14 +539,24 @@ static akm_status rebuild_tables(akm_plan* plan, cudaStream_t s) {
   AKM_CK(plan->bs1.ensure(sizeof(double) * maxNd));
   AKM_CK(plan->bs2.ensure(sizeof(double) * maxNd));
   AKM_CK(plan->bs3.ensure(sizeof(double) * maxNd));
+  if (plan->reg_p > 0) {
+    AKM_CK(plan->reg_coef.ensure(sizeof(double) * plan->P * 2 * kRegStride));
+    AKM_CK(cudaMemsetAsync(plan->reg_coef.p, 0, sizeof(double) * plan->P * 2 * kRegStride, s));
+  }
   for (int w = 0; w < plan->P; ++w) {
     const int d = plan->tab.w[w].d;
     const double ell_eff = plan->ell / plan->c_w[w];
     double* bufs[2] = {plan->bs2.as<double>(), plan->bs3.as<double>()};
+    double* coef = plan->reg_p > 0 ? plan->reg_coef.as<double>() + (long long)w * 2 * kRegStride : nullptr;
+    if (coef) AKM_CK(launch_reg_coef(plan->family, ell_eff, plan->reg_eps_I, plan->eps_B, plan->reg_p, coef, s));
     for (int deriv = 0; deriv < 2; ++deriv) {
       double* a = plan->bs0.as<double>();
       double* b = plan->bs1.as<double>();
-      AKM_CK(launch_kernel_samples(plan->family, d, N, ell_eff, deriv, a, s));
+      if (coef)
+        AKM_CK(launch_kernel_samples_reg(plan->family, d, N, ell_eff, deriv, plan->reg_eps_I, plan->eps_B, plan->reg_p,
+                                         coef, a, s));
+      else
+        AKM_CK(launch_kernel_samples(plan->family, d, N, ell_eff, deriv, a, s));
       for (int t = 0; t < d; ++t) {
         double* out = (t == d - 1) ? bufs[deriv] : b;
         AKM_CK(launch_cos_dft_axis(d, N, t, a, out, s));
@@ -708,6 +728,15 @@ static akm_status enqueue_finish(akm_plan* plan, const double* grid, const doubl
       }
     }
     r0 += rc;
+  }
+  if (plan->near_field()) {  // kappa_R's inner part: add sum_j (kappa - T_I)(r_ij) v_j (regularize.cu)
+    if (set != 0) return plan->fail(AKM_ERR_UNSUPPORTED, "the near-field correction is built for the square products only");
+    const int nitems = (int)plan->items_interp_bin[0].size();
+    AKM_CK(launch_near_field(dtab, plan->items_ib[0].as<WorkItem>(), nitems, plan->bin_start.as<int>(),
+                             plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r, ops, slotK, slotL,
+                             plan->family, plan->ell, plan->reg_eps_I, plan->reg_p, plan->reg_coef.as<double>(),
+                             plan->part.as<double>(), s));
+    if (nitems > 0) plan->launches += near_field_launches(r);
   }
   if (ev) AKM_CK(cudaEventRecord(ev->e[3], s));
   // S7: epilogue
@@ -1022,6 +1051,8 @@ akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p,
   }
   plan->radius_local = plan->radius;
   plan->bin_override.clear();
+  plan->reg_p = 0;
+  plan->reg_eps_I = 0.0;
   plan->c_w.assign(P, 0.0);
   plan->c_w_binned.assign(P, -1.0);
   plan->r_cap = 0;
@@ -1129,6 +1160,8 @@ akm_status akm_kernel_cross_mvm(akm_plan* plan, int64_t n_src, const double* V, 
     return plan->fail(AKM_ERR_STATE, "kernel_cross_mvm called before set_points and set_theta");
   const long long n = plan->n;
   if (n_src < 0 || n_src > n) return plan->fail(AKM_ERR_INVALID_ARG, "n_src = %lld outside [0, n = %lld]", (long long)n_src, n);
+  if (plan->near_field())
+    return plan->fail(AKM_ERR_UNSUPPORTED, "cross product with the inner regularisation (near-field) is not built");
   if (r < 1 || ldv < r || ldy < r) return plan->fail(AKM_ERR_INVALID_ARG, "bad r/ldv/ldy (r=%d ldv=%lld ldy=%lld)", r, (long long)ldv, (long long)ldy);
   const long long n_t = n - n_src;
   if (n_t == 0) return AKM_OK;
@@ -1542,6 +1575,8 @@ akm_status akm_mvm_from_grid(akm_plan* plan, const double* grid, const double* V
     if (o && !is_device_ptr(o)) return plan->fail(AKM_ERR_INVALID_ARG, "outputs must be device memory");
   if (!is_device_ptr(V) || !is_device_ptr(grid)) return plan->fail(AKM_ERR_INVALID_ARG, "V and grid must be device memory");
   if (plan->n_split != plan->n) return plan->fail(AKM_ERR_STATE, "mvm_from_grid on a plan sorted for a cross product");
+  if (plan->near_field())
+    return plan->fail(AKM_ERR_UNSUPPORTED, "point sharding with the inner regularisation (near-field) is not built");
   cudaStream_t s = S(stream);
   AKM_CK(cudaSetDevice(plan->device));
   akm_status st = ensure_rhs_workspace(plan, r);
@@ -1549,6 +1584,20 @@ akm_status akm_mvm_from_grid(akm_plan* plan, const double* grid, const double* V
   akm_plan::EvSet* ev = plan->profiling ? plan->split_ev : nullptr;
   plan->split_ev = nullptr;
   return enqueue_finish(plan, grid, V, ldv, r, Y, dY_ell, dY_sf, ldy, s, 0, ev);
+}
+
+akm_status akm_set_regularization(akm_plan* plan, double eps_I, int32_t p) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points) return plan->fail(AKM_ERR_STATE, "set_regularization before set_points");
+  if (p < 0 || p > kRegMaxP) return plan->fail(AKM_ERR_INVALID_ARG, "p must be in [0, %d]", kRegMaxP);
+  if (!(eps_I >= 0.0 && eps_I < 0.25)) return plan->fail(AKM_ERR_INVALID_ARG, "eps_I must be in [0, 1/4)");
+  if (p > 0 && eps_I > 0.0 && eps_I >= 0.5 - plan->eps_B)
+    return plan->fail(AKM_ERR_INVALID_ARG, "eps_I must stay below 1/2 - eps_B");
+  plan->reg_p = p;
+  plan->reg_eps_I = p > 0 ? eps_I : 0.0;
+  plan->have_theta = false;
+  return AKM_OK;
 }
 
 akm_status akm_get_window_poly(const akm_plan* plan, double* coef, int32_t* taps, int32_t* degree) {

@@ -1,0 +1,313 @@
+// regularize.cu -- boundary-regularised kernel kappa_R ("It is possible
+// to smoothen the inner or outer boundaries") and the near-field correction of the inner part.
+//
+// kappa_R(r), r = ||x~|| in a window's scaled coordinates (f4):
+//   r <= eps_I              T_I(r): the polynomial of degree 2p-1 matching kappa's derivatives of
+//                           orders 0..p-1 at r = +-eps_I (kappa extended evenly to r < 0).  It is even,
+//                           so it is found here as T_I(r) = sum_{k<p} a_k (r/eps_I)^{2k} from the p
+//                           conditions at +eps_I (the mirrored ones then hold by symmetry, and the
+//                           Hermite interpolant is unique);
+//   eps_I < r <= 1/2-eps_B  kappa(r);
+//   1/2-eps_B < r <= 1/2    T_B(r) = sum_{k<2p} c_k t^k, t = (r - (1/2 - eps_B)) / eps_B: kappa's
+//                           derivatives 0..p-1 at t = 0, the constant kappa(1/2) (derivatives 0) at t = 1;
+//   r > 1/2                 kappa(1/2).
+// The samples kappa_R(l/N) feed eq. (3.2) unchanged (setup_kernels.cu k_cos_dft_axis).  Scaled points
+// lie in the ball of radius 1/4 - eps_B/2, so T_B never replaces a kernel value the product uses;
+// T_I does for pairs closer than eps_I, and k_near_field adds sum_j (kappa - T_I)(r_ij) v_j back.
+// kappa^der (the ell-derivative kernel, eq. 2.3) is regularised the same way.
+#include <cuda_runtime.h>
+
+#include "akm_internal.cuh"
+
+namespace akm {
+
+// f^(q)(r), q < p, of f(r) = Q(r) e^{alpha r + beta r^2}: Gaussian alpha = 0, beta = -1/(2 ell^2),
+// Matern alpha = -1/ell, beta = 0; Q = 1 (kappa), r^2/ell^3 (Gaussian kappa^der), r/ell^2 (Matern
+// kappa^der).  Each derivative maps Q to Q' + (alpha + 2 beta r) Q.
+__device__ void radial_derivs(int family, int deriv, double ell, double r, int p, double* out) {
+  constexpr int L = kRegMaxP + 4;
+  double Q[L], Qn[L];
+  for (int k = 0; k < L; ++k) Q[k] = 0.0;
+  double alpha, beta;
+  if (family == 0) {
+    alpha = 0.0;
+    beta = -0.5 / (ell * ell);
+    if (deriv) Q[2] = 1.0 / (ell * ell * ell); else Q[0] = 1.0;
+  } else {
+    alpha = -1.0 / ell;
+    beta = 0.0;
+    if (deriv) Q[1] = 1.0 / (ell * ell); else Q[0] = 1.0;
+  }
+  const double e = exp(alpha * r + beta * r * r);
+  for (int q = 0; q < p; ++q) {
+    double v = 0.0;
+    for (int k = L - 1; k >= 0; --k) v = v * r + Q[k];
+    out[q] = v * e;
+    for (int k = 0; k < L; ++k) {
+      double t = (k + 1 < L ? (k + 1) * Q[k + 1] : 0.0) + alpha * Q[k];
+      if (k >= 1) t += 2.0 * beta * Q[k - 1];
+      Qn[k] = t;
+    }
+    for (int k = 0; k < L; ++k) Q[k] = Qn[k];
+  }
+}
+
+// Gaussian elimination with partial pivoting on a small dense system (n <= kRegMaxP), in place.
+__device__ void small_solve(int n, double* A /* n x n row-major */, double* b) {
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int i = c + 1; i < n; ++i)
+      if (fabs(A[i * n + c]) > fabs(A[piv * n + c])) piv = i;
+    if (piv != c) {
+      for (int k = 0; k < n; ++k) {
+        const double t = A[c * n + k];
+        A[c * n + k] = A[piv * n + k];
+        A[piv * n + k] = t;
+      }
+      const double t = b[c];
+      b[c] = b[piv];
+      b[piv] = t;
+    }
+    for (int i = c + 1; i < n; ++i) {
+      const double f = A[i * n + c] / A[c * n + c];
+      for (int k = c; k < n; ++k) A[i * n + k] -= f * A[c * n + k];
+      b[i] -= f * b[c];
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int k = i + 1; k < n; ++k) s -= A[i * n + k] * b[k];
+    b[i] = s / A[i * n + i];
+  }
+}
+
+// d^q/ds^q s^j at s = 1: j! / (j - q)! (0 if q > j)
+__device__ __forceinline__ double falling(int j, int q) {
+  if (q > j) return 0.0;
+  double v = 1.0;
+  for (int t = 0; t < q; ++t) v *= (double)(j - t);
+  return v;
+}
+
+// One thread per operator (0: kappa, 1: kappa^der) of one window.
+// out[op * kRegStride + 0 .. p-1]:          a_k of T_I (powers (r/eps_I)^{2k});
+// out[op * kRegStride + kRegMaxP .. +2p-1]: c_k of T_B (powers t^k).
+__global__ void k_reg_coef(int family, double ell, double eps_I, double eps_B, int p, double* __restrict__ out) {
+  const int op = threadIdx.x;
+  if (op >= 2 || p <= 0) return;
+  double* o = out + op * kRegStride;
+  double f[kRegMaxP];
+  double A[kRegMaxP * kRegMaxP], b[kRegMaxP];
+  if (eps_I > 0.0) {
+    // sum_k a_k d^q/ds^q s^{2k} |_{s=1} = eps_I^q f^(q)(eps_I),  q < p
+    radial_derivs(family, op, ell, eps_I, p, f);
+    double sc = 1.0;
+    for (int q = 0; q < p; ++q) {
+      for (int k = 0; k < p; ++k) A[q * p + k] = falling(2 * k, q);
+      b[q] = sc * f[q];
+      sc *= eps_I;
+    }
+    small_solve(p, A, b);
+    for (int k = 0; k < p; ++k) o[k] = b[k];
+  }
+  if (eps_B > 0.0) {
+    // t = 0: c_q = eps_B^q f^(q)(1/2 - eps_B) / q!;  t = 1: value f(1/2), derivatives 0
+    radial_derivs(family, op, ell, 0.5 - eps_B, p, f);
+    double sc = 1.0, fact = 1.0;
+    double* c = o + kRegMaxP;
+    for (int q = 0; q < p; ++q) {
+      if (q > 0) fact *= (double)q;
+      c[q] = sc * f[q] / fact;
+      sc *= eps_B;
+    }
+    double fb;
+    radial_derivs(family, op, ell, 0.5, 1, &fb);
+    for (int q = 0; q < p; ++q) {
+      double rhs = (q == 0) ? fb : 0.0;
+      for (int k = 0; k < p; ++k) rhs -= c[k] * falling(k, q);
+      for (int k = 0; k < p; ++k) A[q * p + k] = falling(p + k, q);
+      b[q] = rhs;
+    }
+    small_solve(p, A, b);
+    for (int k = 0; k < p; ++k) c[p + k] = b[k];
+  }
+}
+
+cudaError_t launch_reg_coef(int family, double ell_eff, double eps_I, double eps_B, int p, double* coef, cudaStream_t s) {
+  k_reg_coef<<<1, 32, 0, s>>>(family, ell_eff, eps_I, eps_B, p, coef);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ double kernel_plain(int family, int deriv, double ell, double r) {
+  if (family == 0) {
+    const double k = exp(-r * r / (2.0 * ell * ell));
+    return deriv ? r * r / (ell * ell * ell) * k : k;
+  }
+  const double k = exp(-r / ell);
+  return deriv ? r / (ell * ell) * k : k;
+}
+
+__device__ __forceinline__ double reg_inner(const double* __restrict__ a, int p, double s2) {
+  double v = a[p - 1];
+  for (int k = p - 2; k >= 0; --k) v = fma(v, s2, a[k]);
+  return v;
+}
+
+// kappa_R(r) at the nodes l/N of I_N^d (the samples of eq. 3.2), regularised (see the file comment)
+__global__ void k_kernel_samples_reg(int family, int d, int N, double ell, int deriv, double eps_I, double eps_B,
+                                     int p, const double* __restrict__ coef, double* __restrict__ out) {
+  long long total = 1;
+  for (int t = 0; t < d; ++t) total *= N;
+  const double* a = coef + deriv * kRegStride;
+  const double* c = a + kRegMaxP;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long rem = idx;
+    double rr = 0.0;
+    for (int t = 0; t < d; ++t) {
+      const int li = (int)(rem % N) - N / 2;
+      rem /= N;
+      const double x = (double)li / (double)N;
+      rr += x * x;
+    }
+    const double r = sqrt(rr);
+    double v;
+    if (eps_I > 0.0 && r <= eps_I) {
+      v = reg_inner(a, p, rr / (eps_I * eps_I));
+    } else if (eps_B > 0.0 && r > 0.5) {
+      double cs = 0.0;
+      for (int k = 2 * p - 1; k >= 0; --k) cs = cs + c[k];  // T_B(t = 1)
+      v = cs;
+    } else if (eps_B > 0.0 && r > 0.5 - eps_B) {
+      const double t = (r - (0.5 - eps_B)) / eps_B;
+      double cs = c[2 * p - 1];
+      for (int k = 2 * p - 2; k >= 0; --k) cs = fma(cs, t, c[k]);
+      v = cs;
+    } else {
+      v = kernel_plain(family, deriv, ell, r);
+    }
+    out[idx] = v;
+  }
+}
+
+cudaError_t launch_kernel_samples_reg(int family, int d, int N, double ell_eff, int deriv, double eps_I, double eps_B,
+                                      int p, const double* coef, double* out, cudaStream_t s) {
+  long long total = 1;
+  for (int t = 0; t < d; ++t) total *= N;
+  const int blocks = (int)((total + 255) / 256);
+  k_kernel_samples_reg<<<blocks, 256, 0, s>>>(family, d, N, ell_eff, deriv, eps_I, eps_B, p, coef, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ near-field correction
+// One CTA per interpolation item (<= 128 target points of one bin); the source points of every bin
+// within ceil(eps_I n_g / B) bins are staged through shared memory in tiles of kNfTile (scaled grid
+// coordinates and the rc RHS values of their user rows); each thread accumulates, for its target,
+// sum_{r_ij < eps_I} (kappa - T_I)(r_ij) v_j for kappa (slot K) and kappa^der / c_w (slot L) and adds it to
+// the window's partial output (written by the interpolation before, read by the epilogue after).
+constexpr int kNfThreads = 128;
+constexpr int kNfTile = 128;
+constexpr int kNfMaxRc = 12;
+
+__global__ void __launch_bounds__(kNfThreads) k_near_field(
+    const WinTable* __restrict__ tabp, const WorkItem* __restrict__ items, const int* __restrict__ bin_start,
+    const double* __restrict__ u_sorted, const int* __restrict__ perm, const double* __restrict__ V, long long ldv,
+    long long n, int r0, int rc, int r_total, int ops, int slotK, int slotL, int family, double ell, double eps_I,
+    int p, const double* __restrict__ coef, double* __restrict__ part) {
+  __shared__ double su[3][kNfTile];
+  __shared__ double sv[kNfTile * kNfMaxRc];
+  const WinTable& tab = *tabp;
+  const WorkItem it = items[blockIdx.x];
+  const WinGeom& g = tab.w[it.win];
+  const int w = it.win;
+  const double* uw = u_sorted + (long long)w * 3 * n;
+  const int* pw = perm + (long long)w * n;
+  const double inv_ng = 1.0 / (double)tab.n_g;
+  const double ell_eff = ell * g.scale * inv_ng;  // ell / c_w
+  const double inv_c = g.scale * inv_ng;
+  const double E = eps_I * (double)tab.n_g;       // eps_I in grid units
+  const double E2 = E * E;
+  const double inv_eps2 = 1.0 / (eps_I * eps_I);
+  const double* aK = coef + (long long)w * 2 * kRegStride;
+  const double* aL = aK + kRegStride;
+  const int tid = threadIdx.x;
+  const bool active = tid < it.count;
+  const int pos = it.start + (active ? tid : 0);
+  double ut[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) ut[a] = (a >= 3 - g.d) ? uw[(long long)a * n + pos] : 0.0;
+  double accK[kNfMaxRc], accL[kNfMaxRc];
+#pragma unroll
+  for (int c = 0; c < kNfMaxRc; ++c) accK[c] = accL[c] = 0.0;
+  const int K = (int)ceil(E / (double)g.B);
+  int lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = max(0, it.bin[a] - ((a >= 3 - g.d) ? K : 0));
+    hi[a] = min(g.nbin[a] - 1, it.bin[a] + ((a >= 3 - g.d) ? K : 0));
+  }
+  const int* bs = bin_start + g.bt_off;
+  for (int b0 = lo[0]; b0 <= hi[0]; ++b0)
+    for (int b1 = lo[1]; b1 <= hi[1]; ++b1)
+      for (int b2 = lo[2]; b2 <= hi[2]; ++b2) {
+        const int bi = (b0 * g.nbin[1] + b1) * g.nbin[2] + b2;
+        const int s0 = bs[bi], s1 = bs[bi + 1];
+        for (int t0 = s0; t0 < s1; t0 += kNfTile) {
+          const int cnt = min(kNfTile, s1 - t0);
+          __syncthreads();
+          for (int j = tid; j < cnt; j += kNfThreads) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) su[a][j] = (a >= 3 - g.d) ? uw[(long long)a * n + t0 + j] : 0.0;
+            const long long row = pw[t0 + j];
+            for (int c = 0; c < rc; ++c) sv[j * kNfMaxRc + c] = V[row * ldv + r0 + c];
+          }
+          __syncthreads();
+          if (!active) continue;
+          for (int j = 0; j < cnt; ++j) {
+            const double d0 = ut[0] - su[0][j], d1 = ut[1] - su[1][j], d2 = ut[2] - su[2][j];
+            const double q2 = d0 * d0 + d1 * d1 + d2 * d2;
+            if (q2 >= E2) continue;
+            const double r = sqrt(q2) * inv_ng;
+            const double s2 = r * r * inv_eps2;
+            const double wK = kernel_plain(family, 0, ell_eff, r) - reg_inner(aK, p, s2);
+            const double wL = (slotL >= 0) ? (kernel_plain(family, 1, ell_eff, r) - reg_inner(aL, p, s2)) * inv_c : 0.0;
+#pragma unroll
+            for (int c = 0; c < kNfMaxRc; ++c) {
+              if (c < rc) {
+                accK[c] = fma(wK, sv[j * kNfMaxRc + c], accK[c]);
+                accL[c] = fma(wL, sv[j * kNfMaxRc + c], accL[c]);
+              }
+            }
+          }
+        }
+      }
+  if (!active) return;
+  const long long i = pw[pos];
+  double* out = part + (((long long)w * n + i) * ops) * r_total + r0;
+#pragma unroll
+  for (int c = 0; c < kNfMaxRc; ++c) {
+    if (c < rc) {
+      if (slotK >= 0) out[(long long)slotK * r_total + c] += accK[c];
+      if (slotL >= 0) out[(long long)slotL * r_total + c] += accL[c];
+    }
+  }
+}
+
+cudaError_t launch_near_field(const WinTable* dtab, const WorkItem* items, int n_items, const int* bin_start,
+                              const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
+                              int r, int ops, int slotK, int slotL, int family, double ell, double eps_I, int p,
+                              const double* coef, double* part, cudaStream_t s) {
+  if (n_items <= 0) return cudaSuccess;
+  for (int r0 = 0; r0 < r; r0 += kNfMaxRc) {
+    const int rc = (r - r0 < kNfMaxRc) ? r - r0 : kNfMaxRc;
+    k_near_field<<<n_items, kNfThreads, 0, s>>>(dtab, items, bin_start, u_sorted, perm, V, ldv, n, r0, rc, r, ops,
+                                                slotK, slotL, family, ell, eps_I, p, coef, part);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int near_field_launches(int r) { return (r + kNfMaxRc - 1) / kNfMaxRc; }
+
+}  // namespace akm
