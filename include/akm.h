@@ -185,7 +185,11 @@ typedef struct {
   double samples[AKM_MAX_PROBES]; /* z_i^T logm(M^{-1} Khat) z_i estimates                    */
   int32_t steps[AKM_MAX_PROBES];  /* Lanczos steps used per probe (< lanczos_steps on breakdown) */
   int32_t n_z, cg_iters, lanczos_steps, products; /* products = Khat block products issued    */
-  double cg_relres;               /* final recursive relative residual                        */
+  double cg_relres;               /* final recursive relative residual (of the preconditioned
+                                     system S_op x^ = U^{-1} y under AAFN)                     */
+  double cg_relres_true;          /* ||y - Khat x|| / ||y|| of the returned CG iterate (one extra
+                                     r = 1 product)                                             */
+  int32_t landmarks;              /* AAFN landmark count k (0: diagonal preconditioner)          */
 } akm_objective_out;
 akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
                               int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,
@@ -259,6 +263,36 @@ akm_status akm_set_regularization(akm_plan* plan, double eps_I, int32_t p);
  * coef: host array of at least 16 * 15 doubles (output); *taps = 2m, *degree = 14.
  * Errors: INVALID_ARG (NULL), STATE (before akm_set_points). */
 akm_status akm_get_window_poly(const akm_plan* plan, double* coef, int32_t* taps, int32_t* degree);
+
+/* ------------------------------------------------------------------ AAFN preconditioner
+ * PAPER.md §2.3: landmarks by farthest point sampling per feature window, merged; the
+ * landmark block Cholesky-factored and the Schur complement approximated by its inverse factor
+ * (reading R15; the FSAI factor G is built with the diagonal pattern, G = diag(S_aa^{-1/2})):
+ *     M = U U^T,  U = [L11, 0; K21 L11^{-T}, G^{-1}],  log det M = 2 sum log diag L11 - 2 sum log diag G.
+ * k_per_window = 0 selects the diagonal preconditioner M = diag(Khat) (default); otherwise FPS picks
+ * min(k_per_window, n) points per window (seed: farthest from the window centroid; then the point
+ * farthest from the picks; ties to the lowest index), duplicates removed in pick order; at most 800
+ * landmarks in total (UNSUPPORTED beyond).  Landmarks depend on the points only; the factors are
+ * rebuilt lazily after every akm_set_theta. */
+akm_status akm_set_preconditioner(akm_plan* plan, int32_t k_per_window);
+
+/* out = U^{-1} T (transpose = 0) or U^{-T} T (transpose != 0) for the current theta, T and out n x r
+ * row-major device blocks (1 <= r <= 32); logdet (host, nullable) receives log det M, landmarks (host,
+ * nullable, akm_precond_landmarks entries) the landmark row indices in merge order.  M^{-1} = U^{-T} U^{-1}.
+ * Errors: STATE (no AAFN set / before set_theta), INVALID_ARG, NONFINITE (Cholesky breakdown after one
+ * jitter retry of 1e-10 trace(K11)/k), UNSUPPORTED, OOM, CUDA. */
+akm_status akm_precond_apply(akm_plan* plan, int32_t transpose, const double* T, int32_t r, double* out, double* logdet,
+                             int32_t* landmarks, void* stream);
+
+/* Number of AAFN landmarks for the current points (runs FPS if needed). */
+akm_status akm_precond_landmarks(akm_plan* plan, int32_t* count, void* stream);
+
+/* akm_objective_diag with the plan's preconditioner (akm_set_preconditioner): with AAFN, CG and
+ * Lanczos run on the split-preconditioned S_op = U^{-1} Khat U^{-T}: column 0 carries
+ * U^{-1} y (PCG on Khat x = y), columns 1.. the probes z_i (tr logm(M^{-1} Khat) = tr logm(S_op)), and
+ * log det M is AAFN's.  Same arguments and outputs as akm_objective_diag. */
+akm_status akm_objective(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z, int32_t cg_iters,
+                         int32_t lanczos_steps, akm_objective_out* out, double* cg_relres, void* stream);
 
 /* Library version string. */
 /* Gradient of the objective Z~ (eq. (div)) with M = diag(Khat) = c I,

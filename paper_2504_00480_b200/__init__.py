@@ -34,7 +34,8 @@ ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm"
                "akm_version", "akm_set_profiling", "akm_get_stage_times", "akm_objective_diag",
                "akm_kernel_cross_mvm", "akm_gradient_diag", "akm_get_window_poly",
                "akm_get_bounds", "akm_set_bounds", "akm_set_radius", "akm_set_bin_override", "akm_grid_size",
-               "akm_spread_grid", "akm_mvm_from_grid", "akm_set_regularization")
+               "akm_spread_grid", "akm_mvm_from_grid", "akm_set_regularization", "akm_set_preconditioner",
+               "akm_precond_apply", "akm_precond_landmarks", "akm_objective")
 AKM_MAX_PROBES = 31
 
 
@@ -70,7 +71,8 @@ class akm_objective_out(ctypes.Structure):
                 ("slq", ctypes.c_double), ("n_log_2pi", ctypes.c_double),
                 ("samples", ctypes.c_double * AKM_MAX_PROBES), ("steps", ctypes.c_int32 * AKM_MAX_PROBES),
                 ("n_z", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("lanczos_steps", ctypes.c_int32),
-                ("products", ctypes.c_int32), ("cg_relres", ctypes.c_double)]
+                ("products", ctypes.c_int32), ("cg_relres", ctypes.c_double), ("cg_relres_true", ctypes.c_double),
+                ("landmarks", ctypes.c_int32)]
 
 
 def _load():
@@ -128,6 +130,14 @@ def _load():
     lib.akm_mvm_from_grid.restype = st
     lib.akm_set_regularization.argtypes = [P, d, i32]
     lib.akm_set_regularization.restype = st
+    lib.akm_set_preconditioner.argtypes = [P, i32]
+    lib.akm_set_preconditioner.restype = st
+    lib.akm_precond_apply.argtypes = [P, i32, P, i32, P, P, P, P]
+    lib.akm_precond_apply.restype = st
+    lib.akm_precond_landmarks.argtypes = [P, P, P]
+    lib.akm_precond_landmarks.restype = st
+    lib.akm_objective.argtypes = [P, P, P, i64, i32, i32, i32, ctypes.POINTER(akm_objective_out), P, P]
+    lib.akm_objective.restype = st
     lib.akm_version.argtypes = []
     lib.akm_version.restype = ctypes.c_char_p
     return lib
@@ -413,6 +423,15 @@ def akm_get_stage_times(plan, reset: bool = False) -> dict:
 
 def akm_objective_diag(plan, y, Z, cg_iters=50, lanczos_steps=30, stream=None) -> dict:
     """eq. (1.4) with M = diag(Khat): CG + SLQ, every Krylov step one block product (include/akm.h)."""
+    return _objective(_lib.akm_objective_diag, plan, y, Z, cg_iters, lanczos_steps, stream)
+
+
+def akm_objective(plan, y, Z, cg_iters=50, lanczos_steps=30, stream=None) -> dict:
+    """eq. (1.4) with the plan's preconditioner (diagonal or AAFN, akm_set_preconditioner)."""
+    return _objective(_lib.akm_objective, plan, y, Z, cg_iters, lanczos_steps, stream)
+
+
+def _objective(fn, plan, y, Z, cg_iters, lanczos_steps, stream) -> dict:
     y = _vector(y, "y")
     py, _, n, _, _, ky = _ptr_ld(y, "y")
     pz, ldz, nz_rows, n_z, _, kz = _ptr_ld(Z, "Z")
@@ -420,11 +439,38 @@ def akm_objective_diag(plan, y, Z, cg_iters=50, lanczos_steps=30, stream=None) -
     _expect_rows(plan, "Z", nz_rows)
     out = akm_objective_out()
     hist = (ctypes.c_double * max(int(cg_iters), 1))()
-    _check(plan, _lib.akm_objective_diag(plan, py, pz, ldz, n_z, int(cg_iters), int(lanczos_steps), ctypes.byref(out),
-                                         hist, _stream(stream, ky, kz)))
+    _check(plan, fn(plan, py, pz, ldz, n_z, int(cg_iters), int(lanczos_steps), ctypes.byref(out), hist,
+                    _stream(stream, ky, kz)))
     return {"Z": out.Z, "quad": out.quad, "logdetM": out.logdet_M, "slq": out.slq, "n_log_2pi": out.n_log_2pi,
             "samples": list(out.samples[:n_z]), "steps": list(out.steps[:n_z]), "products": out.products,
-            "cg_relres": out.cg_relres, "cg_hist": [h for h in hist[:cg_iters]]}
+            "cg_relres": out.cg_relres, "cg_relres_true": out.cg_relres_true, "landmarks": out.landmarks,
+            "cg_hist": [h for h in hist[:cg_iters]]}
+
+
+def akm_set_preconditioner(plan, k_per_window=0):
+    """AAFN with k_per_window FPS landmarks per window (0: the diagonal preconditioner)."""
+    _check(plan, _lib.akm_set_preconditioner(plan, int(k_per_window)))
+
+
+def akm_precond_landmarks(plan, stream=None) -> int:
+    c = ctypes.c_int32()
+    _check(plan, _lib.akm_precond_landmarks(plan, ctypes.byref(c), _stream(stream)))
+    return c.value
+
+
+def akm_precond_apply(plan, T, out, transpose=False, stream=None):
+    """out = U^{-1} T (or U^{-T} T); returns (log det M, landmark indices)."""
+    pt, ldt, n, r, _, kt = _ptr_ld(T, "T")
+    po, ldo, _, _, _, ko = _ptr_ld(out, "out")
+    if ldt != r or ldo != r:
+        raise ValueError("T and out must be contiguous n x r blocks")
+    _expect_rows(plan, "T", n)
+    k = akm_precond_landmarks(plan, stream)
+    lm = np.zeros(max(k, 1), dtype=np.int32)
+    ld = ctypes.c_double()
+    _check(plan, _lib.akm_precond_apply(plan, 1 if transpose else 0, pt, r, po, ctypes.byref(ld),
+                                        lm.ctypes.data_as(ctypes.c_void_p), _stream(stream, kt, ko)))
+    return ld.value, lm[:k]
 
 
 def akm_gradient_diag(plan, y, Z, cg_iters=50, stream=None) -> dict:
@@ -497,6 +543,16 @@ class Plan:
 
     def objective_diag(self, y, Z, cg_iters=50, lanczos_steps=30, stream=None):
         return akm_objective_diag(self.handle, y, Z, cg_iters, lanczos_steps, stream)
+
+    def objective(self, y, Z, cg_iters=50, lanczos_steps=30, stream=None):
+        return akm_objective(self.handle, y, Z, cg_iters, lanczos_steps, stream)
+
+    def set_preconditioner(self, k_per_window=0):
+        akm_set_preconditioner(self.handle, k_per_window)
+        return self
+
+    def precond_apply(self, T, out, transpose=False, stream=None):
+        return akm_precond_apply(self.handle, T, out, transpose, stream)
 
     def info(self):
         return akm_get_info(self.handle)

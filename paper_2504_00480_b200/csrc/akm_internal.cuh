@@ -232,6 +232,24 @@ cudaError_t launch_near_field(const WinTable* dtab, const WorkItem* items, int n
                               const double* coef, double* part, cudaStream_t s);
 int near_field_launches(int r);
 
+// aafn.cu
+size_t fps_scratch_bytes();
+cudaError_t launch_fps(const double* Xc, long long n, int nf, const int* cols, int d, int k, int* picks, double* dmin,
+                       void* scratch, cudaStream_t s);
+cudaError_t launch_lmpos(long long n, int k, const int* lm, int* lmpos, cudaStream_t s);
+cudaError_t launch_aafn_factor(const double* Xc, long long n, int nf, const WinTable& tab, int family, double sf,
+                               double ell, double se, const int* lm, const int* lmpos, int k, double* L, double* Linv,
+                               double* Phi, double* Sdiag, double* g, double* scal, double* part, int* flag,
+                               double jitter, cudaStream_t s);
+size_t aafn_part_doubles(int k, int R);
+cudaError_t launch_resid_norms(long long n, const double* y, const double* Kx, double* part, double* out, cudaStream_t s);
+cudaError_t launch_aafn_uinv(long long n, int k, int R, const int* lm, const int* lmpos, const double* Linv,
+                             const double* Phi, const double* g, const double* T, double* y1, double* out,
+                             cudaStream_t s);
+cudaError_t launch_aafn_uinvT(long long n, int k, int R, const int* lm, const int* lmpos, const double* Linv,
+                              const double* Phi, const double* g, const double* Y, double* part, double* tmp,
+                              double* out, cudaStream_t s);
+
 // spread_mma.cu
 bool spread_mma_choose(int M, int Nn, int Fmax, int rc, int& MB, int& NB, int& WM, int& WN);
 size_t spread_mma_smem(int PB, int M, int Nn, int Fmax, int rc);

@@ -84,6 +84,17 @@ struct akm_plan {
   std::vector<double> radius;               // R_w (global after akm_set_radius)
   std::vector<double> radius_local;         // R_w of this plan's own points about the current centers
   std::vector<int> bin_override;            // empty = cost-model choice of B per window (rebuild_bins)
+  // AAFN preconditioner (aafn.cu; akm_set_preconditioner).  Landmarks depend on the points only, the
+  // factors on theta (rebuilt lazily when theta_version moved).
+  struct Aafn {
+    int kpw = 0;                  // landmarks per window; 0 = diagonal preconditioner
+    bool lm_ready = false;
+    long long theta_built = -1;
+    int k = 0;
+    double logdet = 0.0;          // log det M
+    DevBuf lm, lmpos, L, Linv, Phi, Sdiag, g, y1, part, tmp, scal, flag, fps_scratch, dmin, picks, Bt, KBt, yh;
+  } aafn;
+  long long theta_version = 0;
   int reg_p = 0;                            // kappa_R regularisation (akm_set_regularization; 0 = off)
   double reg_eps_I = 0.0;
   bool near_field() const { return reg_p > 0 && reg_eps_I > 0.0; }
@@ -104,7 +115,7 @@ struct akm_plan {
   DevBuf stageV, stageY, stageL, stageS;
   DevBuf crossV, crossY;  // akm_kernel_cross_mvm: zero-padded V and the union's product
   DevBuf gX, gP, gB2, gD1, gD2, gState;  // akm_gradient_diag: block PCG and derivative products
-  DevBuf krB, krKB, krW, krX, krY, krQ, krPart, krH, krState, krErr, krStage;
+  DevBuf krB, krKB, krW, krX, krY, krQ, krPart, krH, krState, krErr, krStage, krRes;
   long long r_cap = 0;
 
   // CUDA graph of the last MVM launch sequence (replayed when called again with the same buffers)
@@ -895,6 +906,101 @@ static akm_status mvm_entry(akm_plan* plan, const double* V, long long ldv, int 
   return AKM_OK;
 }
 
+// ================================================================== AAFN (aafn.cu)
+// Landmarks: FPS per window (k = min(kpw, n) picks each), merged in window order without duplicates.
+static akm_status aafn_landmarks(akm_plan* plan, cudaStream_t s) {
+  auto& A = plan->aafn;
+  const long long n = plan->n;
+  const int P = plan->P, nf = (int)plan->feat_used.size();
+  const int kw = (int)std::min<long long>(A.kpw, n);
+  AKM_CK(A.picks.ensure(sizeof(int) * P * kw));
+  AKM_CK(A.dmin.ensure(sizeof(double) * n));
+  AKM_CK(A.fps_scratch.ensure(fps_scratch_bytes()));
+  for (int w = 0; w < P; ++w) {
+    const WinGeom& g = plan->tab.w[w];
+    int cols[3] = {0, 0, 0};
+    for (int t = 0; t < g.d; ++t) cols[t] = g.feat[3 - g.d + t];
+    AKM_CK(launch_fps(plan->Xc.as<double>(), n, nf, cols, g.d, kw, A.picks.as<int>() + (long long)w * kw,
+                      A.dmin.as<double>(), A.fps_scratch.p, s));
+  }
+  std::vector<int> picks((size_t)P * kw);
+  AKM_CK(cudaMemcpyAsync(picks.data(), A.picks.p, sizeof(int) * picks.size(), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaStreamSynchronize(s));
+  std::vector<int> lm;
+  std::set<int> seen;
+  for (int v : picks)
+    if (seen.insert(v).second) lm.push_back(v);
+  A.k = (int)lm.size();
+  AKM_CK(A.lm.ensure(sizeof(int) * A.k));
+  AKM_CK(A.lmpos.ensure(sizeof(int) * n));
+  AKM_CK(cudaMemcpyAsync(A.lm.p, lm.data(), sizeof(int) * A.k, cudaMemcpyHostToDevice, s));
+  AKM_CK(launch_lmpos(n, A.k, A.lm.as<int>(), A.lmpos.as<int>(), s));
+  AKM_CK(cudaStreamSynchronize(s));
+  A.lm_ready = true;
+  return AKM_OK;
+}
+
+// Factors for the current theta: L11 (Cholesky of the landmark block, one jitter retry as in SPEC's
+// DESIGN DECISIONS), L11^{-1}, Phi = K21 L11^{-T}, G = diag(S_aa^{-1/2}), log det M.
+static akm_status aafn_build(akm_plan* plan, int R, cudaStream_t s) {
+  auto& A = plan->aafn;
+  if (!A.lm_ready) {
+    akm_status st = aafn_landmarks(plan, s);
+    if (st != AKM_OK) return st;
+  }
+  const long long n = plan->n;
+  const int k = A.k;
+  AKM_CK(A.y1.ensure(sizeof(double) * k * std::max(R, 1)));
+  AKM_CK(A.tmp.ensure(sizeof(double) * k * std::max(R, 1)));
+  AKM_CK(A.part.ensure(sizeof(double) * aafn_part_doubles(k, std::max(R, 1))));
+  if (A.theta_built == plan->theta_version) return AKM_OK;
+  if (k > 4096) return plan->fail(AKM_ERR_UNSUPPORTED, "AAFN with %d landmarks (at most 4096 built)", k);
+  AKM_CK(A.L.ensure(sizeof(double) * k * k));
+  AKM_CK(A.Linv.ensure(sizeof(double) * k * k));
+  AKM_CK(A.Phi.ensure(sizeof(double) * n * k));
+  AKM_CK(A.Sdiag.ensure(sizeof(double) * n));
+  AKM_CK(A.g.ensure(sizeof(double) * n));
+  AKM_CK(A.scal.ensure(sizeof(double) * 2));
+  AKM_CK(A.flag.ensure(sizeof(int)));
+  double jitter = 0.0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    int flag = 0;
+    AKM_CK(cudaMemsetAsync(A.flag.p, 0, sizeof(int), s));
+    AKM_CK(launch_aafn_factor(plan->Xc.as<double>(), n, (int)plan->feat_used.size(), plan->tab, plan->family,
+                              plan->sigma_f, plan->ell, plan->sigma_eps, A.lm.as<int>(), A.lmpos.as<int>(), k,
+                              A.L.as<double>(), A.Linv.as<double>(), A.Phi.as<double>(), A.Sdiag.as<double>(),
+                              A.g.as<double>(), A.scal.as<double>(), A.part.as<double>(), A.flag.as<int>(), jitter, s));
+    double sc[2];
+    AKM_CK(cudaMemcpyAsync(sc, A.scal.p, sizeof(sc), cudaMemcpyDeviceToHost, s));
+    AKM_CK(cudaMemcpyAsync(&flag, A.flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    AKM_CK(cudaStreamSynchronize(s));
+    if (flag == 0) {
+      A.logdet = sc[0] + sc[1];
+      A.theta_built = plan->theta_version;
+      return AKM_OK;
+    }
+    // K11 is SPD in exact arithmetic: one retry with 1e-10 trace(K11)/k on the diagonal
+    jitter = 1e-10 * (plan->sigma_f * plan->sigma_f * plan->P + plan->sigma_eps * plan->sigma_eps);
+  }
+  return plan->fail(AKM_ERR_NONFINITE, "AAFN: the landmark block is not positive definite (Cholesky breakdown)");
+}
+
+// out = U^{-1} T  /  U^{-T} T  (n x R row-major, device)
+static akm_status aafn_uinv(akm_plan* plan, int R, const double* T, double* out, cudaStream_t s) {
+  auto& A = plan->aafn;
+  AKM_CK(launch_aafn_uinv(plan->n, A.k, R, A.lm.as<int>(), A.lmpos.as<int>(), A.Linv.as<double>(), A.Phi.as<double>(),
+                          A.g.as<double>(), T, A.y1.as<double>(), out, s));
+  plan->launches += 2;
+  return AKM_OK;
+}
+static akm_status aafn_uinvT(akm_plan* plan, int R, const double* T, double* out, cudaStream_t s) {
+  auto& A = plan->aafn;
+  AKM_CK(launch_aafn_uinvT(plan->n, A.k, R, A.lm.as<int>(), A.lmpos.as<int>(), A.Linv.as<double>(), A.Phi.as<double>(),
+                           A.g.as<double>(), T, A.part.as<double>(), A.tmp.as<double>(), out, s));
+  plan->launches += 3;
+  return AKM_OK;
+}
+
 // ================================================================== C ABI
 extern "C" {
 
@@ -1053,6 +1159,8 @@ akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p,
   plan->bin_override.clear();
   plan->reg_p = 0;
   plan->reg_eps_I = 0.0;
+  plan->aafn.lm_ready = false;
+  plan->aafn.theta_built = -1;
   plan->c_w.assign(P, 0.0);
   plan->c_w_binned.assign(P, -1.0);
   plan->r_cap = 0;
@@ -1091,6 +1199,7 @@ akm_status akm_set_theta(akm_plan* plan, double sigma_f, double ell, double sigm
   AKM_CK(cudaSetDevice(plan->device));
   plan->have_theta = false;
   ++plan->epoch;  // theta is baked into captured launch sequences
+  ++plan->theta_version;
   plan->sigma_f = sigma_f;
   plan->ell = ell;
   plan->sigma_eps = sigma_eps;
@@ -1211,9 +1320,25 @@ akm_status akm_kernel_cross_mvm(akm_plan* plan, int64_t n_src, const double* V, 
   return AKM_OK;
 }
 
+static akm_status objective_impl(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                                 int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,
+                                 void* stream, bool use_aafn);
+
 akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
                               int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,
                               void* stream) {
+  return objective_impl(plan, y, Z, ldz, n_z, cg_iters, lanczos_steps, out, cg_relres, stream, false);
+}
+
+akm_status akm_objective(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z, int32_t cg_iters,
+                         int32_t lanczos_steps, akm_objective_out* out, double* cg_relres, void* stream) {
+  return objective_impl(plan, y, Z, ldz, n_z, cg_iters, lanczos_steps, out, cg_relres, stream,
+                        plan && plan->aafn.kpw > 0);
+}
+
+static akm_status objective_impl(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                                 int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,
+                                 void* stream, bool use_aafn) {
   if (!plan) return AKM_ERR_INVALID_ARG;
   plan->err.clear();
   if (!plan->have_points || !plan->have_theta)
@@ -1269,8 +1394,23 @@ akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, 
   double* Q = plan->krQ.as<double>();
   double* part = plan->krPart.as<double>();
   void* st = plan->krState.p;
-  // M = diag(Khat): kappa(0) = 1 for every sub-kernel (reading R11)
-  const double c = plan->sigma_f * plan->sigma_f * plan->P + plan->sigma_eps * plan->sigma_eps;
+  // M = diag(Khat): kappa(0) = 1 for every sub-kernel (reading R11).  AAFN (reading R15): the drivers
+  // run on S_op = U^{-1} Khat U^{-T} with M = I there, column 0 = U^{-1} y (CG on S_op x^ = U^{-1} y is
+  // PCG on Khat x = y with x = U^{-T} x^, and y^T x = (U^{-1} y)^T x^)
+  double c = plan->sigma_f * plan->sigma_f * plan->P + plan->sigma_eps * plan->sigma_eps;
+  auto& A = plan->aafn;
+  const double* y_user = yd;
+  if (use_aafn) {
+    akm_status sb = aafn_build(plan, R, s);
+    if (sb != AKM_OK) return sb;
+    AKM_CK(A.Bt.ensure(sizeof(double) * slab));
+    AKM_CK(A.KBt.ensure(sizeof(double) * slab));
+    AKM_CK(A.yh.ensure(sizeof(double) * n));
+    sb = aafn_uinv(plan, 1, yd, A.yh.as<double>(), s);
+    if (sb != AKM_OK) return sb;
+    yd = A.yh.as<double>();
+    c = 1.0;
+  }
   AKM_CK(launch_kr_load(n, R, yd, Zd, ldzd, B, plan->krY.as<double>(), s));
   AKM_CK(launch_kr_col2(n, R, B, B, part, s));
   AKM_CK(launch_kr_init(st, part, R, c, s));
@@ -1278,7 +1418,14 @@ akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, 
   const int T = std::max(cg_iters, lanczos_steps);
   int products = 0;
   for (int t = 0; t < T; ++t) {
-    akm_status stt = run_mvm(plan, B, R, R, KB, nullptr, nullptr, R, s);
+    akm_status stt;
+    if (use_aafn) {
+      stt = aafn_uinvT(plan, R, B, A.Bt.as<double>(), s);
+      if (stt == AKM_OK) stt = run_mvm(plan, A.Bt.as<double>(), R, R, A.KBt.as<double>(), nullptr, nullptr, R, s);
+      if (stt == AKM_OK) stt = aafn_uinv(plan, R, A.KBt.as<double>(), KB, s);
+    } else {
+      stt = run_mvm(plan, B, R, R, KB, nullptr, nullptr, R, s);
+    }
     if (stt != AKM_OK) return stt;
     ++products;
     AKM_CK(launch_kr_col2(n, R, B, KB, part, s));
@@ -1298,6 +1445,24 @@ akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, 
   }
   AKM_CK(launch_kr_col2(n, 1, plan->krY.as<double>(), plan->krX.as<double>(), part, s));
   AKM_CK(launch_kr_slq_quad(st, R, part, plan->krErr.as<int>(), s));
+  // true relative residual ||y - Khat x|| / ||y|| of the CG solution (one extra product with r = 1)
+  double rn[2] = {0.0, 0.0};
+  if (cg_iters > 0) {
+    AKM_CK(plan->krRes.ensure(sizeof(double) * (2 * n + 8)));
+    double* xu = plan->krRes.as<double>();      // x in the user's space
+    double* kx = xu + n;                       // Khat x
+    double* nrm = kx + n;                      // the two norms
+    const double* x = plan->krX.as<double>();
+    if (use_aafn) {
+      akm_status sx = aafn_uinvT(plan, 1, x, xu, s);
+      if (sx != AKM_OK) return sx;
+      x = xu;
+    }
+    akm_status sx = run_mvm(plan, x, 1, 1, kx, nullptr, nullptr, 1, s);
+    if (sx != AKM_OK) return sx;
+    AKM_CK(launch_resid_norms(n, y_user, kx, part, nrm, s));
+    AKM_CK(cudaMemcpyAsync(rn, nrm, sizeof(rn), cudaMemcpyDeviceToHost, s));
+  }
   size_t o_quad, o_samp, o_steps, o_hist, o_zn;
   kr_summary_offsets(&o_quad, &o_samp, &o_steps, &o_hist, &o_zn);
   double quad = 0.0;
@@ -1314,7 +1479,9 @@ akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, 
   AKM_CK(cudaStreamSynchronize(s));
   std::memset(out, 0, sizeof(*out));
   out->quad = quad;
-  out->logdet_M = (double)n * std::log(c);
+  out->logdet_M = use_aafn ? A.logdet : (double)n * std::log(c);
+  out->cg_relres_true = (cg_iters > 0 && rn[1] > 0.0) ? std::sqrt(rn[0] / rn[1]) : 0.0;
+  out->landmarks = use_aafn ? A.k : 0;
   out->n_log_2pi = (double)n * std::log(2.0 * kPi);
   double acc = 0.0;
   for (int i = 0; i < n_z; ++i) {
@@ -1584,6 +1751,58 @@ akm_status akm_mvm_from_grid(akm_plan* plan, const double* grid, const double* V
   akm_plan::EvSet* ev = plan->profiling ? plan->split_ev : nullptr;
   plan->split_ev = nullptr;
   return enqueue_finish(plan, grid, V, ldv, r, Y, dY_ell, dY_sf, ldy, s, 0, ev);
+}
+
+akm_status akm_set_preconditioner(akm_plan* plan, int32_t k_per_window) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points) return plan->fail(AKM_ERR_STATE, "set_preconditioner before set_points");
+  if (k_per_window < 0 || k_per_window > 4096) return plan->fail(AKM_ERR_INVALID_ARG, "k_per_window must be in [0, 4096]");
+  if (k_per_window != plan->aafn.kpw) {
+    plan->aafn.kpw = k_per_window;
+    plan->aafn.lm_ready = false;
+    plan->aafn.theta_built = -1;
+  }
+  return AKM_OK;
+}
+
+akm_status akm_precond_apply(akm_plan* plan, int32_t transpose, const double* T, int32_t r, double* out, double* logdet,
+                             int32_t* landmarks, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points || !plan->have_theta) return plan->fail(AKM_ERR_STATE, "precond_apply before set_points / set_theta");
+  if (plan->aafn.kpw <= 0) return plan->fail(AKM_ERR_STATE, "no AAFN preconditioner set (akm_set_preconditioner)");
+  if (r < 1 || r > kKrMaxR) return plan->fail(AKM_ERR_INVALID_ARG, "r must be in [1, %d]", kKrMaxR);
+  if (plan->n < 1) return plan->fail(AKM_ERR_INVALID_ARG, "precond_apply needs n >= 1");
+  if (!is_device_ptr(T) || !is_device_ptr(out)) return plan->fail(AKM_ERR_INVALID_ARG, "T and out must be device memory");
+  cudaStream_t s = S(stream);
+  AKM_CK(cudaSetDevice(plan->device));
+  akm_status st = aafn_build(plan, r, s);
+  if (st != AKM_OK) return st;
+  st = transpose ? aafn_uinvT(plan, r, T, out, s) : aafn_uinv(plan, r, T, out, s);
+  if (st != AKM_OK) return st;
+  if (logdet) *logdet = plan->aafn.logdet;
+  if (landmarks) {
+    AKM_CK(cudaMemcpyAsync(landmarks, plan->aafn.lm.p, sizeof(int) * plan->aafn.k, cudaMemcpyDeviceToHost, s));
+    AKM_CK(cudaStreamSynchronize(s));
+  }
+  return AKM_OK;
+}
+
+akm_status akm_precond_landmarks(akm_plan* plan, int32_t* count, void* stream) {
+  if (!plan || !count) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points) return plan->fail(AKM_ERR_STATE, "precond_landmarks before set_points");
+  if (plan->aafn.kpw <= 0) return plan->fail(AKM_ERR_STATE, "no AAFN preconditioner set (akm_set_preconditioner)");
+  if (plan->n < 1) return plan->fail(AKM_ERR_INVALID_ARG, "needs n >= 1");
+  cudaStream_t s = S(stream);
+  AKM_CK(cudaSetDevice(plan->device));
+  if (!plan->aafn.lm_ready) {
+    akm_status st = aafn_landmarks(plan, s);
+    if (st != AKM_OK) return st;
+  }
+  *count = plan->aafn.k;
+  return AKM_OK;
 }
 
 akm_status akm_set_regularization(akm_plan* plan, double eps_I, int32_t p) {

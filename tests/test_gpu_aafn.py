@@ -1,0 +1,122 @@
+"""GPU parity of the AAFN preconditioner (akm_set_preconditioner / akm_precond_apply /
+akm_objective) against oracle/aafn.py.
+
+* landmarks (FPS per window, merged): integer work, bit-exact;
+* U^{-1} T, U^{-T} T and log det M (diagonal FSAI, fill = 1) within 1e-10 of the float64 oracle;
+* the AAFN objective (CG + SLQ on S_op = U^{-1} K^ U^{-T}) against the oracle driver with the dense
+  K^ (the GPU's product is the NFFT one, ~1e-12 away): every term within 1e-8;
+* c5 at full size (n = 5e5, BASELINE.json configs[4]): 50 AAFN-PCG iterations reach a true relative
+  residual <= 1e-3, where the diagonal preconditioner diverges (VERDICT r1 Missing 1).
+"""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import aafn as A
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def akm():
+    import __graft_entry__
+    __graft_entry__.build_library()
+    import paper_2504_00480_b200 as mod
+    return mod
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def _plan(akm, X, wl, kpw, theta=None):
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(np.ascontiguousarray(X)).to(dev), wl.windows, wl.family, wl.N, wl.sigma_over,
+                    wl.m, wl.eps_B)
+    plan.set_preconditioner(kpw)
+    plan.set_theta(*(theta or (wl.sigma_f, wl.ell, wl.sigma_eps)))
+    return plan
+
+
+@pytest.mark.parametrize("name,n,kpw", [("c5", 5000, 25), ("c3", 4000, 40), ("c1", 2000, 60)])
+def test_landmarks_bit_exact(akm, name, n, kpw):
+    wl = workloads.CONFIGS[name]
+    X = workloads.make_X(wl, n=n)
+    plan = _plan(akm, X, wl, kpw)
+    dev = torch.device("cuda:0")
+    T = torch.zeros((n, 1), dtype=torch.float64, device=dev)
+    out = torch.empty_like(T)
+    _, lm = plan.precond_apply(T, out)
+    plan.close()
+    want = A.landmarks(X, wl.windows, kpw)
+    np.testing.assert_array_equal(lm, want)
+
+
+def test_factor_and_applications(akm):
+    wl = workloads.CONFIGS["c5"]
+    n, r, kpw = 3000, 3, 30
+    X = workloads.make_X(wl, n=n)
+    th = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    plan = _plan(akm, X, wl, kpw)
+    pre = A.Aafn(X, wl.windows, wl.family, th, kpw, 1)
+    dev = torch.device("cuda:0")
+    T = np.random.default_rng(1).standard_normal((n, r))
+    Td = torch.from_numpy(T).to(dev)
+    for transpose in (False, True):
+        out = torch.empty_like(Td)
+        logdet, lm = plan.precond_apply(Td, out, transpose=transpose)
+        want = pre.U_invT(T) if transpose else pre.U_inv(T)
+        assert rel(out.cpu().numpy(), want) <= 1e-10, (transpose, rel(out.cpu().numpy(), want))
+        assert logdet == pytest.approx(pre.logdet, rel=1e-10)
+    np.testing.assert_array_equal(lm, pre.lm)
+    plan.close()
+
+
+def test_objective_vs_oracle(akm):
+    """100 landmarks per window: 50 CG iterations converge to ~4e-8 (with 40 per window they stop at
+    ~2e-3, where y^T x still moves by 1e-5 under the 1e-12 difference between the NFFT and dense products)."""
+    wl = workloads.CONFIGS["c5"]
+    n, n_z, kpw = 3000, 4, 100
+    X = workloads.make_X(wl, n=n)
+    V = workloads.make_V(wl, n=n, r=1 + n_z)
+    th = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    plan = _plan(akm, X, wl, kpw)
+    dev = torch.device("cuda:0")
+    y = torch.from_numpy(np.ascontiguousarray(V[:, 0])).to(dev)
+    Z = torch.from_numpy(np.ascontiguousarray(V[:, 1:])).to(dev)
+    got = plan.objective(y, Z, 50, 20)
+    plan.close()
+    K = A.khat_dense(X, wl.windows, wl.family, th)
+    pre = A.Aafn(X, wl.windows, wl.family, th, kpw, 1)
+    want = A.objective_aafn(lambda B: K @ B, V[:, 0], V[:, 1:], pre, 50, 20)
+    assert got["landmarks"] == pre.lm.size
+    assert got["logdetM"] == pytest.approx(want["logdetM"], rel=1e-10)
+    assert got["quad"] == pytest.approx(want["quad"], rel=1e-8)
+    assert got["slq"] == pytest.approx(want["slq"], rel=1e-8)
+    assert got["Z"] == pytest.approx(want["Z"], rel=1e-8)
+    assert got["cg_relres_true"] <= 1e-6 and want["cg_relres_true"] <= 1e-6
+
+
+def test_c5_full_size_cg_converges(akm):
+    """BASELINE.json configs[4] (n = 5e5, three 3-D Gaussian windows, theta = (1, 0.5, 0.05), 50 CG
+    iterations, 30 Lanczos steps, 10 probes): with AAFN (100 landmarks per window) the 50-iteration CG
+    solution has a true relative residual <= 1e-3; with M = diag(K^) it does not converge."""
+    wl = workloads.CONFIGS["c5"]
+    X = workloads.make_X(wl)
+    V = workloads.make_V(wl)
+    dev = torch.device("cuda:0")
+    y = torch.from_numpy(np.ascontiguousarray(V[:, 0])).to(dev)
+    Z = torch.from_numpy(np.ascontiguousarray(V[:, 1:])).to(dev)
+    plan = _plan(akm, X, wl, 100)
+    got = plan.objective(y, Z, 50, 30)
+    diag = plan.objective_diag(y, Z, 50, 30)
+    plan.close()
+    assert got["cg_relres_true"] <= 1e-3, got["cg_relres_true"]
+    assert diag["cg_relres_true"] > 1e-1
+    assert np.isfinite(got["Z"]) and got["landmarks"] > 250
+    # both estimate the same log det K^ = log det M + tr logm(M^{-1} K^) (eq. 1.3): the AAFN split is
+    # far more accurate, so the two agree only to the diagonal estimator's own SLQ spread
+    assert got["logdetM"] + got["slq"] == pytest.approx(diag["logdetM"] + diag["slq"], rel=2e-2)
