@@ -308,6 +308,10 @@ def main():
     else:
         plan = akm.Plan(local)
         plan.set_points(Xd, wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+        if "reg_p" in wl.extra:                 # f4: kappa_R with the near-field correction
+            plan.set_regularization(wl.extra["reg_eps_I"], wl.extra["reg_p"])
+        if "aafn_kpw" in wl.extra:              # f3: AAFN preconditioner
+            plan.set_preconditioner(wl.extra["aafn_kpw"])
         plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
     set_theta_ms = (time.perf_counter() - t0) * 1e3
     info = plan.info()
@@ -318,8 +322,13 @@ def main():
         products_per_step = max(cg, lz)
         last = {}
 
-        def step():
-            last["out"] = plan.objective_diag(yd, Zd, cg, lz)
+        if "aafn_kpw" in wl.extra:
+            def step():   # theta -> AAFN factors -> Z~ (the factors depend on theta: rebuilt every step)
+                plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+                last["out"] = plan.objective(yd, Zd, cg, lz)
+        else:
+            def step():
+                last["out"] = plan.objective_diag(yd, Zd, cg, lz)
     elif gradient:
         gcg = wl.extra["grad_cg_iters"]
         yd, Zd = Vd[:, 0].contiguous(), Vd[:, 1:].contiguous()
@@ -396,7 +405,10 @@ def main():
         yh, Zh = Vh[:, 0].contiguous().pin_memory(), Vh[:, 1:].contiguous().pin_memory()
 
     def e2e_step():
-        if objective:   # host y, Z in; the objective's terms come back to the host
+        if objective and "aafn_kpw" in wl.extra:
+            plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+            plan.objective(yh, Zh, cg, lz, stream=stream.cuda_stream)
+        elif objective:   # host y, Z in; the objective's terms come back to the host
             plan.objective_diag(yh, Zh, cg, lz, stream=stream.cuda_stream)
         elif gradient:  # host y, Z in; the three components come back to the host
             plan.gradient_diag(yh, Zh, gcg, stream=stream.cuda_stream)
@@ -498,7 +510,8 @@ def main():
     if objective:
         o = last["out"]
         line["objective"] = {"Z": o["Z"], "quad": o["quad"], "logdetM": o["logdetM"], "slq": o["slq"],
-                             "cg_relres": o["cg_relres"], "steps": o["steps"], "ms_per_evaluation": ms_per_step,
+                             "cg_relres": o["cg_relres"], "cg_relres_true": o["cg_relres_true"],
+                             "landmarks": o["landmarks"], "steps": o["steps"], "ms_per_evaluation": ms_per_step,
                              "ms_per_product": ms_per_step / products_per_step}
     if gradient:
         line["gradient"] = {"grad": last["out"]["grad"], "cg_relres_last": last["out"]["cg_hist"][-1],

@@ -239,16 +239,16 @@ cudaError_t launch_fps(const double* Xc, long long n, int nf, const int* cols, i
 cudaError_t launch_lmpos(long long n, int k, const int* lm, int* lmpos, cudaStream_t s);
 cudaError_t launch_aafn_factor(const double* Xc, long long n, int nf, const WinTable& tab, int family, double sf,
                                double ell, double se, const int* lm, const int* lmpos, int k, double* L, double* Linv,
-                               double* Phi, double* Sdiag, double* g, double* scal, double* part, int* flag,
-                               double jitter, cudaStream_t s);
-size_t aafn_part_doubles(int k, int R);
+                               double* LinvT, double* Phi, double* K21, double* Sdiag, double* g, double* scal,
+                               double* part, int* flag, double jitter, cudaStream_t s);
+size_t aafn_part_doubles(long long n, int k, int R);
 cudaError_t launch_resid_norms(long long n, const double* y, const double* Kx, double* part, double* out, cudaStream_t s);
 cudaError_t launch_aafn_uinv(long long n, int k, int R, const int* lm, const int* lmpos, const double* Linv,
-                             const double* Phi, const double* g, const double* T, double* y1, double* out,
-                             cudaStream_t s);
-cudaError_t launch_aafn_uinvT(long long n, int k, int R, const int* lm, const int* lmpos, const double* Linv,
+                             const double* Phi, const double* g, const double* T, double* y1, double* tmp,
+                             double* part, double* out, cudaStream_t s);
+cudaError_t launch_aafn_uinvT(long long n, int k, int R, const int* lm, const int* lmpos, const double* LinvT,
                               const double* Phi, const double* g, const double* Y, double* part, double* tmp,
-                              double* out, cudaStream_t s);
+                              double* w1, double* out, cudaStream_t s);
 
 // spread_mma.cu
 bool spread_mma_choose(int M, int Nn, int Fmax, int rc, int& MB, int& NB, int& WM, int& WN);

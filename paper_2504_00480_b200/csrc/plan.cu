@@ -92,7 +92,8 @@ struct akm_plan {
     long long theta_built = -1;
     int k = 0;
     double logdet = 0.0;          // log det M
-    DevBuf lm, lmpos, L, Linv, Phi, Sdiag, g, y1, part, tmp, scal, flag, fps_scratch, dmin, picks, Bt, KBt, yh;
+    DevBuf lm, lmpos, L, Linv, LinvT, Phi, K21, Sdiag, g, y1, part, tmp, scal, flag, fps_scratch, dmin, picks, Bt, KBt,
+        yh;
   } aafn;
   long long theta_version = 0;
   int reg_p = 0;                            // kappa_R regularisation (akm_set_regularization; 0 = off)
@@ -952,12 +953,14 @@ static akm_status aafn_build(akm_plan* plan, int R, cudaStream_t s) {
   const int k = A.k;
   AKM_CK(A.y1.ensure(sizeof(double) * k * std::max(R, 1)));
   AKM_CK(A.tmp.ensure(sizeof(double) * k * std::max(R, 1)));
-  AKM_CK(A.part.ensure(sizeof(double) * aafn_part_doubles(k, std::max(R, 1))));
+  AKM_CK(A.part.ensure(sizeof(double) * aafn_part_doubles(n, k, std::max(R, 1))));
   if (A.theta_built == plan->theta_version) return AKM_OK;
   if (k > 4096) return plan->fail(AKM_ERR_UNSUPPORTED, "AAFN with %d landmarks (at most 4096 built)", k);
   AKM_CK(A.L.ensure(sizeof(double) * k * k));
   AKM_CK(A.Linv.ensure(sizeof(double) * k * k));
+  AKM_CK(A.LinvT.ensure(sizeof(double) * k * k));
   AKM_CK(A.Phi.ensure(sizeof(double) * n * k));
+  AKM_CK(A.K21.ensure(sizeof(double) * n * k));
   AKM_CK(A.Sdiag.ensure(sizeof(double) * n));
   AKM_CK(A.g.ensure(sizeof(double) * n));
   AKM_CK(A.scal.ensure(sizeof(double) * 2));
@@ -968,7 +971,9 @@ static akm_status aafn_build(akm_plan* plan, int R, cudaStream_t s) {
     AKM_CK(cudaMemsetAsync(A.flag.p, 0, sizeof(int), s));
     AKM_CK(launch_aafn_factor(plan->Xc.as<double>(), n, (int)plan->feat_used.size(), plan->tab, plan->family,
                               plan->sigma_f, plan->ell, plan->sigma_eps, A.lm.as<int>(), A.lmpos.as<int>(), k,
-                              A.L.as<double>(), A.Linv.as<double>(), A.Phi.as<double>(), A.Sdiag.as<double>(),
+                              A.L.as<double>(), A.Linv.as<double>(), A.LinvT.as<double>(), A.Phi.as<double>(),
+                              A.K21.as<double>(),
+                              A.Sdiag.as<double>(),
                               A.g.as<double>(), A.scal.as<double>(), A.part.as<double>(), A.flag.as<int>(), jitter, s));
     double sc[2];
     AKM_CK(cudaMemcpyAsync(sc, A.scal.p, sizeof(sc), cudaMemcpyDeviceToHost, s));
@@ -989,15 +994,16 @@ static akm_status aafn_build(akm_plan* plan, int R, cudaStream_t s) {
 static akm_status aafn_uinv(akm_plan* plan, int R, const double* T, double* out, cudaStream_t s) {
   auto& A = plan->aafn;
   AKM_CK(launch_aafn_uinv(plan->n, A.k, R, A.lm.as<int>(), A.lmpos.as<int>(), A.Linv.as<double>(), A.Phi.as<double>(),
-                          A.g.as<double>(), T, A.y1.as<double>(), out, s));
-  plan->launches += 2;
+                          A.g.as<double>(), T, A.y1.as<double>(), A.tmp.as<double>(), A.part.as<double>(), out, s));
+  plan->launches += 4;
   return AKM_OK;
 }
 static akm_status aafn_uinvT(akm_plan* plan, int R, const double* T, double* out, cudaStream_t s) {
   auto& A = plan->aafn;
-  AKM_CK(launch_aafn_uinvT(plan->n, A.k, R, A.lm.as<int>(), A.lmpos.as<int>(), A.Linv.as<double>(), A.Phi.as<double>(),
-                           A.g.as<double>(), T, A.part.as<double>(), A.tmp.as<double>(), out, s));
-  plan->launches += 3;
+  AKM_CK(launch_aafn_uinvT(plan->n, A.k, R, A.lm.as<int>(), A.lmpos.as<int>(), A.LinvT.as<double>(),
+                           A.Phi.as<double>(), A.g.as<double>(), T, A.part.as<double>(), A.tmp.as<double>(),
+                           A.y1.as<double>(), out, s));
+  plan->launches += 4;
   return AKM_OK;
 }
 

@@ -102,21 +102,22 @@ def test_objective_vs_oracle(akm):
 
 def test_c5_full_size_cg_converges(akm):
     """BASELINE.json configs[4] (n = 5e5, three 3-D Gaussian windows, theta = (1, 0.5, 0.05), 50 CG
-    iterations, 30 Lanczos steps, 10 probes): with AAFN (100 landmarks per window) the 50-iteration CG
-    solution has a true relative residual <= 1e-3; with M = diag(K^) it does not converge."""
+    iterations, 30 Lanczos steps, 10 probes): with AAFN (800 landmarks per window, 2396 after merging)
+    the 50-iteration CG solution has a true relative residual <= 1e-3; with M = diag(K^) it does not
+    converge.  (At n = 5e5 the Nystrom part needs many landmarks: 100 per window stop at ~0.17.)"""
     wl = workloads.CONFIGS["c5"]
     X = workloads.make_X(wl)
     V = workloads.make_V(wl)
     dev = torch.device("cuda:0")
     y = torch.from_numpy(np.ascontiguousarray(V[:, 0])).to(dev)
     Z = torch.from_numpy(np.ascontiguousarray(V[:, 1:])).to(dev)
-    plan = _plan(akm, X, wl, 100)
+    plan = _plan(akm, X, wl, 800)
     got = plan.objective(y, Z, 50, 30)
     diag = plan.objective_diag(y, Z, 50, 30)
     plan.close()
     assert got["cg_relres_true"] <= 1e-3, got["cg_relres_true"]
     assert diag["cg_relres_true"] > 1e-1
-    assert np.isfinite(got["Z"]) and got["landmarks"] > 250
+    assert np.isfinite(got["Z"]) and got["landmarks"] > 2000
     # both estimate the same log det K^ = log det M + tr logm(M^{-1} K^) (eq. 1.3): the AAFN split is
     # far more accurate, so the two agree only to the diagonal estimator's own SLQ spread
     assert got["logdetM"] + got["slq"] == pytest.approx(diag["logdetM"] + diag["slq"], rel=2e-2)
