@@ -357,6 +357,8 @@ def main():
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize(dev)
+    if objective:   # after the Lanczos steps only the CG column is multiplied: count live columns only
+        products_per_step = last["out"]["product_columns"] / wl.r
 
     K = args.steps
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]

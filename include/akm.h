@@ -167,7 +167,8 @@ akm_status akm_get_stage_times(akm_plan* plan, akm_stage_times* out, int32_t res
  * M^{-1/2} Khat M^{-1/2} from z_i/||z_i|| with full reorthogonalisation, stopped early on breakdown
  * beta_j <= 1e-12 ||S q_j|| (reading R14), Gauss quadrature ||z_i||^2 sum_j tau_j^2 log theta_j.
  * Every Krylov step is ONE product of Khat with the n x (1 + n_z) block [CG direction | Lanczos
- * vectors] through the NFFT path (columns that finished are zero; reading R11).
+ * vectors] through the NFFT path (reading R11); once the Lanczos steps are done the remaining CG
+ * steps multiply the CG column alone (r = 1).
  *   y   n float64 (device or host);  Z  n x n_z row-major probes (ld ldz >= n_z; device or host)
  *   1 <= n_z <= AKM_MAX_PROBES, 0 <= cg_iters <= 1024, 0 <= lanczos_steps <= 64
  *   out (host) receives the terms; cg_relres (host, nullable) receives cg_iters relative residuals
@@ -190,6 +191,8 @@ typedef struct {
   double cg_relres_true;          /* ||y - Khat x|| / ||y|| of the returned CG iterate (one extra
                                      r = 1 product)                                             */
   int32_t landmarks;              /* AAFN landmark count k (0: diagonal preconditioner)          */
+  int64_t product_columns;        /* columns multiplied over all products (after the Lanczos
+                                     steps only the CG column is multiplied: r = 1)             */
 } akm_objective_out;
 akm_status akm_objective_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
                               int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,

@@ -72,7 +72,7 @@ class akm_objective_out(ctypes.Structure):
                 ("samples", ctypes.c_double * AKM_MAX_PROBES), ("steps", ctypes.c_int32 * AKM_MAX_PROBES),
                 ("n_z", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("lanczos_steps", ctypes.c_int32),
                 ("products", ctypes.c_int32), ("cg_relres", ctypes.c_double), ("cg_relres_true", ctypes.c_double),
-                ("landmarks", ctypes.c_int32)]
+                ("landmarks", ctypes.c_int32), ("product_columns", ctypes.c_int64)]
 
 
 def _load():
@@ -444,6 +444,7 @@ def _objective(fn, plan, y, Z, cg_iters, lanczos_steps, stream) -> dict:
     return {"Z": out.Z, "quad": out.quad, "logdetM": out.logdet_M, "slq": out.slq, "n_log_2pi": out.n_log_2pi,
             "samples": list(out.samples[:n_z]), "steps": list(out.steps[:n_z]), "products": out.products,
             "cg_relres": out.cg_relres, "cg_relres_true": out.cg_relres_true, "landmarks": out.landmarks,
+            "product_columns": out.product_columns,
             "cg_hist": [h for h in hist[:cg_iters]]}
 
 

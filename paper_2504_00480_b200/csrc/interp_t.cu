@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(32 * kItWarps, 2) k_interp_t(const WinTable* _
 }
 
 // instances: (TAPS, FP, OPS, RC) -> (MT, WN)
-#define AKM_IT_INSTANCES(X) X(12, 12, 1, 11, 2, 1) X(12, 13, 2, 1, 2, 1)
+#define AKM_IT_INSTANCES(X) X(12, 12, 1, 11, 2, 1) X(12, 13, 2, 1, 2, 1) X(12, 12, 2, 1, 2, 1)
 
 bool interp_t_supported(int d, int taps, int fp, int ops, int rc) {
 #define AKM_IT_SUP(T, F, O, R, M, W) \

@@ -132,9 +132,16 @@ struct akm_plan {
     }
   };
   long long epoch = 0;                 // bumped whenever buffers, items or theta change
-  cudaGraphExec_t gexec = nullptr;
-  GraphKey gkey{};
-  long long glaunches = 0, gspread = 0, ginterp = 0;
+  // small LRU of captured launch sequences: the Krylov drivers alternate between a few (V, Y, r)
+  // combinations; entries of an older epoch are never matched and age out
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    GraphKey key{};
+    long long launches = 0, spread = 0, interp = 0, last_use = 0;
+  };
+  static constexpr int kGraphSlots = 4;
+  GraphEntry graphs[kGraphSlots];
+  long long graph_clock = 0;
   cudaStream_t own_stream = nullptr;   // used to capture / replay when the caller passes the legacy stream
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   bool use_graphs = true;
@@ -178,7 +185,8 @@ struct akm_plan {
   ~akm_plan() {
     for (auto& es : ring)
       for (auto& e : es.e) cudaEventDestroy(e);
-    if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
@@ -799,10 +807,19 @@ static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r,
     AKM_CK(cudaEventRecord(plan->ev_in, s));
     AKM_CK(cudaStreamWaitEvent(cs, plan->ev_in, 0));
   }
-  if (!(plan->gexec && plan->gkey == key)) {
-    if (plan->gexec) {
-      cudaGraphExecDestroy(plan->gexec);
-      plan->gexec = nullptr;
+  akm_plan::GraphEntry* ge = nullptr;
+  for (auto& g : plan->graphs)
+    if (g.exec && g.key == key) ge = &g;
+  if (!ge) {
+    ge = &plan->graphs[0];  // least recently used slot (empty slots have last_use 0)
+    for (auto& g : plan->graphs)
+      if (!g.exec || g.last_use < ge->last_use) {
+        ge = &g;
+        if (!g.exec) break;
+      }
+    if (ge->exec) {
+      cudaGraphExecDestroy(ge->exec);
+      ge->exec = nullptr;
     }
     const long long l0 = plan->launches, s0 = plan->spread_launches, i0 = plan->interp_launches;
     cudaGraph_t graph = nullptr;
@@ -814,21 +831,23 @@ static akm_status run_mvm(akm_plan* plan, const double* V, long long ldv, int r,
       return st;
     }
     AKM_CK(ec);
-    cudaError_t ei = cudaGraphInstantiate(&plan->gexec, graph, 0);
+    cudaError_t ei = cudaGraphInstantiate(&ge->exec, graph, 0);
     cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) ge->exec = nullptr;
     AKM_CK(ei);
-    plan->gkey = key;
-    plan->glaunches = plan->launches - l0;
-    plan->gspread = plan->spread_launches - s0;
-    plan->ginterp = plan->interp_launches - i0;
+    ge->key = key;
+    ge->launches = plan->launches - l0;
+    ge->spread = plan->spread_launches - s0;
+    ge->interp = plan->interp_launches - i0;
     plan->launches = l0;  // counted again below, once per replay
     plan->spread_launches = s0;
     plan->interp_launches = i0;
   }
-  AKM_CK(cudaGraphLaunch(plan->gexec, cs));
-  plan->launches += plan->glaunches;
-  plan->spread_launches += plan->gspread;
-  plan->interp_launches += plan->ginterp;
+  ge->last_use = ++plan->graph_clock;
+  AKM_CK(cudaGraphLaunch(ge->exec, cs));
+  plan->launches += ge->launches;
+  plan->spread_launches += ge->spread;
+  plan->interp_launches += ge->interp;
   if (cs != s) {
     AKM_CK(cudaEventRecord(plan->ev_out, cs));
     AKM_CK(cudaStreamWaitEvent(s, plan->ev_out, 0));
@@ -1423,15 +1442,20 @@ static akm_status objective_impl(akm_plan* plan, const double* y, const double* 
   AKM_CK(launch_kr_start(n, R, st, B, W, Q, plan->krX.as<double>(), s));
   const int T = std::max(cg_iters, lanczos_steps);
   int products = 0;
+  long long live_units = 0;  // sum over products of the columns multiplied
   for (int t = 0; t < T; ++t) {
     akm_status stt;
+    // once every Lanczos recurrence has finished (t >= lanczos_steps) only the CG column is live: the
+    // product runs at r = 1 on column 0 (the dead columns of KB keep stale values nobody reads)
+    const int rr = (t >= lanczos_steps) ? 1 : R;
     if (use_aafn) {
       stt = aafn_uinvT(plan, R, B, A.Bt.as<double>(), s);
-      if (stt == AKM_OK) stt = run_mvm(plan, A.Bt.as<double>(), R, R, A.KBt.as<double>(), nullptr, nullptr, R, s);
+      if (stt == AKM_OK) stt = run_mvm(plan, A.Bt.as<double>(), R, rr, A.KBt.as<double>(), nullptr, nullptr, R, s);
       if (stt == AKM_OK) stt = aafn_uinv(plan, R, A.KBt.as<double>(), KB, s);
     } else {
-      stt = run_mvm(plan, B, R, R, KB, nullptr, nullptr, R, s);
+      stt = run_mvm(plan, B, R, rr, KB, nullptr, nullptr, R, s);
     }
+    live_units += rr;
     if (stt != AKM_OK) return stt;
     ++products;
     AKM_CK(launch_kr_col2(n, R, B, KB, part, s));
@@ -1501,6 +1525,7 @@ static akm_status objective_impl(akm_plan* plan, const double* y, const double* 
   out->cg_iters = cg_iters;
   out->lanczos_steps = lanczos_steps;
   out->products = products;
+  out->product_columns = live_units;
   // iterations after an exactly-zero residual are not run (history -1): report the last one run
   out->cg_relres = 1.0;
   for (int t = 0; t < cg_iters; ++t)
