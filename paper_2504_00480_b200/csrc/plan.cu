@@ -96,6 +96,18 @@ struct akm_plan {
         yh;
   } aafn;
   long long theta_version = 0;
+  struct BkKey {
+    bool valid = false;
+    int family = 0, d = 0, N = 0, reg_p = 0;
+    double ell_eff = 0.0, eps_I = 0.0, eps_B = 0.0;
+    bool operator==(const BkKey& o) const {
+      return valid && o.valid && family == o.family && d == o.d && N == o.N && reg_p == o.reg_p &&
+             ell_eff == o.ell_eff && eps_I == o.eps_I && eps_B == o.eps_B;
+    }
+  };
+  std::vector<BkKey> bk_keys;  // per window: what its b_k tables were built for
+  long long bk_stride = 0;
+  DevBuf bk;
   int reg_p = 0;                            // kappa_R regularisation (akm_set_regularization; 0 = off)
   double reg_eps_I = 0.0;
   bool near_field() const { return reg_p > 0 && reg_eps_I > 0.0; }
@@ -557,36 +569,46 @@ static akm_status rebuild_tables(akm_plan* plan, cudaStream_t s) {
   }
   AKM_CK(plan->bs0.ensure(sizeof(double) * maxNd));
   AKM_CK(plan->bs1.ensure(sizeof(double) * maxNd));
-  AKM_CK(plan->bs2.ensure(sizeof(double) * maxNd));
-  AKM_CK(plan->bs3.ensure(sizeof(double) * maxNd));
-  if (plan->reg_p > 0) {
-    AKM_CK(plan->reg_coef.ensure(sizeof(double) * plan->P * 2 * kRegStride));
-    AKM_CK(cudaMemsetAsync(plan->reg_coef.p, 0, sizeof(double) * plan->P * 2 * kRegStride, s));
+  // per-window b_k tables of kappa and kappa^der, kept across set_theta calls: they depend only on
+  // (family, d, N, ell_eff, regularisation), and for Gaussian windows the scale rule keeps ell_eff
+  // fixed while ell moves (reading R2), so only the multipliers (1/c_w) are rebuilt then
+  if (plan->bk_stride != maxNd || plan->bk_keys.size() != (size_t)plan->P) {
+    AKM_CK(plan->bk.ensure(sizeof(double) * 2 * maxNd * plan->P));
+    plan->bk_stride = maxNd;
+    plan->bk_keys.assign(plan->P, akm_plan::BkKey{});
   }
+  if (plan->reg_p > 0) AKM_CK(plan->reg_coef.ensure(sizeof(double) * plan->P * 2 * kRegStride));
   for (int w = 0; w < plan->P; ++w) {
     const int d = plan->tab.w[w].d;
     const double ell_eff = plan->ell / plan->c_w[w];
-    double* bufs[2] = {plan->bs2.as<double>(), plan->bs3.as<double>()};
-    double* coef = plan->reg_p > 0 ? plan->reg_coef.as<double>() + (long long)w * 2 * kRegStride : nullptr;
-    if (coef) AKM_CK(launch_reg_coef(plan->family, ell_eff, plan->reg_eps_I, plan->eps_B, plan->reg_p, coef, s));
-    for (int deriv = 0; deriv < 2; ++deriv) {
-      double* a = plan->bs0.as<double>();
-      double* b = plan->bs1.as<double>();
-      if (coef)
-        AKM_CK(launch_kernel_samples_reg(plan->family, d, N, ell_eff, deriv, plan->reg_eps_I, plan->eps_B, plan->reg_p,
-                                         coef, a, s));
-      else
-        AKM_CK(launch_kernel_samples(plan->family, d, N, ell_eff, deriv, a, s));
-      for (int t = 0; t < d; ++t) {
-        double* out = (t == d - 1) ? bufs[deriv] : b;
-        AKM_CK(launch_cos_dft_axis(d, N, t, a, out, s));
-        std::swap(a, b);
-        if (t == d - 1) break;
-        // after the swap, `a` holds the latest result
+    double* bK = plan->bk.as<double>() + (long long)w * 2 * maxNd;
+    double* bL = bK + maxNd;
+    const akm_plan::BkKey key{true, plan->family, d, N, plan->reg_p, ell_eff, plan->reg_eps_I, plan->eps_B};
+    if (!(plan->bk_keys[w] == key)) {
+      double* bufs[2] = {bK, bL};
+      double* coef = plan->reg_p > 0 ? plan->reg_coef.as<double>() + (long long)w * 2 * kRegStride : nullptr;
+      if (coef) {
+        AKM_CK(cudaMemsetAsync(coef, 0, sizeof(double) * 2 * kRegStride, s));
+        AKM_CK(launch_reg_coef(plan->family, ell_eff, plan->reg_eps_I, plan->eps_B, plan->reg_p, coef, s));
       }
+      for (int deriv = 0; deriv < 2; ++deriv) {
+        double* a = plan->bs0.as<double>();
+        double* b = plan->bs1.as<double>();
+        if (coef)
+          AKM_CK(launch_kernel_samples_reg(plan->family, d, N, ell_eff, deriv, plan->reg_eps_I, plan->eps_B,
+                                           plan->reg_p, coef, a, s));
+        else
+          AKM_CK(launch_kernel_samples(plan->family, d, N, ell_eff, deriv, a, s));
+        for (int t = 0; t < d; ++t) {
+          double* out = (t == d - 1) ? bufs[deriv] : b;
+          AKM_CK(launch_cos_dft_axis(d, N, t, a, out, s));
+          std::swap(a, b);  // after the swap, `a` holds the latest result
+        }
+      }
+      plan->bk_keys[w] = key;
     }
-    AKM_CK(launch_multiplier(plan->tab, plan->dtab.as<WinTable>(), w, plan->bs2.as<double>(), plan->bs3.as<double>(), 3,
-                             1.0 / plan->c_w[w], plan->sigma_over, plan->D.as<double>(), s));
+    AKM_CK(launch_multiplier(plan->tab, plan->dtab.as<WinTable>(), w, bK, bL, 3, 1.0 / plan->c_w[w], plan->sigma_over,
+                             plan->D.as<double>(), s));
   }
   return AKM_OK;
 }
@@ -1186,6 +1208,7 @@ akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p,
   plan->reg_eps_I = 0.0;
   plan->aafn.lm_ready = false;
   plan->aafn.theta_built = -1;
+  plan->bk_keys.clear();
   plan->c_w.assign(P, 0.0);
   plan->c_w_binned.assign(P, -1.0);
   plan->r_cap = 0;
