@@ -226,10 +226,11 @@ cudaError_t launch_window_poly(int m, double beta, double* coef, cudaStream_t s)
 cudaError_t launch_reg_coef(int family, double ell_eff, double eps_I, double eps_B, int p, double* coef, cudaStream_t s);
 cudaError_t launch_kernel_samples_reg(int family, int d, int N, double ell_eff, int deriv, double eps_I, double eps_B,
                                       int p, const double* coef, double* out, cudaStream_t s);
-cudaError_t launch_near_field(const WinTable* dtab, const WorkItem* items, int n_items, const int* bin_start,
-                              const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
-                              int r, int ops, int slotK, int slotL, int family, double ell, double eps_I, int p,
-                              const double* coef, double* part, cudaStream_t s);
+cudaError_t launch_near_field(const WinTable* dtab, const WorkItem* items, int n_items, const int2* cell_tab,
+                              const long long* cell_off, const double* u_sorted, const int* perm, const double* V,
+                              long long ldv, double* Vs, long long n, int P, int r, int ops, int slotK, int slotL,
+                              int family, double ell, double eps_I, int p, const double* coef, double* part,
+                              cudaStream_t s);
 int near_field_launches(int r);
 
 // aafn.cu

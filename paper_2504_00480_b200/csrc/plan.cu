@@ -125,6 +125,7 @@ struct akm_plan {
   long long n_split = 0;  // rows >= n_split are class 1 (cross-product targets); n = no targets
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
   DevBuf reg_coef, bin_start;  // regularisation polynomials [w][op][kRegStride]; per-window bin start tables
+  DevBuf cell_tab, nfV;        // near field: (start, count) per (cell, class) slot; bin-sorted copy of V
   DevBuf stageV, stageY, stageL, stageS;
   DevBuf crossV, crossY;  // akm_kernel_cross_mvm: zero-padded V and the union's product
   DevBuf gX, gP, gB2, gD1, gD2, gState;  // akm_gradient_diag: block PCG and derivative products
@@ -547,6 +548,12 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
                                cudaMemcpyHostToDevice, s));
     }
   }
+  {  // (start, count) of every (cell, class) slot in the window-relative sorted order (near field)
+    std::vector<int2> ct(std::max<long long>(ncells, 1));
+    for (long long q = 0; q < ncells; ++q) ct[q] = make_int2(cell_off[q], hist[q]);
+    AKM_CK(plan->cell_tab.ensure(sizeof(int2) * ct.size()));
+    AKM_CK(cudaMemcpyAsync(plan->cell_tab.p, ct.data(), sizeof(int2) * ct.size(), cudaMemcpyHostToDevice, s));
+  }
   AKM_CK(plan->bin_start.ensure(sizeof(int) * bstart.size()));
   AKM_CK(cudaMemcpyAsync(plan->bin_start.p, bstart.data(), sizeof(int) * bstart.size(), cudaMemcpyHostToDevice, s));
   // twiddles
@@ -625,6 +632,7 @@ static akm_status ensure_rhs_workspace(akm_plan* plan, int r) {
   AKM_CK(plan->C.ensure(sizeof(double2) * std::max<long long>(plan->szC * R, 1)));
   AKM_CK(plan->C2.ensure(sizeof(double2) * std::max<long long>(plan->szC2 * R, 1)));
   AKM_CK(plan->part.ensure(sizeof(double) * std::max<long long>(plan->P * plan->n * 2 * R, 1)));
+  if (plan->near_field()) AKM_CK(plan->nfV.ensure(sizeof(double) * std::max<long long>(plan->P * plan->n * R, 1)));
   plan->r_cap = r;
   return AKM_OK;
 }
@@ -774,10 +782,10 @@ static akm_status enqueue_finish(akm_plan* plan, const double* grid, const doubl
   if (plan->near_field()) {  // kappa_R's inner part: add sum_j (kappa - T_I)(r_ij) v_j (regularize.cu)
     if (set != 0) return plan->fail(AKM_ERR_UNSUPPORTED, "the near-field correction is built for the square products only");
     const int nitems = (int)plan->items_interp_bin[0].size();
-    AKM_CK(launch_near_field(dtab, plan->items_ib[0].as<WorkItem>(), nitems, plan->bin_start.as<int>(),
-                             plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r, ops, slotK, slotL,
-                             plan->family, plan->ell, plan->reg_eps_I, plan->reg_p, plan->reg_coef.as<double>(),
-                             plan->part.as<double>(), s));
+    AKM_CK(launch_near_field(dtab, plan->items_ib[0].as<WorkItem>(), nitems, plan->cell_tab.as<int2>(),
+                             plan->hist_off.as<long long>(), plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv,
+                             plan->nfV.as<double>(), n, plan->P, r, ops, slotK, slotL, plan->family, plan->ell,
+                             plan->reg_eps_I, plan->reg_p, plan->reg_coef.as<double>(), plan->part.as<double>(), s));
     if (nitems > 0) plan->launches += near_field_launches(r);
   }
   if (ev) AKM_CK(cudaEventRecord(ev->e[3], s));
@@ -1870,6 +1878,7 @@ akm_status akm_set_regularization(akm_plan* plan, double eps_I, int32_t p) {
   plan->reg_p = p;
   plan->reg_eps_I = p > 0 ? eps_I : 0.0;
   plan->have_theta = false;
+  plan->r_cap = 0;  // the near-field workspace is sized in ensure_rhs_workspace (never inside a graph capture)
   return AKM_OK;
 }
 

@@ -17,6 +17,8 @@
 // kappa^der (the ell-derivative kernel, eq. 2.3) is regularised the same way.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "akm_internal.cuh"
 
 namespace akm {
@@ -200,28 +202,54 @@ cudaError_t launch_kernel_samples_reg(int family, int d, int N, double ell_eff, 
 }
 
 // ------------------------------------------------------------------ near-field correction
-// One CTA per interpolation item (<= 128 target points of one bin); the source points of every bin
-// within ceil(eps_I n_g / B) bins are staged through shared memory in tiles of kNfTile (scaled grid
-// coordinates and the rc RHS values of their user rows); each thread accumulates, for its target,
-// sum_{r_ij < eps_I} (kappa - T_I)(r_ij) v_j for kappa (slot K) and kappa^der / c_w (slot L) and adds it to
-// the window's partial output (written by the interpolation before, read by the epilogue after).
+// One CTA per interpolation item (<= 128 target points of one bin).  Warp 0 lists, in a fixed order,
+// the (cell, class) point ranges of every grid cell whose box comes closer than eps_I to the bin's box
+// (ballot compaction over the candidate cells); the CTA then streams those source points through
+// shared memory in tiles of kNfTile (scaled coordinates and the rc values of their rows of the
+// bin-sorted copy of V, so every tile load is contiguous).  Each thread accumulates, for its target,
+// sum_{r_ij < eps_I} (kappa - T_I)(r_ij) v_j for kappa (slot K) and kappa^der / c_w (slot L) and adds it
+// to the window's partial output (written by the interpolation before, read by the epilogue after).
 constexpr int kNfThreads = 128;
 constexpr int kNfTile = 128;
 constexpr int kNfMaxRc = 12;
 
+__global__ void k_sort_v(long long n, int P, int r, const int* __restrict__ perm, const double* __restrict__ V,
+                         long long ldv, double* __restrict__ Vs) {
+  const long long total = (long long)P * n * r;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long wp = idx / r;
+    const int c = (int)(idx - wp * r);
+    Vs[idx] = V[(long long)perm[wp] * ldv + c];
+  }
+}
+
+// Warp-independent: each warp owns 32 consecutive targets of its CTA's item, lists the candidate
+// cell ranges itself and streams the candidates through a warp-private slice of shared memory
+// (__syncwarp only: no CTA barrier, a warp with no targets left is done).
+constexpr int kNfWarps = kNfThreads / 32;
+constexpr int kNfWarpRanges = 256;
 __global__ void __launch_bounds__(kNfThreads) k_near_field(
-    const WinTable* __restrict__ tabp, const WorkItem* __restrict__ items, const int* __restrict__ bin_start,
-    const double* __restrict__ u_sorted, const int* __restrict__ perm, const double* __restrict__ V, long long ldv,
-    long long n, int r0, int rc, int r_total, int ops, int slotK, int slotL, int family, double ell, double eps_I,
-    int p, const double* __restrict__ coef, double* __restrict__ part) {
-  __shared__ double su[3][kNfTile];
-  __shared__ double sv[kNfTile * kNfMaxRc];
-  const WinTable& tab = *tabp;
+    const WinTable* __restrict__ tabp, const WorkItem* __restrict__ items, const int2* __restrict__ cell_tab,
+    const long long* __restrict__ cell_off, const double* __restrict__ u_sorted, const int* __restrict__ perm,
+    const double* __restrict__ Vs, long long n, int r0, int rc, int r_total, int ops, int slotK, int slotL, int family,
+    double ell, double eps_I, int p, const double* __restrict__ coef, double* __restrict__ part) {
+  __shared__ double su_all[kNfWarps][3][32];
+  __shared__ double sv_all[kNfWarps][32 * kNfMaxRc];
+  __shared__ int rstart_all[kNfWarps][kNfWarpRanges], rpre_all[kNfWarps][kNfWarpRanges + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const WorkItem it = items[blockIdx.x];
+  if (wid * 32 >= it.count) return;
+  double (*su)[32] = su_all[wid];
+  double* sv = sv_all[wid];
+  int* rstart = rstart_all[wid];
+  int* rpre = rpre_all[wid];
+  const WinTable& tab = *tabp;
   const WinGeom& g = tab.w[it.win];
   const int w = it.win;
   const double* uw = u_sorted + (long long)w * 3 * n;
   const int* pw = perm + (long long)w * n;
+  const double* vw = Vs + (long long)w * n * r_total + r0;
   const double inv_ng = 1.0 / (double)tab.n_g;
   const double ell_eff = ell * g.scale * inv_ng;  // ell / c_w
   const double inv_c = g.scale * inv_ng;
@@ -230,57 +258,104 @@ __global__ void __launch_bounds__(kNfThreads) k_near_field(
   const double inv_eps2 = 1.0 / (eps_I * eps_I);
   const double* aK = coef + (long long)w * 2 * kRegStride;
   const double* aL = aK + kRegStride;
-  const int tid = threadIdx.x;
-  const bool active = tid < it.count;
-  const int pos = it.start + (active ? tid : 0);
+  const bool active = wid * 32 + lane < it.count;
+  const int pos = it.start + (active ? wid * 32 + lane : 0);
   double ut[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) ut[a] = (a >= 3 - g.d) ? uw[(long long)a * n + pos] : 0.0;
   double accK[kNfMaxRc], accL[kNfMaxRc];
 #pragma unroll
   for (int c = 0; c < kNfMaxRc; ++c) accK[c] = accL[c] = 0.0;
-  const int K = (int)ceil(E / (double)g.B);
-  int lo[3], hi[3];
-#pragma unroll
+  // candidate cells: the box of cells within ceil(E) of the bin, enumerated in a fixed order
+  const int Ke = (int)ceil(E);
+  int lo[3], ext[3], blo[3], bhi[3];
   for (int a = 0; a < 3; ++a) {
-    lo[a] = max(0, it.bin[a] - ((a >= 3 - g.d) ? K : 0));
-    hi[a] = min(g.nbin[a] - 1, it.bin[a] + ((a >= 3 - g.d) ? K : 0));
+    const bool real = a >= 3 - g.d;
+    blo[a] = real ? it.bin[a] * g.B : 0;
+    bhi[a] = real ? min(blo[a] + g.B, g.ncell[a]) - 1 : 0;
+    lo[a] = real ? max(0, blo[a] - Ke) : 0;
+    const int hi = real ? min(g.ncell[a] - 1, bhi[a] + Ke) : 0;
+    ext[a] = hi - lo[a] + 1;
   }
-  const int* bs = bin_start + g.bt_off;
-  for (int b0 = lo[0]; b0 <= hi[0]; ++b0)
-    for (int b1 = lo[1]; b1 <= hi[1]; ++b1)
-      for (int b2 = lo[2]; b2 <= hi[2]; ++b2) {
-        const int bi = (b0 * g.nbin[1] + b1) * g.nbin[2] + b2;
-        const int s0 = bs[bi], s1 = bs[bi + 1];
-        for (int t0 = s0; t0 < s1; t0 += kNfTile) {
-          const int cnt = min(kNfTile, s1 - t0);
-          __syncthreads();
-          for (int j = tid; j < cnt; j += kNfThreads) {
+  const int total = ext[0] * ext[1] * ext[2];
+  for (int q0 = 0; q0 < total;) {
+    // the (start, count) ranges of the next cells closer than eps_I to the bin (ballot compaction)
+    int count = 0, acc = 0, q = q0;
+    for (; q < total && count <= kNfWarpRanges - 64; q += 32) {
+      const int qq = q + lane;
+      int cnt[2] = {0, 0}, cs[2] = {0, 0};
+      bool near = false;
+      if (qq < total) {
+        const int cc[3] = {lo[0] + qq / (ext[1] * ext[2]), lo[1] + (qq / ext[2]) % ext[1], lo[2] + qq % ext[2]};
+        double gap2 = 0.0;
+        for (int a = 0; a < 3; ++a) {
+          const double gp = fmax(0.0, fmax((double)(blo[a] - (cc[a] + 1)), (double)(cc[a] - (bhi[a] + 1))));
+          gap2 += gp * gp;
+        }
+        near = gap2 < E2;
+        if (near) {
+          const long long slot = cell_off[w] + 2 * (((long long)cc[0] * g.ncell[1] + cc[1]) * g.ncell[2] + cc[2]);
+          const int2 a0 = cell_tab[slot], a1 = cell_tab[slot + 1];
+          cs[0] = a0.x; cnt[0] = a0.y; cs[1] = a1.x; cnt[1] = a1.y;
+        }
+      }
+      for (int cls = 0; cls < 2; ++cls) {
+        const bool has = near && cnt[cls] > 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        const int before = __popc(bal & ((1u << lane) - 1u));
+        int v = has ? cnt[cls] : 0;  // inclusive running sum of the counts in lane order
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += u;
+        }
+        if (has) {
+          rstart[count + before] = cs[cls];
+          rpre[count + before + 1] = acc + v;
+        }
+        count += __popc(bal);
+        acc += __shfl_sync(0xffffffffu, v, 31);
+      }
+    }
+    if (lane == 0) rpre[0] = 0;
+    __syncwarp();
+    q0 = q;
+    const int nr = count, ncand = acc;
+    for (int f0 = 0; f0 < ncand; f0 += 32) {
+      const int cnt = min(32, ncand - f0);
+      if (lane < cnt) {
+        const int f = f0 + lane;
+        int a = 0, b = nr - 1;  // range with rpre[a] <= f < rpre[a + 1]
+        while (a < b) {
+          const int mid = (a + b + 1) >> 1;
+          if (rpre[mid] <= f) a = mid; else b = mid - 1;
+        }
+        const int sp = rstart[a] + (f - rpre[a]);
 #pragma unroll
-            for (int a = 0; a < 3; ++a) su[a][j] = (a >= 3 - g.d) ? uw[(long long)a * n + t0 + j] : 0.0;
-            const long long row = pw[t0 + j];
-            for (int c = 0; c < rc; ++c) sv[j * kNfMaxRc + c] = V[row * ldv + r0 + c];
-          }
-          __syncthreads();
-          if (!active) continue;
-          for (int j = 0; j < cnt; ++j) {
-            const double d0 = ut[0] - su[0][j], d1 = ut[1] - su[1][j], d2 = ut[2] - su[2][j];
-            const double q2 = d0 * d0 + d1 * d1 + d2 * d2;
-            if (q2 >= E2) continue;
-            const double r = sqrt(q2) * inv_ng;
-            const double s2 = r * r * inv_eps2;
-            const double wK = kernel_plain(family, 0, ell_eff, r) - reg_inner(aK, p, s2);
-            const double wL = (slotL >= 0) ? (kernel_plain(family, 1, ell_eff, r) - reg_inner(aL, p, s2)) * inv_c : 0.0;
+        for (int t = 0; t < 3; ++t) su[t][lane] = (t >= 3 - g.d) ? uw[(long long)t * n + sp] : 0.0;
+        for (int c = 0; c < rc; ++c) sv[lane * kNfMaxRc + c] = vw[(long long)sp * r_total + c];
+      }
+      __syncwarp();
+      if (active) {
+        for (int j = 0; j < cnt; ++j) {
+          const double d0 = ut[0] - su[0][j], d1 = ut[1] - su[1][j], d2 = ut[2] - su[2][j];
+          const double q2 = d0 * d0 + d1 * d1 + d2 * d2;
+          if (q2 >= E2) continue;
+          const double r = sqrt(q2) * inv_ng;
+          const double s2 = r * r * inv_eps2;
+          const double wK = kernel_plain(family, 0, ell_eff, r) - reg_inner(aK, p, s2);
+          const double wL = (slotL >= 0) ? (kernel_plain(family, 1, ell_eff, r) - reg_inner(aL, p, s2)) * inv_c : 0.0;
 #pragma unroll
-            for (int c = 0; c < kNfMaxRc; ++c) {
-              if (c < rc) {
-                accK[c] = fma(wK, sv[j * kNfMaxRc + c], accK[c]);
-                accL[c] = fma(wL, sv[j * kNfMaxRc + c], accL[c]);
-              }
+          for (int c = 0; c < kNfMaxRc; ++c) {
+            if (c < rc) {
+              accK[c] = fma(wK, sv[j * kNfMaxRc + c], accK[c]);
+              accL[c] = fma(wL, sv[j * kNfMaxRc + c], accL[c]);
             }
           }
         }
       }
+      __syncwarp();
+    }
+  }
   if (!active) return;
   const long long i = pw[pos];
   double* out = part + (((long long)w * n + i) * ops) * r_total + r0;
@@ -293,14 +368,20 @@ __global__ void __launch_bounds__(kNfThreads) k_near_field(
   }
 }
 
-cudaError_t launch_near_field(const WinTable* dtab, const WorkItem* items, int n_items, const int* bin_start,
-                              const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
-                              int r, int ops, int slotK, int slotL, int family, double ell, double eps_I, int p,
-                              const double* coef, double* part, cudaStream_t s) {
+cudaError_t launch_near_field(const WinTable* dtab, const WorkItem* items, int n_items, const int2* cell_tab,
+                              const long long* cell_off, const double* u_sorted, const int* perm, const double* V,
+                              long long ldv, double* Vs, long long n, int P, int r, int ops, int slotK, int slotL,
+                              int family, double ell, double eps_I, int p, const double* coef, double* part,
+                              cudaStream_t s) {
   if (n_items <= 0) return cudaSuccess;
+  {
+    const long long total = (long long)P * n * r;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 32);
+    k_sort_v<<<blocks, 256, 0, s>>>(n, P, r, perm, V, ldv, Vs);
+  }
   for (int r0 = 0; r0 < r; r0 += kNfMaxRc) {
     const int rc = (r - r0 < kNfMaxRc) ? r - r0 : kNfMaxRc;
-    k_near_field<<<n_items, kNfThreads, 0, s>>>(dtab, items, bin_start, u_sorted, perm, V, ldv, n, r0, rc, r, ops,
+    k_near_field<<<n_items, kNfThreads, 0, s>>>(dtab, items, cell_tab, cell_off, u_sorted, perm, Vs, n, r0, rc, r, ops,
                                                 slotK, slotL, family, ell, eps_I, p, coef, part);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -308,6 +389,6 @@ cudaError_t launch_near_field(const WinTable* dtab, const WorkItem* items, int n
   return cudaSuccess;
 }
 
-int near_field_launches(int r) { return (r + kNfMaxRc - 1) / kNfMaxRc; }
+int near_field_launches(int r) { return 1 + (r + kNfMaxRc - 1) / kNfMaxRc; }
 
 }  // namespace akm

@@ -89,15 +89,17 @@ def test_matern_3d_at_N32_meets_the_gate(akm):
         assert rel(reg[op], de[op]) <= 0.2 * rel(plain[op], de[op])
 
 
-def test_c3_full_size_per_column(akm):
+@pytest.mark.parametrize("eps_cells,p", [(2, 4), (1, 2)])
+def test_c3_full_size_per_column(akm, eps_cells, p):
     """c3 (n = 1e5, four 2-D Matern windows, N = 128, r = 11) at full size, 2048 seeded rows: with
-    kappa_R (eps_I = 2/N, p = 4) every column -- including the Rademacher probes whose plain-method
-    error reaches ~2e-3 -- is within 1e-3 of the dense sums."""
+    kappa_R (eps_I = 2/N, p = 4, and bench.py's c3r setting eps_I = 1/N, p = 2) every column --
+    including the Rademacher probes whose plain-method error reaches ~2e-3 -- is within 1e-3 of the
+    dense sums."""
     wl = workloads.CONFIGS["c3"]
     X = workloads.make_X(wl)
     V = workloads.make_V(wl)
     th = (wl.sigma_f, wl.ell, wl.sigma_eps)
-    out, _ = run(akm, X, wl.windows, wl.family, th, V, wl.N, wl.m, 2.0 / wl.N, 4, ops=("K",))
+    out, _ = run(akm, X, wl.windows, wl.family, th, V, wl.N, wl.m, eps_cells / wl.N, p, ops=("K",))
     rows = workloads.make_rows(wl, 2048)
     de = dense_apply(X, wl.windows, wl.family, th, V, rows=rows, ops=("K",))["K"]
     col = np.linalg.norm(out["K"][rows] - de, axis=0) / np.linalg.norm(de, axis=0)

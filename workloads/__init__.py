@@ -96,12 +96,13 @@ CONFIGS = {
                     "on the split-preconditioned operator, n=5e5 p=9, 3 Gaussian windows, r=11",
                     extra={"cg_iters": 50, "lanczos_steps": 30, "n_z": 10, "aafn_kpw": 800}),
     # SURVEY.md 8(f) f4 (not a BASELINE.json config): c3 with the boundary-regularised kappa_R
-    # (inner eps_I = 2/N, p = 4, near-field correction; outer eps_B)
+    # (inner eps_I = 1/N, p = 2, near-field correction; outer eps_B): per-column error ~2e-4 at 1/4 of
+    # the near-field pairs of eps_I = 2/N (tests/test_gpu_regularized.py checks both)
     "c3r": Workload("c3r", 3, 100000, 8, _consecutive(0, 2, 4), MATERN12, 1.0, 1.0, 0.1, 11, 128, 2.0, 8, 1.0 / 16,
                     ("K",), "uniform", "normal_plus_rademacher",
-                    "c3 with kappa_R (eps_I = 2/N, p = 4, near-field correction): n=1e5, 4 Matern(1/2) windows of 2, "
+                    "c3 with kappa_R (eps_I = 1/N, p = 2, near-field correction): n=1e5, 4 Matern(1/2) windows of 2, "
                     "r=11, N=128, m=8",
-                    extra={"reg_eps_I": 2.0 / 128, "reg_p": 4}),
+                    extra={"reg_eps_I": 1.0 / 128, "reg_p": 2}),
     # SURVEY.md 8(f) f1 (not a BASELINE.json config): one gradient of Z~ at c5's sizes -- 50 block
     # PCG iterations on [y | Z] (r = 11) and one fused derivative product (dKhat/dell, dKhat/dsigma_f)
     "g5": Workload("g5", 5, 500000, 9, _consecutive(0, 3, 3), GAUSSIAN, 1.0, 0.5, 0.05, 11, 32, 2.0, 6, 1.0 / 16,
