@@ -281,6 +281,7 @@ def main():
     n_src = wl.extra.get("n_src", wl.n)
     objective = "cg_iters" in wl.extra          # c5: one Z~ evaluation per step (S8)
     gradient = "grad_cg_iters" in wl.extra      # g5: one gradient of Z~ per step (f1)
+    probe_sharded = world > 1 and objective     # c5 / c5a: probe columns over the ranks (§8(e) item 2)
     # N > 1: the square products are point-sharded (each rank owns a row block of the SAME problem,
     # one grid all-reduce per product: strong scaling); the Krylov drivers and the cross
     # product run as independent replicas (weak scaling)
@@ -291,7 +292,8 @@ def main():
         Xd = torch.from_numpy(np.ascontiguousarray(X[row0:row1])).to(dev)
     else:
         row0, row1 = 0, wl.n
-        V = workloads.make_V(wl, n=n_src, seed=D.rank_seed(2000 + wl.index, rank))  # independent RHS block per rank
+        # independent RHS block per rank (replicas); the probe-sharded objective shares one problem
+        V = workloads.make_V(wl, n=n_src, seed=None if probe_sharded else D.rank_seed(2000 + wl.index, rank))
         Xd = torch.from_numpy(X).to(dev)
     V = np.ascontiguousarray(V)
     Vd = torch.from_numpy(V).to(dev)
@@ -322,7 +324,15 @@ def main():
         products_per_step = max(cg, lz)
         last = {}
 
-        if "aafn_kpw" in wl.extra:
+        if probe_sharded:
+            def step():   # every rank: the whole problem, a slice of the probes (rank 0 also CG)
+                if "aafn_kpw" in wl.extra:
+                    plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+                res = D.sharded_objective(plan, yd, Zd, cg, lz, preconditioned="aafn_kpw" in wl.extra)
+                loc = res["local"] or {}
+                last["out"] = {**loc, "Z": res["Z"], "quad": res["quad"], "slq": res["slq"],
+                               "product_columns": loc.get("product_columns", 0)}
+        elif "aafn_kpw" in wl.extra:
             def step():   # theta -> AAFN factors -> Z~ (the factors depend on theta: rebuilt every step)
                 plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
                 last["out"] = plan.objective(yd, Zd, cg, lz)
@@ -358,7 +368,12 @@ def main():
         step()
     torch.cuda.synchronize(dev)
     if objective:   # after the Lanczos steps only the CG column is multiplied: count live columns only
-        products_per_step = last["out"]["product_columns"] / wl.r
+        cols = float(last["out"]["product_columns"])
+        if probe_sharded:   # the whole job's columns (every rank's slice)
+            tcols = torch.tensor([cols], dtype=torch.float64, device=dev)
+            dist.all_reduce(tcols)
+            cols = float(tcols.item())
+        products_per_step = cols / wl.r
 
     K = args.steps
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
@@ -383,7 +398,7 @@ def main():
     launches_timed = plan.stage_times(reset=True)["kernel_launches"]
     total_ms = D.max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(starts, ends)), dev)
     ms_per_step = total_ms / K
-    if sharded:
+    if sharded or probe_sharded:
         value = D.strong_throughput(wl.units * products_per_step, ms_per_step)
     else:
         value = D.weak_throughput(wl.units * products_per_step, world, ms_per_step)
@@ -407,7 +422,11 @@ def main():
         yh, Zh = Vh[:, 0].contiguous().pin_memory(), Vh[:, 1:].contiguous().pin_memory()
 
     def e2e_step():
-        if objective and "aafn_kpw" in wl.extra:
+        if probe_sharded:
+            if "aafn_kpw" in wl.extra:
+                plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+            D.sharded_objective(plan, yh, Zh, cg, lz, preconditioned="aafn_kpw" in wl.extra)
+        elif objective and "aafn_kpw" in wl.extra:
             plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
             plan.objective(yh, Zh, cg, lz, stream=stream.cuda_stream)
         elif objective:   # host y, Z in; the objective's terms come back to the host
@@ -438,7 +457,7 @@ def main():
         e_e[i].record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = D.max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(e_s, e_e)), dev)
-    if sharded:
+    if sharded or probe_sharded:
         e2e_value = D.strong_throughput(wl.units * products_per_step, e2e_ms / K)
     else:
         e2e_value = D.weak_throughput(wl.units * products_per_step, world, e2e_ms / K)
@@ -485,10 +504,11 @@ def main():
         "metric": _metric(wl),
         "value": value, "unit": "pts/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "scaling": "strong" if (sharded or probe_sharded) else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": config_dict(wl, f"point-sharded rows x{world} (one grid all-reduce per product)" if sharded else
-                              f"independent replicas x{world}" if world > 1 else "1 GPU"),
+                              f"probe columns sharded x{world} (one scalar all-reduce per evaluation)" if probe_sharded
+                              else f"independent replicas x{world}" if world > 1 else "1 GPU"),
         "e2e": {"value": e2e_value, "unit": "pts/s", "h2d_bytes_per_step": int(V.nbytes),
                 "d2h_bytes_per_step": int(8 * (10 + 2 * wl.r) if objective else 8 * (3 + gcg) if gradient else
                                           sum(o.numel() * 8 for o in Oh.values()))},

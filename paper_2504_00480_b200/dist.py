@@ -13,6 +13,10 @@ process per GPU) holds a disjoint row block of X and V; it
      B200 node), then runs the small DFT / multiply / inverse DFT redundantly and interpolates at its
      own points (``akm_mvm_from_grid``).  No other exchange: the outputs stay row-sharded.
 
+**Probe (column) sharding** (``sharded_objective``, §8(e) item 2).  The CG column and every Lanczos
+probe of the objective are independent recurrences: each rank holds the whole problem and runs a
+slice of the probes (rank 0 also the CG column); one all-reduce of three scalars combines them.
+
 Every step of the arithmetic runs in the library's kernels; this module only orders the calls and
 issues the collectives (torch.distributed: ``nccl`` on GPUs, ``gloo`` in the CPU tests, where a
 test backend stands in for the library).
@@ -22,6 +26,7 @@ seeds, the max-over-ranks timing and the whole-job throughput).
 """
 from __future__ import annotations
 
+import math
 import os
 
 import numpy as np
@@ -146,3 +151,46 @@ class ShardedPlan:
         close = getattr(self.backend, "close", None)
         if close:
             close()
+
+
+def sharded_objective(plan, y, Z, cg_iters=50, lanczos_steps=30, comm_device=None, preconditioned=False):
+    """Z~ (eq. 1.4) with the probe columns sharded over the ranks (the CG column
+    and every Lanczos probe are independent recurrences, so no exchange is needed until the scalars).
+
+    Every rank holds the whole problem (all n points) in ``plan``; the n_z probe columns of ``Z`` are
+    split by ``column_partition``.  Rank 0 runs CG on y together with its probes; the other ranks run
+    their probes with y = 0 (the library's CG column is then inactive) and no CG iterations.  One
+    all-reduce of [y^T x, sum of SLQ samples, probe count] combines them:
+        Z~ = 1/2 (y^T x + log det M + (1/n_z) sum_i samples_i + n log 2 pi).
+    ``preconditioned`` uses ``plan.objective`` (the plan's preconditioner, e.g. AAFN) instead of
+    ``plan.objective_diag``.  Returns the terms as a dict (like ``Plan.objective_diag``)."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    n_z = Z.shape[1]
+    c0, c1 = column_partition(n_z, world, rank)
+    fn = plan.objective if preconditioned else plan.objective_diag
+    quad, ssum, cnt, out = 0.0, 0.0, 0, None
+    if c1 > c0:
+        Zk = Z[:, c0:c1]
+        Zk = Zk.contiguous() if hasattr(Zk, "contiguous") else np.ascontiguousarray(Zk)
+        if rank == 0:
+            out = fn(y, Zk, cg_iters, lanczos_steps)
+            quad = out["quad"]
+        else:
+            y0 = torch.zeros_like(y) if hasattr(y, "new_zeros") else np.zeros_like(y)
+            out = fn(y0, Zk, 0, lanczos_steps)
+        ssum, cnt = float(sum(out["samples"])), c1 - c0
+    dev = comm_device if comm_device is not None else (
+        torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu"))
+    t = torch.tensor([quad, ssum, float(cnt)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t)
+    quad, ssum, cnt = (float(v) for v in t.cpu())
+    n = y.shape[0]
+    logdet = torch.tensor([out["logdetM"] if (out is not None and rank == 0) else 0.0], dtype=torch.float64, device=dev)
+    dist.broadcast(logdet, src=0)
+    logdet = float(logdet.item())
+    slq = ssum / cnt
+    res = {"Z": 0.5 * (quad + logdet + slq + n * math.log(2.0 * math.pi)), "quad": quad, "logdetM": logdet,
+           "slq": slq, "probes": int(cnt), "local": out, "columns": (c0, c1)}
+    return res

@@ -236,3 +236,64 @@ def test_row_partition():
             parts = [D.row_partition(n, world, k) for k in range(world)]
             assert parts[0][0] == 0 and parts[-1][1] == n and all(b > a for a, b in parts)
     assert D.strong_throughput(1e6, 2.0) == pytest.approx(5e8)
+
+
+# ---------------------------------------------------------------- probe-sharded objective (§8(e) item 2)
+class OracleObjectivePlan:
+    """Test stand-in for Plan.objective_diag: the oracle's CG + Lanczos driver on the dense K^."""
+
+    def __init__(self, X, windows, family, theta):
+        from oracle import aafn as A
+        self.K = A.khat_dense(X, windows, family, theta)
+        sf, _, se = theta
+        self.c = sf * sf * len(windows) + se * se
+
+    def objective_diag(self, y, Z, cg_iters, lanczos_steps):
+        from oracle import krylov as KR
+        o = KR.objective_diag(lambda B: self.K @ B, y.numpy(), Z.numpy(), self.c, cg_iters, lanczos_steps)
+        return {"quad": o["quad"], "samples": o["samples"], "logdetM": o["logdetM"], "Z": o["Z"]}
+
+
+def _obj_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wl = workloads.CONFIGS["c5"]
+        n = 600
+        X = workloads.make_X(wl, n=n)
+        V = workloads.make_V(wl, n=n, r=8)
+        plan = OracleObjectivePlan(X, wl.windows, wl.family, (1.0, 0.3, 0.3))
+        res = D.sharded_objective(plan, torch.from_numpy(V[:, 0].copy()), torch.from_numpy(V[:, 1:].copy()), 40, 12)
+        q.put((rank, res["Z"], res["quad"], res["slq"], res["probes"], res["columns"]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_probe_sharded_objective(world):
+    """The probe-sharded objective equals the single-process objective with all probes: the CG term
+    from rank 0, the SLQ samples of every rank averaged over all n_z probes."""
+    from oracle import aafn as A
+    from oracle import krylov as KR
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_obj_worker, args=(k, world, port, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    wl = workloads.CONFIGS["c5"]
+    X = workloads.make_X(wl, n=600)
+    V = workloads.make_V(wl, n=600, r=8)
+    K = A.khat_dense(X, wl.windows, wl.family, (1.0, 0.3, 0.3))
+    ref = KR.objective_diag(lambda B: K @ B, V[:, 0], V[:, 1:], 1.0**2 * 3 + 0.3**2, 40, 12)  # M = (sf^2 P + se^2) I
+    for _, Zt, quad, slq, probes, cols in res:
+        assert probes == 7
+        assert Zt == pytest.approx(ref["Z"], rel=1e-10)
+        assert quad == pytest.approx(ref["quad"], rel=1e-10)
+        assert slq == pytest.approx(ref["slq"], rel=1e-10)
+    assert [r[5] for r in res] == [D.column_partition(7, world, k) for k in range(world)]

@@ -186,3 +186,55 @@ def test_sharded_plan_gloo_world2(akm):
     assert rel(Y, single["K"]) <= 1e-12 and rel(dY, single["dell"]) <= 1e-12
     de = dense_apply(X, wl.windows, wl.family, (wl.sigma_f, wl.ell, wl.sigma_eps), V, ops=("K", "dell"))
     assert rel(Y, de["K"]) <= 1e-6 and rel(dY, de["dell"]) <= 1e-6
+
+
+def _obj_gloo_worker(rank, world, port, q, kpw):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2504_00480_b200 as akm
+        from paper_2504_00480_b200 import dist as D
+        wl = workloads.CONFIGS["c5"]
+        n = 20000
+        X = workloads.make_X(wl, n=n)
+        V = workloads.make_V(wl, n=n)
+        dev = torch.device("cuda:0")
+        plan = akm.Plan(0)
+        plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+        if kpw:
+            plan.set_preconditioner(kpw)
+        plan.set_theta(0.5, 0.5, 1.0)   # CG converges in 50 iterations here (tests/test_gpu_objective.py)
+        y = torch.from_numpy(np.ascontiguousarray(V[:, 0])).to(dev)
+        Z = torch.from_numpy(np.ascontiguousarray(V[:, 1:])).to(dev)
+        res = D.sharded_objective(plan, y, Z, 50, 30, comm_device=torch.device("cpu"), preconditioned=bool(kpw))
+        single = (plan.objective if kpw else plan.objective_diag)(y, Z, 50, 30)
+        plan.close()
+        q.put((rank, res["Z"], res["quad"], res["slq"], single["Z"], single["quad"], single["slq"]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kpw", [0, 60])
+def test_probe_sharded_objective_gloo_world2(akm, kpw):
+    """SURVEY.md §8(e) item 2: each rank runs a slice of the probes (rank 0 also CG) through the library;
+    the combined Z~ equals the single-process Z~ (theta where 50 CG iterations converge: the two runs
+    multiply differently sized blocks, so their products differ by rounding only)."""
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_obj_gloo_worker, args=(k, world, port, q, kpw)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, Zs, quad, slq, Z1, quad1, slq1 in res:
+        assert Zs == pytest.approx(Z1, rel=1e-9)
+        assert quad == pytest.approx(quad1, rel=1e-8)
+        assert slq == pytest.approx(slq1, rel=1e-8)
