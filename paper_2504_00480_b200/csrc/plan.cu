@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/akm.h"
 #include "akm_internal.cuh"
 
@@ -216,6 +218,12 @@ struct akm_plan {
   }
 };
 
+// NVTX ranges per stage: visible in Nsight Systems / ncu --nvtx; header-only NVTX3
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 #define AKM_CK(call)                                                                              \
   do {                                                                                            \
     cudaError_t e_ = (call);                                                                      \
@@ -264,6 +272,7 @@ cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, 
 // Build per-window boxes for the current c_w, histogram the points per cell on the device,
 // choose the bin edge B per window from the histogram, lay the cells out bin-major, scatter.
 static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
+  NvtxRange nvtx("akm S0 bin sort");
   ++plan->epoch;
   const int P = plan->P, m = plan->m, n_g = plan->n_g;
   const long long n = plan->n;
@@ -567,6 +576,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
 
 // b_k of eq. (3.2) for kappa and kappa^der at ell_eff, then the multiplier tables.
 static akm_status rebuild_tables(akm_plan* plan, cudaStream_t s) {
+  NvtxRange nvtx("akm S1 b_k + multipliers");
   const int N = plan->N;
   long long maxNd = 1;
   for (int w = 0; w < plan->P; ++w) {
@@ -672,6 +682,7 @@ static bool choose_spread_tile(int M, int Nn, int& MT, int& NT, int& threads) {
 // akm_mvm_from_grid) sums the ranks' grids in between.
 static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv, int r, double* grid, cudaStream_t s,
                                  int set) {
+  NvtxRange nvtx("akm S2 spread");
   const long long n = plan->n;
   const WinTable* dtab = plan->dtab.as<WinTable>();
   AKM_CK(launch_zero(grid, plan->total_taps * r, s));
@@ -726,6 +737,7 @@ static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv,
 static akm_status enqueue_finish(akm_plan* plan, const double* grid, const double* V, long long ldv, int r, double* Y,
                                  double* dYl, double* dYsf, long long ldy, cudaStream_t s, int set,
                                  akm_plan::EvSet* ev) {
+  NvtxRange nvtx("akm S3-S7 DFT, multiply, interpolate, epilogue");
   const bool needK = (Y != nullptr) || (dYsf != nullptr);
   const bool needL = dYl != nullptr;
   const int ops = (needK ? 1 : 0) + (needL ? 1 : 0);
@@ -993,6 +1005,7 @@ static akm_status aafn_landmarks(akm_plan* plan, cudaStream_t s) {
 // Factors for the current theta: L11 (Cholesky of the landmark block, one jitter retry as in SPEC's
 // DESIGN DECISIONS), L11^{-1}, Phi = K21 L11^{-T}, G = diag(S_aa^{-1/2}), log det M.
 static akm_status aafn_build(akm_plan* plan, int R, cudaStream_t s) {
+  NvtxRange nvtx("akm AAFN build");
   auto& A = plan->aafn;
   if (!A.lm_ready) {
     akm_status st = aafn_landmarks(plan, s);
@@ -1396,6 +1409,7 @@ static akm_status objective_impl(akm_plan* plan, const double* y, const double* 
                                  int32_t cg_iters, int32_t lanczos_steps, akm_objective_out* out, double* cg_relres,
                                  void* stream, bool use_aafn) {
   if (!plan) return AKM_ERR_INVALID_ARG;
+  NvtxRange nvtx("akm S8 objective");
   plan->err.clear();
   if (!plan->have_points || !plan->have_theta)
     return plan->fail(AKM_ERR_STATE, "objective_diag called before set_points and set_theta");
