@@ -313,6 +313,15 @@ akm_status akm_objective(akm_plan* plan, const double* y, const double* Z, int64
 akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
                              int32_t cg_iters, double* grad, double* cg_relres, void* stream);
 
+/* akm_gradient_diag with the plan's preconditioner (akm_set_preconditioner).  With AAFN the block CG
+ * runs on S_op = U^{-1} Khat U^{-T} from U^{-1} [y | Z] and the solutions are mapped back by U^{-T};
+ * eq. (div)'s control-variate term needs dM/dtheta, which AAFN does not define, so
+ * the plain Hutchinson form is returned (reading R15):
+ *   grad[k] = 1/2 ( -alpha^T dKhat_k alpha + (1/n_z) sum_i (Khat^{-1} z_i)^T dKhat_k z_i ).
+ * cg_relres then holds the preconditioned system's residuals.  Same arguments as akm_gradient_diag. */
+akm_status akm_gradient(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z, int32_t cg_iters,
+                        double* grad, double* cg_relres, void* stream);
+
 const char* akm_version(void);
 
 #ifdef __cplusplus

@@ -156,3 +156,26 @@ def objective_aafn(apply_K, y, Z, pre, cg_iters, lanczos_steps):
     out["x"] = x
     out["cg_relres_true"] = float(np.linalg.norm(y - apply_K(x[:, None])[:, 0]) / np.linalg.norm(y))
     return out
+
+
+def gradient_aafn(apply_K, apply_dK, y, Z, pre, cg_iters):
+    """Gradient of Z~ with AAFN solves (SPEC krylov-estimators DESIGN DECISIONS: eq. (div)'s
+    control-variate term needs dM/dtheta, which AAFN does not define, so the plain Hutchinson form
+    with preconditioned solves is used -- reading R15):
+        dZ~/dtheta_j ~= 1/2 ( -alpha^T dKhat_j alpha + (1/n_z) sum_i (Khat^{-1} z_i)^T dKhat_j z_i ),
+    every Khat^{-1} b by CG on S_op = U^{-1} Khat U^{-T} from U^{-1} b, mapped back by U^{-T}."""
+    from . import krylov
+    y = np.asarray(y, dtype=np.float64)
+    Z = np.asarray(Z, dtype=np.float64)
+    S = lambda B: pre.U_inv(apply_K(pre.U_invT(B)))
+
+    def solve(b):
+        xh, _ = krylov.pcg(S, pre.U_inv(b[:, None])[:, 0], cg_iters)
+        return pre.U_invT(xh[:, None])[:, 0]
+
+    alpha = solve(y)
+    W = np.stack([solve(Z[:, i]) for i in range(Z.shape[1])], axis=1)
+    D = apply_dK(np.column_stack([alpha, Z]))
+    grad = {j: 0.5 * (-float(alpha @ Dj[:, 0]) + np.mean([float(W[:, i] @ Dj[:, 1 + i]) for i in range(Z.shape[1])]))
+            for j, Dj in D.items()}
+    return {"grad": grad, "alpha": alpha, "W": W}

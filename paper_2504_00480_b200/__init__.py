@@ -35,7 +35,7 @@ ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm"
                "akm_kernel_cross_mvm", "akm_gradient_diag", "akm_get_window_poly",
                "akm_get_bounds", "akm_set_bounds", "akm_set_radius", "akm_set_bin_override", "akm_grid_size",
                "akm_spread_grid", "akm_mvm_from_grid", "akm_set_regularization", "akm_set_preconditioner",
-               "akm_precond_apply", "akm_precond_landmarks", "akm_objective")
+               "akm_precond_apply", "akm_precond_landmarks", "akm_objective", "akm_gradient")
 AKM_MAX_PROBES = 31
 
 
@@ -138,6 +138,8 @@ def _load():
     lib.akm_precond_landmarks.restype = st
     lib.akm_objective.argtypes = [P, P, P, i64, i32, i32, i32, ctypes.POINTER(akm_objective_out), P, P]
     lib.akm_objective.restype = st
+    lib.akm_gradient.argtypes = [P, P, P, i64, i32, i32, P, P, P]
+    lib.akm_gradient.restype = st
     lib.akm_version.argtypes = []
     lib.akm_version.restype = ctypes.c_char_p
     return lib
@@ -474,8 +476,17 @@ def akm_precond_apply(plan, T, out, transpose=False, stream=None):
     return ld.value, lm[:k]
 
 
+def akm_gradient(plan, y, Z, cg_iters=50, stream=None) -> dict:
+    """Gradient of Z~ with the plan's preconditioner (AAFN: plain Hutchinson form, include/akm.h)."""
+    return _gradient(_lib.akm_gradient, plan, y, Z, cg_iters, stream)
+
+
 def akm_gradient_diag(plan, y, Z, cg_iters=50, stream=None) -> dict:
     """eq. (div) with M = diag(Khat): block PCG on [y | Z], one fused derivative product (include/akm.h)."""
+    return _gradient(_lib.akm_gradient_diag, plan, y, Z, cg_iters, stream)
+
+
+def _gradient(fn, plan, y, Z, cg_iters, stream) -> dict:
     y = _vector(y, "y")
     py, _, n, _, _, ky = _ptr_ld(y, "y")
     pz, ldz, nz_rows, n_z, _, kz = _ptr_ld(Z, "Z")
@@ -483,7 +494,7 @@ def akm_gradient_diag(plan, y, Z, cg_iters=50, stream=None) -> dict:
     _expect_rows(plan, "Z", nz_rows)
     grad = (ctypes.c_double * 3)()
     hist = (ctypes.c_double * max(int(cg_iters), 1))()
-    _check(plan, _lib.akm_gradient_diag(plan, py, pz, ldz, n_z, int(cg_iters), grad, hist, _stream(stream, ky, kz)))
+    _check(plan, fn(plan, py, pz, ldz, n_z, int(cg_iters), grad, hist, _stream(stream, ky, kz)))
     return {"grad": {"sf": grad[0], "ell": grad[1], "se": grad[2]}, "cg_hist": [h for h in hist[:cg_iters]],
             "products": int(cg_iters) + 1}
 
@@ -541,6 +552,9 @@ class Plan:
 
     def gradient_diag(self, y, Z, cg_iters=50, stream=None):
         return akm_gradient_diag(self.handle, y, Z, cg_iters, stream)
+
+    def gradient(self, y, Z, cg_iters=50, stream=None):
+        return akm_gradient(self.handle, y, Z, cg_iters, stream)
 
     def objective_diag(self, y, Z, cg_iters=50, lanczos_steps=30, stream=None):
         return akm_objective_diag(self.handle, y, Z, cg_iters, lanczos_steps, stream)

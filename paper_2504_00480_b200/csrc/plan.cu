@@ -95,7 +95,7 @@ struct akm_plan {
     int k = 0;
     double logdet = 0.0;          // log det M
     DevBuf lm, lmpos, L, Linv, LinvT, Phi, K21, Sdiag, g, y1, part, tmp, scal, flag, fps_scratch, dmin, picks, Bt, KBt,
-        yh;
+        yh, Bh;
   } aafn;
   long long theta_version = 0;
   struct BkKey {
@@ -1581,9 +1581,23 @@ static akm_status objective_impl(akm_plan* plan, const double* y, const double* 
   return AKM_OK;
 }
 
+static akm_status gradient_impl(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                                int32_t cg_iters, double* grad, double* cg_relres, void* stream, bool use_aafn);
+
 akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
                              int32_t cg_iters, double* grad, double* cg_relres, void* stream) {
+  return gradient_impl(plan, y, Z, ldz, n_z, cg_iters, grad, cg_relres, stream, false);
+}
+
+akm_status akm_gradient(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z, int32_t cg_iters,
+                        double* grad, double* cg_relres, void* stream) {
+  return gradient_impl(plan, y, Z, ldz, n_z, cg_iters, grad, cg_relres, stream, plan && plan->aafn.kpw > 0);
+}
+
+static akm_status gradient_impl(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                                int32_t cg_iters, double* grad, double* cg_relres, void* stream, bool use_aafn) {
   if (!plan) return AKM_ERR_INVALID_ARG;
+  NvtxRange nvtx("akm f1 gradient");
   plan->err.clear();
   if (!plan->have_points || !plan->have_theta)
     return plan->fail(AKM_ERR_STATE, "gradient_diag called before set_points and set_theta");
@@ -1635,15 +1649,36 @@ akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, i
   double* P = plan->gP.as<double>();
   double* part = plan->krPart.as<double>();
   void* st = plan->gState.p;
-  // M = diag(Khat) = c I (reading R11); dc/dsigma_f = 2 sigma_f P, dc/dsigma_eps = 2 sigma_eps
-  const double c = plan->sigma_f * plan->sigma_f * plan->P + plan->sigma_eps * plan->sigma_eps;
+  // M = diag(Khat) = c I (reading R11); dc/dsigma_f = 2 sigma_f P, dc/dsigma_eps = 2 sigma_eps.
+  // AAFN (reading R15): block CG on S_op = U^{-1} Khat U^{-T} from U^{-1} [y | Z] (M = I there), the
+  // solutions mapped back by U^{-T}; the plain Hutchinson form (no dM/dtheta terms: dc = 0 below)
+  const double c = use_aafn ? 1.0 : plan->sigma_f * plan->sigma_f * plan->P + plan->sigma_eps * plan->sigma_eps;
+  auto& A = plan->aafn;
   AKM_CK(launch_kr_load(n, R, yd, Zd, ldzd, B, plan->krY.as<double>(), s));
-  AKM_CK(launch_kr_col2(n, R, B, B, part, s));
+  const double* Bcg = B;  // right-hand sides of the CG
+  if (use_aafn) {
+    akm_status sb = aafn_build(plan, R, s);
+    if (sb != AKM_OK) return sb;
+    AKM_CK(A.Bt.ensure(sizeof(double) * blk));
+    AKM_CK(A.KBt.ensure(sizeof(double) * blk));
+    AKM_CK(A.Bh.ensure(sizeof(double) * blk));
+    sb = aafn_uinv(plan, R, B, A.Bh.as<double>(), s);
+    if (sb != AKM_OK) return sb;
+    Bcg = A.Bh.as<double>();
+  }
+  AKM_CK(launch_kr_col2(n, R, Bcg, Bcg, part, s));
   AKM_CK(launch_bcg_init(st, part, R, c, s));
-  AKM_CK(launch_bcg_start(n, R, st, B, Rr, P, X, s));
+  AKM_CK(launch_bcg_start(n, R, st, Bcg, Rr, P, X, s));
   plan->launches += 5;
   for (int t = 0; t < cg_iters; ++t) {
-    akm_status stt = run_mvm(plan, P, R, R, KP, nullptr, nullptr, R, s);
+    akm_status stt;
+    if (use_aafn) {
+      stt = aafn_uinvT(plan, R, P, A.Bt.as<double>(), s);
+      if (stt == AKM_OK) stt = run_mvm(plan, A.Bt.as<double>(), R, R, A.KBt.as<double>(), nullptr, nullptr, R, s);
+      if (stt == AKM_OK) stt = aafn_uinv(plan, R, A.KBt.as<double>(), KP, s);
+    } else {
+      stt = run_mvm(plan, P, R, R, KP, nullptr, nullptr, R, s);
+    }
     if (stt != AKM_OK) return stt;
     AKM_CK(launch_kr_col2(n, R, P, KP, part, s));
     AKM_CK(launch_bcg_after_dots(st, part, R, s));
@@ -1652,6 +1687,11 @@ akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, i
     AKM_CK(launch_bcg_after_norms(st, part, R, t, s));
     AKM_CK(launch_bcg_dir(n, R, st, Rr, P, s));
     plan->launches += 6;
+  }
+  if (use_aafn) {  // X = U^{-T} X^ (the solutions of Khat X = [y | Z])
+    akm_status sx = aafn_uinvT(plan, R, X, A.Bt.as<double>(), s);
+    if (sx != AKM_OK) return sx;
+    AKM_CK(cudaMemcpyAsync(X, A.Bt.p, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
   }
   // one fused derivative product on [alpha | Z]
   double* B2 = plan->gB2.as<double>();
@@ -1678,7 +1718,7 @@ akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, i
   // eq. (div): 1/2 (-alpha^T dK alpha + n dc/c + (1/n_z) sum_i [(Khat^{-1} z_i)^T dK z_i - dc/c ||z_i||^2])
   const double sf = plan->sigma_f, se = plan->sigma_eps;
   const double scale[3] = {1.0, 1.0, 2.0 * se};          // dK applied: D1, D2 as computed; 2 se * B2
-  const double dc[3] = {0.0, 2.0 * sf * plan->P, 2.0 * se};
+  const double dc[3] = {0.0, use_aafn ? 0.0 : 2.0 * sf * plan->P, use_aafn ? 0.0 : 2.0 * se};
   const int slot_of_param[3] = {1, 0, 2};                  // grad order (sigma_f, ell, sigma_eps)
   for (int k = 0; k < 3; ++k) {
     const int j = slot_of_param[k];

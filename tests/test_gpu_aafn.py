@@ -121,3 +121,33 @@ def test_c5_full_size_cg_converges(akm):
     # both estimate the same log det K^ = log det M + tr logm(M^{-1} K^) (eq. 1.3): the AAFN split is
     # far more accurate, so the two agree only to the diagonal estimator's own SLQ spread
     assert got["logdetM"] + got["slq"] == pytest.approx(diag["logdetM"] + diag["slq"], rel=2e-2)
+
+
+def test_gradient_aafn_vs_oracle(akm):
+    """akm_gradient with AAFN (plain Hutchinson form with AAFN-PCG solves) against oracle/aafn.py
+    gradient_aafn on the dense K^ (theta where 50 iterations converge: 1e-8), and against the diagonal-M
+    estimator there (the control variates cancel for Rademacher probes once the solves converge)."""
+    from oracle import dense_apply
+    wl = workloads.CONFIGS["c5"]
+    n, n_z, kpw = 3000, 4, 100
+    X = workloads.make_X(wl, n=n)
+    V = workloads.make_V(wl, n=n, r=1 + n_z)
+    th = (0.5, 0.5, 1.0)
+    plan = _plan(akm, X, wl, kpw, th)
+    dev = torch.device("cuda:0")
+    y = torch.from_numpy(np.ascontiguousarray(V[:, 0])).to(dev)
+    Z = torch.from_numpy(np.ascontiguousarray(V[:, 1:])).to(dev)
+    got = plan.gradient(y, Z, 50)["grad"]
+    diag = plan.gradient_diag(y, Z, 50)["grad"]
+    plan.close()
+    K = A.khat_dense(X, wl.windows, wl.family, th)
+
+    def dK(B):
+        o = dense_apply(X, wl.windows, wl.family, th, np.ascontiguousarray(B), ops=("dell", "dsf", "dse"))
+        return {"ell": o["dell"], "sf": o["dsf"], "se": o["dse"]}
+
+    pre = A.Aafn(X, wl.windows, wl.family, th, kpw, 1)
+    want = A.gradient_aafn(lambda B: K @ B, dK, V[:, 0], V[:, 1:], pre, 50)["grad"]
+    for j in ("sf", "ell", "se"):
+        assert got[j] == pytest.approx(want[j], rel=1e-8, abs=1e-8 * abs(want["se"])), j
+        assert got[j] == pytest.approx(diag[j], rel=1e-7, abs=1e-7 * abs(want["se"])), j

@@ -132,3 +132,42 @@ def test_fig3_in_miniature(family):
         counts.append((plain, pc))
         assert pc <= plain, (ell, plain, pc)
     assert max(p - q for p, q in counts) >= 10, counts
+
+
+@pytest.mark.parametrize("family", [0, 1])
+def test_gradient_aafn_exact_trace_matches_fd(family):
+    """With probes sqrt(n) e_j (exact trace) and converged solves the AAFN gradient is the exact gradient
+    of eq. (1.2) -> central finite differences of the dense objective; with Rademacher probes it equals
+    the diagonal-M estimator once both solves have converged (the control variates cancel there)."""
+    from oracle import dense_apply
+    rng = np.random.default_rng(family)
+    n = 30
+    X = rng.random((n, 5))
+    W = [(0, 1, 2), (3, 4)]
+    y = rng.standard_normal(n)
+    theta = (1.2, 0.4, 0.3)
+    K = A.khat_dense(X, W, family, theta)
+
+    def dK(B):
+        o = dense_apply(X, W, family, theta, B, ops=("dell", "dsf", "dse"))
+        return {"ell": o["dell"], "sf": o["dsf"], "se": o["dse"]}
+
+    pre = A.Aafn(X, W, family, theta, 4, 3)
+    g = A.gradient_aafn(lambda B: K @ B, dK, y, math.sqrt(n) * np.eye(n), pre, 200)["grad"]
+
+    def Zd(th):
+        Kt = A.khat_dense(X, W, family, th)
+        return 0.5 * (y @ np.linalg.solve(Kt, y) + np.linalg.slogdet(Kt)[1])
+
+    for j, idx in (("sf", 0), ("ell", 1), ("se", 2)):
+        h = 1e-5 * theta[idx]
+        tp, tm = list(theta), list(theta)
+        tp[idx] += h
+        tm[idx] -= h
+        assert g[j] == pytest.approx((Zd(tuple(tp)) - Zd(tuple(tm))) / (2 * h), rel=1e-7), j
+    Zr = np.where(rng.random((n, 5)) < 0.5, -1.0, 1.0)
+    ga = A.gradient_aafn(lambda B: K @ B, dK, y, Zr, pre, 200)["grad"]
+    c = theta[0] ** 2 * 2 + theta[2] ** 2
+    gd = KR.gradient_diag(lambda B: K @ B, dK, y, Zr, c, {"sf": 4 * theta[0], "ell": 0.0, "se": 2 * theta[2]}, 200)["grad"]
+    for j in ("sf", "ell", "se"):
+        assert ga[j] == pytest.approx(gd[j], rel=1e-9)
