@@ -268,6 +268,20 @@ cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, 
 
 }  // namespace
 
+// Work items ordered by decreasing point count, ties kept in their order (= std::stable_sort with
+// a.count > b.count): a counting sort, O(items + max count).
+static void sort_larger_first(std::vector<WorkItem>& v) {
+  if (v.size() < 2) return;
+  int mx = 0;
+  for (const WorkItem& it : v) mx = std::max(mx, it.count);
+  std::vector<int> pos((size_t)mx + 2, 0);
+  for (const WorkItem& it : v) ++pos[(size_t)(mx - it.count) + 1];
+  for (int i = 1; i <= mx + 1; ++i) pos[i] += pos[i - 1];
+  std::vector<WorkItem> out(v.size());
+  for (const WorkItem& it : v) out[pos[mx - it.count]++] = it;
+  v.swap(out);
+}
+
 // ================================================================== geometry / binning
 // Build per-window boxes for the current c_w, histogram the points per cell on the device,
 // choose the bin edge B per window from the histogram, lay the cells out bin-major, scatter.
@@ -359,6 +373,18 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     int bestB = 1;
     double bestCost = 1e300;
     const bool forced = !plan->bin_override.empty();
+    // occupied cells (0.15-10% of the box at the BASELINE.json configs): the candidates below loop
+    // over these only
+    struct Occ { int c0, c1, c2, v; };
+    std::vector<Occ> occ;
+    for (int c0 = 0; c0 < g.ncell[0]; ++c0)
+      for (int c1 = 0; c1 < g.ncell[1]; ++c1)
+        for (int c2 = 0; c2 < g.ncell[2]; ++c2) {
+          const long long ci = ((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2;
+          const int v = hc[2 * ci] + hc[2 * ci + 1];
+          if (v) occ.push_back(Occ{c0, c1, c2, v});
+        }
+    std::vector<long long> bc;
     for (int B : {1, 2, 3, 4, 6, 8}) {
       if (forced && B != plan->bin_override[w]) continue;
       const int F = B + 2 * m - 1;
@@ -377,19 +403,18 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
       int nb[3];
       for (int a = 0; a < 3; ++a) nb[a] = (g.ncell[a] + B - 1) / (a < 3 - d ? 1 : B);
       for (int a = 0; a < 3 - d; ++a) nb[a] = 1;
-      std::vector<long long> bc((size_t)nb[0] * nb[1] * nb[2], 0);
-      for (int c0 = 0; c0 < g.ncell[0]; ++c0)
-        for (int c1 = 0; c1 < g.ncell[1]; ++c1)
-          for (int c2 = 0; c2 < g.ncell[2]; ++c2) {
-            const long long ci = ((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2;
-            const int v = hc[2 * ci] + hc[2 * ci + 1];
-            if (!v) continue;
-            const int b0 = (3 - d > 0) ? 0 : c0 / B, b1 = (3 - d > 1) ? 0 : c1 / B, b2 = c2 / B;
-            bc[((size_t)b0 * nb[1] + b1) * nb[2] + b2] += v;
-          }
+      bc.assign((size_t)nb[0] * nb[1] * nb[2], 0);
+      for (const Occ& o : occ) {
+        const int b0 = (3 - d > 0) ? 0 : o.c0 / B, b1 = (3 - d > 1) ? 0 : o.c1 / B, b2 = o.c2 / B;
+        bc[((size_t)b0 * nb[1] + b1) * nb[2] + b2] += o.v;
+      }
       double chunks_s = 0;
-      for (long long v : bc)
+      for (const Occ& o : occ) {  // each occupied bin once (zeroed after it is counted)
+        const int b0 = (3 - d > 0) ? 0 : o.c0 / B, b1 = (3 - d > 1) ? 0 : o.c1 / B, b2 = o.c2 / B;
+        long long& v = bc[((size_t)b0 * nb[1] + b1) * nb[2] + b2];
         if (v) chunks_s += (double)((v + ch_s - 1) / ch_s);
+        v = 0;
+      }
       // spreading: F^d FMAs per point and RHS, plus one footprint flush of F^d RED.ADD.F64
       // (~34 FMA-equivalents each, profiles/r01_fp64_peaks.txt) per work item.  Interpolation
       // works per cell and does not depend on B.
@@ -489,10 +514,9 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
         gi.insert(gi.end(), its_i[set][w].begin(), its_i[set][w].end());
         gib.insert(gib.end(), its_ib[set][w].begin(), its_ib[set][w].end());
       }
-      auto larger_first = [](const WorkItem& a, const WorkItem& b) { return a.count > b.count; };
-      std::stable_sort(gs.begin(), gs.end(), larger_first);
-      std::stable_sort(gi.begin(), gi.end(), larger_first);
-      std::stable_sort(gib.begin(), gib.end(), larger_first);
+      sort_larger_first(gs);
+      sort_larger_first(gi);
+      sort_larger_first(gib);
       ItemSlice& sl = grp.sl[set];
       sl.spread_begin = (int)plan->items_spread[set].size();
       sl.spread_count = (int)gs.size();
