@@ -281,7 +281,7 @@ def main():
     n_src = wl.extra.get("n_src", wl.n)
     objective = "cg_iters" in wl.extra          # c5: one Z~ evaluation per step (S8)
     gradient = "grad_cg_iters" in wl.extra      # g5: one gradient of Z~ per step (f1)
-    probe_sharded = world > 1 and objective     # c5 / c5a: probe columns over the ranks (§8(e) item 2)
+    probe_sharded = world > 1 and (objective or gradient)  # c5 / c5a / g5: probe columns over the ranks (§8(e) 2)
     # N > 1: the square products are point-sharded (each rank owns a row block of the SAME problem,
     # one grid all-reduce per product: strong scaling); the Krylov drivers and the cross
     # product run as independent replicas (weak scaling)
@@ -339,6 +339,15 @@ def main():
         else:
             def step():
                 last["out"] = plan.objective_diag(yd, Zd, cg, lz)
+    elif gradient and probe_sharded:
+        gcg = wl.extra["grad_cg_iters"]
+        yd, Zd = Vd[:, 0].contiguous(), Vd[:, 1:].contiguous()
+        products_per_step = gcg + 1
+        last = {}
+
+        def step():   # every rank: the whole problem, a slice of the probes (rank 0 also alpha)
+            g = D.sharded_gradient(plan, yd, Zd, (wl.sigma_f, wl.ell, wl.sigma_eps), len(wl.windows), gcg)
+            last["out"] = {"grad": {k: g[k] for k in ("sf", "ell", "se")}, "cg_hist": [float("nan")]}
     elif gradient:
         gcg = wl.extra["grad_cg_iters"]
         yd, Zd = Vd[:, 0].contiguous(), Vd[:, 1:].contiguous()
@@ -422,7 +431,9 @@ def main():
         yh, Zh = Vh[:, 0].contiguous().pin_memory(), Vh[:, 1:].contiguous().pin_memory()
 
     def e2e_step():
-        if probe_sharded:
+        if probe_sharded and gradient:
+            D.sharded_gradient(plan, yh, Zh, (wl.sigma_f, wl.ell, wl.sigma_eps), len(wl.windows), gcg)
+        elif probe_sharded:
             if "aafn_kpw" in wl.extra:
                 plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
             D.sharded_objective(plan, yh, Zh, cg, lz, preconditioned="aafn_kpw" in wl.extra)

@@ -322,6 +322,17 @@ akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, i
 akm_status akm_gradient(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z, int32_t cg_iters,
                         double* grad, double* cg_relres, void* stream);
 
+/* The raw per-column terms of the gradient (for probe sharding): with
+ * R = 1 + n_z, X = Khat^{-1} [y | Z] from cg_iters CG iterations (preconditioned != 0: the plan's
+ * preconditioner, else M = diag Khat), dots[k*R + i] = X_i^T (dKhat_k B_i) with B = [X_0 | Z] (i = 0:
+ * alpha^T dKhat_k alpha; i >= 1: (Khat^{-1} z_i)^T dKhat_k z_i), k in (sigma_f, ell, sigma_eps), and
+ * sqnorms[i] = ||b_i||^2 (host arrays of 3R and R doubles).  akm_gradient_diag combines them as
+ *   grad[k] = 1/2 ( -dots[k*R] + n dc_k/c + (1/n_z) sum_{i>=1} (dots[k*R+i] - dc_k/c sqnorms[i]) ),
+ * c = sigma_f^2 P + sigma_eps^2, dc = (2 sigma_f P, 0, 2 sigma_eps) (dc = 0 under AAFN). */
+akm_status akm_gradient_columns(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                                int32_t cg_iters, int32_t preconditioned, double* dots, double* sqnorms,
+                                double* cg_relres, void* stream);
+
 const char* akm_version(void);
 
 #ifdef __cplusplus

@@ -35,7 +35,8 @@ ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm"
                "akm_kernel_cross_mvm", "akm_gradient_diag", "akm_get_window_poly",
                "akm_get_bounds", "akm_set_bounds", "akm_set_radius", "akm_set_bin_override", "akm_grid_size",
                "akm_spread_grid", "akm_mvm_from_grid", "akm_set_regularization", "akm_set_preconditioner",
-               "akm_precond_apply", "akm_precond_landmarks", "akm_objective", "akm_gradient")
+               "akm_precond_apply", "akm_precond_landmarks", "akm_objective", "akm_gradient",
+               "akm_gradient_columns")
 AKM_MAX_PROBES = 31
 
 
@@ -140,6 +141,8 @@ def _load():
     lib.akm_objective.restype = st
     lib.akm_gradient.argtypes = [P, P, P, i64, i32, i32, P, P, P]
     lib.akm_gradient.restype = st
+    lib.akm_gradient_columns.argtypes = [P, P, P, i64, i32, i32, i32, P, P, P, P]
+    lib.akm_gradient_columns.restype = st
     lib.akm_version.argtypes = []
     lib.akm_version.restype = ctypes.c_char_p
     return lib
@@ -486,6 +489,23 @@ def akm_gradient_diag(plan, y, Z, cg_iters=50, stream=None) -> dict:
     return _gradient(_lib.akm_gradient_diag, plan, y, Z, cg_iters, stream)
 
 
+def akm_gradient_columns(plan, y, Z, cg_iters=50, preconditioned=False, stream=None) -> dict:
+    """Raw per-column gradient terms (include/akm.h): dots (3, 1 + n_z) and sqnorms (1 + n_z)."""
+    y = _vector(y, "y")
+    py, _, n, _, _, ky = _ptr_ld(y, "y")
+    pz, ldz, nz_rows, n_z, _, kz = _ptr_ld(Z, "Z")
+    _expect_rows(plan, "y", n)
+    _expect_rows(plan, "Z", nz_rows)
+    R = 1 + n_z
+    dots = np.zeros(3 * R)
+    sq = np.zeros(R)
+    hist = (ctypes.c_double * max(int(cg_iters), 1))()
+    _check(plan, _lib.akm_gradient_columns(plan, py, pz, ldz, n_z, int(cg_iters), 1 if preconditioned else 0,
+                                           dots.ctypes.data_as(ctypes.c_void_p), sq.ctypes.data_as(ctypes.c_void_p),
+                                           hist, _stream(stream, ky, kz)))
+    return {"dots": dots.reshape(3, R), "sqnorms": sq, "cg_hist": [h for h in hist[:cg_iters]]}
+
+
 def _gradient(fn, plan, y, Z, cg_iters, stream) -> dict:
     y = _vector(y, "y")
     py, _, n, _, _, ky = _ptr_ld(y, "y")
@@ -555,6 +575,9 @@ class Plan:
 
     def gradient(self, y, Z, cg_iters=50, stream=None):
         return akm_gradient(self.handle, y, Z, cg_iters, stream)
+
+    def gradient_columns(self, y, Z, cg_iters=50, preconditioned=False, stream=None):
+        return akm_gradient_columns(self.handle, y, Z, cg_iters, preconditioned, stream)
 
     def objective_diag(self, y, Z, cg_iters=50, lanczos_steps=30, stream=None):
         return akm_objective_diag(self.handle, y, Z, cg_iters, lanczos_steps, stream)

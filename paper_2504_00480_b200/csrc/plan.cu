@@ -1606,7 +1606,8 @@ static akm_status objective_impl(akm_plan* plan, const double* y, const double* 
 }
 
 static akm_status gradient_impl(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
-                                int32_t cg_iters, double* grad, double* cg_relres, void* stream, bool use_aafn);
+                                int32_t cg_iters, double* grad, double* cg_relres, void* stream, bool use_aafn,
+                                double* dots = nullptr, double* sqnorms = nullptr);
 
 akm_status akm_gradient_diag(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
                              int32_t cg_iters, double* grad, double* cg_relres, void* stream) {
@@ -1618,8 +1619,18 @@ akm_status akm_gradient(akm_plan* plan, const double* y, const double* Z, int64_
   return gradient_impl(plan, y, Z, ldz, n_z, cg_iters, grad, cg_relres, stream, plan && plan->aafn.kpw > 0);
 }
 
+akm_status akm_gradient_columns(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
+                                int32_t cg_iters, int32_t preconditioned, double* dots, double* sqnorms,
+                                double* cg_relres, void* stream) {
+  if (plan && (!dots || !sqnorms)) return plan->fail(AKM_ERR_INVALID_ARG, "dots / sqnorms are NULL");
+  double grad[3];
+  return gradient_impl(plan, y, Z, ldz, n_z, cg_iters, grad, cg_relres, stream,
+                       plan && preconditioned && plan->aafn.kpw > 0, dots, sqnorms);
+}
+
 static akm_status gradient_impl(akm_plan* plan, const double* y, const double* Z, int64_t ldz, int32_t n_z,
-                                int32_t cg_iters, double* grad, double* cg_relres, void* stream, bool use_aafn) {
+                                int32_t cg_iters, double* grad, double* cg_relres, void* stream, bool use_aafn,
+                                double* dots, double* sqnorms) {
   if (!plan) return AKM_ERR_INVALID_ARG;
   NvtxRange nvtx("akm f1 gradient");
   plan->err.clear();
@@ -1744,6 +1755,13 @@ static akm_status gradient_impl(akm_plan* plan, const double* y, const double* Z
   const double scale[3] = {1.0, 1.0, 2.0 * se};          // dK applied: D1, D2 as computed; 2 se * B2
   const double dc[3] = {0.0, use_aafn ? 0.0 : 2.0 * sf * plan->P, use_aafn ? 0.0 : 2.0 * se};
   const int slot_of_param[3] = {1, 0, 2};                  // grad order (sigma_f, ell, sigma_eps)
+  if (dots) {  // raw per-column terms for the probe-sharded gradient (dist.sharded_gradient)
+    for (int k = 0; k < 3; ++k) {
+      const int j = slot_of_param[k];
+      for (int i = 0; i < R; ++i) dots[k * R + i] = scale[j] * outv[j * 2 * kKrMaxR + 2 * i];
+    }
+    for (int i = 0; i < R; ++i) sqnorms[i] = bn[i] * bn[i];
+  }
   for (int k = 0; k < 3; ++k) {
     const int j = slot_of_param[k];
     const double* o = outv.data() + j * 2 * kKrMaxR;

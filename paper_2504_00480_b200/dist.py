@@ -194,3 +194,44 @@ def sharded_objective(plan, y, Z, cg_iters=50, lanczos_steps=30, comm_device=Non
     res = {"Z": 0.5 * (quad + logdet + slq + n * math.log(2.0 * math.pi)), "quad": quad, "logdetM": logdet,
            "slq": slq, "probes": int(cnt), "local": out, "columns": (c0, c1)}
     return res
+
+
+def sharded_gradient(plan, y, Z, theta, P, cg_iters=50, comm_device=None, preconditioned=False):
+    """grad Z~ (eq. (div)) with the probe columns sharded over the ranks.
+
+    Rank 0 solves for alpha = Khat^{-1} y with its probes, the other ranks their probes with y = 0;
+    every rank returns its raw per-column terms (``Plan.gradient_columns``), one all-reduce sums them,
+    and the components are assembled as akm_gradient_diag does (include/akm.h):
+        grad_k = 1/2 ( -alpha^T dK_k alpha + n dc_k/c + (1/n_z) sum_i (z_i^T Khat^{-1} dK_k z_i - dc_k/c ||z_i||^2) ),
+    c = sigma_f^2 P + sigma_eps^2, dc = (2 sigma_f P, 0, 2 sigma_eps); under AAFN (``preconditioned``) dc = 0.
+    ``theta`` = (sigma_f, ell, sigma_eps) of the plan, ``P`` its window count.  Returns the gradient
+    in the order (sigma_f, ell, sigma_eps)."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    n_z = Z.shape[1]
+    c0, c1 = column_partition(n_z, world, rank)
+    acc = np.zeros(3 * 2 + 1)  # [alpha terms (3) | probe sums (3) | probe count]
+    if c1 > c0:
+        Zk = Z[:, c0:c1]
+        Zk = Zk.contiguous() if hasattr(Zk, "contiguous") else np.ascontiguousarray(Zk)
+        y_k = y if rank == 0 else (torch.zeros_like(y) if hasattr(y, "new_zeros") else np.zeros_like(y))
+        out = plan.gradient_columns(y_k, Zk, cg_iters if rank == 0 else cg_iters, preconditioned)
+        sf, _, se = theta
+        c = sf * sf * P + se * se
+        dc = np.zeros(3) if preconditioned else np.array([2.0 * sf * P, 0.0, 2.0 * se])
+        dots, sq = out["dots"], out["sqnorms"]
+        acc[0:3] = dots[:, 0] if rank == 0 else 0.0
+        acc[3:6] = (dots[:, 1:] - (dc / c)[:, None] * sq[None, 1:]).sum(axis=1)
+        acc[6] = c1 - c0
+    dev = comm_device if comm_device is not None else (
+        torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu"))
+    t = torch.as_tensor(acc, dtype=torch.float64, device=dev)
+    dist.all_reduce(t)
+    acc = t.cpu().numpy()
+    sf, _, se = theta
+    c = sf * sf * P + se * se
+    dc = np.zeros(3) if preconditioned else np.array([2.0 * sf * P, 0.0, 2.0 * se])
+    n = y.shape[0]
+    g = 0.5 * (-acc[0:3] + n * dc / c + acc[3:6] / acc[6])
+    return {"sf": float(g[0]), "ell": float(g[1]), "se": float(g[2]), "probes": int(acc[6])}

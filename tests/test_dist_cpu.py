@@ -297,3 +297,81 @@ def test_gloo_probe_sharded_objective(world):
         assert quad == pytest.approx(ref["quad"], rel=1e-10)
         assert slq == pytest.approx(ref["slq"], rel=1e-10)
     assert [r[5] for r in res] == [D.column_partition(7, world, k) for k in range(world)]
+
+
+class OracleGradientPlan:
+    """Test stand-in for Plan.gradient_columns: oracle PCG (M = c I) and dense derivative products."""
+
+    def __init__(self, X, windows, family, theta):
+        from oracle import aafn as A
+        from oracle import dense_apply
+        self.K = A.khat_dense(X, windows, family, theta)
+        self.X, self.windows, self.family, self.theta = X, windows, family, theta
+        sf, _, se = theta
+        self.c = sf * sf * len(windows) + se * se
+        self.dense_apply = dense_apply
+
+    def gradient_columns(self, y, Z, cg_iters, preconditioned=False):
+        from oracle import krylov as KR
+        y, Z = np.asarray(y), np.asarray(Z)
+        minv = np.full(y.size, 1.0 / self.c)
+        B = np.column_stack([y, Z])
+        Xs = np.stack([KR.pcg(lambda V: self.K @ V, B[:, i], cg_iters, minv)[0] for i in range(B.shape[1])], axis=1)
+        B2 = np.column_stack([Xs[:, 0], Z])
+        o = self.dense_apply(self.X, self.windows, self.family, self.theta, B2, ops=("dsf", "dell", "dse"))
+        dots = np.stack([(Xs * o[k]).sum(axis=0) for k in ("dsf", "dell", "dse")])
+        return {"dots": dots, "sqnorms": (B * B).sum(axis=0)}
+
+
+def _grad_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wl = workloads.CONFIGS["c5"]
+        X = workloads.make_X(wl, n=400)
+        V = workloads.make_V(wl, n=400, r=6)
+        th = (0.9, 0.3, 0.4)
+        plan = OracleGradientPlan(X, wl.windows, wl.family, th)
+        g = D.sharded_gradient(plan, torch.from_numpy(V[:, 0].copy()), torch.from_numpy(V[:, 1:].copy()), th,
+                               len(wl.windows), 60)
+        q.put((rank, g))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_probe_sharded_gradient():
+    """The probe-sharded gradient (raw per-column terms summed over ranks, then eq. (div) with M = c I)
+    equals the single-process oracle gradient_diag."""
+    from oracle import dense_apply
+    from oracle import krylov as KR
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_worker, args=(k, world, port, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    wl = workloads.CONFIGS["c5"]
+    X = workloads.make_X(wl, n=400)
+    V = workloads.make_V(wl, n=400, r=6)
+    th = (0.9, 0.3, 0.4)
+    from oracle import aafn as A
+    K = A.khat_dense(X, wl.windows, wl.family, th)
+
+    def dK(B):
+        o = dense_apply(X, wl.windows, wl.family, th, np.ascontiguousarray(B), ops=("dell", "dsf", "dse"))
+        return {"ell": o["dell"], "sf": o["dsf"], "se": o["dse"]}
+
+    P = len(wl.windows)
+    c = th[0] ** 2 * P + th[2] ** 2
+    ref = KR.gradient_diag(lambda B: K @ B, dK, V[:, 0], V[:, 1:], c, {"sf": 2 * th[0] * P, "ell": 0.0, "se": 2 * th[2]},
+                           60)["grad"]
+    for _, g in res:
+        assert g["probes"] == 5
+        for j in ("sf", "ell", "se"):
+            assert g[j] == pytest.approx(ref[j], rel=1e-10), j

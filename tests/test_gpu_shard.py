@@ -238,3 +238,57 @@ def test_probe_sharded_objective_gloo_world2(akm, kpw):
         assert Zs == pytest.approx(Z1, rel=1e-9)
         assert quad == pytest.approx(quad1, rel=1e-8)
         assert slq == pytest.approx(slq1, rel=1e-8)
+
+
+def _grad_gloo_worker(rank, world, port, q, kpw):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2504_00480_b200 as akm
+        from paper_2504_00480_b200 import dist as D
+        wl = workloads.CONFIGS["c5"]
+        n = 8000
+        X = workloads.make_X(wl, n=n)
+        V = workloads.make_V(wl, n=n)
+        dev = torch.device("cuda:0")
+        plan = akm.Plan(0)
+        plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+        if kpw:
+            plan.set_preconditioner(kpw)
+        th = (0.5, 0.5, 2.0)           # 50 CG iterations converge to rounding here (asserted below)
+        plan.set_theta(*th)
+        y = torch.from_numpy(np.ascontiguousarray(V[:, 0])).to(dev)
+        Z = torch.from_numpy(np.ascontiguousarray(V[:, 1:])).to(dev)
+        g = D.sharded_gradient(plan, y, Z, th, len(wl.windows), 50, comm_device=torch.device("cpu"),
+                               preconditioned=bool(kpw))
+        one = (plan.gradient if kpw else plan.gradient_diag)(y, Z, 50)
+        single, last = one["grad"], one["cg_hist"][-1]
+        plan.close()
+        q.put((rank, g, single, last))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kpw", [0, 60])
+def test_probe_sharded_gradient_gloo_world2(akm, kpw):
+    """SURVEY.md §8(e) item 2 for the gradient: per-column raw terms (akm_gradient_columns) summed over
+    the ranks reproduce the single-process gradient (diagonal M and AAFN)."""
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_gloo_worker, args=(k, world, port, q, kpw)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, g, single, last in res:
+        assert last < 1e-11, last      # converged: the products' rounding does not move the solves
+        for j in ("sf", "ell", "se"):
+            assert g[j] == pytest.approx(single[j], rel=1e-9, abs=1e-9 * abs(single["se"])), j
