@@ -151,3 +151,42 @@ def test_gradient_aafn_vs_oracle(akm):
     for j in ("sf", "ell", "se"):
         assert got[j] == pytest.approx(want[j], rel=1e-8, abs=1e-8 * abs(want["se"])), j
         assert got[j] == pytest.approx(diag[j], rel=1e-7, abs=1e-7 * abs(want["se"])), j
+
+
+def test_aafn_edge_cases(akm):
+    """Every point a landmark (k_per_window >= n): M = K^, so S_op = I and one CG step solves the
+    system; n = 1; switching back to the diagonal preconditioner; argument errors."""
+    wl = workloads.CONFIGS["c2"]
+    dev = torch.device("cuda:0")
+    X = workloads.make_X(wl, n=60)
+    V = workloads.make_V(wl, n=60, r=3)
+    th = (wl.sigma_f, wl.ell, wl.sigma_eps)
+    plan = _plan(akm, X, wl, 100)                 # 100 per window >= n = 60: all points are landmarks
+    y = torch.from_numpy(np.ascontiguousarray(V[:, 0])).to(dev)
+    Z = torch.from_numpy(np.ascontiguousarray(V[:, 1:])).to(dev)
+    o = plan.objective(y, Z, 3, 3)
+    assert o["landmarks"] == 60
+    K = A.khat_dense(X, wl.windows, wl.family, th)
+    assert o["logdetM"] == pytest.approx(np.linalg.slogdet(K)[1], rel=1e-10)
+    assert abs(o["slq"]) <= 1e-7 * 60                      # logm(M^{-1} K^) = 0 up to the NFFT product's error
+    assert o["cg_relres_true"] <= 1e-8
+    plan.set_preconditioner(0)                            # back to M = diag K^
+    d = plan.objective(y, Z, 3, 3)
+    assert d["landmarks"] == 0
+    assert d["logdetM"] == pytest.approx(60 * np.log(th[0] ** 2 * 3 + th[2] ** 2), rel=1e-14)
+    with pytest.raises(akm.AkmError):
+        plan.set_preconditioner(-1)
+    plan.close()
+    # n = 1: M = [sigma_f^2 P + sigma_eps^2]
+    X1 = np.array([[0.2, 0.5, 0.9]])
+    p1 = akm.Plan(0)
+    p1.set_points(torch.from_numpy(X1).to(dev), [(0, 1), (2,)], 0)
+    p1.set_preconditioner(5)
+    p1.set_theta(1.3, 0.4, 0.5)
+    T = torch.ones((1, 1), dtype=torch.float64, device=dev)
+    out = torch.empty_like(T)
+    logdet, lm = p1.precond_apply(T, out)
+    assert list(lm) == [0]
+    assert logdet == pytest.approx(np.log(1.3**2 * 2 + 0.25), rel=1e-14)
+    assert out.item() == pytest.approx(1.0 / np.sqrt(1.3**2 * 2 + 0.25), rel=1e-14)
+    p1.close()

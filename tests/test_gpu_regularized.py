@@ -150,3 +150,27 @@ def test_p0_restores_plain_and_cross_refuses(akm):
         with pytest.raises(akm.AkmError):
             plan.set_regularization(*bad)
     plan.close()
+
+
+def test_regularisation_refused_where_not_built(akm):
+    """The near-field correction is built for the square products: the point-sharded split refuses it."""
+    wl = workloads.CONFIGS["c2"]
+    X = workloads.make_X(wl, n=800)
+    V = workloads.make_V(wl, n=800, r=1)
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family)
+    plan.set_regularization(1 / 32, 3)
+    plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    Vd = torch.from_numpy(V).to(dev)
+    grid = torch.zeros(plan.grid_size(1), dtype=torch.float64, device=dev)
+    plan.spread_grid(Vd, grid)
+    with pytest.raises(akm.AkmError) as e:
+        plan.mvm_from_grid(grid, Vd, Y=torch.empty_like(Vd))
+    assert e.value.status == akm.AKM_ERR_UNSUPPORTED
+    plan.set_regularization(0.0, 3)          # outer smoothing only: no near field, the split works
+    plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    plan.spread_grid(Vd, grid)
+    Y = torch.empty_like(Vd)
+    plan.mvm_from_grid(grid, Vd, Y=Y)
+    plan.close()
