@@ -416,9 +416,11 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
         v = 0;
       }
       // spreading: F^d FMAs per point and RHS, plus one footprint flush of F^d RED.ADD.F64
-      // (~34 FMA-equivalents each, profiles/r01_fp64_peaks.txt) per work item.  Interpolation
-      // works per cell and does not depend on B.
-      const double cost = Fd * ((double)n + 34.0 * chunks_s);
+      // (~34 FMA-equivalents each, profiles/r01_fp64_peaks.txt) per work item.  2-D windows: the
+      // per-item prologue and flush weigh more against the few points of a bin (~140 at c3) -- 60
+      // per footprint tap matches the measured optimum (c3: B = 4 0.724 ms, B = 3 0.771, B = 6 0.833)
+      const double per_item = (d == 2) ? 60.0 : 34.0;
+      const double cost = Fd * ((double)n + per_item * chunks_s);
       if (cost < bestCost * 0.999) {
         bestCost = cost;
         bestB = B;
