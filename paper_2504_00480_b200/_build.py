@@ -58,7 +58,10 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
             for f in futs:
                 f.result()
     newest = max(os.path.getmtime(o) for o in objs)
-    if force or todo or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
+    stamp = os.path.join(BUILD, "objects.txt")  # the unit list of the last link
+    units = "\n".join(os.path.basename(o) for o in objs)
+    relink = not os.path.exists(stamp) or open(stamp).read() != units
+    if force or todo or relink or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         if verbose:
             print(" ".join(cmd), flush=True)
@@ -66,6 +69,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
         os.replace(LIB + ".tmp", LIB)
+        with open(stamp, "w") as f:
+            f.write(units)
     return LIB
 
 
