@@ -13,6 +13,7 @@
 //     spectra are stored box-local.  cell_t = floor(u_t) - (box_lo_t + m - 1) in [0, ncell_t).
 //   * Bins are B^d blocks of cells; a bin's footprint is F = B + 2m - 1 nodes per real axis.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -183,6 +184,13 @@ __host__ __device__ inline double bessel_i0(double x) {
   return sum;
 }
 
+// Tensor maps of the interpolation grids H per window (TMA staging in k_interp_mma; interp.cu builds
+// them, interp_impl.cuh consumes them as a __grid_constant__ kernel parameter).
+constexpr int kTmaWin = 8;
+struct TmaMaps {
+  CUtensorMap m[kTmaWin];
+};
+
 // Opt-ins to more than 48 KB of dynamic shared memory (cudaFuncSetAttribute) hold per device: each
 // launch site keeps one bit per device.  Two threads racing on the first launch both set
 // the attribute, which is idempotent.
@@ -316,11 +324,14 @@ cudaError_t launch_kr_advance(void* st, int R, cudaStream_t s);
 cudaError_t launch_kr_slq_quad(void* st, int R, const double* part_yx, int* err, cudaStream_t s);
 void kr_summary_offsets(size_t* off_quad, size_t* off_samples, size_t* off_steps, size_t* off_hist, size_t* off_znorm);
 
-// interp.cu
+// interp.cu (tma: host TmaMaps of the H grids for the TMA-staged k_interp_mma, or nullptr)
+size_t interp_tma_maps_bytes();
+bool interp_tma_build(const WinTable& tab, const double* H, int ops, int r, void* maps);
 int interp_rc_for(int r_remaining);
 cudaError_t launch_interp(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                           int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm, const double* H,
-                          int d, int taps, int ops, int r, int r0, int rc, double* part, long long n, cudaStream_t s);
+                          int d, int taps, int ops, int r, int r0, int rc, double* part, long long n, const void* tma,
+                          cudaStream_t s);
 cudaError_t launch_epilogue_cross(long long n, long long n_src, int P, int r, int ops, int slotK, const double* part,
                                   double sigma_f, double* Yt, long long ldy, cudaStream_t s);
 cudaError_t launch_epilogue(long long n, int P, int r, int ops, const double* part, const double* V, long long ldv,

@@ -1,6 +1,8 @@
 // interp.cu -- dispatch of the NFFT interpolation kernels (kernel template in
 // interp_impl.cuh) and the epilogue S7: Y = sigma_f^2 S + sigma_eps^2 V, dY_ell = sigma_f^2 S^ell,
 // dY_sf = 2 sigma_f S, with the windows summed in a fixed order.
+#include <cstdlib>
+
 #include "akm_internal.cuh"
 
 namespace akm {
@@ -8,39 +10,39 @@ namespace akm {
 cudaError_t launch_interp_d1_t8(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                               int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                              cudaStream_t s);
+                              const void* tma, cudaStream_t s);
 cudaError_t launch_interp_d1_t12(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                               int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                              cudaStream_t s);
+                              const void* tma, cudaStream_t s);
 cudaError_t launch_interp_d1_t16(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                               int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                              cudaStream_t s);
+                              const void* tma, cudaStream_t s);
 cudaError_t launch_interp_d2_t8(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                               int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                              cudaStream_t s);
+                              const void* tma, cudaStream_t s);
 cudaError_t launch_interp_d2_t12(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                               int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                              cudaStream_t s);
+                              const void* tma, cudaStream_t s);
 cudaError_t launch_interp_d2_t16(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                               int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                              cudaStream_t s);
+                              const void* tma, cudaStream_t s);
 cudaError_t launch_interp_d3_t8(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                               int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                              cudaStream_t s);
+                              const void* tma, cudaStream_t s);
 cudaError_t launch_interp_d3_t12(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                               int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                              cudaStream_t s);
+                              const void* tma, cudaStream_t s);
 cudaError_t launch_interp_d3_t16(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                               int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                               const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                              cudaStream_t s);
+                              const void* tma, cudaStream_t s);
 
 
 // Largest instantiated RHS chunk not exceeding r_remaining.
@@ -53,36 +55,89 @@ int interp_rc_for(int r_remaining) {
 
 cudaError_t launch_interp(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                           int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm, const double* H,
-                          int d, int taps, int ops, int r, int r0, int rc, double* part, long long n, cudaStream_t s) {
+                          int d, int taps, int ops, int r, int r0, int rc, double* part, long long n, const void* tma,
+                          cudaStream_t s) {
   if (n_items <= 0 && n_items_bin <= 0) return cudaSuccess;
   if (d == 1 && taps == 8)
     return launch_interp_d1_t8(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
-                                   r, r0, rc, part, n, s);
+                                   r, r0, rc, part, n, tma, s);
   if (d == 1 && taps == 12)
     return launch_interp_d1_t12(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
-                                   r, r0, rc, part, n, s);
+                                   r, r0, rc, part, n, tma, s);
   if (d == 1 && taps == 16)
     return launch_interp_d1_t16(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
-                                   r, r0, rc, part, n, s);
+                                   r, r0, rc, part, n, tma, s);
   if (d == 2 && taps == 8)
     return launch_interp_d2_t8(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
-                                   r, r0, rc, part, n, s);
+                                   r, r0, rc, part, n, tma, s);
   if (d == 2 && taps == 12)
     return launch_interp_d2_t12(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
-                                   r, r0, rc, part, n, s);
+                                   r, r0, rc, part, n, tma, s);
   if (d == 2 && taps == 16)
     return launch_interp_d2_t16(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
-                                   r, r0, rc, part, n, s);
+                                   r, r0, rc, part, n, tma, s);
   if (d == 3 && taps == 8)
     return launch_interp_d3_t8(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
-                                   r, r0, rc, part, n, s);
+                                   r, r0, rc, part, n, tma, s);
   if (d == 3 && taps == 12)
     return launch_interp_d3_t12(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
-                                   r, r0, rc, part, n, s);
+                                   r, r0, rc, part, n, tma, s);
   if (d == 3 && taps == 16)
     return launch_interp_d3_t16(dtab, items, n_items, items_bin, n_items_bin, Fb1, Fb2, sparse, u_sorted, perm, H, ops,
-                                   r, r0, rc, part, n, s);
+                                   r, r0, rc, part, n, tma, s);
   return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------- TMA tensor maps of H (k_interp_mma)
+// Per 3-D window w < kTmaWin: a 3-D map over the window's box of H with dims (values per node V,
+// axis-2 nodes L2, (axis-0, axis-1) rows L0*L1), element pitch 8 bytes, node pitch 8V bytes (V even:
+// 16-byte multiples), box (LDH, 2m, 2m) with LDH the kernel's padded plane row (values past V are
+// outside the tensor: TMA writes zeros there).  The driver entry point is looked up at run time.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+size_t interp_tma_maps_bytes() { return sizeof(TmaMaps); }
+
+bool interp_tma_build(const WinTable& tab, const double* H, int ops, int r, void* maps) {
+  static const bool off = getenv("AKM_INTERP_TMA") && atoi(getenv("AKM_INTERP_TMA")) == 0;
+  const int V = ops * r;
+  if (off || (V % 2) != 0 || tab.P > kTmaWin) return false;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  TmaMaps* tm = static_cast<TmaMaps*>(maps);
+  const int taps = 2 * tab.m;
+  const cuuint32_t ldh = (cuuint32_t)mma_ld(((V + 7) / 8) * 8);
+  for (int w = 0; w < tab.P; ++w) {
+    const WinGeom& g = tab.w[w];
+    if (g.d != 3) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)V, (cuuint64_t)g.L[2], (cuuint64_t)g.L[0] * g.L[1]};
+    const cuuint64_t strides[2] = {(cuuint64_t)V * 8, (cuuint64_t)g.L[2] * V * 8};
+    const cuuint32_t box[3] = {ldh, (cuuint32_t)taps, (cuuint32_t)taps};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    void* base = const_cast<double*>(H + g.tap_off * (long long)V);
+    if (enc(&tm->m[w], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
 }
 
 // ---------------------------------------------------------------- epilogue (S7)

@@ -7,6 +7,8 @@
 // scalar FP64 with the last axis sum-factorised).  Window weights come from the Chebyshev
 // polynomials of the window (window_taps / window_taps_estrin).
 #pragma once
+#include <cuda.h>
+
 #include "akm_internal.cuh"
 
 namespace akm {
@@ -25,12 +27,26 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int D, int TAPS, int OPS, int RC>
+// TMA staging (TMA = true): every footprint plane [o1][o2][v] is ONE cp.async.bulk.tensor.3d of the
+// window's tensor map (dims: values per node, axis-2 nodes, (axis-0, axis-1) rows; 16-byte node
+// pitch needs an even number of values per node), box [LDH][TAPS][T1]: the values past V fall
+// outside the tensor and arrive as zeros, which is exactly the padded plane layout of the cp.async
+// path.  One elected thread issues the copy; the plane's mbarrier (expect_tx) signals its arrival.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ bool mbar_try_wait(unsigned bar, unsigned phase) {
+  unsigned ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+  return ok != 0;
+}
+
+template <int D, int TAPS, int OPS, int RC, bool TMA = false>
 __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restrict__ tabp,
                                                     const WorkItem* __restrict__ items,
                                                     const double* __restrict__ u_sorted, const int* __restrict__ perm,
                                                     const double* __restrict__ H, int r, int r0,
-                                                    double* __restrict__ part, long long n) {
+                                                    double* __restrict__ part, long long n,
+                                                    const __grid_constant__ TmaMaps maps) {
   constexpr int V = OPS * RC;
   constexpr int NT = (V + 7) / 8;
   constexpr int LDH = mma_ld(NT * 8);
@@ -43,15 +59,37 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
   const WorkItem it = items[blockIdx.x];
   const WinGeom& g = tab.w[it.win];
   __shared__ double poly[TAPS * kPolyLen];
-  extern __shared__ double sm[];  // [2][SLAB][LDH]
+  __shared__ __align__(8) unsigned long long pbar[2];  // TMA: one mbarrier per plane buffer
+  extern __shared__ __align__(128) double sm[];  // [2][SLAB][LDH]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < TAPS * kPolyLen; idx += blockDim.x) poly[idx] = tab.poly[idx];
+  if (TMA && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&pbar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&pbar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  unsigned pphase[2] = {0u, 0u};
 
   const int cell0 = it.bin[0], cell1 = it.bin[1], cell2 = it.bin[2];
   const long long row_vals = (long long)OPS * r;
   const bool contiguous = (RC == r && r0 == 0);  // all V values of a node adjacent in H
   const long long L1g = g.L[1], L2g = g.L[2], toff = g.tap_off;
   auto stage = [&](int o0, double* buf) {
+    if constexpr (TMA) {
+      if (tid == 0) {
+        const int slot = (buf == sm) ? 0 : 1;
+        constexpr unsigned bytes = (unsigned)(SLAB * LDH * sizeof(double));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of buf -> async write
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&pbar[slot])),
+                     "r"(bytes) : "memory");
+        const int row = (int)((cell0 + o0) * L1g + cell1);
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+            ::"r"(smem_u32(buf)), "l"(&maps.m[it.win]), "r"(0), "r"(cell2), "r"(row), "r"(smem_u32(&pbar[slot]))
+            : "memory");
+      }
+      return;
+    }
     if (contiguous) {
       // each footprint row (o0, o1) is one run of TAPS * V consecutive doubles of H, copied by
       // warp o1 % 8 with consecutive lanes on consecutive doubles (immediate source offsets)
@@ -78,6 +116,7 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
     }
     cp_async_commit();
   };
+  if (TMA) __syncthreads();  // mbarriers initialised before the first copy
   stage(0, sm);
   __syncthreads();  // poly
 
@@ -132,13 +171,17 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
 
   for (int o0 = 0; o0 < T0; ++o0) {
     double* cur = sm + (o0 & 1) * SLAB * LDH;
-    if (o0 + 1 < T0) {
-      stage(o0 + 1, sm + ((o0 + 1) & 1) * SLAB * LDH);
-      cp_async_wait<1>();
+    if (o0 + 1 < T0) stage(o0 + 1, sm + ((o0 + 1) & 1) * SLAB * LDH);
+    if constexpr (TMA) {
+      const int slot = o0 & 1;
+      while (!mbar_try_wait(smem_u32(&pbar[slot]), pphase[slot])) {
+      }
+      pphase[slot] ^= 1u;
     } else {
-      cp_async_wait<0>();
+      if (o0 + 1 < T0) cp_async_wait<1>();
+      else cp_async_wait<0>();
+      __syncthreads();
     }
-    __syncthreads();
     double wa[MT];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) wa[mt] = w0s[warp * 16 + mt * 8 + (lane >> 2)][o0];
@@ -343,7 +386,7 @@ template <int D, int T>
 cudaError_t launch_interp_dt(const WinTable* dtab, const WorkItem* items, int n_items, const WorkItem* items_bin,
                              int n_items_bin, int Fb1, int Fb2, bool sparse, const double* u_sorted, const int* perm,
                              const double* H, int ops, int r, int r0, int rc, double* part, long long n,
-                             cudaStream_t s) {
+                             const void* tma, cudaStream_t s) {
 #define AKM_CASE(O, R)                                                                                              \
   if (ops == O && rc == R) {                                                                                        \
     if (O * R >= 8 && !sparse) {                                                                                    \
@@ -355,7 +398,22 @@ cudaError_t launch_interp_dt(const WinTable* dtab, const WorkItem* items, int n_
         if (e != cudaSuccess) return e;                                                                             \
         optin_mark(attr_set);                                                                                            \
       }                                                                                                             \
-      k_interp_mma<D, T, O, R><<<n_items, 256, smem, s>>>(dtab, items, u_sorted, perm, H, r, r0, part, n);         \
+      if constexpr (D == 3 && T == 12 && O == 2 && R == 11) {                                                     \
+        if (tma && rc == r && r0 == 0) {                                                                            \
+          static std::atomic<unsigned long long> attr_tma{0};                                                       \
+          if (!optin_done(attr_tma)) {                                                                              \
+            cudaError_t e = cudaFuncSetAttribute(k_interp_mma<D, T, O, R, true>,                                    \
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 128);     \
+            if (e != cudaSuccess) return e;                                                                         \
+            optin_mark(attr_tma);                                                                                   \
+          }                                                                                                         \
+          k_interp_mma<D, T, O, R, true><<<n_items, 256, smem, s>>>(dtab, items, u_sorted, perm, H, r, r0, part, n, \
+                                                                   *static_cast<const TmaMaps*>(tma));              \
+          return cudaGetLastError();                                                                                \
+        }                                                                                                           \
+      }                                                                                                             \
+      k_interp_mma<D, T, O, R><<<n_items, 256, smem, s>>>(dtab, items, u_sorted, perm, H, r, r0, part, n,         \
+                                                         TmaMaps{});                                               \
     } else {                                                                                                        \
       if (n_items_bin <= 0) return cudaSuccess;                                                                     \
       int whole = 0;                                                                                                \

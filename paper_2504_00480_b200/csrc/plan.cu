@@ -128,6 +128,7 @@ struct akm_plan {
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
   DevBuf reg_coef, bin_start;  // regularisation polynomials [w][op][kRegStride]; per-window bin start tables
   DevBuf cell_tab, nfV;        // near field: (start, count) per (cell, class) slot; bin-sorted copy of V
+  std::vector<unsigned char> tma_maps = std::vector<unsigned char>(interp_tma_maps_bytes());  // TmaMaps (host)
   DevBuf stageV, stageY, stageL, stageS;
   DevBuf crossV, crossY;  // akm_kernel_cross_mvm: zero-padded V and the union's product
   DevBuf gX, gP, gB2, gD1, gD2, gState;  // akm_gradient_diag: block PCG and derivative products
@@ -805,11 +806,14 @@ static akm_status enqueue_finish(akm_plan* plan, const double* grid, const doubl
         }
         continue;
       }
+      const bool tma = rc == r && r0 == 0 &&
+                       interp_tma_build(plan->tab, plan->H.as<double>(), ops, r, plan->tma_maps.data());
       AKM_CK(launch_interp(dtab, plan->items_i[set].as<WorkItem>() + grp.sl[set].interp_begin, grp.sl[set].interp_count,
                            plan->items_ib[set].as<WorkItem>() + grp.sl[set].interp_bin_begin, grp.sl[set].interp_bin_count,
                            grp.d >= 2 ? grp.F : 1, grp.F, grp.sl[set].sparse, plan->u_sorted.as<double>(), plan->perm.as<int>(),
                            plan->H.as<double>(), grp.d,
-                           2 * plan->m, ops, r, r0, rc, plan->part.as<double>(), n, s));
+                           2 * plan->m, ops, r, r0, rc, plan->part.as<double>(), n,
+                           tma ? plan->tma_maps.data() : nullptr, s));
       if (grp.sl[set].interp_count > 0) {
         ++plan->launches;
         ++plan->interp_launches;
