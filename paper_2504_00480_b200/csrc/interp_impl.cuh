@@ -59,16 +59,19 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
   const WorkItem it = items[blockIdx.x];
   const WinGeom& g = tab.w[it.win];
   __shared__ double poly[TAPS * kPolyLen];
-  __shared__ __align__(8) unsigned long long pbar[2];  // TMA: one mbarrier per plane buffer
+  __shared__ __align__(8) unsigned long long pbar[2];  // TMA: "full" mbarrier per plane buffer
+  __shared__ __align__(8) unsigned long long ebar[2];  // TMA: "empty" mbarrier per plane buffer (8 warp arrivals)
   extern __shared__ __align__(128) double sm[];  // [2][SLAB][LDH]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < TAPS * kPolyLen; idx += blockDim.x) poly[idx] = tab.poly[idx];
   if (TMA && tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&pbar[0])) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&pbar[1])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" ::"r"(smem_u32(&ebar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" ::"r"(smem_u32(&ebar[1])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  unsigned pphase[2] = {0u, 0u};
+  unsigned pphase[2] = {0u, 0u}, ephase[2] = {0u, 0u};
 
   const int cell0 = it.bin[0], cell1 = it.bin[1], cell2 = it.bin[2];
   const long long row_vals = (long long)OPS * r;
@@ -118,6 +121,7 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
   };
   if (TMA) __syncthreads();  // mbarriers initialised before the first copy
   stage(0, sm);
+  if (TMA && T0 > 1) stage(1, sm + SLAB * LDH);  // TMA: both buffers in flight from the start
   __syncthreads();  // poly
 
   __shared__ double w1s[8 * MT * 8][T1];  // [point of the CTA][o1]
@@ -171,7 +175,7 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
 
   for (int o0 = 0; o0 < T0; ++o0) {
     double* cur = sm + (o0 & 1) * SLAB * LDH;
-    if (o0 + 1 < T0) stage(o0 + 1, sm + ((o0 + 1) & 1) * SLAB * LDH);
+    if (!TMA && o0 + 1 < T0) stage(o0 + 1, sm + ((o0 + 1) & 1) * SLAB * LDH);
     if constexpr (TMA) {
       const int slot = o0 & 1;
       while (!mbar_try_wait(smem_u32(&pbar[slot]), pphase[slot])) {
@@ -219,7 +223,21 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
         }
       }
     }
-    __syncthreads();  // buffer `cur` is re-filled two planes later
+    if constexpr (TMA) {
+      // release the buffer: each warp arrives on its "empty" barrier; thread 0 waits for all 8 and
+      // refills it with plane o0 + 2 (no CTA-wide barrier per plane)
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&ebar[o0 & 1])) : "memory");
+      if (tid == 0 && o0 + 2 < T0) {
+        while (!mbar_try_wait(smem_u32(&ebar[o0 & 1]), ephase[o0 & 1])) {
+        }
+        ephase[o0 & 1] ^= 1u;
+        stage(o0 + 2, cur);
+      }
+    } else {
+      __syncthreads();  // buffer `cur` is re-filled two planes later
+    }
   }
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
