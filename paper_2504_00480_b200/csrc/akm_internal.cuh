@@ -30,7 +30,9 @@ constexpr int kKrMaxR = 32;               // Krylov driver: 1 CG column + <= 31 
 constexpr int kKrMaxSteps = 64;           // Lanczos steps
 constexpr int kKrMaxIters = 1024;         // CG iterations
 constexpr int kRegMaxP = 8;               // regularisation order p (regularize.cu)
-constexpr int kRegStride = 3 * kRegMaxP;  // per (window, operator): T_I (p) then T_B (2p) coefficients
+constexpr int kRegNfOff = 3 * kRegMaxP;   // per (window, operator): T_I (p) then T_B (2p) coefficients,
+constexpr int kRegNfLen = 24;             // then the near-field series: degree (or -1), coefficients
+constexpr int kRegStride = kRegNfOff + kRegNfLen;
 
 // Per-window geometry passed (by value, inside WinTable) to kernels.
 struct WinGeom {

@@ -111,6 +111,38 @@ __global__ void k_reg_coef(int family, double ell, double eps_I, double eps_B, i
     }
     small_solve(p, A, b);
     for (int k = 0; k < p; ++k) o[k] = b[k];
+    // Near-field weight (kappa - T_I)(r), r < eps_I, as one polynomial in t = s (Matern) or s^2
+    // (Gaussian), s = r / eps_I: kappa = pre * t^op * exp(-x t) (x = eps_I/ell resp. eps_I^2/(2 ell^2);
+    // pre = 1 for kappa, eps_I/ell^2 resp. eps_I^2/ell^3 for kappa^der) expanded in its Taylor series,
+    // truncated where the tail bound pre x^(J+1)/(J+1)! e^x (t <= 1) drops below 1e-17, minus T_I.
+    // nf[0] = degree, or -1 where the series is too long or x > 1.5 (cancellation): the kernel then
+    // evaluates kappa directly.
+    double* nf = o + kRegNfOff;
+    const double x = (family == 0) ? eps_I * eps_I / (2.0 * ell * ell) : eps_I / ell;
+    const double pre = (op == 0) ? 1.0 : ((family == 0) ? eps_I * eps_I / (ell * ell * ell) : eps_I / (ell * ell));
+    const int tdeg = (family == 0) ? p - 1 : 2 * p - 2;  // degree of T_I in t
+    for (int k = 0; k < kRegNfLen; ++k) nf[k] = 0.0;
+    nf[0] = -1.0;
+    if (x <= 1.5) {
+      const double ex = exp(x);
+      double term = pre;  // pre x^j / j!
+      int J = 0;
+      double c[kRegNfLen - 1];
+      for (int k = 0; k < kRegNfLen - 1; ++k) c[k] = 0.0;
+      bool ok = false;
+      for (; J + op < kRegNfLen - 1; ++J) {
+        c[J + op] = ((J & 1) ? -term : term);
+        const double next = term * x / (double)(J + 1);
+        if (next * ex < 1e-17) { ok = true; break; }
+        term = next;
+      }
+      if (ok) {
+        const int deg = max(J + op, tdeg);
+        for (int k = 0; k < p; ++k) c[(family == 0) ? k : 2 * k] -= o[k];
+        nf[0] = (double)deg;
+        for (int k = 0; k <= deg; ++k) nf[1 + k] = c[k];
+      }
+    }
   }
   if (eps_B > 0.0) {
     // t = 0: c_q = eps_B^q f^(q)(1/2 - eps_B) / q!;  t = 1: value f(1/2), derivatives 0
@@ -202,15 +234,16 @@ cudaError_t launch_kernel_samples_reg(int family, int d, int N, double ell_eff, 
 }
 
 // ------------------------------------------------------------------ near-field correction
-// One CTA per interpolation item (<= 128 target points of one bin).  Warp 0 lists, in a fixed order,
-// the (cell, class) point ranges of every grid cell whose box comes closer than eps_I to the bin's box
-// (ballot compaction over the candidate cells); the CTA then streams those source points through
-// shared memory in tiles of kNfTile (scaled coordinates and the rc values of their rows of the
-// bin-sorted copy of V, so every tile load is contiguous).  Each thread accumulates, for its target,
-// sum_{r_ij < eps_I} (kappa - T_I)(r_ij) v_j for kappa (slot K) and kappa^der / c_w (slot L) and adds it
-// to the window's partial output (written by the interpolation before, read by the epilogue after).
+// One CTA per interpolation item (<= 128 target points of one bin), each warp on its own 32 targets:
+// it lists, in a fixed order, the (cell, class) point ranges of every grid cell whose box comes
+// closer than eps_I to the bounding box of its targets (ballot compaction over the candidate cells),
+// then streams those source points through a warp-private slice of shared memory, 32 at a time
+// (scaled coordinates and the rc values of their rows of the bin-sorted copy of V).  Each lane
+// accumulates, for its target, sum_{r_ij < eps_I} (kappa - T_I)(r_ij) v_j for kappa (slot K) and
+// kappa^der / c_w (slot L) -- the weights as one series in r (k_reg_coef) where it converges fast,
+// else kappa evaluated directly -- and adds it to the window's partial output (written by the
+// interpolation before, read by the epilogue after).
 constexpr int kNfThreads = 128;
-constexpr int kNfTile = 128;
 constexpr int kNfMaxRc = 12;
 
 __global__ void k_sort_v(long long n, int P, int r, const int* __restrict__ perm, const double* __restrict__ V,
@@ -229,13 +262,29 @@ __global__ void k_sort_v(long long n, int P, int r, const int* __restrict__ perm
 // (__syncwarp only: no CTA barrier, a warp with no targets left is done).
 constexpr int kNfWarps = kNfThreads / 32;
 constexpr int kNfWarpRanges = 256;
-__global__ void __launch_bounds__(kNfThreads) k_near_field(
+constexpr int kNfUnroll = 4;
+constexpr int kNfCoef = 28;  // series coefficients 0..22, zero-padded to 27 (Horner in steps of 4)
+
+// sqrt(x) for x in [0, 1]: rsqrt.approx, one Newton step, then a residual correction (t + y (x - t^2)/2)
+// to within an ulp; x is clamped away from 0 (t(0) = 1e-140 instead of 0: below rounding in the weight)
+__device__ __forceinline__ double sqrt_unit(double x) {
+  x = fmax(x, 1e-280);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  const double t = x * y;
+  return fma(0.5 * y, fma(-t, t, x), t);
+}
+// HAS_L: the kappa^der operator is applied too (its 12 accumulators cost registers otherwise).
+template <bool HAS_L>
+__global__ void __launch_bounds__(kNfThreads, HAS_L ? 3 : 5) k_near_field(
     const WinTable* __restrict__ tabp, const WorkItem* __restrict__ items, const int2* __restrict__ cell_tab,
     const long long* __restrict__ cell_off, const double* __restrict__ u_sorted, const int* __restrict__ perm,
     const double* __restrict__ Vs, long long n, int r0, int rc, int r_total, int ops, int slotK, int slotL, int family,
     double ell, double eps_I, int p, const double* __restrict__ coef, double* __restrict__ part) {
   __shared__ double su_all[kNfWarps][3][32];
-  __shared__ double sv_all[kNfWarps][32 * kNfMaxRc];
+  __shared__ __align__(16) double sv_all[kNfWarps][32 * kNfMaxRc];
+  __shared__ double sc_all[kNfWarps][2][kNfCoef];
   __shared__ int rstart_all[kNfWarps][kNfWarpRanges], rpre_all[kNfWarps][kNfWarpRanges + 1];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const WorkItem it = items[blockIdx.x];
@@ -263,20 +312,43 @@ __global__ void __launch_bounds__(kNfThreads) k_near_field(
   double ut[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) ut[a] = (a >= 3 - g.d) ? uw[(long long)a * n + pos] : 0.0;
-  double accK[kNfMaxRc], accL[kNfMaxRc];
+  double accK[kNfMaxRc], accL[HAS_L ? kNfMaxRc : 1];
 #pragma unroll
-  for (int c = 0; c < kNfMaxRc; ++c) accK[c] = accL[c] = 0.0;
-  // candidate cells: the box of cells within ceil(E) of the bin, enumerated in a fixed order
-  const int Ke = (int)ceil(E);
-  int lo[3], ext[3], blo[3], bhi[3];
+  for (int c = 0; c < kNfMaxRc; ++c) accK[c] = 0.0;
+#pragma unroll
+  for (int c = 0; c < (HAS_L ? kNfMaxRc : 1); ++c) accL[c] = 0.0;
+  // the near-field series of both operators (k_reg_coef), if usable, in warp-private shared memory
+  const int degK = (int)aK[kRegNfOff], degL = HAS_L ? (int)aL[kRegNfOff] : 0;
+  const bool poly = degK >= 0 && degL >= 0;
+  const int degK4 = (degK + 3) & ~3, degL4 = (degL + 3) & ~3;  // Horner runs in steps of 4
+  double (*sc)[kNfCoef] = sc_all[wid];
+  if (lane < kNfCoef) {
+    sc[0][lane] = (lane < kRegNfLen - 1) ? aK[kRegNfOff + 1 + lane] : 0.0;
+    if constexpr (HAS_L) sc[1][lane] = (lane < kRegNfLen - 1) ? aL[kRegNfOff + 1 + lane] : 0.0;
+  }
+  const double inv_E2 = 1.0 / E2;
+  // candidate cells: those whose box comes closer than eps_I to the bounding box of this warp's
+  // targets (cell c of axis a covers u - (box_lo + m - 1) in [c, c + 1)), in a fixed order; the
+  // index window is widened by one cell and the gap test given a relative slack of 1e-12, so rounding
+  // can only add candidates (the per-pair test q2 < E2 decides)
+  int lo[3], ext[3];
+  double tlo[3], thi[3];
+#pragma unroll
   for (int a = 0; a < 3; ++a) {
     const bool real = a >= 3 - g.d;
-    blo[a] = real ? it.bin[a] * g.B : 0;
-    bhi[a] = real ? min(blo[a] + g.B, g.ncell[a]) - 1 : 0;
-    lo[a] = real ? max(0, blo[a] - Ke) : 0;
-    const int hi = real ? min(g.ncell[a] - 1, bhi[a] + Ke) : 0;
-    ext[a] = hi - lo[a] + 1;
+    double mn = active ? ut[a] : 1e300, mx = active ? ut[a] : -1e300;
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const double off = (double)(g.box_lo[a] + tab.m - 1);
+    tlo[a] = real ? mn - off : 0.0;
+    thi[a] = real ? mx - off : 0.0;
+    lo[a] = real ? max(0, (int)floor(tlo[a] - E) - 1) : 0;
+    const int hi = real ? min(g.ncell[a] - 1, (int)floor(thi[a] + E) + 1) : 0;
+    ext[a] = max(0, hi - lo[a] + 1);
   }
+  const double E2s = E2 * (1.0 + 1e-12);
   const int total = ext[0] * ext[1] * ext[2];
   for (int q0 = 0; q0 < total;) {
     // the (start, count) ranges of the next cells closer than eps_I to the bin (ballot compaction)
@@ -288,11 +360,13 @@ __global__ void __launch_bounds__(kNfThreads) k_near_field(
       if (qq < total) {
         const int cc[3] = {lo[0] + qq / (ext[1] * ext[2]), lo[1] + (qq / ext[2]) % ext[1], lo[2] + qq % ext[2]};
         double gap2 = 0.0;
+#pragma unroll
         for (int a = 0; a < 3; ++a) {
-          const double gp = fmax(0.0, fmax((double)(blo[a] - (cc[a] + 1)), (double)(cc[a] - (bhi[a] + 1))));
+          const double gp =
+              (a >= 3 - g.d) ? fmax(0.0, fmax(tlo[a] - (double)(cc[a] + 1), (double)cc[a] - thi[a])) : 0.0;
           gap2 += gp * gp;
         }
-        near = gap2 < E2;
+        near = gap2 < E2s;
         if (near) {
           const long long slot = cell_off[w] + 2 * (((long long)cc[0] * g.ncell[1] + cc[1]) * g.ncell[2] + cc[2]);
           const int2 a0 = cell_tab[slot], a1 = cell_tab[slot + 1];
@@ -332,23 +406,87 @@ __global__ void __launch_bounds__(kNfThreads) k_near_field(
         const int sp = rstart[a] + (f - rpre[a]);
 #pragma unroll
         for (int t = 0; t < 3; ++t) su[t][lane] = (t >= 3 - g.d) ? uw[(long long)t * n + sp] : 0.0;
-        for (int c = 0; c < rc; ++c) sv[lane * kNfMaxRc + c] = vw[(long long)sp * r_total + c];
+#pragma unroll
+        for (int c = 0; c < kNfMaxRc; ++c) sv[lane * kNfMaxRc + c] = (c < rc) ? vw[(long long)sp * r_total + c] : 0.0;
+      } else {  // padding sources: far away (weight 0 for every target), zero values
+#pragma unroll
+        for (int t = 0; t < 3; ++t) su[t][lane] = 1e150;
+#pragma unroll
+        for (int c = 0; c < kNfMaxRc; ++c) sv[lane * kNfMaxRc + c] = 0.0;
       }
       __syncwarp();
-      if (active) {
-        for (int j = 0; j < cnt; ++j) {
-          const double d0 = ut[0] - su[0][j], d1 = ut[1] - su[1][j], d2 = ut[2] - su[2][j];
-          const double q2 = d0 * d0 + d1 * d1 + d2 * d2;
-          if (q2 >= E2) continue;
-          const double r = sqrt(q2) * inv_ng;
-          const double s2 = r * r * inv_eps2;
-          const double wK = kernel_plain(family, 0, ell_eff, r) - reg_inner(aK, p, s2);
-          const double wL = (slotL >= 0) ? (kernel_plain(family, 1, ell_eff, r) - reg_inner(aL, p, s2)) * inv_c : 0.0;
+      // kNfUnroll sources at a time (independent weight chains); every lane takes part, lanes without
+      // a target or out of range with q2 = E2 (weight 0), and groups no lane needs are skipped
+      for (int j0 = 0; j0 < cnt; j0 += kNfUnroll) {
+        double q2[kNfUnroll];
+        bool in[kNfUnroll], any = false;
 #pragma unroll
-          for (int c = 0; c < kNfMaxRc; ++c) {
-            if (c < rc) {
-              accK[c] = fma(wK, sv[j * kNfMaxRc + c], accK[c]);
-              accL[c] = fma(wL, sv[j * kNfMaxRc + c], accL[c]);
+        for (int u = 0; u < kNfUnroll; ++u) {
+          const int j = j0 + u;  // < 32: rows cnt..31 hold padding sources
+          const double d0 = ut[0] - su[0][j], d1 = ut[1] - su[1][j], d2 = ut[2] - su[2][j];
+          q2[u] = fma(d2, d2, fma(d1, d1, d0 * d0));
+          in[u] = active && q2[u] < E2;
+          any |= in[u];
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;
+        double wK[kNfUnroll], wL[kNfUnroll];
+        if (poly) {
+          double t[kNfUnroll];
+#pragma unroll
+          for (int u = 0; u < kNfUnroll; ++u) {
+            const double s2 = fmin(q2[u] * inv_E2, 1.0);
+            t[u] = (family == 0) ? s2 : sqrt_unit(s2);
+            wK[u] = sc[0][degK4];
+            if constexpr (HAS_L) wL[u] = sc[1][degL4];
+          }
+          // Horner from the padded degree (the coefficients past the degree are zero: exact)
+          for (int k = degK4 - 4; k >= 0; k -= 4) {
+#pragma unroll
+            for (int kk = 3; kk >= 0; --kk) {
+              const double c = sc[0][k + kk];
+#pragma unroll
+              for (int u = 0; u < kNfUnroll; ++u) wK[u] = fma(wK[u], t[u], c);
+            }
+          }
+          if constexpr (HAS_L) {
+            for (int k = degL4 - 4; k >= 0; k -= 4) {
+#pragma unroll
+              for (int kk = 3; kk >= 0; --kk) {
+                const double c = sc[1][k + kk];
+#pragma unroll
+                for (int u = 0; u < kNfUnroll; ++u) wL[u] = fma(wL[u], t[u], c);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kNfUnroll; ++u) {
+            wK[u] = in[u] ? wK[u] : 0.0;
+            if constexpr (HAS_L) wL[u] = in[u] ? wL[u] * inv_c : 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kNfUnroll; ++u) {
+            wK[u] = 0.0;
+            if constexpr (HAS_L) wL[u] = 0.0;
+            if (in[u]) {
+              const double r = sqrt(q2[u]) * inv_ng;
+              const double s2 = r * r * inv_eps2;
+              wK[u] = kernel_plain(family, 0, ell_eff, r) - reg_inner(aK, p, s2);
+              if constexpr (HAS_L) wL[u] = (kernel_plain(family, 1, ell_eff, r) - reg_inner(aL, p, s2)) * inv_c;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kNfUnroll; ++u) {  // all kNfMaxRc columns (zero-padded past rc)
+          const double2* vrow = reinterpret_cast<const double2*>(sv + (j0 + u) * kNfMaxRc);
+#pragma unroll
+          for (int c2 = 0; c2 < kNfMaxRc / 2; ++c2) {
+            const double2 v = vrow[c2];
+            accK[2 * c2] = fma(wK[u], v.x, accK[2 * c2]);
+            accK[2 * c2 + 1] = fma(wK[u], v.y, accK[2 * c2 + 1]);
+            if constexpr (HAS_L) {
+              accL[2 * c2] = fma(wL[u], v.x, accL[2 * c2]);
+              accL[2 * c2 + 1] = fma(wL[u], v.y, accL[2 * c2 + 1]);
             }
           }
         }
@@ -363,7 +501,7 @@ __global__ void __launch_bounds__(kNfThreads) k_near_field(
   for (int c = 0; c < kNfMaxRc; ++c) {
     if (c < rc) {
       if (slotK >= 0) out[(long long)slotK * r_total + c] += accK[c];
-      if (slotL >= 0) out[(long long)slotL * r_total + c] += accL[c];
+      if constexpr (HAS_L) out[(long long)slotL * r_total + c] += accL[HAS_L ? c : 0];
     }
   }
 }
@@ -381,8 +519,9 @@ cudaError_t launch_near_field(const WinTable* dtab, const WorkItem* items, int n
   }
   for (int r0 = 0; r0 < r; r0 += kNfMaxRc) {
     const int rc = (r - r0 < kNfMaxRc) ? r - r0 : kNfMaxRc;
-    k_near_field<<<n_items, kNfThreads, 0, s>>>(dtab, items, cell_tab, cell_off, u_sorted, perm, Vs, n, r0, rc, r, ops,
-                                                slotK, slotL, family, ell, eps_I, p, coef, part);
+    auto kern = (slotL >= 0) ? k_near_field<true> : k_near_field<false>;
+    kern<<<n_items, kNfThreads, 0, s>>>(dtab, items, cell_tab, cell_off, u_sorted, perm, Vs, n, r0, rc, r, ops, slotK,
+                                        slotL, family, ell, eps_I, p, coef, part);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

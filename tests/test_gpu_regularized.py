@@ -52,17 +52,24 @@ def run(akm, X, windows, family, th, V, N=32, m=6, eps_I=0.0, p=0, ops=("K", "de
 
 
 # tolerance: the NFFT window error (m = 6: ~1e-12, m = 8: ~1e-14) plus the rounding of the near-field
-# weights kappa - T_I, whose polynomial terms cancel to ~1e-11 of the product at p = 8
-@pytest.mark.parametrize("family,m,N,eps_I,p,tol", [(1, 6, 32, 1 / 16, 4, 1e-9), (1, 8, 32, 1 / 32, 3, 1e-11),
-                                                    (0, 6, 32, 1 / 32, 4, 1e-9), (1, 6, 16, 0.0, 4, 1e-9),
-                                                    (1, 8, 32, 1 / 8, 8, 1e-10)])
-def test_vs_regularised_oracle(akm, family, m, N, eps_I, p, tol):
+# weights kappa - T_I, whose polynomial terms cancel to ~1e-11 of the product at p = 8.
+# ell = 0.45 puts x = eps_I / ell_eff (Matern) or eps_I^2 / (2 ell_eff^2) (Gaussian) below 1.5, where the
+# near field evaluates its weights as one truncated series (regularize.cu k_reg_coef); ell = 0.05
+# puts it above, where kappa is evaluated directly: both paths against the oracle's direct sums.
+@pytest.mark.parametrize("family,m,N,eps_I,p,tol,ell", [(1, 6, 32, 1 / 16, 4, 1e-9, 0.45),
+                                                        (1, 8, 32, 1 / 32, 3, 1e-11, 0.45),
+                                                        (0, 6, 32, 1 / 32, 4, 1e-9, 0.45),
+                                                        (1, 6, 16, 0.0, 4, 1e-9, 0.45),
+                                                        (1, 8, 32, 1 / 8, 8, 1e-10, 0.45),
+                                                        (1, 6, 32, 1 / 16, 4, 1e-9, 0.05),
+                                                        (0, 6, 32, 1 / 16, 3, 1e-9, 0.05)])
+def test_vs_regularised_oracle(akm, family, m, N, eps_I, p, tol, ell):
     rng = np.random.default_rng(int(1000 * eps_I) + m + p)
     n = 1500
     X = rng.random((n, 7))
     windows = [(0, 1, 2), (3, 4), (6,)]
     V = rng.standard_normal((n, 3))
-    th = (0.8, 0.45, 0.2)
+    th = (0.8, ell, 0.2)
     ops = ("K", "dell", "dsf")
     out, _ = run(akm, X, windows, family, th, V, N, m, eps_I, p, ops)
     want = R.additive_fastsum_R(X, windows, family, th, V, N, 1.0 / 16, eps_I, p, ops=ops)
