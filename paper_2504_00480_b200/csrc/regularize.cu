@@ -266,9 +266,9 @@ constexpr int kNfUnroll = 4;
 constexpr int kNfCoef = 28;  // series coefficients 0..22, zero-padded to 27 (Horner in steps of 4)
 
 // sqrt(x) for x in [0, 1]: rsqrt.approx, one Newton step, then a residual correction (t + y (x - t^2)/2)
-// to within an ulp; x is clamped away from 0 (t(0) = 1e-140 instead of 0: below rounding in the weight)
+// to within an ulp; x is moved off 0 by 1e-280 (t(0) = 1e-140 instead of 0: below rounding in the weight)
 __device__ __forceinline__ double sqrt_unit(double x) {
-  x = fmax(x, 1e-280);
+  x += 1e-280;
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   y = y * fma(-0.5 * x, y * y, 1.5);
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kNfThreads, HAS_L ? 3 : 5) k_near_field(
           double t[kNfUnroll];
 #pragma unroll
           for (int u = 0; u < kNfUnroll; ++u) {
-            const double s2 = fmin(q2[u] * inv_E2, 1.0);
+            const double s2 = in[u] ? q2[u] * inv_E2 : 1.0;  // < 1 where the weight is used
             t[u] = (family == 0) ? s2 : sqrt_unit(s2);
             wK[u] = sc[0][degK4];
             if constexpr (HAS_L) wL[u] = sc[1][degL4];
