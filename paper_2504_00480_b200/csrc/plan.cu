@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdarg>
@@ -14,6 +15,7 @@
 #include <cstring>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -52,6 +54,30 @@ struct DevBuf {
   T* as() const { return static_cast<T*>(p); }
 };
 
+// page-locked host staging, grow-only (kept across set_theta calls: no page faults, async DMA)
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMallocHost(&p, need);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      return e;
+    }
+    bytes = need;
+    return cudaSuccess;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
 struct ItemSlice {  // a group's slice of the concatenated work items of one item set
   int spread_begin = 0, spread_count = 0;
   int interp_begin = 0, interp_count = 0;
@@ -66,6 +92,50 @@ struct Group {  // windows sharing (d, F) -> one spread / interp launch
 };
 
 }  // namespace
+
+// One work-item list, built in page-locked memory (its upload is an async copy)
+struct HostItems {
+  PinnedBuf buf;
+  size_t count = 0;
+  WorkItem* data() const { return buf.as<WorkItem>(); }
+  size_t size() const { return count; }
+  bool empty() const { return count == 0; }
+};
+
+// Host scratch of the bin sort, kept across set_theta calls (cleared, capacity kept): re-allocating
+// these megabytes per call costs more in page faults than the loops that fill them.
+struct OccCell {
+  int c0, c1, c2, v;
+};
+struct BinScratch {
+  std::vector<std::vector<WorkItem>> its_s[2], its_i[2], its_ib[2];  // [set][window]
+  std::vector<std::vector<int>> bst;                                   // [window] bin starts
+  std::vector<std::vector<OccCell>> occ;                               // [window] occupied cells
+  std::vector<std::vector<long long>> bc, bcnt;                        // [window] per-bin counts
+  std::vector<WorkItem> gs, gi, gib, tmp;                              // group concatenation, sort
+  std::vector<int> pos;                                                // counting sort
+  std::vector<int> bstart;                                             // all windows' bin starts
+  void resize(int P) {
+    for (int set = 0; set < 2; ++set) {
+      its_s[set].resize(P);
+      its_i[set].resize(P);
+      its_ib[set].resize(P);
+      for (int w = 0; w < P; ++w) {
+        its_s[set][w].clear();
+        its_i[set][w].clear();
+        its_ib[set][w].clear();
+      }
+    }
+    bst.resize(P);
+    occ.resize(P);
+    bc.resize(P);
+    bcnt.resize(P);
+    for (int w = 0; w < P; ++w) {
+      bst[w].clear();
+      occ[w].clear();
+    }
+  }
+};
 
 struct akm_plan {
   int device = 0;
@@ -116,7 +186,7 @@ struct akm_plan {
   std::vector<double> c_w, c_w_binned;      // current scale, scale the bins were built for
   WinTable tab{};                           // host copy
   PolyParam poly_param{};                   // window polynomials, passed to kernels by value
-  std::vector<WorkItem> items_spread[2], items_interp[2], items_interp_bin[2];  // [item set]
+  HostItems items_spread[2], items_interp[2], items_interp_bin[2];  // [item set]
   std::vector<Group> groups;
   std::vector<long long> occupied, maxbin;
   long long total_taps = 0, szA1 = 0, szA2 = 0, szA3 = 0, szC = 0, szC2 = 0, szTW = 0, szD = 0;
@@ -128,6 +198,11 @@ struct akm_plan {
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
   DevBuf reg_coef, bin_start;  // regularisation polynomials [w][op][kRegStride]; per-window bin start tables
   DevBuf cell_tab, nfV;        // near field: (start, count) per (cell, class) slot; bin-sorted copy of V
+  PinnedBuf h_hist, h_cell_off;  // host: points and sorted start per (cell, class) slot of the last bin sort
+  long long h_ncells = 0;
+  bool cell_tab_ok = false;      // cell_tab matches the last bin sort (built on demand: near field only)
+  std::vector<int2> h_cell_tab;
+  BinScratch bs;
   std::vector<unsigned char> tma_maps = std::vector<unsigned char>(interp_tma_maps_bytes());  // TmaMaps (host)
   DevBuf stageV, stageY, stageL, stageS;
   DevBuf crossV, crossY;  // akm_kernel_cross_mvm: zero-padded V and the union's product
@@ -269,25 +344,78 @@ cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, 
 
 }  // namespace
 
-// Work items ordered by decreasing point count, ties kept in their order (= std::stable_sort with
-// a.count > b.count): a counting sort, O(items + max count).
-static void sort_larger_first(std::vector<WorkItem>& v) {
-  if (v.size() < 2) return;
+// Appends the work items of `src` (concatenated in order) to `dst` ordered by decreasing point count,
+// ties kept in their order (= std::stable_sort with a.count > b.count): a counting sort,
+// O(items + max count).  Returns the number appended.
+static size_t append_larger_first(const std::vector<const std::vector<WorkItem>*>& src, HostItems& dst,
+                                  std::vector<int>& pos) {
+  size_t total = 0;
   int mx = 0;
-  for (const WorkItem& it : v) mx = std::max(mx, it.count);
-  std::vector<int> pos((size_t)mx + 2, 0);
-  for (const WorkItem& it : v) ++pos[(size_t)(mx - it.count) + 1];
+  for (const auto* v : src) {
+    total += v->size();
+    for (const WorkItem& it : *v) mx = std::max(mx, it.count);
+  }
+  const size_t base = dst.count;
+  if (!total) return 0;
+  WorkItem* out = dst.data();  // capacity ensured by the caller
+  pos.assign((size_t)mx + 2, 0);
+  for (const auto* v : src)
+    for (const WorkItem& it : *v) ++pos[(size_t)(mx - it.count) + 1];
   for (int i = 1; i <= mx + 1; ++i) pos[i] += pos[i - 1];
-  std::vector<WorkItem> out(v.size());
-  for (const WorkItem& it : v) out[pos[mx - it.count]++] = it;
-  v.swap(out);
+  for (const auto* v : src)
+    for (const WorkItem& it : *v) out[base + pos[mx - it.count]++] = it;
+  dst.count += total;
+  return total;
 }
 
 // ================================================================== geometry / binning
 // Build per-window boxes for the current c_w, histogram the points per cell on the device,
 // choose the bin edge B per window from the histogram, lay the cells out bin-major, scatter.
+// (start, count) of every (cell, class) slot in the window-relative sorted order of the last bin
+// sort, for the near-field correction; built on demand (only kappa_R's inner part reads it)
+static akm_status ensure_cell_tab(akm_plan* plan, cudaStream_t s) {
+  if (plan->cell_tab_ok) return AKM_OK;
+  const long long nc = std::max<long long>(plan->h_ncells, 1);
+  const int* hist = plan->h_hist.as<int>();
+  const int* off = plan->h_cell_off.as<int>();
+  plan->h_cell_tab.resize(nc);
+  for (long long q = 0; q < plan->h_ncells; ++q) plan->h_cell_tab[q] = make_int2(hist[q] ? off[q] : 0, hist[q]);
+  AKM_CK(plan->cell_tab.ensure(sizeof(int2) * nc));
+  AKM_CK(cudaMemcpyAsync(plan->cell_tab.p, plan->h_cell_tab.data(), sizeof(int2) * nc, cudaMemcpyHostToDevice, s));
+  AKM_CK(cudaStreamSynchronize(s));
+  plan->cell_tab_ok = true;
+  return AKM_OK;
+}
+
+static std::string strf(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  return buf;
+}
+
+// AKM_SETUP_TIMES=1: the stages of set_theta / rebuild_bins on stderr (stream synchronised at each mark)
+struct SetupTimer {
+  cudaStream_t s;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit SetupTimer(cudaStream_t st) : s(st), on(std::getenv("AKM_SETUP_TIMES") != nullptr) {
+    if (on) t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[akm setup] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   NvtxRange nvtx("akm S0 bin sort");
+  SetupTimer tm(s);
   ++plan->epoch;
   const int P = plan->P, m = plan->m, n_g = plan->n_g;
   const long long n = plan->n;
@@ -340,19 +468,24 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   AKM_CK(launch_scale_and_key(plan->Xc.as<double>(), n, nf, tab, plan->dtab.as<WinTable>(), plan->u_tmp.as<double>(),
                               nullptr, plan->hist.as<int>(), plan->hist_off.as<long long>(), plan->err_flag.as<int>(),
                               plan->n_split, s));
-  std::vector<int> hist(std::max<long long>(ncells, 1));
+  AKM_CK(plan->h_hist.ensure(sizeof(int) * std::max<long long>(ncells, 1)));
+  AKM_CK(plan->h_cell_off.ensure(sizeof(int) * std::max<long long>(ncells, 1)));
+  plan->h_ncells = ncells;
+  plan->cell_tab_ok = false;
+  const int* hist = plan->h_hist.as<int>();
   int errf = 0;
-  AKM_CK(cudaMemcpyAsync(hist.data(), plan->hist.p, sizeof(int) * std::max<long long>(ncells, 1), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaMemcpyAsync(plan->h_hist.p, plan->hist.p, sizeof(int) * std::max<long long>(ncells, 1), cudaMemcpyDeviceToHost, s));
   AKM_CK(cudaMemcpyAsync(&errf, plan->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   AKM_CK(cudaStreamSynchronize(s));
   if (errf) return plan->fail(AKM_ERR_CUDA, "internal error: a scaled point fell outside its grid box");
+  tm.mark("scale+histogram+readback");
 
   // choose B per window (cost model in FMA-equivalents per RHS)
-  std::vector<int> cell_off(std::max<long long>(ncells, 1), 0);
+  int* cell_off = plan->h_cell_off.as<int>();  // written for the cells of occupied bins only (others never read)
   for (int set = 0; set < 2; ++set) {
-    plan->items_spread[set].clear();
-    plan->items_interp[set].clear();
-    plan->items_interp_bin[set].clear();
+    plan->items_spread[set].count = 0;
+    plan->items_interp[set].count = 0;
+    plan->items_interp_bin[set].count = 0;
   }
   plan->occupied.assign(P, 0);
   plan->maxbin.assign(P, 0);
@@ -362,22 +495,40 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   const int ch_i = 128;  // interpolation: one cell per work item (64 thr x 2 pts, or 8 warps x 16 pts on DMMA)
   // item set 0: the square product over all points; set 1: the cross product (spread the class-0
   // sources, interpolate at the class-1 targets; akm_kernel_cross_mvm)
-  std::vector<std::vector<WorkItem>> its_s[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
-  std::vector<std::vector<WorkItem>> its_i[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
-  std::vector<std::vector<WorkItem>> its_ib[2] = {std::vector<std::vector<WorkItem>>(P), std::vector<std::vector<WorkItem>>(P)};
+  BinScratch& bs = plan->bs;
+  bs.resize(P);
+  auto& its_s = bs.its_s;
+  auto& its_i = bs.its_i;
+  auto& its_ib = bs.its_ib;
   const int ch_ib = 128;  // per-bin interpolation items: up to 128 points of one bin
-  std::vector<int> bstart;  // per window: sorted start of every bin (bin-major order), then n
-  for (int w = 0; w < P; ++w) {
+  // per window (independent: one host thread each): B, the bin-major cell offsets, the work items and
+  // the bin start table (sorted start of every bin, then n)
+  auto& bst = bs.bst;
+  std::vector<akm_status> wst(P, AKM_OK);
+  std::vector<std::string> werr(P);
+  auto wfail = [&](int w, akm_status code, const std::string& msg) {
+    wst[w] = code;
+    werr[w] = msg;
+  };
+  const bool split = plan->n_split < n;
+  auto do_window = [&](int w) {
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!tm.on) return;
+      const auto t1 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[akm setup]   w%d %-22s %8.3f ms\n", w, what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+      t0 = t1;
+    };
     WinGeom& g = tab.w[w];
-    const int* hc = hist.data() + hoff[w];
+    const int* hc = hist + hoff[w];
     const int d = g.d;
     int bestB = 1;
     double bestCost = 1e300;
     const bool forced = !plan->bin_override.empty();
     // occupied cells (0.15-10% of the box at the BASELINE.json configs): the candidates below loop
     // over these only
-    struct Occ { int c0, c1, c2, v; };
-    std::vector<Occ> occ;
+    using Occ = OccCell;
+    std::vector<Occ>& occ = bs.occ[w];
     for (int c0 = 0; c0 < g.ncell[0]; ++c0)
       for (int c1 = 0; c1 < g.ncell[1]; ++c1)
         for (int c2 = 0; c2 < g.ncell[2]; ++c2) {
@@ -385,7 +536,8 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
           const int v = hc[2 * ci] + hc[2 * ci + 1];
           if (v) occ.push_back(Occ{c0, c1, c2, v});
         }
-    std::vector<long long> bc;
+    lap("occupied cells");
+    std::vector<long long>& bc = bs.bc[w];
     for (int B : {1, 2, 3, 4, 6, 8}) {
       if (forced && B != plan->bin_override[w]) continue;
       const int F = B + 2 * m - 1;
@@ -428,8 +580,9 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
       }
     }
     if (forced && bestCost >= 1e300)
-      return plan->fail(AKM_ERR_UNSUPPORTED, "window %d: forced bin edge %d does not fit the grid box", w,
-                        plan->bin_override[w]);
+      return wfail(w, AKM_ERR_UNSUPPORTED,
+                   strf("window %d: forced bin edge %d does not fit the grid box", w, plan->bin_override[w]));
+    lap("B choice");
     // finalize geometry for bestB
     const int B = bestB;
     g.B = B;
@@ -442,20 +595,32 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
       g.F[a] = B + 2 * m - 1;
       g.L[a] = g.nbin[a] * B + 2 * m - 1;  // covers the last bin's footprint
       if (g.L[a] > n_g)
-        return plan->fail(AKM_ERR_UNSUPPORTED,
-                          "window %d: grid box of %d nodes exceeds the oversampled grid (n_g = %d); "
-                          "increase N or sigma_over, or decrease m", w, g.L[a], n_g);
+        return wfail(w, AKM_ERR_UNSUPPORTED,
+                     strf("window %d: grid box of %d nodes exceeds the oversampled grid (n_g = %d); "
+                          "increase N or sigma_over, or decrease m", w, g.L[a], n_g));
     }
     // cell offsets in bin-major order (inside a bin: the class-0 points cell by cell, then the
     // class-1 points cell by cell) and work items
     long long pos = 0;
     const int Bd0 = (3 - d > 0) ? 1 : B, Bd1 = (3 - d > 1) ? 1 : B, Bd2 = B;
-    g.bt_off = (int)bstart.size();
+    // points per bin (from the occupied cells): empty bins only take their bin-start entry (the
+    // offsets of empty cells are never read)
+    std::vector<long long>& bcnt = bs.bcnt[w];
+    bcnt.assign((size_t)g.nbin[0] * g.nbin[1] * g.nbin[2], 0);
+    for (const Occ& o : occ) {
+      const int b0 = (3 - d > 0) ? 0 : o.c0 / B, b1 = (3 - d > 1) ? 0 : o.c1 / B, b2 = o.c2 / B;
+      bcnt[((size_t)b0 * g.nbin[1] + b1) * g.nbin[2] + b2] += o.v;
+    }
+    lap("bin counts");
+    its_i[0][w].reserve(occ.size() + n / ch_i + 1);
+    its_ib[0][w].reserve(occ.size() + n / ch_ib + 1);
+    bst[w].reserve(bcnt.size() + 1);
     for (int b0 = 0; b0 < g.nbin[0]; ++b0)
       for (int b1 = 0; b1 < g.nbin[1]; ++b1)
         for (int b2 = 0; b2 < g.nbin[2]; ++b2) {
           const long long start = pos;
-          bstart.push_back((int)pos);
+          bst[w].push_back((int)pos);
+          if (!bcnt[((size_t)b0 * g.nbin[1] + b1) * g.nbin[2] + b2]) continue;
           long long cls_start[2] = {pos, pos};
           for (int cls = 0; cls < 2; ++cls) {
             cls_start[cls] = pos;
@@ -470,7 +635,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
                   for (int q = 0; q < cc; q += ch_i) {
                     const WorkItem wi{w, {c0, c1, c2}, (int)(pos + q), std::min(ch_i, cc - q)};
                     its_i[0][w].push_back(wi);
-                    if (cls == 1) its_i[1][w].push_back(wi);
+                    if (cls == 1) its_i[1][w].push_back(wi);  // (class 1 is empty without a split)
                   }
                   pos += cc;
                 }
@@ -485,13 +650,34 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
           };
           chunk(its_s[0][w], start, pos, ch_s);
           chunk(its_ib[0][w], start, pos, ch_ib);
-          chunk(its_s[1][w], cls_start[0], cls_start[1], ch_s);  // sources
-          chunk(its_ib[1][w], cls_start[1], pos, ch_ib);         // targets
+          if (split) {  // item set 1 serves only the cross product
+            chunk(its_s[1][w], cls_start[0], cls_start[1], ch_s);  // sources
+            chunk(its_ib[1][w], cls_start[1], pos, ch_ib);         // targets
+          }
         }
-    if (pos != n) return plan->fail(AKM_ERR_CUDA, "internal error: histogram of window %d holds %lld of %lld points",
-                                    w, pos, n);
-    bstart.push_back((int)n);
+    if (pos != n) return wfail(w, AKM_ERR_CUDA, strf("internal error: histogram of window %d holds %lld of %lld points",
+                                    w, pos, n));
+    bst[w].push_back((int)n);
+    lap("offsets + items");
+  };
+  {
+    static const bool threads = !(std::getenv("AKM_SETUP_THREADS") && std::atoi(std::getenv("AKM_SETUP_THREADS")) == 0);
+    std::vector<std::thread> th;
+    for (int w = 1; w < P; ++w) {
+      if (threads) th.emplace_back(do_window, w);
+      else do_window(w);
+    }
+    if (P > 0) do_window(0);
+    for (auto& t : th) t.join();
   }
+  std::vector<int>& bstart = bs.bstart;
+  bstart.clear();
+  for (int w = 0; w < P; ++w) {
+    if (wst[w] != AKM_OK) return plan->fail(wst[w], "%s", werr[w].c_str());
+    tab.w[w].bt_off = (int)bstart.size();
+    bstart.insert(bstart.end(), bst[w].begin(), bst[w].end());
+  }
+  tm.mark("host: B choice, offsets, items");
   // groups of windows with equal (d, F); work items concatenated group by group,
   // larger chunks first inside a group (better tail behaviour)
   plan->groups.clear();
@@ -509,32 +695,38 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     }
     grp->wins.push_back(w);
   }
+  for (int set = 0; set < 2; ++set) {  // page-locked capacity of the six lists
+    size_t ts = 0, ti = 0, tib = 0;
+    for (int w = 0; w < P; ++w) {
+      ts += its_s[set][w].size();
+      ti += its_i[set][w].size();
+      tib += its_ib[set][w].size();
+    }
+    AKM_CK(plan->items_spread[set].buf.ensure(sizeof(WorkItem) * std::max<size_t>(ts, 1)));
+    AKM_CK(plan->items_interp[set].buf.ensure(sizeof(WorkItem) * std::max<size_t>(ti, 1)));
+    AKM_CK(plan->items_interp_bin[set].buf.ensure(sizeof(WorkItem) * std::max<size_t>(tib, 1)));
+  }
   for (auto& grp : plan->groups) {
     for (int set = 0; set < 2; ++set) {
-      std::vector<WorkItem> gs, gi, gib;
+      std::vector<const std::vector<WorkItem>*> ss, si, sib;
       for (int w : grp.wins) {
-        gs.insert(gs.end(), its_s[set][w].begin(), its_s[set][w].end());
-        gi.insert(gi.end(), its_i[set][w].begin(), its_i[set][w].end());
-        gib.insert(gib.end(), its_ib[set][w].begin(), its_ib[set][w].end());
+        ss.push_back(&its_s[set][w]);
+        si.push_back(&its_i[set][w]);
+        sib.push_back(&its_ib[set][w]);
       }
-      sort_larger_first(gs);
-      sort_larger_first(gi);
-      sort_larger_first(gib);
       ItemSlice& sl = grp.sl[set];
       sl.spread_begin = (int)plan->items_spread[set].size();
-      sl.spread_count = (int)gs.size();
+      sl.spread_count = (int)append_larger_first(ss, plan->items_spread[set], bs.pos);
       sl.interp_begin = (int)plan->items_interp[set].size();
-      sl.interp_count = (int)gi.size();
-      plan->items_spread[set].insert(plan->items_spread[set].end(), gs.begin(), gs.end());
-      plan->items_interp[set].insert(plan->items_interp[set].end(), gi.begin(), gi.end());
+      sl.interp_count = (int)append_larger_first(si, plan->items_interp[set], bs.pos);
       // per-cell DMMA items pay a whole cell footprint per item: with few points per occupied cell
       // the per-bin scalar kernel wins (c3: ~16 points per cell; c4/c5: hundreds)
       long long pts = 0;
-      for (const WorkItem& it : gi) pts += it.count;
-      sl.sparse = gi.size() > 0 && (double)pts / (double)gi.size() < 48.0;
+      for (const auto* v : si)
+        for (const WorkItem& it : *v) pts += it.count;
+      sl.sparse = sl.interp_count > 0 && (double)pts / (double)sl.interp_count < 48.0;
       sl.interp_bin_begin = (int)plan->items_interp_bin[set].size();
-      sl.interp_bin_count = (int)gib.size();
-      plan->items_interp_bin[set].insert(plan->items_interp_bin[set].end(), gib.begin(), gib.end());
+      sl.interp_bin_count = (int)append_larger_first(sib, plan->items_interp_bin[set], bs.pos);
     }
   }
 
@@ -565,8 +757,9 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   plan->szA1 = a1; plan->szA2 = a2; plan->szA3 = a3; plan->szC = cc; plan->szC2 = c2; plan->szTW = twc; plan->szD = dd;
   plan->r_cap = 0;  // grid workspace must be re-sized
 
+  tm.mark("host: groups, sort, layout");
   // scatter into bin-major order
-  AKM_CK(cudaMemcpyAsync(plan->hist.p, cell_off.data(), sizeof(int) * std::max<long long>(ncells, 1),
+  AKM_CK(cudaMemcpyAsync(plan->hist.p, cell_off, sizeof(int) * std::max<long long>(ncells, 1),
                          cudaMemcpyHostToDevice, s));
   AKM_CK(plan->dtab.ensure(sizeof(WinTable)));
   AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
@@ -574,8 +767,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
                         plan->hist_off.as<long long>(), plan->u_sorted.as<double>(), plan->perm.as<int>(), plan->n_split,
                         s));
   for (int set = 0; set < 2; ++set) {
-    const std::vector<WorkItem>* lists[3] = {&plan->items_spread[set], &plan->items_interp[set],
-                                             &plan->items_interp_bin[set]};
+    const HostItems* lists[3] = {&plan->items_spread[set], &plan->items_interp[set], &plan->items_interp_bin[set]};
     DevBuf* bufs[3] = {&plan->items_s[set], &plan->items_i[set], &plan->items_ib[set]};
     for (int k = 0; k < 3; ++k) {
       AKM_CK(bufs[k]->ensure(sizeof(WorkItem) * std::max<size_t>(lists[k]->size(), 1)));
@@ -584,12 +776,11 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
                                cudaMemcpyHostToDevice, s));
     }
   }
-  {  // (start, count) of every (cell, class) slot in the window-relative sorted order (near field)
-    std::vector<int2> ct(std::max<long long>(ncells, 1));
-    for (long long q = 0; q < ncells; ++q) ct[q] = make_int2(cell_off[q], hist[q]);
-    AKM_CK(plan->cell_tab.ensure(sizeof(int2) * ct.size()));
-    AKM_CK(cudaMemcpyAsync(plan->cell_tab.p, ct.data(), sizeof(int2) * ct.size(), cudaMemcpyHostToDevice, s));
+  if (plan->near_field()) {
+    akm_status st = ensure_cell_tab(plan, s);
+    if (st != AKM_OK) return st;
   }
+  tm.mark("scatter + item uploads");
   AKM_CK(plan->bin_start.ensure(sizeof(int) * bstart.size()));
   AKM_CK(cudaMemcpyAsync(plan->bin_start.p, bstart.data(), sizeof(int) * bstart.size(), cudaMemcpyHostToDevice, s));
   // twiddles
@@ -597,6 +788,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   AKM_CK(launch_twiddles(tab, plan->dtab.as<WinTable>(), plan->tw.as<double2>(), s));
   AKM_CK(plan->D.ensure(sizeof(double) * std::max<long long>(dd, 1)));
   AKM_CK(cudaStreamSynchronize(s));  // host vectors (cell_off, items) go out of scope / may change
+  tm.mark("bin starts, twiddles, D");
   plan->c_w_binned = plan->c_w;
   return AKM_OK;
 }
@@ -823,6 +1015,7 @@ static akm_status enqueue_finish(akm_plan* plan, const double* grid, const doubl
   }
   if (plan->near_field()) {  // kappa_R's inner part: add sum_j (kappa - T_I)(r_ij) v_j (regularize.cu)
     if (set != 0) return plan->fail(AKM_ERR_UNSUPPORTED, "the near-field correction is built for the square products only");
+    if (!plan->cell_tab_ok) return plan->fail(AKM_ERR_STATE, "internal error: near-field cell table not built");
     const int nitems = (int)plan->items_interp_bin[0].size();
     AKM_CK(launch_near_field(dtab, plan->items_ib[0].as<WorkItem>(), nitems, plan->cell_tab.as<int2>(),
                              plan->hist_off.as<long long>(), plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv,
@@ -1324,8 +1517,14 @@ akm_status akm_set_theta(akm_plan* plan, double sigma_f, double ell, double sigm
     akm_status st = rebuild_bins(plan, s);
     if (st != AKM_OK) return st;
   }
+  if (plan->near_field()) {
+    akm_status st = ensure_cell_tab(plan, s);
+    if (st != AKM_OK) return st;
+  }
+  SetupTimer tm(s);
   akm_status st = rebuild_tables(plan, s);
   if (st != AKM_OK) return st;
+  tm.mark("b_k + multipliers");
   AKM_CK(cudaGetLastError());
   plan->have_theta = true;
   return AKM_OK;

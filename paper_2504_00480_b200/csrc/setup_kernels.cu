@@ -236,7 +236,16 @@ cudaError_t launch_kernel_samples(int family, int d, int N, double ell_eff, int 
 // The samples are even in every axis separately (kappa depends on |l_t| and the node -N/2 is its
 // own mirror on the torus), so the sine parts of eq. (3.2) vanish axis by axis and b_k is real.
 // Axis index t counts from the fastest-varying (t = 0) dimension of the flat array.
+// The N cosines cos(2 pi j / N) are computed once per CTA into shared memory (cospi, exact phase
+// reduction j = k l mod N as before); each term is then a table lookup (N <= kCosTabMax; larger N
+// evaluate cospi per term).
+constexpr int kCosTabMax = 4096;
 __global__ void k_cos_dft_axis(int d, int N, int axis, const double* __restrict__ in, double* __restrict__ out) {
+  extern __shared__ double cos_tab[];
+  const bool tab = N <= kCosTabMax;
+  if (tab)
+    for (int j = threadIdx.x; j < N; j += blockDim.x) cos_tab[j] = cospi(2.0 * (double)j / (double)N);
+  __syncthreads();
   long long total = 1;
   for (int t = 0; t < d; ++t) total *= N;
   long long stride = 1;
@@ -246,12 +255,14 @@ __global__ void k_cos_dft_axis(int d, int N, int axis, const double* __restrict_
     const int ki = (int)((idx / stride) % N);
     const long long base = idx - (long long)ki * stride;
     const int k = ki - N / 2;
+    int j = (int)(((long long)k * (-N / 2)) % N);  // k l mod N for l = -N/2, then += k per step
+    if (j < 0) j += N;
+    const int kstep = ((k % N) + N) % N;
     double acc = 0.0;
     for (int li = 0; li < N; ++li) {
-      const int l = li - N / 2;
-      int j = (int)(((long long)k * l) % N);
-      if (j < 0) j += N;
-      acc += cospi(2.0 * (double)j / (double)N) * in[base + (long long)li * stride];
+      acc += (tab ? cos_tab[j] : cospi(2.0 * (double)j / (double)N)) * in[base + (long long)li * stride];
+      j += kstep;
+      if (j >= N) j -= N;
     }
     out[idx] = acc / (double)N;
   }
@@ -261,7 +272,7 @@ cudaError_t launch_cos_dft_axis(int d, int N, int axis, const double* in, double
   long long total = 1;
   for (int t = 0; t < d; ++t) total *= N;
   int blocks = (int)((total + 255) / 256);
-  k_cos_dft_axis<<<blocks, 256, 0, s>>>(d, N, axis, in, out);
+  k_cos_dft_axis<<<blocks, 256, N <= kCosTabMax ? sizeof(double) * N : 0, s>>>(d, N, axis, in, out);
   return cudaGetLastError();
 }
 
