@@ -225,6 +225,47 @@ cudaError_t launch_scale_and_key(const double* X, long long n, long long ldx, co
 cudaError_t launch_scatter(long long n, const WinTable& tab, const WinTable* dtab, const double* u_tmp,
                            const int* key, int* cursor, const long long* hist_off, double* u_sorted, int* perm,
                            long long n_split, cudaStream_t s);
+// binsort.cu: S0 on the device (candidate bin statistics, bin-major layout, cursors, work items)
+constexpr int kBinCands = 6;  // candidate bin edges B = 1, 2, 3, 4, 6, 8
+struct BinCandParam {
+  long long off[kMaxWin][kBinCands];  // offset of each (window, candidate) per-bin count array
+  int B[kBinCands];
+  int mask[kMaxWin];                  // candidates that fit, per window
+};
+struct BinLayout {
+  long long keybase[kMaxWin];  // first key of each window in the (group-ordered) key space
+  long long binbase[kMaxWin];  // first bin of each window in the (group-ordered) bin space
+};
+constexpr int kItemLists = 6;  // per-cell interp (set 0, 1), spread set 0, per-bin set 0, spread set 1, per-bin set 1
+struct ListScanParam {
+  const int* cnt[kItemLists];
+  const int* off[kItemLists];
+  long long len[kItemLists];
+  long long gbeg[kItemLists][kMaxWin + 1];  // index-space start of every group, then len
+  int nlists;
+};
+cudaError_t launch_bin_costs(const WinTable& tab, const WinTable* dtab, const int* hist, const long long* hist_off,
+                             const BinCandParam& cp, long long bc_total, int* bc, long long ch_s, int* stats,
+                             cudaStream_t s);
+cudaError_t launch_slot_keys(const WinTable& tab, const WinTable* dtab, const int* hist, const long long* hist_off,
+                             const BinLayout& L, long long* key_cnt, int* i0cnt, int* i1cnt, int ch_i, cudaStream_t s);
+cudaError_t launch_slot_cursor(const WinTable& tab, const WinTable* dtab, const long long* hist_off, const BinLayout& L,
+                               const long long* key_cnt, const long long* key_off, int* cursor, int2* cell_tab,
+                               cudaStream_t s);
+cudaError_t launch_bin_pass(const WinTable& tab, const WinTable* dtab, const BinLayout& L, const long long* key_off,
+                            long long n, long long ch_s, int ch_ib, int* bin_start, int* s0, int* b0, int* s1, int* b1,
+                            cudaStream_t s);
+cudaError_t launch_group_bounds(const ListScanParam& lp, int ngroups, int* bounds, cudaStream_t s);
+cudaError_t launch_emit_items(const WinTable& tab, const WinTable* dtab, const BinLayout& L, const long long* key_cnt,
+                              const long long* key_off, long long n, long long ch_s, int ch_i, int ch_ib,
+                              const int* const off[6], WorkItem* const out[6], cudaStream_t s);
+cudaError_t scan_excl_ll(const long long* in, long long* out, long long len, void** temp, size_t* temp_bytes,
+                         cudaStream_t s);
+cudaError_t scan_excl_int(const int* in, int* out, long long len, void** temp, size_t* temp_bytes, cudaStream_t s);
+cudaError_t sort_items_larger_first(const WorkItem* in, long long cnt, int maxc, int nseg, const int* seg_begin,
+                                    const int* seg_end, unsigned* keys, unsigned* keys_alt, int* idx, int* idx_alt,
+                                    void** temp, size_t* temp_bytes, WorkItem* out, cudaStream_t s);
+
 cudaError_t launch_kernel_samples(int family, int d, int N, double ell_eff, int deriv, double* out, cudaStream_t s);
 cudaError_t launch_cos_dft_axis(int d, int N, int axis, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_multiplier(const WinTable& tab, const WinTable* dtab, int win, const double* bK, const double* bL,

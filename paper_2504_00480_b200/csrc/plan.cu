@@ -15,7 +15,6 @@
 #include <cstring>
 #include <set>
 #include <string>
-#include <thread>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -54,29 +53,6 @@ struct DevBuf {
   T* as() const { return static_cast<T*>(p); }
 };
 
-// page-locked host staging, grow-only (kept across set_theta calls: no page faults, async DMA)
-struct PinnedBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  ~PinnedBuf() {
-    if (p) cudaFreeHost(p);
-  }
-  cudaError_t ensure(size_t need) {
-    if (need <= bytes) return cudaSuccess;
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMallocHost(&p, need);
-    if (e != cudaSuccess) {
-      p = nullptr;
-      cudaGetLastError();
-      return e;
-    }
-    bytes = need;
-    return cudaSuccess;
-  }
-  template <class T> T* as() const { return static_cast<T*>(p); }
-};
 
 struct ItemSlice {  // a group's slice of the concatenated work items of one item set
   int spread_begin = 0, spread_count = 0;
@@ -93,49 +69,6 @@ struct Group {  // windows sharing (d, F) -> one spread / interp launch
 
 }  // namespace
 
-// One work-item list, built in page-locked memory (its upload is an async copy)
-struct HostItems {
-  PinnedBuf buf;
-  size_t count = 0;
-  WorkItem* data() const { return buf.as<WorkItem>(); }
-  size_t size() const { return count; }
-  bool empty() const { return count == 0; }
-};
-
-// Host scratch of the bin sort, kept across set_theta calls (cleared, capacity kept): re-allocating
-// these megabytes per call costs more in page faults than the loops that fill them.
-struct OccCell {
-  int c0, c1, c2, v;
-};
-struct BinScratch {
-  std::vector<std::vector<WorkItem>> its_s[2], its_i[2], its_ib[2];  // [set][window]
-  std::vector<std::vector<int>> bst;                                   // [window] bin starts
-  std::vector<std::vector<OccCell>> occ;                               // [window] occupied cells
-  std::vector<std::vector<long long>> bc, bcnt;                        // [window] per-bin counts
-  std::vector<WorkItem> gs, gi, gib, tmp;                              // group concatenation, sort
-  std::vector<int> pos;                                                // counting sort
-  std::vector<int> bstart;                                             // all windows' bin starts
-  void resize(int P) {
-    for (int set = 0; set < 2; ++set) {
-      its_s[set].resize(P);
-      its_i[set].resize(P);
-      its_ib[set].resize(P);
-      for (int w = 0; w < P; ++w) {
-        its_s[set][w].clear();
-        its_i[set][w].clear();
-        its_ib[set][w].clear();
-      }
-    }
-    bst.resize(P);
-    occ.resize(P);
-    bc.resize(P);
-    bcnt.resize(P);
-    for (int w = 0; w < P; ++w) {
-      bst[w].clear();
-      occ[w].clear();
-    }
-  }
-};
 
 struct akm_plan {
   int device = 0;
@@ -186,7 +119,7 @@ struct akm_plan {
   std::vector<double> c_w, c_w_binned;      // current scale, scale the bins were built for
   WinTable tab{};                           // host copy
   PolyParam poly_param{};                   // window polynomials, passed to kernels by value
-  HostItems items_spread[2], items_interp[2], items_interp_bin[2];  // [item set]
+  size_t n_items_spread[2] = {0, 0}, n_items_interp[2] = {0, 0}, n_items_interp_bin[2] = {0, 0};  // [item set]
   std::vector<Group> groups;
   std::vector<long long> occupied, maxbin;
   long long total_taps = 0, szA1 = 0, szA2 = 0, szA3 = 0, szC = 0, szC2 = 0, szTW = 0, szD = 0;
@@ -198,11 +131,14 @@ struct akm_plan {
   DevBuf grid, H, A1, A2, A3, C, C2, tw, D, part, bs0, bs1, bs2, bs3;
   DevBuf reg_coef, bin_start;  // regularisation polynomials [w][op][kRegStride]; per-window bin start tables
   DevBuf cell_tab, nfV;        // near field: (start, count) per (cell, class) slot; bin-sorted copy of V
-  PinnedBuf h_hist, h_cell_off;  // host: points and sorted start per (cell, class) slot of the last bin sort
-  long long h_ncells = 0;
   bool cell_tab_ok = false;      // cell_tab matches the last bin sort (built on demand: near field only)
-  std::vector<int2> h_cell_tab;
-  BinScratch bs;
+  // S0 on the device (binsort.cu): candidate statistics, key space (bin-major slot order) counts and
+  // offsets, per-list item counts / offsets, unsorted items, sort scratch, group bounds
+  DevBuf bs_bc, bs_stats, key_cnt, key_off, lcnt[kItemLists], loff[kItemLists], items_u[kItemLists];
+  DevBuf sort_keys, sort_idx, bounds;
+  void* cub_temp = nullptr;
+  size_t cub_temp_bytes = 0;
+  BinLayout bl{};
   std::vector<unsigned char> tma_maps = std::vector<unsigned char>(interp_tma_maps_bytes());  // TmaMaps (host)
   DevBuf stageV, stageY, stageL, stageS;
   DevBuf crossV, crossY;  // akm_kernel_cross_mvm: zero-padded V and the union's product
@@ -274,6 +210,7 @@ struct akm_plan {
     return &es;
   }
   ~akm_plan() {
+    if (cub_temp) cudaFree(cub_temp);
     for (auto& es : ring)
       for (auto& e : es.e) cudaEventDestroy(e);
     for (auto& g : graphs)
@@ -344,57 +281,25 @@ cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, 
 
 }  // namespace
 
-// Appends the work items of `src` (concatenated in order) to `dst` ordered by decreasing point count,
-// ties kept in their order (= std::stable_sort with a.count > b.count): a counting sort,
-// O(items + max count).  Returns the number appended.
-static size_t append_larger_first(const std::vector<const std::vector<WorkItem>*>& src, HostItems& dst,
-                                  std::vector<int>& pos) {
-  size_t total = 0;
-  int mx = 0;
-  for (const auto* v : src) {
-    total += v->size();
-    for (const WorkItem& it : *v) mx = std::max(mx, it.count);
-  }
-  const size_t base = dst.count;
-  if (!total) return 0;
-  WorkItem* out = dst.data();  // capacity ensured by the caller
-  pos.assign((size_t)mx + 2, 0);
-  for (const auto* v : src)
-    for (const WorkItem& it : *v) ++pos[(size_t)(mx - it.count) + 1];
-  for (int i = 1; i <= mx + 1; ++i) pos[i] += pos[i - 1];
-  for (const auto* v : src)
-    for (const WorkItem& it : *v) out[base + pos[mx - it.count]++] = it;
-  dst.count += total;
-  return total;
-}
 
 // ================================================================== geometry / binning
 // Build per-window boxes for the current c_w, histogram the points per cell on the device,
 // choose the bin edge B per window from the histogram, lay the cells out bin-major, scatter.
 // (start, count) of every (cell, class) slot in the window-relative sorted order of the last bin
-// sort, for the near-field correction; built on demand (only kappa_R's inner part reads it)
+// sort, for the near-field correction; built on demand (only kappa_R's inner part reads it) from the
+// device key counts and offsets of that sort (binsort.cu)
 static akm_status ensure_cell_tab(akm_plan* plan, cudaStream_t s) {
   if (plan->cell_tab_ok) return AKM_OK;
-  const long long nc = std::max<long long>(plan->h_ncells, 1);
-  const int* hist = plan->h_hist.as<int>();
-  const int* off = plan->h_cell_off.as<int>();
-  plan->h_cell_tab.resize(nc);
-  for (long long q = 0; q < plan->h_ncells; ++q) plan->h_cell_tab[q] = make_int2(hist[q] ? off[q] : 0, hist[q]);
-  AKM_CK(plan->cell_tab.ensure(sizeof(int2) * nc));
-  AKM_CK(cudaMemcpyAsync(plan->cell_tab.p, plan->h_cell_tab.data(), sizeof(int2) * nc, cudaMemcpyHostToDevice, s));
-  AKM_CK(cudaStreamSynchronize(s));
+  long long ncells = 0;
+  for (int w = 0; w < plan->P; ++w) ncells += 2LL * plan->tab.w[w].ncell[0] * plan->tab.w[w].ncell[1] * plan->tab.w[w].ncell[2];
+  AKM_CK(plan->cell_tab.ensure(sizeof(int2) * std::max<long long>(ncells, 1)));
+  AKM_CK(launch_slot_cursor(plan->tab, plan->dtab.as<WinTable>(), plan->hist_off.as<long long>(), plan->bl,
+                            plan->key_cnt.as<long long>(), plan->key_off.as<long long>(), nullptr,
+                            plan->cell_tab.as<int2>(), s));
   plan->cell_tab_ok = true;
   return AKM_OK;
 }
 
-static std::string strf(const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  return buf;
-}
 
 // AKM_SETUP_TIMES=1: the stages of set_theta / rebuild_bins on stderr (stream synchronised at each mark)
 struct SetupTimer {
@@ -468,77 +373,27 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   AKM_CK(launch_scale_and_key(plan->Xc.as<double>(), n, nf, tab, plan->dtab.as<WinTable>(), plan->u_tmp.as<double>(),
                               nullptr, plan->hist.as<int>(), plan->hist_off.as<long long>(), plan->err_flag.as<int>(),
                               plan->n_split, s));
-  AKM_CK(plan->h_hist.ensure(sizeof(int) * std::max<long long>(ncells, 1)));
-  AKM_CK(plan->h_cell_off.ensure(sizeof(int) * std::max<long long>(ncells, 1)));
-  plan->h_ncells = ncells;
-  plan->cell_tab_ok = false;
-  const int* hist = plan->h_hist.as<int>();
-  int errf = 0;
-  AKM_CK(cudaMemcpyAsync(plan->h_hist.p, plan->hist.p, sizeof(int) * std::max<long long>(ncells, 1), cudaMemcpyDeviceToHost, s));
-  AKM_CK(cudaMemcpyAsync(&errf, plan->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AKM_CK(cudaStreamSynchronize(s));
-  if (errf) return plan->fail(AKM_ERR_CUDA, "internal error: a scaled point fell outside its grid box");
-  tm.mark("scale+histogram+readback");
-
-  // choose B per window (cost model in FMA-equivalents per RHS)
-  int* cell_off = plan->h_cell_off.as<int>();  // written for the cells of occupied bins only (others never read)
-  for (int set = 0; set < 2; ++set) {
-    plan->items_spread[set].count = 0;
-    plan->items_interp[set].count = 0;
-    plan->items_interp_bin[set].count = 0;
-  }
-  plan->occupied.assign(P, 0);
-  plan->maxbin.assign(P, 0);
+  // S0 on the device (binsort.cu): statistics of every candidate bin edge -> B per window (host, the
+  // cost model below) -> bin-major layout, scatter cursors, bin starts and work items on the device
   const long long total_pts = n * P;
   long long ch_s = total_pts / (148 * 2);
   ch_s = std::max(32LL, std::min(4096LL, ch_s));
-  const int ch_i = 128;  // interpolation: one cell per work item (64 thr x 2 pts, or 8 warps x 16 pts on DMMA)
-  // item set 0: the square product over all points; set 1: the cross product (spread the class-0
-  // sources, interpolate at the class-1 targets; akm_kernel_cross_mvm)
-  BinScratch& bs = plan->bs;
-  bs.resize(P);
-  auto& its_s = bs.its_s;
-  auto& its_i = bs.its_i;
-  auto& its_ib = bs.its_ib;
+  const int ch_i = 128;   // per-cell interpolation items (64 thr x 2 pts, or 8 warps x 16 pts on DMMA)
   const int ch_ib = 128;  // per-bin interpolation items: up to 128 points of one bin
-  // per window (independent: one host thread each): B, the bin-major cell offsets, the work items and
-  // the bin start table (sorted start of every bin, then n)
-  auto& bst = bs.bst;
-  std::vector<akm_status> wst(P, AKM_OK);
-  std::vector<std::string> werr(P);
-  auto wfail = [&](int w, akm_status code, const std::string& msg) {
-    wst[w] = code;
-    werr[w] = msg;
-  };
+  // item set 0: the square product over all points; set 1: the cross product (spread the class-0
+  // sources, interpolate at the class-1 targets; akm_kernel_cross_mvm) -- built only with a split
   const bool split = plan->n_split < n;
-  auto do_window = [&](int w) {
-    auto t0 = std::chrono::steady_clock::now();
-    auto lap = [&](const char* what) {
-      if (!tm.on) return;
-      const auto t1 = std::chrono::steady_clock::now();
-      std::fprintf(stderr, "[akm setup]   w%d %-22s %8.3f ms\n", w, what, std::chrono::duration<double, std::milli>(t1 - t0).count());
-      t0 = t1;
-    };
-    WinGeom& g = tab.w[w];
-    const int* hc = hist + hoff[w];
+  const bool forced = !plan->bin_override.empty();
+  static const int kB[kBinCands] = {1, 2, 3, 4, 6, 8};
+  BinCandParam cp{};
+  long long bc_total = 0;
+  for (int k = 0; k < kBinCands; ++k) cp.B[k] = kB[k];
+  for (int w = 0; w < P; ++w) {
+    const WinGeom& g = tab.w[w];
     const int d = g.d;
-    int bestB = 1;
-    double bestCost = 1e300;
-    const bool forced = !plan->bin_override.empty();
-    // occupied cells (0.15-10% of the box at the BASELINE.json configs): the candidates below loop
-    // over these only
-    using Occ = OccCell;
-    std::vector<Occ>& occ = bs.occ[w];
-    for (int c0 = 0; c0 < g.ncell[0]; ++c0)
-      for (int c1 = 0; c1 < g.ncell[1]; ++c1)
-        for (int c2 = 0; c2 < g.ncell[2]; ++c2) {
-          const long long ci = ((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2;
-          const int v = hc[2 * ci] + hc[2 * ci + 1];
-          if (v) occ.push_back(Occ{c0, c1, c2, v});
-        }
-    lap("occupied cells");
-    std::vector<long long>& bc = bs.bc[w];
-    for (int B : {1, 2, 3, 4, 6, 8}) {
+    cp.mask[w] = 0;
+    for (int k = 0; k < kBinCands; ++k) {
+      const int B = kB[k];
       if (forced && B != plan->bin_override[w]) continue;
       const int F = B + 2 * m - 1;
       double Fd = 1;
@@ -553,37 +408,58 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
         if (d >= 2) fits = fits && spread_v5_choose(Mr, F, MB_, NB_, WN_);
       }
       if (!fits) continue;
-      int nb[3];
-      for (int a = 0; a < 3; ++a) nb[a] = (g.ncell[a] + B - 1) / (a < 3 - d ? 1 : B);
-      for (int a = 0; a < 3 - d; ++a) nb[a] = 1;
-      bc.assign((size_t)nb[0] * nb[1] * nb[2], 0);
-      for (const Occ& o : occ) {
-        const int b0 = (3 - d > 0) ? 0 : o.c0 / B, b1 = (3 - d > 1) ? 0 : o.c1 / B, b2 = o.c2 / B;
-        bc[((size_t)b0 * nb[1] + b1) * nb[2] + b2] += o.v;
-      }
-      double chunks_s = 0;
-      for (const Occ& o : occ) {  // each occupied bin once (zeroed after it is counted)
-        const int b0 = (3 - d > 0) ? 0 : o.c0 / B, b1 = (3 - d > 1) ? 0 : o.c1 / B, b2 = o.c2 / B;
-        long long& v = bc[((size_t)b0 * nb[1] + b1) * nb[2] + b2];
-        if (v) chunks_s += (double)((v + ch_s - 1) / ch_s);
-        v = 0;
-      }
-      // spreading: F^d FMAs per point and RHS, plus one footprint flush of F^d RED.ADD.F64
-      // (~34 FMA-equivalents each, profiles/r01_fp64_peaks.txt) per work item.  2-D windows: the
-      // per-item prologue and flush weigh more against the few points of a bin (~140 at c3) -- 60
-      // per footprint tap matches the measured optimum (c3: B = 4 0.724 ms, B = 3 0.771, B = 6 0.833)
+      cp.mask[w] |= 1 << k;
+      long long nb = 1;
+      for (int a = 3 - d; a < 3; ++a) nb *= (g.ncell[a] + B - 1) / B;
+      cp.off[w][k] = bc_total;
+      bc_total += nb;
+    }
+    if (forced && !cp.mask[w])
+      return plan->fail(AKM_ERR_UNSUPPORTED, "window %d: forced bin edge %d does not fit the grid box", w,
+                        plan->bin_override[w]);
+  }
+  AKM_CK(plan->bs_bc.ensure(sizeof(int) * std::max<long long>(bc_total, 1)));
+  AKM_CK(plan->bs_stats.ensure(sizeof(int) * P * kBinCands * 3));
+  AKM_CK(launch_bin_costs(tab, plan->dtab.as<WinTable>(), plan->hist.as<int>(), plan->hist_off.as<long long>(), cp,
+                          bc_total, plan->bs_bc.as<int>(), ch_s, plan->bs_stats.as<int>(), s));
+  std::vector<int> stats(P * kBinCands * 3);
+  int errf = 0;
+  AKM_CK(cudaMemcpyAsync(stats.data(), plan->bs_stats.p, sizeof(int) * stats.size(), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaMemcpyAsync(&errf, plan->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaStreamSynchronize(s));
+  if (errf) return plan->fail(AKM_ERR_CUDA, "internal error: a scaled point fell outside its grid box");
+  tm.mark("scale, histogram, B statistics");
+
+  // B per window: cost model in FMA-equivalents per RHS.  Spreading: F^d FMAs per
+  // point and RHS, plus one footprint flush of F^d RED.ADD.F64 (~34 FMA-equivalents each,
+  // profiles/r01_fp64_peaks.txt) per work item.  2-D windows: the per-item prologue and flush weigh
+  // more against the few points of a bin (~140 at c3) -- 60 per footprint tap matches the measured
+  // optimum (c3: B = 4 0.724 ms, B = 3 0.771, B = 6 0.833)
+  plan->occupied.assign(P, 0);
+  plan->maxbin.assign(P, 0);
+  long long nbins_total = 0;
+  for (int w = 0; w < P; ++w) {
+    WinGeom& g = tab.w[w];
+    const int d = g.d;
+    int bestB = 1, bestK = -1;
+    double bestCost = 1e300;
+    for (int k = 0; k < kBinCands; ++k) {
+      if (!(cp.mask[w] & (1 << k))) continue;
+      const int F = kB[k] + 2 * m - 1;
+      double Fd = 1;
+      for (int t = 0; t < d; ++t) Fd *= F;
+      const double chunks_s = (double)stats[(w * kBinCands + k) * 3 + 0];
       const double per_item = (d == 2) ? 60.0 : 34.0;
       const double cost = Fd * ((double)n + per_item * chunks_s);
       if (cost < bestCost * 0.999) {
         bestCost = cost;
-        bestB = B;
+        bestB = kB[k];
+        bestK = k;
       }
     }
-    if (forced && bestCost >= 1e300)
-      return wfail(w, AKM_ERR_UNSUPPORTED,
-                   strf("window %d: forced bin edge %d does not fit the grid box", w, plan->bin_override[w]));
-    lap("B choice");
-    // finalize geometry for bestB
+    if (bestK < 0) return plan->fail(AKM_ERR_UNSUPPORTED, "window %d: no bin edge fits the grid box", w);
+    plan->occupied[w] = stats[(w * kBinCands + bestK) * 3 + 1];
+    plan->maxbin[w] = stats[(w * kBinCands + bestK) * 3 + 2];
     const int B = bestB;
     g.B = B;
     for (int a = 0; a < 3; ++a) {
@@ -595,91 +471,15 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
       g.F[a] = B + 2 * m - 1;
       g.L[a] = g.nbin[a] * B + 2 * m - 1;  // covers the last bin's footprint
       if (g.L[a] > n_g)
-        return wfail(w, AKM_ERR_UNSUPPORTED,
-                     strf("window %d: grid box of %d nodes exceeds the oversampled grid (n_g = %d); "
-                          "increase N or sigma_over, or decrease m", w, g.L[a], n_g));
+        return plan->fail(AKM_ERR_UNSUPPORTED,
+                          "window %d: grid box of %d nodes exceeds the oversampled grid (n_g = %d); "
+                          "increase N or sigma_over, or decrease m", w, g.L[a], n_g);
     }
-    // cell offsets in bin-major order (inside a bin: the class-0 points cell by cell, then the
-    // class-1 points cell by cell) and work items
-    long long pos = 0;
-    const int Bd0 = (3 - d > 0) ? 1 : B, Bd1 = (3 - d > 1) ? 1 : B, Bd2 = B;
-    // points per bin (from the occupied cells): empty bins only take their bin-start entry (the
-    // offsets of empty cells are never read)
-    std::vector<long long>& bcnt = bs.bcnt[w];
-    bcnt.assign((size_t)g.nbin[0] * g.nbin[1] * g.nbin[2], 0);
-    for (const Occ& o : occ) {
-      const int b0 = (3 - d > 0) ? 0 : o.c0 / B, b1 = (3 - d > 1) ? 0 : o.c1 / B, b2 = o.c2 / B;
-      bcnt[((size_t)b0 * g.nbin[1] + b1) * g.nbin[2] + b2] += o.v;
-    }
-    lap("bin counts");
-    its_i[0][w].reserve(occ.size() + n / ch_i + 1);
-    its_ib[0][w].reserve(occ.size() + n / ch_ib + 1);
-    bst[w].reserve(bcnt.size() + 1);
-    for (int b0 = 0; b0 < g.nbin[0]; ++b0)
-      for (int b1 = 0; b1 < g.nbin[1]; ++b1)
-        for (int b2 = 0; b2 < g.nbin[2]; ++b2) {
-          const long long start = pos;
-          bst[w].push_back((int)pos);
-          if (!bcnt[((size_t)b0 * g.nbin[1] + b1) * g.nbin[2] + b2]) continue;
-          long long cls_start[2] = {pos, pos};
-          for (int cls = 0; cls < 2; ++cls) {
-            cls_start[cls] = pos;
-            for (int s0 = 0; s0 < Bd0; ++s0)
-              for (int s1 = 0; s1 < Bd1; ++s1)
-                for (int s2 = 0; s2 < Bd2; ++s2) {
-                  const int c0 = b0 * Bd0 + s0, c1 = b1 * Bd1 + s1, c2 = b2 * Bd2 + s2;
-                  if (c0 >= g.ncell[0] || c1 >= g.ncell[1] || c2 >= g.ncell[2]) continue;
-                  const long long ci = ((long long)c0 * g.ncell[1] + c1) * g.ncell[2] + c2;
-                  cell_off[hoff[w] + 2 * ci + cls] = (int)pos;
-                  const int cc = hc[2 * ci + cls];
-                  for (int q = 0; q < cc; q += ch_i) {
-                    const WorkItem wi{w, {c0, c1, c2}, (int)(pos + q), std::min(ch_i, cc - q)};
-                    its_i[0][w].push_back(wi);
-                    if (cls == 1) its_i[1][w].push_back(wi);  // (class 1 is empty without a split)
-                  }
-                  pos += cc;
-                }
-          }
-          const long long cnt = pos - start;
-          if (!cnt) continue;
-          plan->occupied[w] += 1;
-          plan->maxbin[w] = std::max(plan->maxbin[w], cnt);
-          auto chunk = [&](std::vector<WorkItem>& out, long long a, long long e, long long ch) {
-            for (long long q = a; q < e; q += ch)
-              out.push_back(WorkItem{w, {b0, b1, b2}, (int)q, (int)std::min<long long>(ch, e - q)});
-          };
-          chunk(its_s[0][w], start, pos, ch_s);
-          chunk(its_ib[0][w], start, pos, ch_ib);
-          if (split) {  // item set 1 serves only the cross product
-            chunk(its_s[1][w], cls_start[0], cls_start[1], ch_s);  // sources
-            chunk(its_ib[1][w], cls_start[1], pos, ch_ib);         // targets
-          }
-        }
-    if (pos != n) return wfail(w, AKM_ERR_CUDA, strf("internal error: histogram of window %d holds %lld of %lld points",
-                                    w, pos, n));
-    bst[w].push_back((int)n);
-    lap("offsets + items");
-  };
-  {
-    static const bool threads = !(std::getenv("AKM_SETUP_THREADS") && std::atoi(std::getenv("AKM_SETUP_THREADS")) == 0);
-    std::vector<std::thread> th;
-    for (int w = 1; w < P; ++w) {
-      if (threads) th.emplace_back(do_window, w);
-      else do_window(w);
-    }
-    if (P > 0) do_window(0);
-    for (auto& t : th) t.join();
+    g.bt_off = (int)(nbins_total + w);  // per window: start of every bin, then n
+    nbins_total += (long long)g.nbin[0] * g.nbin[1] * g.nbin[2];
   }
-  std::vector<int>& bstart = bs.bstart;
-  bstart.clear();
-  for (int w = 0; w < P; ++w) {
-    if (wst[w] != AKM_OK) return plan->fail(wst[w], "%s", werr[w].c_str());
-    tab.w[w].bt_off = (int)bstart.size();
-    bstart.insert(bstart.end(), bst[w].begin(), bst[w].end());
-  }
-  tm.mark("host: B choice, offsets, items");
-  // groups of windows with equal (d, F); work items concatenated group by group,
-  // larger chunks first inside a group (better tail behaviour)
+  // groups of windows with equal (d, F); work items concatenated group by group, larger chunks first
+  // inside a group (better tail behaviour); the key and bin spaces are laid out in group order
   plan->groups.clear();
   for (int w = 0; w < P; ++w) {
     const WinGeom& g = tab.w[w];
@@ -695,38 +495,125 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     }
     grp->wins.push_back(w);
   }
-  for (int set = 0; set < 2; ++set) {  // page-locked capacity of the six lists
-    size_t ts = 0, ti = 0, tib = 0;
-    for (int w = 0; w < P; ++w) {
-      ts += its_s[set][w].size();
-      ti += its_i[set][w].size();
-      tib += its_ib[set][w].size();
+  const int ngroups = (int)plan->groups.size();
+  BinLayout& L = plan->bl;
+  long long nkeys = 0, nbins = 0;
+  std::vector<long long> gkey(ngroups + 1), gbin(ngroups + 1);
+  for (int gi = 0; gi < ngroups; ++gi) {
+    gkey[gi] = nkeys;
+    gbin[gi] = nbins;
+    for (int w : plan->groups[gi].wins) {
+      const WinGeom& g = tab.w[w];
+      long long bb = 1;
+      for (int a = 3 - g.d; a < 3; ++a) bb *= g.B;
+      const long long nb = (long long)g.nbin[0] * g.nbin[1] * g.nbin[2];
+      L.keybase[w] = nkeys;
+      L.binbase[w] = nbins;
+      nkeys += nb * 2 * bb;
+      nbins += nb;
     }
-    AKM_CK(plan->items_spread[set].buf.ensure(sizeof(WorkItem) * std::max<size_t>(ts, 1)));
-    AKM_CK(plan->items_interp[set].buf.ensure(sizeof(WorkItem) * std::max<size_t>(ti, 1)));
-    AKM_CK(plan->items_interp_bin[set].buf.ensure(sizeof(WorkItem) * std::max<size_t>(tib, 1)));
   }
-  for (auto& grp : plan->groups) {
+  gkey[ngroups] = nkeys;
+  gbin[ngroups] = nbins;
+  AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
+  // keys: counts, offsets, cursors
+  AKM_CK(plan->key_cnt.ensure(sizeof(long long) * std::max<long long>(nkeys, 1)));
+  AKM_CK(plan->key_off.ensure(sizeof(long long) * std::max<long long>(nkeys, 1)));
+  const long long llen[kItemLists] = {nkeys, split ? nkeys : 0, nbins, nbins, split ? nbins : 0, split ? nbins : 0};
+  for (int l = 0; l < kItemLists; ++l) {
+    AKM_CK(plan->lcnt[l].ensure(sizeof(int) * std::max<long long>(llen[l], 1)));
+    AKM_CK(plan->loff[l].ensure(sizeof(int) * std::max<long long>(llen[l], 1)));
+  }
+  AKM_CK(cudaMemsetAsync(plan->key_cnt.p, 0, sizeof(long long) * std::max<long long>(nkeys, 1), s));
+  AKM_CK(cudaMemsetAsync(plan->lcnt[0].p, 0, sizeof(int) * std::max<long long>(nkeys, 1), s));
+  if (split) AKM_CK(cudaMemsetAsync(plan->lcnt[1].p, 0, sizeof(int) * std::max<long long>(nkeys, 1), s));
+  AKM_CK(launch_slot_keys(tab, plan->dtab.as<WinTable>(), plan->hist.as<int>(), plan->hist_off.as<long long>(), L,
+                          plan->key_cnt.as<long long>(), plan->lcnt[0].as<int>(), split ? plan->lcnt[1].as<int>() : nullptr,
+                          ch_i, s));
+  AKM_CK(scan_excl_ll(plan->key_cnt.as<long long>(), plan->key_off.as<long long>(), nkeys, &plan->cub_temp,
+                      &plan->cub_temp_bytes, s));
+  int2* ctab = nullptr;
+  if (plan->near_field()) {
+    AKM_CK(plan->cell_tab.ensure(sizeof(int2) * std::max<long long>(ncells, 1)));
+    ctab = plan->cell_tab.as<int2>();
+  }
+  AKM_CK(launch_slot_cursor(tab, plan->dtab.as<WinTable>(), plan->hist_off.as<long long>(), L,
+                            plan->key_cnt.as<long long>(), plan->key_off.as<long long>(), plan->hist.as<int>(), ctab, s));
+  plan->cell_tab_ok = ctab != nullptr;
+  AKM_CK(plan->bin_start.ensure(sizeof(int) * (nbins_total + P)));
+  AKM_CK(launch_bin_pass(tab, plan->dtab.as<WinTable>(), L, plan->key_off.as<long long>(), n, ch_s, ch_ib,
+                         plan->bin_start.as<int>(), plan->lcnt[2].as<int>(), plan->lcnt[3].as<int>(),
+                         split ? plan->lcnt[4].as<int>() : nullptr, split ? plan->lcnt[5].as<int>() : nullptr, s));
+  // item offsets per list, then each group's [begin, end)
+  ListScanParam lp{};
+  lp.nlists = kItemLists;
+  for (int l = 0; l < kItemLists; ++l) {
+    AKM_CK(scan_excl_int(plan->lcnt[l].as<int>(), plan->loff[l].as<int>(), llen[l], &plan->cub_temp,
+                         &plan->cub_temp_bytes, s));
+    lp.cnt[l] = plan->lcnt[l].as<int>();
+    lp.off[l] = plan->loff[l].as<int>();
+    lp.len[l] = llen[l];
+    const std::vector<long long>& gb = (l < 2) ? gkey : gbin;
+    for (int gi = 0; gi <= ngroups; ++gi) lp.gbeg[l][gi] = llen[l] ? gb[gi] : 0;
+  }
+  AKM_CK(plan->bounds.ensure(sizeof(int) * kItemLists * 2 * ngroups));
+  AKM_CK(launch_group_bounds(lp, ngroups, plan->bounds.as<int>(), s));
+  std::vector<int> bounds(kItemLists * 2 * ngroups);
+  AKM_CK(cudaMemcpyAsync(bounds.data(), plan->bounds.p, sizeof(int) * bounds.size(), cudaMemcpyDeviceToHost, s));
+  AKM_CK(cudaStreamSynchronize(s));
+  tm.mark("device layout + item scans");
+  // list l of the final item sets: 0 -> items_i[0], 1 -> items_i[1], 2 -> items_s[0], 3 -> items_ib[0],
+  // 4 -> items_s[1], 5 -> items_ib[1]
+  DevBuf* finals[kItemLists] = {&plan->items_i[0], &plan->items_i[1], &plan->items_s[0],
+                                &plan->items_ib[0], &plan->items_s[1], &plan->items_ib[1]};
+  const int maxc[kItemLists] = {ch_i, ch_i, (int)ch_s, ch_ib, (int)ch_s, ch_ib};
+  long long ltot[kItemLists];
+  const int* offs[kItemLists];
+  WorkItem* outs[kItemLists];
+  for (int l = 0; l < kItemLists; ++l) {
+    ltot[l] = ngroups ? bounds[(l * 2 + 1) * ngroups + ngroups - 1] : 0;
+    AKM_CK(plan->items_u[l].ensure(sizeof(WorkItem) * std::max<long long>(ltot[l], 1)));
+    AKM_CK(finals[l]->ensure(sizeof(WorkItem) * std::max<long long>(ltot[l], 1)));
+    offs[l] = plan->loff[l].as<int>();
+    outs[l] = llen[l] ? plan->items_u[l].as<WorkItem>() : nullptr;
+  }
+  AKM_CK(launch_emit_items(tab, plan->dtab.as<WinTable>(), L, plan->key_cnt.as<long long>(),
+                           plan->key_off.as<long long>(), n, ch_s, ch_i, ch_ib, offs, outs, s));
+  long long lmax = 1;
+  for (int l = 0; l < kItemLists; ++l) lmax = std::max(lmax, ltot[l]);
+  AKM_CK(plan->sort_keys.ensure(sizeof(unsigned) * 2 * lmax));
+  AKM_CK(plan->sort_idx.ensure(sizeof(int) * 2 * lmax));
+  for (int l = 0; l < kItemLists; ++l) {
+    if (!ltot[l]) continue;
+    AKM_CK(sort_items_larger_first(plan->items_u[l].as<WorkItem>(), ltot[l], maxc[l], ngroups,
+                                   plan->bounds.as<int>() + (l * 2 + 0) * ngroups,
+                                   plan->bounds.as<int>() + (l * 2 + 1) * ngroups, plan->sort_keys.as<unsigned>(),
+                                   plan->sort_keys.as<unsigned>() + lmax, plan->sort_idx.as<int>(),
+                                   plan->sort_idx.as<int>() + lmax, &plan->cub_temp, &plan->cub_temp_bytes,
+                                   finals[l]->as<WorkItem>(), s));
+  }
+  for (int set = 0; set < 2; ++set) {
+    plan->n_items_spread[set] = (size_t)ltot[set == 0 ? 2 : 4];
+    plan->n_items_interp[set] = (size_t)ltot[set == 0 ? 0 : 1];
+    plan->n_items_interp_bin[set] = (size_t)ltot[set == 0 ? 3 : 5];
+  }
+  for (int gi = 0; gi < ngroups; ++gi) {
+    Group& grp = plan->groups[gi];
     for (int set = 0; set < 2; ++set) {
-      std::vector<const std::vector<WorkItem>*> ss, si, sib;
-      for (int w : grp.wins) {
-        ss.push_back(&its_s[set][w]);
-        si.push_back(&its_i[set][w]);
-        sib.push_back(&its_ib[set][w]);
-      }
+      const int ls = set == 0 ? 2 : 4, li = set == 0 ? 0 : 1, lb = set == 0 ? 3 : 5;
+      auto beg = [&](int l) { return bounds[(l * 2 + 0) * ngroups + gi]; };
+      auto end = [&](int l) { return bounds[(l * 2 + 1) * ngroups + gi]; };
       ItemSlice& sl = grp.sl[set];
-      sl.spread_begin = (int)plan->items_spread[set].size();
-      sl.spread_count = (int)append_larger_first(ss, plan->items_spread[set], bs.pos);
-      sl.interp_begin = (int)plan->items_interp[set].size();
-      sl.interp_count = (int)append_larger_first(si, plan->items_interp[set], bs.pos);
+      sl.spread_begin = beg(ls);
+      sl.spread_count = end(ls) - beg(ls);
+      sl.interp_begin = beg(li);
+      sl.interp_count = end(li) - beg(li);
+      sl.interp_bin_begin = beg(lb);
+      sl.interp_bin_count = end(lb) - beg(lb);
       // per-cell DMMA items pay a whole cell footprint per item: with few points per occupied cell
       // the per-bin scalar kernel wins (c3: ~16 points per cell; c4/c5: hundreds)
-      long long pts = 0;
-      for (const auto* v : si)
-        for (const WorkItem& it : *v) pts += it.count;
-      sl.sparse = sl.interp_count > 0 && (double)pts / (double)sl.interp_count < 48.0;
-      sl.interp_bin_begin = (int)plan->items_interp_bin[set].size();
-      sl.interp_bin_count = (int)append_larger_first(sib, plan->items_interp_bin[set], bs.pos);
+      const double pts = (double)(set == 0 ? n : n - plan->n_split) * (double)grp.wins.size();
+      sl.sparse = sl.interp_count > 0 && pts / (double)sl.interp_count < 48.0;
     }
   }
 
@@ -757,38 +644,16 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   plan->szA1 = a1; plan->szA2 = a2; plan->szA3 = a3; plan->szC = cc; plan->szC2 = c2; plan->szTW = twc; plan->szD = dd;
   plan->r_cap = 0;  // grid workspace must be re-sized
 
-  tm.mark("host: groups, sort, layout");
-  // scatter into bin-major order
-  AKM_CK(cudaMemcpyAsync(plan->hist.p, cell_off, sizeof(int) * std::max<long long>(ncells, 1),
-                         cudaMemcpyHostToDevice, s));
-  AKM_CK(plan->dtab.ensure(sizeof(WinTable)));
+  // scatter into bin-major order (the cursors are the slot starts written above)
   AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
   AKM_CK(launch_scatter(n, tab, plan->dtab.as<WinTable>(), plan->u_tmp.as<double>(), nullptr, plan->hist.as<int>(),
                         plan->hist_off.as<long long>(), plan->u_sorted.as<double>(), plan->perm.as<int>(), plan->n_split,
                         s));
-  for (int set = 0; set < 2; ++set) {
-    const HostItems* lists[3] = {&plan->items_spread[set], &plan->items_interp[set], &plan->items_interp_bin[set]};
-    DevBuf* bufs[3] = {&plan->items_s[set], &plan->items_i[set], &plan->items_ib[set]};
-    for (int k = 0; k < 3; ++k) {
-      AKM_CK(bufs[k]->ensure(sizeof(WorkItem) * std::max<size_t>(lists[k]->size(), 1)));
-      if (!lists[k]->empty())
-        AKM_CK(cudaMemcpyAsync(bufs[k]->p, lists[k]->data(), sizeof(WorkItem) * lists[k]->size(),
-                               cudaMemcpyHostToDevice, s));
-    }
-  }
-  if (plan->near_field()) {
-    akm_status st = ensure_cell_tab(plan, s);
-    if (st != AKM_OK) return st;
-  }
-  tm.mark("scatter + item uploads");
-  AKM_CK(plan->bin_start.ensure(sizeof(int) * bstart.size()));
-  AKM_CK(cudaMemcpyAsync(plan->bin_start.p, bstart.data(), sizeof(int) * bstart.size(), cudaMemcpyHostToDevice, s));
   // twiddles
   AKM_CK(plan->tw.ensure(sizeof(double2) * std::max<long long>(twc, 1)));
   AKM_CK(launch_twiddles(tab, plan->dtab.as<WinTable>(), plan->tw.as<double2>(), s));
   AKM_CK(plan->D.ensure(sizeof(double) * std::max<long long>(dd, 1)));
-  AKM_CK(cudaStreamSynchronize(s));  // host vectors (cell_off, items) go out of scope / may change
-  tm.mark("bin starts, twiddles, D");
+  tm.mark("items, scatter, twiddles");
   plan->c_w_binned = plan->c_w;
   return AKM_OK;
 }
@@ -1016,7 +881,7 @@ static akm_status enqueue_finish(akm_plan* plan, const double* grid, const doubl
   if (plan->near_field()) {  // kappa_R's inner part: add sum_j (kappa - T_I)(r_ij) v_j (regularize.cu)
     if (set != 0) return plan->fail(AKM_ERR_UNSUPPORTED, "the near-field correction is built for the square products only");
     if (!plan->cell_tab_ok) return plan->fail(AKM_ERR_STATE, "internal error: near-field cell table not built");
-    const int nitems = (int)plan->items_interp_bin[0].size();
+    const int nitems = (int)plan->n_items_interp_bin[0];
     AKM_CK(launch_near_field(dtab, plan->items_ib[0].as<WorkItem>(), nitems, plan->cell_tab.as<int2>(),
                              plan->hist_off.as<long long>(), plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv,
                              plan->nfV.as<double>(), n, plan->P, r, ops, slotK, slotL, plan->family, plan->ell,
@@ -2242,8 +2107,8 @@ akm_status akm_get_info(const akm_plan* plan, akm_info* out) {
     out->occupied_bins[w] = plan->occupied.empty() ? 0 : plan->occupied[w];
     out->max_bin_points[w] = plan->maxbin.empty() ? 0 : plan->maxbin[w];
   }
-  out->work_items_spread = (int64_t)plan->items_spread[0].size();
-  out->work_items_interp = (int64_t)plan->items_interp[0].size();
+  out->work_items_spread = (int64_t)plan->n_items_spread[0];
+  out->work_items_interp = (int64_t)plan->n_items_interp[0];
   long long ws = 0;
   const DevBuf* bufs[] = {&plan->Xc, &plan->u_tmp, &plan->u_sorted, &plan->perm, &plan->hist, &plan->grid, &plan->H,
                           &plan->A1, &plan->A2, &plan->A3, &plan->C, &plan->C2, &plan->tw, &plan->D, &plan->part,
