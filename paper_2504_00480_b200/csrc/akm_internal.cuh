@@ -222,9 +222,6 @@ cudaError_t launch_window_radius(const double* X, long long n, long long ldx, co
 cudaError_t launch_scale_and_key(const double* X, long long n, long long ldx, const WinTable& tab,
                                  const WinTable* dtab, double* u_tmp, int* key, int* hist, const long long* hist_off,
                                  int* err_flag, long long n_split, cudaStream_t s);
-cudaError_t launch_scatter(long long n, const WinTable& tab, const WinTable* dtab, const double* u_tmp,
-                           const int* key, int* cursor, const long long* hist_off, double* u_sorted, int* perm,
-                           long long n_split, cudaStream_t s);
 // binsort.cu: S0 on the device (candidate bin statistics, bin-major layout, cursors, work items)
 constexpr int kBinCands = 6;  // candidate bin edges B = 1, 2, 3, 4, 6, 8
 struct BinCandParam {
@@ -262,14 +259,22 @@ cudaError_t launch_emit_items(const WinTable& tab, const WinTable* dtab, const B
 cudaError_t scan_excl_ll(const long long* in, long long* out, long long len, void** temp, size_t* temp_bytes,
                          cudaStream_t s);
 cudaError_t scan_excl_int(const int* in, int* out, long long len, void** temp, size_t* temp_bytes, cudaStream_t s);
-cudaError_t sort_items_larger_first(const WorkItem* in, long long cnt, int maxc, int nseg, const int* seg_begin,
-                                    const int* seg_end, unsigned* keys, unsigned* keys_alt, int* idx, int* idx_alt,
-                                    void** temp, size_t* temp_bytes, WorkItem* out, cudaStream_t s);
+struct WinGroupMap {
+  int group[kMaxWin];  // window -> its group's position in the launch order
+};
+cudaError_t sort_points(long long n, const WinTable& tab, const WinTable* dtab, const BinLayout& L, long long nkeys,
+                        const WinGroupMap& order, const double* u_tmp, long long n_split, unsigned* keys,
+                        unsigned* keys_alt, int* vals, int* vals_alt, void** temp, size_t* temp_bytes,
+                        double* u_sorted, int* perm, cudaStream_t s);
+cudaError_t sort_items_larger_first(const WorkItem* in, long long cnt, int maxc, const WinGroupMap& gm, int ngroups,
+                                    unsigned* keys, unsigned* keys_alt, int* idx, int* idx_alt, void** temp,
+                                    size_t* temp_bytes, WorkItem* out, cudaStream_t s);
 
 cudaError_t launch_kernel_samples(int family, int d, int N, double ell_eff, int deriv, double* out, cudaStream_t s);
 cudaError_t launch_cos_dft_axis(int d, int N, int axis, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_deconv_table(int N, int n_g, int m, double sigma_over, double* i0sq, cudaStream_t s);
 cudaError_t launch_multiplier(const WinTable& tab, const WinTable* dtab, int win, const double* bK, const double* bL,
-                              int ops_mask, double inv_c, double sigma_over, double* D, cudaStream_t s);
+                              int ops_mask, double inv_c, const double* i0sq, double* D, cudaStream_t s);
 cudaError_t launch_twiddles(const WinTable& tab, const WinTable* dtab, double2* tw, cudaStream_t s);
 cudaError_t launch_window_poly(int m, double beta, double* coef, cudaStream_t s);
 

@@ -1,6 +1,6 @@
 // binsort.cu -- S0 on the device: bin-edge costs, the bin-major layout of the (cell, class) slots,
-// the cell cursors of the scatter, the bin-start table and the three work-item lists, sorted larger
-// first per window group (north_star "warp-level bin sort").
+// the bin-start table, the three work-item lists (sorted larger first per window group) and the
+// points themselves in bin-major order (north_star "bin sort").
 //
 // The host keeps only what sizes launches: it reads back the per-candidate statistics (to choose B,
 // DESIGN.md §binning) and the per-group item counts.  Everything proportional to the cells, the bins
@@ -10,12 +10,13 @@
 //   k_bin_stats     per (window, B): spreading chunks, occupied bins, largest bin
 //   k_slot_keys     slot -> key in the bin-major order (bin, class, cell in bin); counts per key
 //   [scan]          key offsets = sorted start of every slot (exclusive sum)
-//   k_slot_cursor   scatter cursors (and the near-field cell table)
+//   k_slot_cursor   the near-field cell table (start, count) per slot
 //   k_bin_pass      bin starts; per-bin item counts (spreading chunks, per-bin interpolation chunks)
 //   [scans]         item offsets per list
 //   k_group_bounds  per-group [begin, end) of every list
 //   k_emit_*        the items, in key order (= the order the host loops produced)
-//   [segmented radix sort per group, stable] + gather: larger items first, ties in order
+//   [radix sort on (group, -count), stable] + gather: group by group, larger items first, ties in order
+//   k_point_keys    slot key of every (window, point); [stable radix sort]; k_point_gather -> u_sorted, perm
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
 
@@ -142,8 +143,8 @@ __global__ void k_slot_keys(const WinTable* __restrict__ tabp, const int* __rest
   }
 }
 
-// cursor[slot] = window-relative sorted start of the slot (the scatter advances it); optionally the
-// near-field table (start, count) per slot
+// cursor[slot] = window-relative sorted start of the slot (optional); the near-field table (start,
+// count) per slot (optional)
 __global__ void k_slot_cursor(const WinTable* __restrict__ tabp, const long long* __restrict__ hist_off, BinLayout L,
                               const long long* __restrict__ key_cnt, const long long* __restrict__ key_off,
                               int* __restrict__ cursor, int2* __restrict__ cell_tab) {
@@ -284,10 +285,12 @@ __global__ void k_emit_bin_items(const WinTable* __restrict__ tabp, BinLayout L,
   }
 }
 
-__global__ void k_item_keys(const WorkItem* __restrict__ it, long long cnt, int maxc, unsigned* __restrict__ keys,
-                            int* __restrict__ idx) {
+// sort key = (group of the item's window, maxc - count): one device-wide stable radix sort then orders
+// the list group by group, larger items first inside a group, ties in list order
+__global__ void k_item_keys(const WorkItem* __restrict__ it, long long cnt, int maxc, int cbits, WinGroupMap gm,
+                            unsigned* __restrict__ keys, int* __restrict__ idx) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x) {
-    keys[i] = (unsigned)(maxc - it[i].count);
+    keys[i] = ((unsigned)gm.group[it[i].win] << cbits) | (unsigned)(maxc - it[i].count);
     idx[i] = (int)i;
   }
 }
@@ -299,6 +302,43 @@ __global__ void k_item_gather(const WorkItem* __restrict__ in, const int* __rest
 }
 
 static int grid_for(long long work) { return (int)std::max<long long>(1, std::min<long long>((work + 255) / 256, 148 * 8)); }
+
+// ------------------------------------------------------------------ point sort (replaces the atomic scatter)
+// key of (window w, point i) = its slot's key: a stable radix sort by key puts every window's points
+// in bin-major order, inside a slot by increasing point index (deterministic, unlike cursor atomics)
+__global__ void k_point_keys(long long n, const WinTable* __restrict__ tabp, BinLayout L,
+                             const double* __restrict__ u_tmp, long long n_split, unsigned* __restrict__ keys,
+                             int* __restrict__ vals) {
+  const WinTable& tab = *tabp;
+  const int w = blockIdx.y;
+  const WinGeom& g = tab.w[w];
+  const int m = tab.m;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    int c[3] = {0, 0, 0};
+    for (int a = 3 - g.d; a < 3; ++a) c[a] = (int)floor(u_tmp[((long long)w * 3 + a) * n + i]) - (g.box_lo[a] + m - 1);
+    long long bin;
+    const long long key = slot_key(g, L, w, c, i >= n_split ? 1 : 0, bin);
+    keys[(long long)w * n + i] = (unsigned)key;
+    vals[(long long)w * n + i] = (int)i;
+  }
+}
+
+// sorted index j: window order[j / n] (every window holds n points; windows in group order), position
+// j % n; gathers the scaled coordinates into u_sorted and the point index into perm
+__global__ void k_point_gather(long long n, int P, const WinTable* __restrict__ tabp, WinGroupMap order,
+                               const int* __restrict__ vals, const double* __restrict__ u_tmp,
+                               double* __restrict__ u_sorted, int* __restrict__ perm) {
+  const WinTable& tab = *tabp;
+  const long long total = n * P;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < total; j += (long long)gridDim.x * blockDim.x) {
+    const int w = order.group[j / n];
+    const long long pos = j % n;
+    const WinGeom& g = tab.w[w];
+    const int i = vals[j];
+    perm[(long long)w * n + pos] = i;
+    for (int a = 3 - g.d; a < 3; ++a) u_sorted[((long long)w * 3 + a) * n + pos] = u_tmp[((long long)w * 3 + a) * n + i];
+  }
+}
 
 cudaError_t launch_slot_keys(const WinTable& tab, const WinTable* dtab, const int* hist, const long long* hist_off,
                              const BinLayout& L, long long* key_cnt, int* i0cnt, int* i1cnt, int ch_i, cudaStream_t s) {
@@ -377,19 +417,20 @@ cudaError_t scan_excl_int(const int* in, int* out, long long len, void** temp, s
   return scan_excl(in, out, len, temp, temp_bytes, s);
 }
 
-// Stable sort of one list by decreasing count inside each group segment, then gather into `out`.
-cudaError_t sort_items_larger_first(const WorkItem* in, long long cnt, int maxc, int nseg, const int* seg_begin,
-                                    const int* seg_end, unsigned* keys, unsigned* keys_alt, int* idx, int* idx_alt,
-                                    void** temp, size_t* temp_bytes, WorkItem* out, cudaStream_t s) {
+// Stable sort of one list by (group, decreasing count), then gather into `out`.
+cudaError_t sort_items_larger_first(const WorkItem* in, long long cnt, int maxc, const WinGroupMap& gm, int ngroups,
+                                    unsigned* keys, unsigned* keys_alt, int* idx, int* idx_alt, void** temp,
+                                    size_t* temp_bytes, WorkItem* out, cudaStream_t s) {
   if (cnt <= 0) return cudaSuccess;
-  k_item_keys<<<grid_for(cnt), 256, 0, s>>>(in, cnt, maxc, keys, idx);
+  int cbits = 1;
+  while ((1 << cbits) <= maxc) ++cbits;
+  int gbits = 0;
+  while ((1 << gbits) < ngroups) ++gbits;
+  k_item_keys<<<grid_for(cnt), 256, 0, s>>>(in, cnt, maxc, cbits, gm, keys, idx);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  int bits = 1;
-  while ((1 << bits) <= maxc) ++bits;
   size_t need = 0;
-  e = cub::DeviceSegmentedRadixSort::SortPairs(nullptr, need, keys, keys_alt, idx, idx_alt, (int)cnt, nseg, seg_begin,
-                                               seg_end, 0, bits, s);
+  e = cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_alt, idx, idx_alt, (int)cnt, 0, cbits + gbits, s);
   if (e != cudaSuccess) return e;
   if (need > *temp_bytes) {
     if (*temp) cudaFree(*temp);
@@ -399,10 +440,37 @@ cudaError_t sort_items_larger_first(const WorkItem* in, long long cnt, int maxc,
     if (e != cudaSuccess) return e;
     *temp_bytes = need;
   }
-  e = cub::DeviceSegmentedRadixSort::SortPairs(*temp, need, keys, keys_alt, idx, idx_alt, (int)cnt, nseg, seg_begin,
-                                               seg_end, 0, bits, s);
+  e = cub::DeviceRadixSort::SortPairs(*temp, need, keys, keys_alt, idx, idx_alt, (int)cnt, 0, cbits + gbits, s);
   if (e != cudaSuccess) return e;
   k_item_gather<<<grid_for(cnt), 256, 0, s>>>(in, idx_alt, cnt, out);
+  return cudaGetLastError();
+}
+
+cudaError_t sort_points(long long n, const WinTable& tab, const WinTable* dtab, const BinLayout& L, long long nkeys,
+                        const WinGroupMap& order, const double* u_tmp, long long n_split, unsigned* keys,
+                        unsigned* keys_alt, int* vals, int* vals_alt, void** temp, size_t* temp_bytes,
+                        double* u_sorted, int* perm, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const long long total = n * tab.P;
+  k_point_keys<<<dim3(grid_for(n), tab.P), 256, 0, s>>>(n, dtab, L, u_tmp, n_split, keys, vals);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int bits = 1;
+  while ((1LL << bits) < nkeys) ++bits;
+  size_t need = 0;
+  e = cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_alt, vals, vals_alt, (int)total, 0, bits, s);
+  if (e != cudaSuccess) return e;
+  if (need > *temp_bytes) {
+    if (*temp) cudaFree(*temp);
+    *temp = nullptr;
+    *temp_bytes = 0;
+    e = cudaMalloc(temp, need);
+    if (e != cudaSuccess) return e;
+    *temp_bytes = need;
+  }
+  e = cub::DeviceRadixSort::SortPairs(*temp, need, keys, keys_alt, vals, vals_alt, (int)total, 0, bits, s);
+  if (e != cudaSuccess) return e;
+  k_point_gather<<<grid_for(total), 256, 0, s>>>(n, tab.P, dtab, order, vals_alt, u_tmp, u_sorted, perm);
   return cudaGetLastError();
 }
 

@@ -132,10 +132,12 @@ struct akm_plan {
   DevBuf reg_coef, bin_start;  // regularisation polynomials [w][op][kRegStride]; per-window bin start tables
   DevBuf cell_tab, nfV;        // near field: (start, count) per (cell, class) slot; bin-sorted copy of V
   bool cell_tab_ok = false;      // cell_tab matches the last bin sort (built on demand: near field only)
+  DevBuf deconv;                 // [3][N + 1] per-axis deconvolution factors (setup_kernels.cu k_deconv_table)
+  bool deconv_ok = false;
   // S0 on the device (binsort.cu): candidate statistics, key space (bin-major slot order) counts and
   // offsets, per-list item counts / offsets, unsorted items, sort scratch, group bounds
   DevBuf bs_bc, bs_stats, key_cnt, key_off, lcnt[kItemLists], loff[kItemLists], items_u[kItemLists];
-  DevBuf sort_keys, sort_idx, bounds;
+  DevBuf sort_keys, sort_idx, bounds, pt_keys, pt_vals;
   void* cub_temp = nullptr;
   size_t cub_temp_bytes = 0;
   BinLayout bl{};
@@ -283,8 +285,6 @@ cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, 
 
 
 // ================================================================== geometry / binning
-// Build per-window boxes for the current c_w, histogram the points per cell on the device,
-// choose the bin edge B per window from the histogram, lay the cells out bin-major, scatter.
 // (start, count) of every (cell, class) slot in the window-relative sorted order of the last bin
 // sort, for the near-field correction; built on demand (only kappa_R's inner part reads it) from the
 // device key counts and offsets of that sort (binsort.cu)
@@ -374,7 +374,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
                               nullptr, plan->hist.as<int>(), plan->hist_off.as<long long>(), plan->err_flag.as<int>(),
                               plan->n_split, s));
   // S0 on the device (binsort.cu): statistics of every candidate bin edge -> B per window (host, the
-  // cost model below) -> bin-major layout, scatter cursors, bin starts and work items on the device
+  // cost model below) -> bin-major layout, bin starts, work items and the point sort on the device
   const long long total_pts = n * P;
   long long ch_s = total_pts / (148 * 2);
   ch_s = std::max(32LL, std::min(4096LL, ch_s));
@@ -514,6 +514,7 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     }
   }
   gkey[ngroups] = nkeys;
+  if (nkeys >= (1LL << 32)) return plan->fail(AKM_ERR_UNSUPPORTED, "bin layout of %lld slots exceeds 2^32", nkeys);
   gbin[ngroups] = nbins;
   AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
   // keys: counts, offsets, cursors
@@ -537,8 +538,9 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     AKM_CK(plan->cell_tab.ensure(sizeof(int2) * std::max<long long>(ncells, 1)));
     ctab = plan->cell_tab.as<int2>();
   }
-  AKM_CK(launch_slot_cursor(tab, plan->dtab.as<WinTable>(), plan->hist_off.as<long long>(), L,
-                            plan->key_cnt.as<long long>(), plan->key_off.as<long long>(), plan->hist.as<int>(), ctab, s));
+  if (ctab)
+    AKM_CK(launch_slot_cursor(tab, plan->dtab.as<WinTable>(), plan->hist_off.as<long long>(), L,
+                              plan->key_cnt.as<long long>(), plan->key_off.as<long long>(), nullptr, ctab, s));
   plan->cell_tab_ok = ctab != nullptr;
   AKM_CK(plan->bin_start.ensure(sizeof(int) * (nbins_total + P)));
   AKM_CK(launch_bin_pass(tab, plan->dtab.as<WinTable>(), L, plan->key_off.as<long long>(), n, ch_s, ch_ib,
@@ -583,14 +585,15 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   for (int l = 0; l < kItemLists; ++l) lmax = std::max(lmax, ltot[l]);
   AKM_CK(plan->sort_keys.ensure(sizeof(unsigned) * 2 * lmax));
   AKM_CK(plan->sort_idx.ensure(sizeof(int) * 2 * lmax));
+  WinGroupMap gm{};
+  for (int gi = 0; gi < ngroups; ++gi)
+    for (int w : plan->groups[gi].wins) gm.group[w] = gi;
   for (int l = 0; l < kItemLists; ++l) {
     if (!ltot[l]) continue;
-    AKM_CK(sort_items_larger_first(plan->items_u[l].as<WorkItem>(), ltot[l], maxc[l], ngroups,
-                                   plan->bounds.as<int>() + (l * 2 + 0) * ngroups,
-                                   plan->bounds.as<int>() + (l * 2 + 1) * ngroups, plan->sort_keys.as<unsigned>(),
-                                   plan->sort_keys.as<unsigned>() + lmax, plan->sort_idx.as<int>(),
-                                   plan->sort_idx.as<int>() + lmax, &plan->cub_temp, &plan->cub_temp_bytes,
-                                   finals[l]->as<WorkItem>(), s));
+    AKM_CK(sort_items_larger_first(plan->items_u[l].as<WorkItem>(), ltot[l], maxc[l], gm, ngroups,
+                                   plan->sort_keys.as<unsigned>(), plan->sort_keys.as<unsigned>() + lmax,
+                                   plan->sort_idx.as<int>(), plan->sort_idx.as<int>() + lmax, &plan->cub_temp,
+                                   &plan->cub_temp_bytes, finals[l]->as<WorkItem>(), s));
   }
   for (int set = 0; set < 2; ++set) {
     plan->n_items_spread[set] = (size_t)ltot[set == 0 ? 2 : 4];
@@ -644,16 +647,25 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   plan->szA1 = a1; plan->szA2 = a2; plan->szA3 = a3; plan->szC = cc; plan->szC2 = c2; plan->szTW = twc; plan->szD = dd;
   plan->r_cap = 0;  // grid workspace must be re-sized
 
-  // scatter into bin-major order (the cursors are the slot starts written above)
+  // points into bin-major order: stable radix sort by slot key (binsort.cu sort_points)
   AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
-  AKM_CK(launch_scatter(n, tab, plan->dtab.as<WinTable>(), plan->u_tmp.as<double>(), nullptr, plan->hist.as<int>(),
-                        plan->hist_off.as<long long>(), plan->u_sorted.as<double>(), plan->perm.as<int>(), plan->n_split,
-                        s));
+  {
+    WinGroupMap order{};  // window of each n-point block of the sorted sequence (group order)
+    int q = 0;
+    for (const Group& grp : plan->groups)
+      for (int w : grp.wins) order.group[q++] = w;
+    AKM_CK(plan->pt_keys.ensure(sizeof(unsigned) * 2 * std::max<long long>(n * P, 1)));
+    AKM_CK(plan->pt_vals.ensure(sizeof(int) * 2 * std::max<long long>(n * P, 1)));
+    AKM_CK(sort_points(n, tab, plan->dtab.as<WinTable>(), L, nkeys, order, plan->u_tmp.as<double>(), plan->n_split,
+                       plan->pt_keys.as<unsigned>(), plan->pt_keys.as<unsigned>() + n * P, plan->pt_vals.as<int>(),
+                       plan->pt_vals.as<int>() + n * P, &plan->cub_temp, &plan->cub_temp_bytes,
+                       plan->u_sorted.as<double>(), plan->perm.as<int>(), s));
+  }
   // twiddles
   AKM_CK(plan->tw.ensure(sizeof(double2) * std::max<long long>(twc, 1)));
   AKM_CK(launch_twiddles(tab, plan->dtab.as<WinTable>(), plan->tw.as<double2>(), s));
   AKM_CK(plan->D.ensure(sizeof(double) * std::max<long long>(dd, 1)));
-  tm.mark("items, scatter, twiddles");
+  tm.mark("items, point sort, twiddles");
   plan->c_w_binned = plan->c_w;
   return AKM_OK;
 }
@@ -679,6 +691,11 @@ static akm_status rebuild_tables(akm_plan* plan, cudaStream_t s) {
     plan->bk_keys.assign(plan->P, akm_plan::BkKey{});
   }
   if (plan->reg_p > 0) AKM_CK(plan->reg_coef.ensure(sizeof(double) * plan->P * 2 * kRegStride));
+  if (!plan->deconv_ok) {  // per-axis deconvolution factors: fixed by (N, n_g, m, sigma) at set_points
+    AKM_CK(plan->deconv.ensure(sizeof(double) * 3 * (N + 1)));
+    AKM_CK(launch_deconv_table(N, plan->n_g, plan->m, plan->sigma_over, plan->deconv.as<double>(), s));
+    plan->deconv_ok = true;
+  }
   for (int w = 0; w < plan->P; ++w) {
     const int d = plan->tab.w[w].d;
     const double ell_eff = plan->ell / plan->c_w[w];
@@ -708,8 +725,8 @@ static akm_status rebuild_tables(akm_plan* plan, cudaStream_t s) {
       }
       plan->bk_keys[w] = key;
     }
-    AKM_CK(launch_multiplier(plan->tab, plan->dtab.as<WinTable>(), w, bK, bL, 3, 1.0 / plan->c_w[w], plan->sigma_over,
-                             plan->D.as<double>(), s));
+    AKM_CK(launch_multiplier(plan->tab, plan->dtab.as<WinTable>(), w, bK, bL, 3, 1.0 / plan->c_w[w],
+                             plan->deconv.as<double>(), plan->D.as<double>(), s));
   }
   return AKM_OK;
 }
@@ -1231,6 +1248,7 @@ akm_status akm_set_points(akm_plan* plan, const double* X, int64_t n, int32_t p,
   plan->family = family;
   plan->N = N;
   plan->m = m;
+  plan->deconv_ok = false;  // (N, m, sigma) may change: rebuild the deconvolution table
   plan->n_g = n_g;
   plan->sigma_over = sigma_over;
   plan->eps_B = eps_B;

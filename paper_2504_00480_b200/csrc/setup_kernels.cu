@@ -2,10 +2,9 @@
 //
 //   window_minmax / window_radius : per-window bounding box and radius R_w (reading R2)
 //   scale_and_key                 : scaled grid coordinates u = (x - center) n_g / c_w,
-//                                   cell index, cell histogram (bin sort, pass 1)
-//   scatter                       : counting-sort scatter into bin-major order (pass 2)
+//                                   cell index, cell histogram (the rest of the bin sort: binsort.cu)
 //   kernel_samples, cos_dft_axis  : b_k of eq. (3.2) for kappa and kappa^der
-//   multiplier                    : D_k = omega_k b_k / prod_t I0(m sqrt(beta^2-(2 pi k_t/n_g)^2))^2
+//   deconv_table, multiplier      : D_k = omega_k b_k / prod_t I0(m sqrt(beta^2-(2 pi k_t/n_g)^2))^2
 //                                   (App. A deconvolution; reading R5 for omega)
 //   twiddles                      : e^{-2 pi i k (box_lo + l) / n_g} tables of the box-local DFTs
 #include "akm_internal.cuh"
@@ -118,31 +117,33 @@ __device__ __forceinline__ long long cell_linear(const WinGeom& g, const int c[3
 
 // Histogram key = (cell, class): class 1 marks the rows i >= n_split (the targets of a cross
 // product, akm_kernel_cross_mvm), so the two classes can be laid out apart inside every bin.
+// One thread per point for all windows: the point's row of X is read once (the later windows hit L1).
 __global__ void k_scale_and_key(const double* __restrict__ X, long long n, long long ldx, const WinTable* __restrict__ tabp,
                                 double* __restrict__ u_tmp, int* __restrict__ hist,
                                 const long long* __restrict__ hist_off, int* __restrict__ err_flag, long long n_split) {
   const WinTable& tab = *tabp;
-  const int w = blockIdx.y;
-  const WinGeom& g = tab.w[w];
   const int m = tab.m;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    int c[3] = {0, 0, 0};
-    bool ok = true;
-    for (int a = 3 - g.d; a < 3; ++a) {
-      const double u = (X[i * ldx + g.feat[a]] - g.center[a]) * g.scale;
-      u_tmp[((long long)w * 3 + a) * n + i] = u;
-      const int cc = (int)floor(u) - (g.box_lo[a] + m - 1);
-      ok = ok && cc >= 0 && cc < g.ncell[a];
-      c[a] = cc;
+    for (int w = 0; w < tab.P; ++w) {
+      const WinGeom& g = tab.w[w];
+      int c[3] = {0, 0, 0};
+      bool ok = true;
+      for (int a = 3 - g.d; a < 3; ++a) {
+        const double u = (__ldg(X + i * ldx + g.feat[a]) - g.center[a]) * g.scale;
+        u_tmp[((long long)w * 3 + a) * n + i] = u;
+        const int cc = (int)floor(u) - (g.box_lo[a] + m - 1);
+        ok = ok && cc >= 0 && cc < g.ncell[a];
+        c[a] = cc;
+      }
+      if (!ok) atomicOr(err_flag, 1);
+      // warp-level aggregation: lanes with the same (cell, class) key elect one leader that adds the
+      // group's size (points concentrate in few cells, up to 2.5e4 per cell: contended atomics otherwise)
+      const long long key = ok ? hist_off[w] + 2 * cell_linear(g, c) + (i >= n_split ? 1 : 0) : -1;
+      const unsigned act = __activemask();
+      const unsigned peers = __match_any_sync(act, key);
+      const int leader = __ffs(peers) - 1;
+      if (ok && (int)(threadIdx.x & 31) == leader) atomicAdd(hist + key, __popc(peers));
     }
-    if (!ok) atomicOr(err_flag, 1);
-    // warp-level aggregation: lanes with the same (cell, class) key elect one leader that adds the
-    // group's size (points concentrate in few cells, up to 2.5e4 per cell: contended atomics otherwise)
-    const long long key = ok ? hist_off[w] + 2 * cell_linear(g, c) + (i >= n_split ? 1 : 0) : -1;
-    const unsigned act = __activemask();
-    const unsigned peers = __match_any_sync(act, key);
-    const int leader = __ffs(peers) - 1;
-    if (ok && (int)(threadIdx.x & 31) == leader) atomicAdd(hist + key, __popc(peers));
   }
 }
 
@@ -151,50 +152,11 @@ cudaError_t launch_scale_and_key(const double* X, long long n, long long ldx, co
                                  cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   long long blocks = (n + 255) / 256;
-  if (blocks > 4736) blocks = 4736;
-  k_scale_and_key<<<dim3((unsigned)blocks, tab.P), 256, 0, s>>>(X, n, ldx, dtab, u_tmp, hist, hist_off, err_flag, n_split);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_scale_and_key<<<(unsigned)blocks, 256, 0, s>>>(X, n, ldx, dtab, u_tmp, hist, hist_off, err_flag, n_split);
   return cudaGetLastError();
 }
 
-// cursor[hist_off[w] + 2 cell + class] holds the (window-relative) sorted position of the next
-// point of that cell and class.
-__global__ void k_scatter(long long n, const WinTable* __restrict__ tabp, const double* __restrict__ u_tmp, int* __restrict__ cursor,
-                          const long long* __restrict__ hist_off, double* __restrict__ u_sorted,
-                          int* __restrict__ perm, long long n_split) {
-  const WinTable& tab = *tabp;
-  const int w = blockIdx.y;
-  const WinGeom& g = tab.w[w];
-  const int m = tab.m;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    int c[3] = {0, 0, 0};
-    double u[3] = {0.0, 0.0, 0.0};
-    for (int a = 3 - g.d; a < 3; ++a) {
-      u[a] = u_tmp[((long long)w * 3 + a) * n + i];
-      c[a] = (int)floor(u[a]) - (g.box_lo[a] + m - 1);
-    }
-    // warp-level bin sort: the lanes of one (cell, class) key take consecutive slots from one atomic
-    const long long key = hist_off[w] + 2 * cell_linear(g, c) + (i >= n_split ? 1 : 0);
-    const unsigned act = __activemask();
-    const unsigned peers = __match_any_sync(act, key);
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(peers) - 1;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(cursor + key, __popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    const int pos = base + __popc(peers & ((1u << lane) - 1u));
-    perm[(long long)w * n + pos] = (int)i;
-    for (int a = 3 - g.d; a < 3; ++a) u_sorted[((long long)w * 3 + a) * n + pos] = u[a];
-  }
-}
-
-cudaError_t launch_scatter(long long n, const WinTable& tab, const WinTable* dtab, const double* u_tmp, const int* /*key*/, int* cursor,
-                           const long long* hist_off, double* u_sorted, int* perm, long long n_split, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
-  long long blocks = (n + 255) / 256;
-  if (blocks > 4736) blocks = 4736;
-  k_scatter<<<dim3((unsigned)blocks, tab.P), 256, 0, s>>>(n, dtab, u_tmp, cursor, hist_off, u_sorted, perm, n_split);
-  return cudaGetLastError();
-}
 
 // ---------------------------------------------------------------- b_k (eq. 3.2)
 // samples s[l] = kappa(l/N; ell_eff) (or kappa^der) for l in I_N^d, stored at index (l + N/2).
@@ -284,12 +246,31 @@ cudaError_t launch_cos_dft_axis(int d, int N, int axis, const double* in, double
 //   n_g c_k(phi) = I0(m sqrt(beta^2 - (2 pi k / n_g)^2))   (reading R4),
 //   omega_k = (1[k in I_N^d] + 1[-k in I_N^d]) / 2          (reading R5: real part of eq. 3.3),
 // and for the ell-derivative table the joint-scaling factor 1/c_w (reading R7).
+// i0sq[a * (N + 1) + ki] = I0(m sqrt(beta^2 - (2 pi k / n_g)^2))^2, k = ki (a = 2) or ki - N/2: the
+// per-axis factors of the deconvolution; they depend on (N, n_g, m, sigma) only (set_points)
+__global__ void k_deconv_table(int N, int n_g, int m, double beta, double* __restrict__ i0sq) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 3 * (N + 1); idx += gridDim.x * blockDim.x) {
+    const int a = idx / (N + 1), ki = idx % (N + 1);
+    const int k = (a == 2) ? ki : ki - N / 2;
+    const double wk = 2.0 * kPi * (double)k / (double)n_g;
+    const double i0 = bessel_i0((double)m * sqrt(beta * beta - wk * wk));
+    i0sq[idx] = i0 * i0;
+  }
+}
+
+cudaError_t launch_deconv_table(int N, int n_g, int m, double sigma_over, double* i0sq, cudaStream_t s) {
+  const double beta = kPi * (2.0 - 1.0 / sigma_over);
+  k_deconv_table<<<(3 * (N + 1) + 255) / 256, 256, 0, s>>>(N, n_g, m, beta, i0sq);
+  return cudaGetLastError();
+}
+
 __global__ void k_multiplier(const WinTable* __restrict__ tabp, int win, const double* __restrict__ bK, const double* __restrict__ bL,
-                             int ops_mask, double inv_c, double beta, double* __restrict__ D) {
+                             int ops_mask, double inv_c, const double* __restrict__ i0sq, double* __restrict__ D) {
   const WinTable& tab = *tabp;
   const WinGeom& g = tab.w[win];
   const int N = tab.N, n_g = tab.n_g, m = tab.m, d = g.d;
   const long long per = (long long)g.K[0] * g.K[1] * g.K[2];
+  // the deconvolution factorises over the axes: I0(.)^2 per axis and frequency (k_deconv_table)
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < per;
        idx += (long long)gridDim.x * blockDim.x) {
     int kk[3];
@@ -306,9 +287,7 @@ __global__ void k_multiplier(const WinTable* __restrict__ tabp, int win, const d
     for (int a = 3 - d; a < 3; ++a) {
       inI = inI && (k[a] >= -N / 2) && (k[a] <= N / 2 - 1);
       negInI = negInI && (-k[a] >= -N / 2) && (-k[a] <= N / 2 - 1);
-      const double wk = 2.0 * kPi * (double)k[a] / (double)n_g;
-      const double i0 = bessel_i0((double)m * sqrt(beta * beta - wk * wk));
-      deconv *= i0 * i0;
+      deconv *= i0sq[a * (N + 1) + kk[a]];
       int km = k[a] % N;  // periodic index of b: k mod N in I_N
       if (km >= N / 2) km -= N;
       if (km < -N / 2) km += N;
@@ -322,12 +301,11 @@ __global__ void k_multiplier(const WinTable* __restrict__ tabp, int win, const d
 }
 
 cudaError_t launch_multiplier(const WinTable& tab, const WinTable* dtab, int win, const double* bK, const double* bL, int ops_mask,
-                              double inv_c, double sigma_over, double* D, cudaStream_t s) {
+                              double inv_c, const double* i0sq, double* D, cudaStream_t s) {
   const WinGeom& g = tab.w[win];
   const long long per = (long long)g.K[0] * g.K[1] * g.K[2];
-  const double beta = kPi * (2.0 - 1.0 / sigma_over);
-  int blocks = (int)((per + 255) / 256);
-  k_multiplier<<<blocks, 256, 0, s>>>(dtab, win, bK, bL, ops_mask, inv_c, beta, D);
+  int blocks = (int)std::min<long long>((per + 255) / 256, 148 * 4);
+  k_multiplier<<<blocks, 256, 0, s>>>(dtab, win, bK, bL, ops_mask, inv_c, i0sq, D);
   return cudaGetLastError();
 }
 
