@@ -315,7 +315,20 @@ def main():
         if "aafn_kpw" in wl.extra:              # f3: AAFN preconditioner
             plan.set_preconditioner(wl.extra["aafn_kpw"])
         plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
-    set_theta_ms = (time.perf_counter() - t0) * 1e3
+    torch.cuda.synchronize(dev)
+    set_theta_ms = (time.perf_counter() - t0) * 1e3   # set_points + the first set_theta (allocations)
+    # a theta step as an optimizer takes it: ell moved by 1% (Gaussian windows re-bin: c_w follows
+    # ell), median of 3, host wall clock around the synchronised call; theta restored afterwards
+    setter = sp if sharded else plan
+    warm = []
+    for k in range(3):
+        a = time.perf_counter()
+        setter.set_theta(wl.sigma_f, wl.ell * (1.0 + 0.01 * (k + 1)), wl.sigma_eps)
+        torch.cuda.synchronize(dev)
+        warm.append((time.perf_counter() - a) * 1e3)
+    setter.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+    torch.cuda.synchronize(dev)
+    set_theta_warm_ms = float(np.median(warm))
     info = plan.info()
 
     if objective:
@@ -535,6 +548,7 @@ def main():
                 "peak_gbs": peaks.get("hbm_gbs"), "frac": alg_bytes / (ms_per_step * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)},
         "hbm_stages": hbm_stages,
         "set_theta_ms": set_theta_ms,
+        "set_theta_warm_ms": set_theta_warm_ms,
         "products_per_step": products_per_step,
         "plan": {"bin": info["bin"], "box": info["box"], "c_w": info["c_w"], "work_items_spread": info["work_items_spread"],
                  "work_items_interp": info["work_items_interp"], "max_bin_points": info["max_bin_points"]},
