@@ -13,6 +13,12 @@ process per GPU) holds a disjoint row block of X and V; it
      B200 node), then runs the small DFT / multiply / inverse DFT redundantly and interpolates at its
      own points (``akm_mvm_from_grid``).  No other exchange: the outputs stay row-sharded.
 
+**Window sharding** (``WindowShardedPlan``, §8(e) item 3).  K-hat = sigma_f^2 sum_w K_w +
+sigma_eps^2 I is a sum over the windows, each with its own frame (reading R2: c_w depends on that
+window's points only).  Each rank holds all rows and a contiguous block of the windows, applies its
+windows (rank 0 also the sigma_eps^2 V term), and ONE all-reduce (sum) of each n x r output combines
+them.  At most W ranks do work (W <= 4 in BASELINE.json's configs).
+
 **Probe (column) sharding** (``sharded_objective``, §8(e) item 2).  The CG column and every Lanczos
 probe of the objective are independent recurrences: each rank holds the whole problem and runs a
 slice of the probes (rank 0 also the CG column); one all-reduce of three scalars combines them.
@@ -145,6 +151,70 @@ class ShardedPlan:
         self.backend.spread_grid(V_local, grid)
         self.dist.all_reduce(grid)
         self.backend.mvm_from_grid(grid, V_local, Y, dY_ell, dY_sf)
+        return Y, dY_ell, dY_sf
+
+    def close(self):
+        close = getattr(self.backend, "close", None)
+        if close:
+            close()
+
+
+def window_partition(P: int, world: int, rank: int):
+    """Contiguous [start, stop) of the ``P`` windows owned by ``rank`` (empty when world > P for the
+    last ranks; rank 0 always holds one when P >= 1)."""
+    return column_partition(P, world, rank)
+
+
+class WindowShardedPlan:
+    """Window-sharded additive-kernel product over the default process group (module docstring).
+
+    Every rank passes ALL rows of ``X``; it builds a plan for its block of ``windows``
+    (``window_partition``).  ``mvm_multi`` returns the full products on every rank: the local windows'
+    sum (rank 0 adds sigma_eps^2 V), then one all-reduce per requested output.  ``backend`` defaults to
+    the library's ``Plan`` on ``device``; the CPU tests pass an object with the same methods."""
+
+    def __init__(self, X, windows, family=0, N=32, sigma_over=2.0, m=6, eps_B=1.0 / 16, *, device=None,
+                 backend=None, comm_device=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.world = dist.get_world_size()
+        self.rank = dist.get_rank()
+        self.w0, self.w1 = window_partition(len(windows), self.world, self.rank)
+        self.windows = [tuple(w) for w in windows][self.w0:self.w1]
+        self.comm_device = comm_device
+        self.backend = None
+        if self.windows:
+            if backend is None:
+                from . import Plan
+                backend = Plan(0 if device is None else int(torch.device(device).index or 0))
+            self.backend = backend
+            backend.set_points(X, self.windows, family, N, sigma_over, m, eps_B)
+
+    def set_theta(self, sigma_f, ell, sigma_eps):
+        """theta on the local windows; the sigma_eps^2 I term belongs to rank 0 only."""
+        if self.backend is not None:
+            self.backend.set_theta(sigma_f, ell, sigma_eps if self.rank == 0 else 0.0)
+        return self
+
+    def info(self):
+        return self.backend.info() if self.backend is not None else {"P": 0}
+
+    def mvm_multi(self, V, Y=None, dY_ell=None, dY_sf=None):
+        """The full products on every rank: the local windows' part, then one all-reduce per output."""
+        outs = [t for t in (Y, dY_ell, dY_sf) if t is not None]
+        if self.backend is not None:
+            self.backend.mvm_multi(V, Y=Y, dY_ell=dY_ell, dY_sf=dY_sf)
+        else:
+            for t in outs:
+                t.zero_()
+        for t in outs:
+            if self.comm_device is None or t.device == self.comm_device:
+                self.dist.all_reduce(t)
+            else:  # the collective's device differs from the output's (gloo on CPU for GPU outputs)
+                c = t.to(self.comm_device)
+                self.dist.all_reduce(c)
+                t.copy_(c)
         return Y, dY_ell, dY_sf
 
     def close(self):

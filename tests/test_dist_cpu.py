@@ -375,3 +375,73 @@ def test_gloo_probe_sharded_gradient():
         assert g["probes"] == 5
         for j in ("sf", "ell", "se"):
             assert g[j] == pytest.approx(ref[j], rel=1e-10), j
+
+
+# ---------------------------------------------------------------- window-sharded product (§8(e) item 3)
+class OracleWindowBackend:
+    """Test stand-in for the library behind WindowShardedPlan: the truncated-Fourier product (eq. 3.3,
+    scaling reading R2) of the oracle over this rank's windows."""
+
+    def set_points(self, X, windows, family, N, sigma_over, m, eps_B):
+        self.X, self.windows, self.family, self.N, self.eps_B = np.asarray(X), windows, family, N, eps_B
+
+    def set_theta(self, sf, ell, se):
+        self.theta = (sf, ell, se)
+
+    def mvm_multi(self, V, Y=None, dY_ell=None, dY_sf=None):
+        from oracle import fourier as F
+        out = F.additive_fastsum(self.X, self.windows, self.family, self.theta, V.numpy(), self.N, self.eps_B,
+                                 ops=("K", "dell", "dsf"))
+        for t, k in ((Y, "K"), (dY_ell, "dell"), (dY_sf, "dsf")):
+            if t is not None:
+                t.copy_(torch.from_numpy(out[k]))
+
+
+def _window_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wl = workloads.CONFIGS["c2"]
+        n, r = 400, 2
+        X = workloads.make_X(wl, n=n)
+        V = torch.from_numpy(np.ascontiguousarray(workloads.make_V(wl, n=n, r=r)))
+        sp = D.WindowShardedPlan(X, wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B,
+                                 backend=OracleWindowBackend())
+        sp.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+        Y, dY, dS = torch.empty_like(V), torch.empty_like(V), torch.empty_like(V)
+        sp.mvm_multi(V, Y=Y, dY_ell=dY, dY_sf=dS)
+        q.put((rank, (sp.w0, sp.w1), Y.numpy(), dY.numpy(), dS.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_window_sharded_product(world):
+    """world 2 (windows 2 + 1) and world 4 (> W = 3: one rank holds no window): the sum over the ranks'
+    window blocks (sigma_eps^2 V on rank 0 only) and one all-reduce per output reproduce the
+    single-process oracle product on every rank, to rounding."""
+    from oracle import fourier as F
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_window_worker, args=(k, world, port, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    wl = workloads.CONFIGS["c2"]
+    X = workloads.make_X(wl, n=400)
+    V = workloads.make_V(wl, n=400, r=2)
+    want = F.additive_fastsum(X, wl.windows, wl.family, (wl.sigma_f, wl.ell, wl.sigma_eps), V, wl.N, wl.eps_B,
+                              ops=("K", "dell", "dsf"))
+    blocks = [b for _, b, *_ in res]
+    assert blocks[0][0] == 0 and blocks[-1][1] == len(wl.windows)
+    assert all(blocks[k][1] == blocks[k + 1][0] for k in range(world - 1))
+    if world > len(wl.windows):
+        assert any(b == a for a, b in blocks)              # a rank without windows took part
+    for _, _, Y, dY, dS in res:
+        for got, key in ((Y, "K"), (dY, "dell"), (dS, "dsf")):
+            assert np.abs(got - want[key]).max() <= 1e-12 * np.abs(want[key]).max(), key

@@ -2,7 +2,8 @@
 
 The split entry points (akm_get_bounds / akm_set_bounds / akm_set_radius, akm_spread_grid,
 akm_mvm_from_grid) let G shards of the rows each spread onto the same grids; summing the grids and
-finishing on every shard must reproduce the single-plan product.  Two checks:
+finishing on every shard must reproduce the single-plan product.  Two checks (and the window-sharded
+plan at world 2 and 3, §8(e) item 3, at the end):
   * one process, two plans on cuda:0, grids summed by a device add (the library calls alone);
   * the ShardedPlan driver at world_size 2 over gloo, both ranks on cuda:0 (host-mediated all-reduce,
     no rank's kernels wait on another's: the NCCL/NVLink path differs only in the transport).
@@ -292,3 +293,55 @@ def test_probe_sharded_gradient_gloo_world2(akm, kpw):
         assert last < 1e-11, last      # converged: the products' rounding does not move the solves
         for j in ("sf", "ell", "se"):
             assert g[j] == pytest.approx(single[j], rel=1e-9, abs=1e-9 * abs(single["se"])), j
+
+
+# ---------------------------------------------------------------- window sharding (§8(e) item 3)
+def _win_gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2504_00480_b200 import dist as D
+        wl = workloads.CONFIGS["c4"]
+        n, r = 20000, 3
+        X = workloads.make_X(wl, n=n)
+        V = workloads.make_V(wl, n=n, r=r)
+        dev = torch.device("cuda:0")
+        sp = D.WindowShardedPlan(torch.from_numpy(X).to(dev), wl.windows, wl.family, wl.N, wl.sigma_over, wl.m,
+                                 wl.eps_B, device=dev, comm_device=torch.device("cpu"))
+        sp.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+        Vd = torch.from_numpy(V).to(dev)
+        Y, dY, dS = torch.empty_like(Vd), torch.empty_like(Vd), torch.empty_like(Vd)
+        sp.mvm_multi(Vd, Y=Y, dY_ell=dY, dY_sf=dS)
+        torch.cuda.synchronize()
+        q.put((rank, (sp.w0, sp.w1), Y.cpu().numpy(), dY.cpu().numpy(), dS.cpu().numpy()))
+        sp.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_window_sharded_plan_gloo(akm, world):
+    """c4's four windows over 2 ranks (2 + 2) and 3 ranks (2 + 1 + 1), both on cuda:0: every rank's
+    all-reduced products equal the single plan's to rounding (the per-window frames are independent,
+    reading R2; sigma_eps^2 V is added once)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_win_gloo_worker, args=(k, world, port, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    wl = workloads.CONFIGS["c4"]
+    X = workloads.make_X(wl, n=20000)
+    V = workloads.make_V(wl, n=20000, r=3)
+    single, _ = _single(akm, X, wl, V, ("K", "dell", "dsf"))
+    assert [b for _, b, *_ in res][-1][1] == len(wl.windows)
+    for _, _, Y, dY, dS in res:
+        assert rel(Y, single["K"]) <= 1e-12 and rel(dY, single["dell"]) <= 1e-12 and rel(dS, single["dsf"]) <= 1e-12
