@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "akm_internal.cuh"
 
 namespace akm {
@@ -325,13 +327,14 @@ __global__ void k_point_keys(long long n, const WinTable* __restrict__ tabp, Bin
 
 // sorted index j: window order[j / n] (every window holds n points; windows in group order), position
 // j % n; gathers the scaled coordinates into u_sorted and the point index into perm
+// (fixed_w >= 0: the sorted sequence of that window alone, j = position)
 __global__ void k_point_gather(long long n, int P, const WinTable* __restrict__ tabp, WinGroupMap order,
                                const int* __restrict__ vals, const double* __restrict__ u_tmp,
-                               double* __restrict__ u_sorted, int* __restrict__ perm) {
+                               double* __restrict__ u_sorted, int* __restrict__ perm, int fixed_w) {
   const WinTable& tab = *tabp;
-  const long long total = n * P;
+  const long long total = fixed_w >= 0 ? n : n * P;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < total; j += (long long)gridDim.x * blockDim.x) {
-    const int w = order.group[j / n];
+    const int w = fixed_w >= 0 ? fixed_w : order.group[j / n];
     const long long pos = j % n;
     const WinGeom& g = tab.w[w];
     const int i = vals[j];
@@ -457,8 +460,13 @@ cudaError_t sort_points(long long n, const WinTable& tab, const WinTable* dtab, 
   if (e != cudaSuccess) return e;
   int bits = 1;
   while ((1LL << bits) < nkeys) ++bits;
+  // one sort over every (window, point) while the count fits CUB's int sizes, else one per window
+  // (AKM_SORT_PER_WINDOW=1 forces the per-window path: tests exercise it at small sizes)
+  static const bool per_window_env = getenv("AKM_SORT_PER_WINDOW") && atoi(getenv("AKM_SORT_PER_WINDOW")) == 1;
+  const bool whole = total < (1LL << 31) - 1 && !per_window_env;
+  const long long len = whole ? total : n;
   size_t need = 0;
-  e = cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_alt, vals, vals_alt, (int)total, 0, bits, s);
+  e = cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_alt, vals, vals_alt, (int)len, 0, bits, s);
   if (e != cudaSuccess) return e;
   if (need > *temp_bytes) {
     if (*temp) cudaFree(*temp);
@@ -468,10 +476,22 @@ cudaError_t sort_points(long long n, const WinTable& tab, const WinTable* dtab, 
     if (e != cudaSuccess) return e;
     *temp_bytes = need;
   }
-  e = cub::DeviceRadixSort::SortPairs(*temp, need, keys, keys_alt, vals, vals_alt, (int)total, 0, bits, s);
-  if (e != cudaSuccess) return e;
-  k_point_gather<<<grid_for(total), 256, 0, s>>>(n, tab.P, dtab, order, vals_alt, u_tmp, u_sorted, perm);
-  return cudaGetLastError();
+  if (whole) {
+    e = cub::DeviceRadixSort::SortPairs(*temp, need, keys, keys_alt, vals, vals_alt, (int)total, 0, bits, s);
+    if (e != cudaSuccess) return e;
+    k_point_gather<<<grid_for(total), 256, 0, s>>>(n, tab.P, dtab, order, vals_alt, u_tmp, u_sorted, perm, -1);
+    return cudaGetLastError();
+  }
+  for (int w = 0; w < tab.P; ++w) {
+    const long long o = (long long)w * n;
+    e = cub::DeviceRadixSort::SortPairs(*temp, need, keys + o, keys_alt + o, vals + o, vals_alt + o, (int)n, 0, bits,
+                                        s);
+    if (e != cudaSuccess) return e;
+    k_point_gather<<<grid_for(n), 256, 0, s>>>(n, tab.P, dtab, order, vals_alt + o, u_tmp, u_sorted, perm, w);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace akm

@@ -9,11 +9,14 @@ Gates:
     (eq. A.3) of this build is ~1e-12 / ~1e-14, so any wrong constant, sign or index fails.
 """
 import math
+import os
 
 import numpy as np
 import pytest
 
 import workloads
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 from oracle import dense_apply
 from oracle import fourier as F
 
@@ -485,3 +488,36 @@ def test_run_to_run_agreement(akm):
     b, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B, ("K", "dell"))
     for op in ("K", "dell"):
         assert rel(a[op], b[op]) <= 1e-13
+
+
+def test_per_window_point_sort_path(akm, tmp_path):
+    """The bin sort orders the points with one radix sort over every (window, point) key, or one per
+    window when n * P exceeds CUB's int sizes (binsort.cu sort_points); AKM_SORT_PER_WINDOW=1 forces
+    the second path (read once per process: run in a child).  Same layout, so the products agree to
+    rounding (reading R13: float64 atomics in the spreading)."""
+    import subprocess
+    import sys
+    wl, X, V = _wl_inputs("c4", n=6000, r=3)
+    base, _ = gpu_apply(akm, X, wl.windows, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B,
+                        ("K", "dell"))
+    np.save(tmp_path / "X.npy", X)
+    np.save(tmp_path / "V.npy", V)
+    code = f"""
+import sys, numpy as np, torch
+sys.path.insert(0, {repr(str(ROOT))})
+import paper_2504_00480_b200 as akm, workloads
+wl = workloads.CONFIGS["c4"]
+X = torch.from_numpy(np.load({repr(str(tmp_path / "X.npy"))})).cuda()
+V = torch.from_numpy(np.load({repr(str(tmp_path / "V.npy"))})).cuda()
+p = akm.Plan(0)
+p.set_points(X, wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+p.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+Y, dY = torch.empty_like(V), torch.empty_like(V)
+p.mvm_multi(V, Y=Y, dY_ell=dY)
+np.save({repr(str(tmp_path / "Y.npy"))}, Y.cpu().numpy())
+np.save({repr(str(tmp_path / "dY.npy"))}, dY.cpu().numpy())
+"""
+    env = dict(os.environ, AKM_SORT_PER_WINDOW="1")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+    assert rel(np.load(tmp_path / "Y.npy"), base["K"]) <= 1e-13
+    assert rel(np.load(tmp_path / "dY.npy"), base["dell"]) <= 1e-13
