@@ -514,7 +514,8 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
     }
   }
   gkey[ngroups] = nkeys;
-  if (nkeys >= (1LL << 32)) return plan->fail(AKM_ERR_UNSUPPORTED, "bin layout of %lld slots exceeds 2^32", nkeys);
+  if (nkeys >= (1LL << 31) - 1)  // (CUB scans take int sizes; keys are 32-bit)
+    return plan->fail(AKM_ERR_UNSUPPORTED, "bin layout of %lld slots exceeds 2^31 - 1", nkeys);
   gbin[ngroups] = nbins;
   AKM_CK(cudaMemcpyAsync(plan->dtab.p, &tab, sizeof(WinTable), cudaMemcpyHostToDevice, s));
   // keys: counts, offsets, cursors
