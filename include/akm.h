@@ -259,6 +259,16 @@ akm_status akm_mvm_from_grid(akm_plan* plan, const double* grid, const double* V
  * akm_kernel_cross_mvm and akm_mvm_from_grid return UNSUPPORTED while eps_I > 0. */
 akm_status akm_set_regularization(akm_plan* plan, double eps_I, int32_t p);
 
+/* Deterministic products (SURVEY.md §4 tier 3).  on != 0: every product (and so every Krylov driver
+ * result) is bitwise reproducible from run to run on the same GPU model.  The only order-dependent
+ * sums on the path are the spreading's footprint flushes (float64 atomics, reading R13);
+ * in this mode they add v * 2^S_c as three signed 40-bit integer limbs with 64-bit integer atomics
+ * (exact and associative; S_c = 112 - ceil(log2(rows * max_j |v_jc|)) per RHS column, resolution
+ * ~1e-34 of the column's scale) and one pass converts the limb sums to float64.  The bin sort,
+ * the DFTs, the interpolation, the epilogue and the Krylov reductions are order-fixed already.
+ * Results differ from the default mode by rounding only.  on = 0 (default): float64 atomics. */
+akm_status akm_set_deterministic(akm_plan* plan, int32_t on);
+
 /* Test hook: the window polynomials the kernels evaluate.  For tap o in [0, 2m) of a
  * point with fractional grid position t = u - floor(u), the Kaiser-Bessel weight (App. A,
  * P:1240-1247) phi((t + m - 1 - o) / n_g) is replaced by sum_k coef[o*(degree+1) + k] x^k with

@@ -36,7 +36,7 @@ ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm"
                "akm_get_bounds", "akm_set_bounds", "akm_set_radius", "akm_set_bin_override", "akm_grid_size",
                "akm_spread_grid", "akm_mvm_from_grid", "akm_set_regularization", "akm_set_preconditioner",
                "akm_precond_apply", "akm_precond_landmarks", "akm_objective", "akm_gradient",
-               "akm_gradient_columns")
+               "akm_gradient_columns", "akm_set_deterministic")
 AKM_MAX_PROBES = 31
 
 
@@ -131,6 +131,8 @@ def _load():
     lib.akm_mvm_from_grid.restype = st
     lib.akm_set_regularization.argtypes = [P, d, i32]
     lib.akm_set_regularization.restype = st
+    lib.akm_set_deterministic.argtypes = [P, i32]
+    lib.akm_set_deterministic.restype = st
     lib.akm_set_preconditioner.argtypes = [P, i32]
     lib.akm_set_preconditioner.restype = st
     lib.akm_precond_apply.argtypes = [P, i32, P, i32, P, P, P, P]
@@ -416,6 +418,11 @@ def akm_set_regularization(plan, eps_I=0.0, p=0):
     _check(plan, _lib.akm_set_regularization(plan, float(eps_I), int(p)))
 
 
+def akm_set_deterministic(plan, on: bool):
+    """Bitwise run-to-run reproducible products (integer-limb spreading flushes; include/akm.h)."""
+    _check(plan, _lib.akm_set_deterministic(plan, 1 if on else 0))
+
+
 def akm_set_profiling(plan, enable: bool):
     _check(plan, _lib.akm_set_profiling(plan, 1 if enable else 0))
 
@@ -548,6 +555,10 @@ class Plan:
 
     def set_regularization(self, eps_I=0.0, p=0):
         akm_set_regularization(self.handle, eps_I, p)
+        return self
+
+    def set_deterministic(self, on=True):
+        akm_set_deterministic(self.handle, on)
         return self
 
     def set_scale_override(self, c_w=None):

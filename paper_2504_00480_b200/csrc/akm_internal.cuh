@@ -85,6 +85,33 @@ struct WorkItem {
   int count;        // number of points
 };
 
+// Deterministic spreading (akm_set_deterministic; spread_det.cu): each footprint flush adds v * 2^S_c
+// (S_c per RHS column, from its max |v| and n) as three signed 40-bit integer limbs with 64-bit
+// integer atomics -- exact and order-independent -- and one pass converts the limb sums to float64.
+struct DetAcc {
+  unsigned long long* limbs = nullptr;  // [3][stride]; nullptr = float64 atomics into the grid
+  const int* S = nullptr;               // [window][r_total] scale exponents
+  long long stride = 0;                 // total_taps * r_total
+  int r_total = 0;
+};
+// per-window bounds of the scale exponents (the window product W^d differs by ~1e12 per axis)
+struct DetWin {
+  int wbits[kMaxWin];            // ceil(d_w log2 W) + 1
+  long long tap_off[kMaxWin + 1];  // window w's grid nodes: [tap_off[w], tap_off[w + 1])
+  int P;
+};
+__device__ __forceinline__ void det_add(const DetAcc& da, int win, long long idx, int col, double v) {
+  const double x = ldexp(v, da.S[win * da.r_total + col]);  // exact (power-of-two scaling)
+  const double h2 = trunc(ldexp(x, -80));
+  const double r1 = x - ldexp(h2, 80);        // exact: the bits of x below 2^80
+  const double h1 = trunc(ldexp(r1, -40));
+  const double r0 = r1 - ldexp(h1, 40);       // exact
+  const double h0 = trunc(r0);                // drops the bits below one unit (2^-S)
+  atomicAdd(da.limbs + idx, (unsigned long long)(long long)h0);
+  atomicAdd(da.limbs + da.stride + idx, (unsigned long long)(long long)h1);
+  atomicAdd(da.limbs + 2 * da.stride + idx, (unsigned long long)(long long)h2);
+}
+
 // ------------------------------------------------------------------ device helpers
 // Kaiser-Bessel window (App. A) at a distance delta = n_g * x in grid cells:
 //   phi = (1/pi) sinh(beta sqrt(m^2 - delta^2)) / sqrt(m^2 - delta^2) for |delta| < m,
@@ -314,7 +341,7 @@ cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const W
                               const double* u_sorted,
                               const int* perm, const double* V, long long ldv, long long n, int r0, int rc,
                               int r_total, double* grid, int MB, int NB, int WM, int WN, int PB, size_t smem,
-                              cudaStream_t s);
+                              cudaStream_t s, const DetAcc& da = DetAcc{});
 
 // spread_v5.cu (one warp per SM sub-partition, fragments formed on the fly)
 bool spread_v5_choose(int M, int Nn, int& MB, int& NB, int& WN);
@@ -322,7 +349,7 @@ size_t spread_v5_smem(int Fmax, int rc, int MB, int NB, int WN);
 cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
                              const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
                              int r0, int rc, int r_total, double* grid, int MB, int NB, int WN, size_t smem,
-                             cudaStream_t s);
+                             cudaStream_t s, const DetAcc& da = DetAcc{});
 
 // interp_t.cu (3-D windows, many values per node: GEMM over (o0, o1) with N = (o2, v))
 bool interp_t_supported(int d, int taps, int fp, int ops, int rc);
@@ -337,6 +364,12 @@ cudaError_t launch_fft_multiply_inverse(const WinTable& tab, const WinTable* dta
                                         double2* C, double2* C2, const double2* tw, const double* D, int ops, int dslot0, int r,
                                         double* H, cudaStream_t s);
 cudaError_t launch_zero(double* p, long long count, cudaStream_t s);
+
+cudaError_t launch_det_prepare(const double* V, long long ldv, long long n, int r, const DetWin& dw,
+                               unsigned long long* colmax, int* S, unsigned long long* limbs, long long stride,
+                               cudaStream_t s);
+cudaError_t launch_det_finish(const unsigned long long* limbs, const int* S, long long stride, int r,
+                              const DetWin& dw, double* grid, cudaStream_t s);
 int fft_launch_count(const WinTable& tab, int r);
 
 // krylov.cu (config-5 objective driver)

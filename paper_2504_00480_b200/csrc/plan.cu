@@ -133,6 +133,9 @@ struct akm_plan {
   DevBuf cell_tab, nfV;        // near field: (start, count) per (cell, class) slot; bin-sorted copy of V
   bool cell_tab_ok = false;      // cell_tab matches the last bin sort (built on demand: near field only)
   DevBuf deconv;                 // [3][N + 1] per-axis deconvolution factors (setup_kernels.cu k_deconv_table)
+  bool det = false;              // deterministic spreading (akm_set_deterministic)
+  DevBuf det_limbs, det_colmax, det_S;
+  DetWin det_win{};
   bool deconv_ok = false;
   // S0 on the device (binsort.cu): candidate statistics, key space (bin-major slot order) counts and
   // offsets, per-list item counts / offsets, unsorted items, sort scratch, group bounds
@@ -745,6 +748,11 @@ static akm_status ensure_rhs_workspace(akm_plan* plan, int r) {
   AKM_CK(plan->C2.ensure(sizeof(double2) * std::max<long long>(plan->szC2 * R, 1)));
   AKM_CK(plan->part.ensure(sizeof(double) * std::max<long long>(plan->P * plan->n * 2 * R, 1)));
   if (plan->near_field()) AKM_CK(plan->nfV.ensure(sizeof(double) * std::max<long long>(plan->P * plan->n * R, 1)));
+  if (plan->det) {  // deterministic spreading: integer limbs of the grids, per-column scales (spread_det.cu)
+    AKM_CK(plan->det_limbs.ensure(sizeof(unsigned long long) * 3 * std::max<long long>(plan->total_taps * R, 1)));
+    AKM_CK(plan->det_colmax.ensure(sizeof(unsigned long long) * R));
+    AKM_CK(plan->det_S.ensure(sizeof(int) * plan->P * R));
+  }
   plan->r_cap = r;
   return AKM_OK;
 }
@@ -787,8 +795,32 @@ static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv,
   NvtxRange nvtx("akm S2 spread");
   const long long n = plan->n;
   const WinTable* dtab = plan->dtab.as<WinTable>();
-  AKM_CK(launch_zero(grid, plan->total_taps * r, s));
+  if (n == 0 || !plan->det) AKM_CK(launch_zero(grid, plan->total_taps * r, s));
   if (n == 0) return AKM_OK;
+  DetAcc da{};
+  if (plan->det) {  // integer-limb accumulation, converted into `grid` after the launches
+    const long long rows = (set == 1) ? plan->n_split : n;  // the cross product's V holds the sources only
+    da.limbs = plan->det_limbs.as<unsigned long long>();
+    da.S = plan->det_S.as<int>();
+    da.stride = plan->total_taps * r;
+    // W^d_w bound of a contribution's window product: W = max over taps of sum_k |c_k| >= max |tap|
+    double W = 1.0;
+    for (int q = 0; q < 2 * plan->m; ++q) {
+      double sum = 0.0;
+      for (int k = 0; k < kPolyLen; ++k) sum += std::fabs(plan->poly_param.c[q * kPolyLen + k]);
+      W = std::max(W, sum);
+    }
+    DetWin& dw = plan->det_win;
+    dw.P = plan->P;
+    for (int w = 0; w < plan->P; ++w) {
+      dw.wbits[w] = (int)std::ceil(plan->tab.w[w].d * std::log2(W)) + 1;
+      dw.tap_off[w] = plan->tab.w[w].tap_off;
+    }
+    dw.tap_off[plan->P] = plan->total_taps;
+    da.r_total = r;
+    AKM_CK(launch_det_prepare(V, ldv, rows, r, dw, plan->det_colmax.as<unsigned long long>(),
+                              plan->det_S.as<int>(), da.limbs, da.stride, s));
+  }
   for (const Group& grp : plan->groups) {
     const int F = grp.F, d = grp.d;
     int M = 1;
@@ -806,7 +838,7 @@ static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv,
         return plan->fail(AKM_ERR_UNSUPPORTED, "no spread tile for footprint %d x %d", M, F * rc);
       AKM_CK(launch_spread_v5(dtab, plan->poly_param, plan->items_s[set].as<WorkItem>() + grp.sl[set].spread_begin,
                               grp.sl[set].spread_count, plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc,
-                              r, grid, MB, NB, WN, spread_v5_smem(F, rc, MB, NB, WN), s));
+                              r, grid, MB, NB, WN, spread_v5_smem(F, rc, MB, NB, WN), s, da));
       if (grp.sl[set].spread_count > 0) {
         ++plan->launches;
         ++plan->spread_launches;
@@ -825,7 +857,7 @@ static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv,
       const size_t smem = spread_mma_smem(PB, M, F * rc, F, rc);
       AKM_CK(launch_spread_mma(dtab, plan->poly_param, plan->items_s[set].as<WorkItem>() + grp.sl[set].spread_begin, grp.sl[set].spread_count,
                                plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv, n, r0, rc, r,
-                               grid, MB, NB, WM, WN, PB, smem, s));
+                               grid, MB, NB, WM, WN, PB, smem, s, da));
       if (grp.sl[set].spread_count > 0) {
         ++plan->launches;
         ++plan->spread_launches;
@@ -833,6 +865,7 @@ static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv,
       r0 += rc;
     }
   }
+  if (da.limbs) AKM_CK(launch_det_finish(da.limbs, da.S, da.stride, r, plan->det_win, grid, s));
   return AKM_OK;
 }
 
@@ -2064,6 +2097,15 @@ akm_status akm_set_regularization(akm_plan* plan, double eps_I, int32_t p) {
   plan->reg_eps_I = p > 0 ? eps_I : 0.0;
   plan->have_theta = false;
   plan->r_cap = 0;  // the near-field workspace is sized in ensure_rhs_workspace (never inside a graph capture)
+  return AKM_OK;
+}
+
+akm_status akm_set_deterministic(akm_plan* plan, int32_t on) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  plan->det = on != 0;
+  ++plan->epoch;     // captured launch sequences bake the flush mode in
+  plan->r_cap = 0;   // the limb workspace is sized in ensure_rhs_workspace (never inside a graph capture)
   return AKM_OK;
 }
 

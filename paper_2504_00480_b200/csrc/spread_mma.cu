@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(kSpreadThreads, spread_minb(MB, NB)) k_spread_
                                                                   const double* __restrict__ V, long long ldv,
                                                                   long long n, int r0, int rc, int r_total,
                                                                   double* __restrict__ grid, int WN,
-                                                                  const __grid_constant__ PolyParam pp) {
+                                                                  const __grid_constant__ PolyParam pp,
+                                                                  const DetAcc da) {
   constexpr int PB = spread_pb(MB, NB);
   constexpr int NT = kSpreadThreads;
   const WinTable& tab = *tabp;
@@ -258,7 +259,8 @@ __global__ void __launch_bounds__(kSpreadThreads, spread_minb(MB, NB)) k_spread_
         const double v = acc[i][j][h];
         if (col >= Nn || v == 0.0) continue;
         const int c = fdiv(col, inv_F2), o2 = col - c * F2;  // B columns are ordered (c, o2)
-        atomicAdd(gbase + (toff + line + o2) * r_total + c, v);
+        if (da.limbs) det_add(da, it.win, (toff + line + o2) * r_total + r0 + c, r0 + c, v);
+        else atomicAdd(gbase + (toff + line + o2) * r_total + c, v);
       }
     }
   }
@@ -316,7 +318,7 @@ size_t spread_mma_smem(int /*PB*/, int M, int Nn, int Fmax, int rc) {
 cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
                               const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
                               int r0, int rc, int r_total, double* grid, int MB, int NB, int /*WM*/, int WN,
-                              int /*PB*/, size_t smem, cudaStream_t s) {
+                              int /*PB*/, size_t smem, cudaStream_t s, const DetAcc& da) {
   if (n_items <= 0) return cudaSuccess;
 #define AKM_CASE(a, b)                                                                                         \
   if (MB == a && NB == b) {                                                                                    \
@@ -328,7 +330,7 @@ cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const W
       optin_mark(attr_set);                                                                                         \
     }                                                                                                          \
     k_spread_mma<a, b><<<n_items, kSpreadThreads, smem, s>>>(dtab, items, u_sorted, perm, V, ldv, n, r0, rc,   \
-                                                             r_total, grid, WN, pp);                           \
+                                                             r_total, grid, WN, pp, da);                       \
     return cudaGetLastError();                                                                                 \
   }
   AKM_MMA_TILES(AKM_CASE)

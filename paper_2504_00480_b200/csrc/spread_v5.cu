@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_
                                                              const int* __restrict__ perm, const double* __restrict__ V,
                                                              long long ldv, long long n, int r0, int rc, int r_total,
                                                              double* __restrict__ grid, int WN,
-                                                             const __grid_constant__ PolyParam pp) {
+                                                             const __grid_constant__ PolyParam pp, const DetAcc da) {
   constexpr int PB = kV5PB;
   constexpr int NT = kV5Threads;
   const WinTable& tab = *tabp;
@@ -313,7 +313,8 @@ __global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_
         const double v = acc[i][j][h];
         if (col >= Nn || v == 0.0) continue;
         const int o2 = fdiv(col, inv_rc);
-        atomicAdd(gbase + (toff + line + o2) * r_total + (col - o2 * rc), v);
+        if (da.limbs) det_add(da, it.win, (toff + line + o2) * r_total + r0 + (col - o2 * rc), r0 + (col - o2 * rc), v);
+        else atomicAdd(gbase + (toff + line + o2) * r_total + (col - o2 * rc), v);
       }
     }
   }
@@ -358,7 +359,7 @@ size_t spread_v5_smem(int Fmax, int rc, int MB, int NB, int WN) {
 cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
                              const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
                              int r0, int rc, int r_total, double* grid, int MB, int NB, int WN, size_t smem,
-                             cudaStream_t s) {
+                             cudaStream_t s, const DetAcc& da) {
   if (n_items <= 0) return cudaSuccess;
   // warp-specialised variant for small register tiles (few RHS, e.g. c2: the helpers' latency-bound
   // weight and ring work overlaps the MMAs) and for launches with fewer than 2 x 148 work items
@@ -377,7 +378,7 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
     }                                                                                                           \
     k_spread_v5<a, b, o><<<n_items, o ? 2 * kV5Threads : kV5Threads, smem, s>>>(dtab, items, u_sorted, perm, V, \
                                                                                 ldv, n, r0, rc,                \
-                                                           r_total, grid, WN, pp);                              \
+                                                           r_total, grid, WN, pp, da);                          \
     return cudaGetLastError();                                                                                  \
   }
 #define AKM_CASE(a, b) AKM_CASE1(a, b, true) AKM_CASE1(a, b, false)

@@ -521,3 +521,64 @@ np.save({repr(str(tmp_path / "dY.npy"))}, dY.cpu().numpy())
     subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
     assert rel(np.load(tmp_path / "Y.npy"), base["K"]) <= 1e-13
     assert rel(np.load(tmp_path / "dY.npy"), base["dell"]) <= 1e-13
+
+
+def _det_products(akm, X, windows, family, theta, V, N, sigma, m, eps_B, det, calls=2):
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(np.ascontiguousarray(X)).to(dev), windows, family, N, sigma, m, eps_B)
+    plan.set_deterministic(det)
+    plan.set_theta(*theta)
+    Vd = torch.from_numpy(np.ascontiguousarray(V)).to(dev)
+    res = []
+    for _ in range(calls):  # the second call replays the captured graph
+        Y, dY, dS = torch.empty_like(Vd), torch.empty_like(Vd), torch.empty_like(Vd)
+        plan.mvm_multi(Vd, Y=Y, dY_ell=dY, dY_sf=dS)
+        torch.cuda.synchronize()
+        res.append([t.cpu().numpy() for t in (Y, dY, dS)])
+    n_src = X.shape[0] // 2
+    Yt = torch.empty(X.shape[0] - n_src, Vd.shape[1], dtype=torch.float64, device=dev)
+    plan.cross_mvm(n_src, Vd[:n_src].contiguous(), Yt)
+    torch.cuda.synchronize()
+    res.append([Yt.cpu().numpy()])
+    plan.close()
+    return res
+
+
+@pytest.mark.parametrize("name,n,r,windows", [("c4", 20000, 11, None), ("c3", 12000, 4, None),
+                                               ("c2", 6000, 2, [(0, 1, 2), (3,), (4, 5)])])
+def test_deterministic_mode_is_bitwise_reproducible(akm, name, n, r, windows):
+    """akm_set_deterministic (SURVEY.md §4 tier 3 "determinism"): two plans, two calls each (graph
+    replay) and the cross product give bitwise-equal outputs; they equal the default (float64
+    atomics) mode to rounding.  3-D, 2-D and mixed 1-D/2-D/3-D windows (both spreading kernels)."""
+    wl, X, V = _wl_inputs(name, n=n, r=r)
+    win = wl.windows if windows is None else windows
+    args = (X, win, wl.family, _theta(wl), V, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+    a = _det_products(akm, *args, det=True)
+    b = _det_products(akm, *args, det=True)
+    ref = _det_products(akm, *args, det=False, calls=1)
+    for call in (0, 1, 2):
+        for x, y in zip(a[call], b[call]):
+            assert np.array_equal(x, y)
+    for x, y in zip(a[0], a[1]):
+        assert np.array_equal(x, y)
+    for x, y in zip(a[0], ref[0]):
+        assert rel(x, y) <= 1e-13
+    assert rel(a[2][0], ref[1][0]) <= 1e-13
+
+
+def test_deterministic_objective_is_bitwise_reproducible(akm):
+    """The Krylov drivers' reductions are order-fixed; with deterministic spreading Z~ repeats bit for bit."""
+    wl, X, V = _wl_inputs("c5", n=20000, r=6)
+    dev = torch.device("cuda:0")
+    outs = []
+    for _ in range(2):
+        plan = akm.Plan(0)
+        plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+        plan.set_deterministic(True)
+        plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+        Vd = torch.from_numpy(np.ascontiguousarray(V)).to(dev)
+        o = plan.objective_diag(Vd[:, 0].contiguous(), Vd[:, 1:].contiguous(), 20, 10)
+        outs.append((o["Z"], o["quad"], tuple(o["samples"])))
+        plan.close()
+    assert outs[0] == outs[1]
