@@ -582,3 +582,50 @@ def test_deterministic_objective_is_bitwise_reproducible(akm):
         outs.append((o["Z"], o["quad"], tuple(o["samples"])))
         plan.close()
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("name,n,windows", [("c1", 1500, [(0, 1, 2)]), ("c3", 1500, [(0, 1), (2, 3)])])
+def test_spread_grid_vs_oracle_adjoint_grid(akm, name, n, windows):
+    """S2 alone (SURVEY.md §4 tier 3 "spread-only check"): akm_spread_grid's box-local grids equal the
+    oracle's n_g^d spreading grid g_l = sum_j v_j phi~(x_j - l/n_g) (App. A) node by node.
+    The box origin is recovered from the phase of the unit frequencies (the grids are otherwise
+    compared in full, including every node outside the points' footprints)."""
+    wl, X, V = _wl_inputs(name, n=n, r=2)
+    dev = torch.device("cuda:0")
+    plan = akm.Plan(0)
+    plan.set_points(torch.from_numpy(X).to(dev), windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+    plan.set_theta(*_theta(wl))
+    r = V.shape[1]
+    grid = torch.zeros(plan.grid_size(r), dtype=torch.float64, device=dev)
+    plan.spread_grid(torch.from_numpy(np.ascontiguousarray(V)).to(dev), grid)
+    torch.cuda.synchronize()
+    info = plan.info()
+    plan.close()
+    g_all = grid.cpu().numpy()
+    n_g = int(round(wl.sigma_over * wl.N))
+    off = 0
+    for w, win in enumerate(windows):
+        d = len(win)
+        center, c, xs = F.window_scaling(X[:, list(win)], wl.family, wl.ell, wl.N, wl.eps_B)
+        assert info["c_w"][w] == pytest.approx(c, rel=1e-15)
+        want = F.nfft_adjoint_grid(xs, V, n_g, wl.m, wl.sigma_over)          # (r, n_g, ..., n_g)
+        L = list(info["box"][w])[3 - d:]
+        size = int(np.prod(L))
+        g = g_all[off * r:(off + size) * r].reshape(L + [r])
+        off += size
+        g = np.moveaxis(g, -1, 0)                                            # (r, L...)
+        ghat = np.fft.fftn(want, axes=tuple(range(1, d + 1)))
+        lo = []
+        for t in range(d):  # box origin from the unit frequency e_t: ghat = e^{-2 pi i lo_t/n_g} G
+            ph = np.exp(-2j * np.pi * np.arange(L[t]) / n_g)
+            Gt = np.tensordot(g[0], ph, axes=([t], [0]))
+            Gt = Gt.sum() if np.ndim(Gt) else Gt
+            kk = [0] * d
+            kk[t] = 1
+            ratio = ghat[(0,) + tuple(kk)] / Gt
+            lo.append(int(round(-np.angle(ratio) * n_g / (2 * np.pi))) % n_g)
+        full = np.zeros_like(want)
+        idx = np.ix_(*[np.mod(lo[t] + np.arange(L[t]), n_g) for t in range(d)])
+        for cc in range(r):
+            full[cc][idx] = g[cc]
+        assert rel(full, want) <= 1e-12, (name, w, rel(full, want))
