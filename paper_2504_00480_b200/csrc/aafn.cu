@@ -612,11 +612,23 @@ __global__ void k_uinv_finish(long long n, int R, int ntiles, const int* __restr
 // 4 x 64 contiguous bytes per load; Phi is read exactly once over the grid.
 constexpr int kUtBlocks = 296;
 constexpr int kUtWarps = 4;
+// w2 = g Y on the non-landmark rows (0 on the landmark rows), also written to out (k_w2 below; the
+// landmark tiles of k_uinvT_mma re-read it from L2 instead of re-forming it per tile)
+__global__ void k_w2(long long n, int R, const int* __restrict__ lmpos, const double* __restrict__ g,
+                     const double* __restrict__ Y, double* __restrict__ W2, double* __restrict__ out) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n * R;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long row = idx / R;
+    const bool rest = lmpos[row] < 0;
+    const double w = rest ? g[row] * Y[idx] : 0.0;
+    W2[idx] = w;
+    if (rest) out[idx] = w;
+  }
+}
+
 template <int NT>
-__global__ void __launch_bounds__(128) k_uinvT_mma(long long n, int k, int R, const int* __restrict__ lmpos,
-                                                   const double* __restrict__ Phi, const double* __restrict__ g,
-                                                   const double* __restrict__ Y, double* __restrict__ out,
-                                                   double* __restrict__ part) {
+__global__ void __launch_bounds__(128) k_uinvT_mma(long long n, int k, int R, const double* __restrict__ Phi,
+                                                   const double* __restrict__ W2, double* __restrict__ part) {
   constexpr int LDW = NT * 8 + 4;
   __shared__ double ws[32 * LDW];
   const long long per = (n + gridDim.x - 1) / gridDim.x;
@@ -634,28 +646,22 @@ __global__ void __launch_bounds__(128) k_uinvT_mma(long long n, int k, int R, co
   for (int mt = 0; mt < 4; ++mt) jj[mt] = min(jw + mt * 8 + ar, k - 1);
   for (long long b0 = a0; b0 < a1; b0 += 32) {
     const int cnt = (int)min((long long)32, a1 - b0);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < 32 * NT * 8; idx += blockDim.x) {
-      const int rr = idx / (NT * 8), c = idx % (NT * 8);
-      double w = 0.0;
-      if (rr < cnt && c < R) {
-        const long long row = b0 + rr;
-        const bool rest = lmpos[row] < 0;
-        w = rest ? g[row] * Y[row * R + c] : 0.0;
-        if (blockIdx.y == 0 && rest) out[row * R + c] = w;
-      }
-      ws[rr * LDW + c] = w;
-    }
-    __syncthreads();
-    if (jw >= k) continue;
+    // the chunk's Phi fragments first (independent of w2): their latency overlaps the staging below
     double fa[8][4];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int rr = 4 * u + ac;
       const long long row = b0 + min(rr, cnt - 1);
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) fa[u][mt] = (rr < cnt) ? __ldg(Phi + row * k + jj[mt]) : 0.0;
+      for (int mt = 0; mt < 4; ++mt) fa[u][mt] = (rr < cnt && jw < k) ? __ldg(Phi + row * k + jj[mt]) : 0.0;
     }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 32 * NT * 8; idx += blockDim.x) {
+      const int rr = idx / (NT * 8), c = idx % (NT * 8);
+      ws[rr * LDW + c] = (rr < cnt && c < R) ? W2[(b0 + rr) * R + c] : 0.0;
+    }
+    __syncthreads();
+    if (jw >= k) continue;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const double* wrow = ws + (4 * u + ac) * LDW + ar;
@@ -815,14 +821,16 @@ static cudaError_t launch_tall_mma(long long m, int K, int R, const double* A, c
 
 cudaError_t launch_aafn_uinvT(long long n, int k, int R, const int* lm, const int* lmpos, const double* LinvT,
                               const double* Phi, const double* g, const double* Y, double* part, double* tmp,
-                              double* w1, double* out, cudaStream_t s) {
+                              double* w1, double* w2buf, double* out, cudaStream_t s) {
   const dim3 grid(kUtBlocks, (k + 32 * kUtWarps - 1) / (32 * kUtWarps));
+  double* W2 = w2buf;
+  k_w2<<<(int)std::min<long long>((n * R + 255) / 256, 148 * 8), 256, 0, s>>>(n, R, lmpos, g, Y, W2, out);
   if (R <= 8)
-    k_uinvT_mma<1><<<grid, 32 * kUtWarps, 0, s>>>(n, k, R, lmpos, Phi, g, Y, out, part);
+    k_uinvT_mma<1><<<grid, 32 * kUtWarps, 0, s>>>(n, k, R, Phi, W2, part);
   else if (R <= 16)
-    k_uinvT_mma<2><<<grid, 32 * kUtWarps, 0, s>>>(n, k, R, lmpos, Phi, g, Y, out, part);
+    k_uinvT_mma<2><<<grid, 32 * kUtWarps, 0, s>>>(n, k, R, Phi, W2, part);
   else
-    k_uinvT_mma<4><<<grid, 32 * kUtWarps, 0, s>>>(n, k, R, lmpos, Phi, g, Y, out, part);
+    k_uinvT_mma<4><<<grid, 32 * kUtWarps, 0, s>>>(n, k, R, Phi, W2, part);
   k_ut_reduce<<<(k * R + 127) / 128, 128, 0, s>>>(k, R, kUtBlocks, lm, Y, part, tmp);
   cudaError_t e0 = launch_tall_mma(k, k, R, LinvT, tmp, part, w1, s);  // w1 = L11^{-T} tmp
   if (e0 != cudaSuccess) return e0;

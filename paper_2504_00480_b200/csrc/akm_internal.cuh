@@ -332,7 +332,7 @@ cudaError_t launch_aafn_uinv(long long n, int k, int R, const int* lm, const int
                              double* part, double* out, cudaStream_t s);
 cudaError_t launch_aafn_uinvT(long long n, int k, int R, const int* lm, const int* lmpos, const double* LinvT,
                               const double* Phi, const double* g, const double* Y, double* part, double* tmp,
-                              double* w1, double* out, cudaStream_t s);
+                              double* w1, double* w2buf, double* out, cudaStream_t s);
 
 // spread_mma.cu
 bool spread_mma_choose(int M, int Nn, int Fmax, int rc, int& MB, int& NB, int& WM, int& WN);

@@ -98,7 +98,7 @@ struct akm_plan {
     int k = 0;
     double logdet = 0.0;          // log det M
     DevBuf lm, lmpos, L, Linv, LinvT, Phi, K21, Sdiag, g, y1, part, tmp, scal, flag, fps_scratch, dmin, picks, Bt, KBt,
-        yh, Bh;
+        yh, Bh, w2;
   } aafn;
   long long theta_version = 0;
   struct BkKey {
@@ -1155,6 +1155,7 @@ static akm_status aafn_build(akm_plan* plan, int R, cudaStream_t s) {
   AKM_CK(A.y1.ensure(sizeof(double) * k * std::max(R, 1)));
   AKM_CK(A.tmp.ensure(sizeof(double) * k * std::max(R, 1)));
   AKM_CK(A.part.ensure(sizeof(double) * aafn_part_doubles(n, k, std::max(R, 1))));
+  AKM_CK(A.w2.ensure(sizeof(double) * std::max<long long>(n, 1) * std::max(R, 1)));
   if (A.theta_built == plan->theta_version) return AKM_OK;
   if (k > 4096) return plan->fail(AKM_ERR_UNSUPPORTED, "AAFN with %d landmarks (at most 4096 built)", k);
   AKM_CK(A.L.ensure(sizeof(double) * k * k));
@@ -1203,8 +1204,8 @@ static akm_status aafn_uinvT(akm_plan* plan, int R, const double* T, double* out
   auto& A = plan->aafn;
   AKM_CK(launch_aafn_uinvT(plan->n, A.k, R, A.lm.as<int>(), A.lmpos.as<int>(), A.LinvT.as<double>(),
                            A.Phi.as<double>(), A.g.as<double>(), T, A.part.as<double>(), A.tmp.as<double>(),
-                           A.y1.as<double>(), out, s));
-  plan->launches += 4;
+                           A.y1.as<double>(), A.w2.as<double>(), out, s));
+  plan->launches += 5;
   return AKM_OK;
 }
 

@@ -1,7 +1,8 @@
 """Kernel-time breakdown of one objective evaluation (c5) with the CUDA activity profiler (CUPTI via
 torch.profiler; no nsys on this image).  Not a bench number: profiler overhead is included.
 
-    python tools/prof_objective.py --config c5
+    python tools/prof_objective.py --config c5      (diagonal M)
+    python tools/prof_objective.py --config c5a     (AAFN: set_theta builds the factors, then Z~)
 """
 import argparse
 import collections
@@ -28,12 +29,23 @@ def main():
     yd, Zd = Vd[:, 0].contiguous(), Vd[:, 1:].contiguous()
     plan = akm.Plan(0)
     plan.set_points(Xd, wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+    aafn = "aafn_kpw" in wl.extra
+    if aafn:
+        plan.set_preconditioner(wl.extra["aafn_kpw"])
     plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
     cg, lz = wl.extra["cg_iters"], wl.extra["lanczos_steps"]
-    plan.objective_diag(yd, Zd, cg, lz)
+
+    def step():
+        if aafn:
+            plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
+            plan.objective(yd, Zd, cg, lz)
+        else:
+            plan.objective_diag(yd, Zd, cg, lz)
+
+    step()
     torch.cuda.synchronize()
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
-        plan.objective_diag(yd, Zd, cg, lz)
+        step()
         torch.cuda.synchronize()
     tot = collections.defaultdict(lambda: [0, 0.0])
     for ev in prof.events():
