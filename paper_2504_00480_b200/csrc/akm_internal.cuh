@@ -351,6 +351,12 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
                              int r0, int rc, int r_total, double* grid, int MB, int NB, int WN, size_t smem,
                              cudaStream_t s, const DetAcc& da = DetAcc{});
 
+// interp_strip.cu (2-D windows: per bin, one DMMA GEMM per strip of 1 x B cells, K = axis-2 nodes)
+bool interp_strip_supported(int d, int taps, int F, int ops, int rc);
+cudaError_t launch_interp_strip(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
+                                const double* u_sorted, const int* perm, const double* H, int taps, int F, int ops,
+                                int r, int r0, int rc, double* part, long long n, cudaStream_t s);
+
 // interp_t.cu (3-D windows, many values per node: GEMM over (o0, o1) with N = (o2, v))
 bool interp_t_supported(int d, int taps, int fp, int ops, int rc);
 cudaError_t launch_interp_t(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,

@@ -900,6 +900,19 @@ static akm_status enqueue_finish(akm_plan* plan, const double* grid, const doubl
   while (r0 < r) {
     const int rc = interp_rc_for(r - r0);
     for (const Group& grp : plan->groups) {
+      // 2-D windows: per-bin strips of 1 x B cells as DMMA GEMMs (interp_strip.cu)
+      if (interp_strip_supported(grp.d, 2 * plan->m, grp.F, ops, rc)) {
+        AKM_CK(launch_interp_strip(dtab, plan->poly_param,
+                                   plan->items_ib[set].as<WorkItem>() + grp.sl[set].interp_bin_begin,
+                                   grp.sl[set].interp_bin_count, plan->u_sorted.as<double>(), plan->perm.as<int>(),
+                                   plan->H.as<double>(), 2 * plan->m, grp.F, ops, r, r0, rc, plan->part.as<double>(),
+                                   n, s));
+        if (grp.sl[set].interp_bin_count > 0) {
+          ++plan->launches;
+          ++plan->interp_launches;
+        }
+        continue;
+      }
       // 3-D windows: per-bin GEMM over the footprint rows (o0, o1), N = (o2, v) (interp_t.cu);
       // AKM_INTERP_T=0 selects the per-plane kernel (A/B measurement)
       static const bool it_off = getenv("AKM_INTERP_T") && atoi(getenv("AKM_INTERP_T")) == 0;

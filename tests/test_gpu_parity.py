@@ -629,3 +629,36 @@ def test_spread_grid_vs_oracle_adjoint_grid(akm, name, n, windows):
         for cc in range(r):
             full[cc][idx] = g[cc]
         assert rel(full, want) <= 1e-12, (name, w, rel(full, want))
+
+
+@pytest.mark.parametrize("m,N", [(8, 32), (4, 16)])
+@pytest.mark.parametrize("B", [1, 2, 3, 4, 6, 8])
+def test_2d_strip_interpolation_every_bin_edge(akm, m, N, B):
+    """2-D windows go through the per-strip DMMA interpolation (interp_strip.cu) for >= 4 values per
+    node: every bin edge B (footprint F = B + 2m - 1, so K padding 4 ceil(F / 4) and row offsets
+    s1, s2 in [0, B)), RHS chunks 11 + 2 (ragged tail) and 4, two operators, points concentrated
+    enough that bins split into several 128-point items.  Gate: the exact truncated-Fourier
+    operator (eq. 3.3), block and per row."""
+    rng = np.random.default_rng(700 + 10 * B + m)
+    n = 3000
+    X = np.concatenate([rng.random((n // 2, 4)), 0.5 + 0.05 * rng.standard_normal((n - n // 2, 4))])
+    windows = [(0, 1), (2, 3)]
+    th = (0.9, 0.3, 0.2)
+    tol = {4: 1e-6, 8: 1e-11}[m]
+    for r in (13, 4):
+        V = rng.standard_normal((n, r))
+        dev = torch.device("cuda:0")
+        plan = akm.Plan(0)
+        plan.set_points(torch.from_numpy(X).to(dev), windows, 1, N, 2.0, m, 1.0 / 16)
+        plan.set_bin_override([B, B])
+        plan.set_theta(*th)
+        Va = torch.from_numpy(V).to(dev)
+        Y, dL = torch.empty_like(Va), torch.empty_like(Va)
+        plan.mvm_multi(Va, Y=Y, dY_ell=dL)
+        torch.cuda.synchronize()
+        plan.close()
+        nd = F.additive_fastsum(X, windows, 1, th, V, N, 1.0 / 16, ops=("K", "dell"))
+        for op, out in (("K", Y), ("dell", dL)):
+            o = out.cpu().numpy()
+            assert rel(o, nd[op]) <= tol, (r, op, rel(o, nd[op]))
+            assert row_max(o, nd[op]) <= 10 * tol, (r, op, row_max(o, nd[op]))
