@@ -351,6 +351,13 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
                              int r0, int rc, int r_total, double* grid, int MB, int NB, int WN, size_t smem,
                              cudaStream_t s, const DetAcc& da = DetAcc{});
 
+// spread_strip.cu (2-D windows: per bin, one DMMA GEMM per strip of 1 x B cells, M = the 2m axis-1 taps)
+int spread_strip_nb(int d, int taps, int F, int rc);
+cudaError_t launch_spread_strip(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
+                                const double* u_sorted, const int* perm, const double* V, long long ldv, long long n,
+                                int r0, int rc, int r_total, double* grid, int taps, int F, int nb, cudaStream_t s,
+                                const DetAcc& da);
+
 // interp_strip.cu (2-D windows: per bin, one DMMA GEMM per strip of 1 x B cells, K = axis-2 nodes)
 bool interp_strip_supported(int d, int taps, int F, int ops, int rc);
 cudaError_t launch_interp_strip(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,

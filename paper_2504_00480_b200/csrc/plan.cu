@@ -831,6 +831,23 @@ static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv,
     static const int v5_env = getenv("AKM_SPREAD_V5") ? atoi(getenv("AKM_SPREAD_V5")) : -1;
     const bool v5 = v5_env >= 0 ? v5_env != 0 : d >= 2;
     while (v5 && r0 < r) {
+      // 2-D windows: strips of 1 x B cells as their own GEMMs (spread_strip.cu), when a tile exists
+      if (d == 2 && spread_strip_nb(d, 2 * plan->m, F, 1) > 0) {
+        int rc = std::min(12, r - r0);
+        while (rc > 1 && spread_strip_nb(d, 2 * plan->m, F, rc) == 0) --rc;
+        if (rc < r - r0 && rc > (r - r0 + 1) / 2) rc = (r - r0 + 1) / 2;
+        const int nb = spread_strip_nb(d, 2 * plan->m, F, rc);
+        AKM_CK(launch_spread_strip(dtab, plan->poly_param,
+                                   plan->items_s[set].as<WorkItem>() + grp.sl[set].spread_begin,
+                                   grp.sl[set].spread_count, plan->u_sorted.as<double>(), plan->perm.as<int>(), V, ldv,
+                                   n, r0, rc, r, grid, 2 * plan->m, F, nb, s, da));
+        if (grp.sl[set].spread_count > 0) {
+          ++plan->launches;
+          ++plan->spread_launches;
+        }
+        r0 += rc;
+        continue;
+      }
       int rc = std::min(12, r - r0), MB = 0, NB = 0, WN = 0;
       while (rc > 1 && !(spread_v5_choose(M, F * rc, MB, NB, WN) && spread_v5_smem(F, rc, MB, NB, WN) <= 220 * 1024)) --rc;
       if (rc < r - r0 && rc > (r - r0 + 1) / 2) rc = (r - r0 + 1) / 2;
