@@ -196,11 +196,14 @@ __global__ void __launch_bounds__(kDftThreads) k_dft_axis(const WinTable* __rest
 // Y_o[k][i] = sum_l M[k][l] X_o[l][i] with M = T (kFB) or M[k][l] = conj(T[l][k]) (kFD), computed
 // as the real product C (2K x I) = A (2K x 2L) B (2L x I): A is the 2x2 real block form of M
 // (rows 2k + q: component q of the output; columns 2l + p: component p of the input), B's row
-// 2l + p holds component p of X[l][i].  A CTA owns 16 complex rows x 32 columns (2x2 warps of
-// 2x2 DMMA tiles: many CTAs for latency hiding); the K loop stages 8 complex l per step.
-constexpr int kMmaK = 8;  // complex l per staged step (16 real k)
-constexpr int kMmaT = 2;  // DMMA tiles per warp along each of m and n (2 x 2 warps per CTA)
-constexpr int kMmaRows = 2 * kMmaT * 8, kMmaCols = 2 * kMmaT * 8;  // real rows / columns per CTA
+// 2l + p holds component p of X[l][i].  A CTA owns 16 complex rows x 64 columns (2x2 warps of
+// 2x4 DMMA tiles); the K loop stages 16 complex l per chunk, double-buffered: the global loads of
+// chunk c + 1 are issued into registers before the MMAs of chunk c, so their L2 latency hides
+// under the MMAs (the first version staged 8 l synchronously and stalled on every load).
+constexpr int kMmaK = 16;  // complex l per staged chunk (32 real k)
+constexpr int kMmaTM = 2, kMmaTN = 4;  // DMMA tiles per warp along m and n (2 x 2 warps per CTA)
+constexpr int kMmaRows = 2 * kMmaTM * 8, kMmaCols = 2 * kMmaTN * 8;  // real rows / columns per CTA
+constexpr int kMmaXE = kMmaK * kMmaCols / 128, kMmaME = (kMmaRows / 2) * kMmaK / 128;  // loads per thread
 // FUSED_D (kFD, every window without an axis 0): the input is A2 itself times the multiplier
 // D_op[k0 = 0][k1][k2] (the FC1 copy and the FC2 multiply folded into the load).
 template <int MODE, bool FUSED_D = false>
@@ -220,75 +223,92 @@ __global__ void __launch_bounds__(128) k_dft_mma(const WinTable* __restrict__ ta
   const long long ybase = (MODE == kFB ? g.a2_off : g.c2_off) * r + (long long)o * sh.yo;
   const double2* T = tw + g.tw_off[1];
   const int Lt = g.L[1];
-  __shared__ double2 Xs[kMmaK][kMmaCols];
-  __shared__ double2 Ms[CK][kMmaK + 1];
+  __shared__ double2 Xs[2][kMmaK][kMmaCols];
+  __shared__ double2 Ms[2][CK][kMmaK + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wm = warp >> 1, wn = warp & 1;
-  double acc[kMmaT][kMmaT][2];
+  double acc[kMmaTM][kMmaTN][2];
 #pragma unroll
-  for (int a = 0; a < kMmaT; ++a)
+  for (int a = 0; a < kMmaTM; ++a)
 #pragma unroll
-    for (int b = 0; b < kMmaT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (int l0 = 0; l0 < sh.L; l0 += kMmaK) {
-    for (int idx = tid; idx < kMmaK * kMmaCols; idx += 128) {
-      const int l = idx / kMmaCols, j = idx - l * kMmaCols;
+    for (int b = 0; b < kMmaTN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // raw values only (no arithmetic on them here: the loads stay in flight under the MMAs of the
+  // current chunk; the multiplier and the conjugation are applied when they are stored)
+  double2 xr[kMmaXE], mr[kMmaME];
+  double dr[FUSED_D ? kMmaXE : 1];
+  auto gload = [&](int l0) {
+#pragma unroll
+    for (int e = 0; e < kMmaXE; ++e) {
+      const int idx = tid + 128 * e, l = idx / kMmaCols, j = idx - l * kMmaCols;
       const long long i = i0 + j;
       double2 v = make_double2(0.0, 0.0);
+      double dd = 0.0;
       if (l0 + l < sh.L && i < sh.I) {
         v = X[xbase + (long long)(l0 + l) * sh.xl + i];
-        if (FUSED_D) {  // D_op[k1 = l][k2 = i / r]
-          const double dd = D[dbase + (long long)(l0 + l) * g.K[2] + i / r];
-          v.x *= dd;
-          v.y *= dd;
-        }
+        if (FUSED_D) dd = D[dbase + (long long)(l0 + l) * g.K[2] + (int)i / r];  // D_op[k1 = l][k2 = i / r]
       }
-      Xs[l][j] = v;
+      xr[e] = v;
+      if constexpr (FUSED_D) dr[e] = dd;
     }
-    for (int idx = tid; idx < CK * kMmaK; idx += 128) {
-      const int k = idx / kMmaK, l = idx - k * kMmaK;
+#pragma unroll
+    for (int e = 0; e < kMmaME; ++e) {
+      const int idx = tid + 128 * e, k = idx / kMmaK, l = idx - k * kMmaK;
       double2 m = make_double2(0.0, 0.0);
-      if (k0 + k < sh.K && l0 + l < sh.L) {
-        if (MODE == kFB) {
-          m = T[(long long)(k0 + k) * Lt + l0 + l];
-        } else {
-          const double2 t = T[(long long)(l0 + l) * Lt + k0 + k];
-          m = make_double2(t.x, -t.y);
-        }
-      }
-      Ms[k][l] = m;
+      if (k0 + k < sh.K && l0 + l < sh.L)
+        m = (MODE == kFB) ? T[(long long)(k0 + k) * Lt + l0 + l] : T[(long long)(l0 + l) * Lt + k0 + k];
+      mr[e] = m;
     }
-    __syncthreads();
+  };
+  gload(0);
+  for (int l0 = 0, c = 0; l0 < sh.L; l0 += kMmaK, ++c) {
+    const int buf = c & 1;
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
+    for (int e = 0; e < kMmaXE; ++e) {
+      const int idx = tid + 128 * e, l = idx / kMmaCols, j = idx - l * kMmaCols;
+      double2 v = xr[e];
+      if constexpr (FUSED_D) {
+        v.x *= dr[e];
+        v.y *= dr[e];
+      }
+      Xs[buf][l][j] = v;
+    }
+#pragma unroll
+    for (int e = 0; e < kMmaME; ++e) {
+      const int idx = tid + 128 * e, k = idx / kMmaK, l = idx - k * kMmaK;
+      Ms[buf][k][l] = (MODE == kFB) ? mr[e] : make_double2(mr[e].x, -mr[e].y);  // kFD: conj(T[l][k])
+    }
+    __syncthreads();  // chunk c visible; buffer buf ^ 1 (chunk c - 1) free for the next store
+    if (l0 + kMmaK < sh.L) gload(l0 + kMmaK);
+#pragma unroll
+    for (int ks = 0; ks < 2 * kMmaK / 4; ++ks) {
       const int kr = ks * 4 + (lane & 3), ll = kr >> 1, p = kr & 1;
-      double af[kMmaT], bf[kMmaT];
+      double af[kMmaTM], bf[kMmaTN];
 #pragma unroll
-      for (int mt = 0; mt < kMmaT; ++mt) {
-        const int row = (wm * kMmaT + mt) * 8 + (lane >> 2), q = row & 1;
-        const double2 m = Ms[row >> 1][ll];
+      for (int mt = 0; mt < kMmaTM; ++mt) {
+        const int row = (wm * kMmaTM + mt) * 8 + (lane >> 2), q = row & 1;
+        const double2 m = Ms[buf][row >> 1][ll];
         af[mt] = (q == 0) ? (p == 0 ? m.x : -m.y) : (p == 0 ? m.y : m.x);
       }
 #pragma unroll
-      for (int nt = 0; nt < kMmaT; ++nt) {
-        const double2 x = Xs[ll][(wn * kMmaT + nt) * 8 + (lane >> 2)];
+      for (int nt = 0; nt < kMmaTN; ++nt) {
+        const double2 x = Xs[buf][ll][(wn * kMmaTN + nt) * 8 + (lane >> 2)];
         bf[nt] = p == 0 ? x.x : x.y;
       }
 #pragma unroll
-      for (int mt = 0; mt < kMmaT; ++mt)
+      for (int mt = 0; mt < kMmaTM; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < kMmaT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        for (int nt = 0; nt < kMmaTN; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
     }
-    __syncthreads();
   }
   // rows 2k (real) and 2k + 1 (imaginary) sit in lanes l and l ^ 4
 #pragma unroll
-  for (int mt = 0; mt < kMmaT; ++mt) {
-    const int row = (wm * kMmaT + mt) * 8 + (lane >> 2), k = k0 + (row >> 1);
+  for (int mt = 0; mt < kMmaTM; ++mt) {
+    const int row = (wm * kMmaTM + mt) * 8 + (lane >> 2), k = k0 + (row >> 1);
 #pragma unroll
-    for (int nt = 0; nt < kMmaT; ++nt) {
+    for (int nt = 0; nt < kMmaTN; ++nt) {
       const double im0 = __shfl_xor_sync(0xffffffffu, acc[mt][nt][0], 4);
       const double im1 = __shfl_xor_sync(0xffffffffu, acc[mt][nt][1], 4);
       if ((row & 1) || k >= sh.K) continue;
-      const long long i = i0 + (wn * kMmaT + nt) * 8 + 2 * (lane & 3);
+      const long long i = i0 + (wn * kMmaTN + nt) * 8 + 2 * (lane & 3);
       if (i < sh.I) Y[ybase + (long long)k * sh.yk + i] = make_double2(acc[mt][nt][0], im0);
       if (i + 1 < sh.I) Y[ybase + (long long)k * sh.yk + i + 1] = make_double2(acc[mt][nt][1], im1);
     }
@@ -316,97 +336,118 @@ static cudaError_t launch_dft_mma(const WinTable& tab, const WinTable* dtab, con
 // the Hermitian weights) as FP64 tensor-core GEMMs over the columns (o, c):
 //   kFA:  C[2k + q][(o, c)] = sum_l  {Re, Im} T[k][l] * x[o][l][c]
 //   kFE:  C[l][(o, c)]      = sum_{k, p} w_k {Re, Im} T[k][l] * {Re, Im} X[o][k][c]   (w_0 = 1, else 2)
-// A CTA owns 32 real rows x 32 columns (2x2 warps of 2x2 DMMA tiles); K is staged 8 (complex for kFE) at a time.
+// A CTA owns 32 real rows x 64 columns (2x2 warps of 2x4 DMMA tiles); K is staged 16 (complex for
+// kFE) at a time, double-buffered through registers like k_dft_mma.
+constexpr int kMrK = 16, kMrCols = 64;
 template <int MODE>
 __global__ void __launch_bounds__(128) k_dft_mma_r(const WinTable* __restrict__ tabp, const void* __restrict__ Xv,
                                                    void* __restrict__ Yv, const double2* __restrict__ tw, int r,
                                                    int ops) {
+  constexpr int XE = kMrK * kMrCols / 128, ME = 32 * kMrK / 128;
   const WinGeom& g = tabp->w[blockIdx.z];
   const DftShape sh = dft_shape(g, MODE, r, ops);
-  const long long ncol = sh.O * sh.I, c0 = (long long)blockIdx.x * 32;
+  const long long ncol = sh.O * sh.I, c0 = (long long)blockIdx.x * kMrCols;
   const int rows = (MODE == kFA) ? 2 * sh.K : sh.K;  // real output rows
   const int row0 = blockIdx.y * 32;
   if (c0 >= ncol || row0 >= rows) return;
   const double2* T = tw + g.tw_off[2];
   const int Lt = g.L[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wm = warp >> 1, wn = warp & 1;
-  __shared__ double2 Xs[8][33];  // kFA: .x only (real input), [l][col]; kFE: [k][col]
-  __shared__ double2 Ms[32][9];  // kFA: [k (16 used)][l]; kFE: [l][k]
-  double acc[2][2][2];
+  __shared__ double2 Xs[2][kMrK][kMrCols];  // kFA: .x only (real input), [l][col]; kFE: [k][col]
+  __shared__ double2 Ms[2][32][kMrK];  // kFA: [k (16 used)][l]; kFE: [l][k]; column swizzled by row & 7
+  double acc[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const long long xbase = (MODE == kFA) ? g.tap_off * r : g.c2_off * r;
-  for (int l0 = 0; l0 < sh.L; l0 += 8) {  // sh.L: kFA nodes l2, kFE frequencies k2
-    for (int idx = tid; idx < 8 * 32; idx += 128) {
-      const int l = idx >> 5, j = idx & 31;
+  double2 xr[XE], mr[ME];
+  auto gload = [&](int l0) {  // l0: kFA nodes l2, kFE frequencies k2
+#pragma unroll
+    for (int e = 0; e < XE; ++e) {
+      const int idx = tid + 128 * e, l = idx / kMrCols, j = idx - l * kMrCols;
       const long long col = c0 + j;
       double2 v = make_double2(0.0, 0.0);
       if (l0 + l < sh.L && col < ncol) {
-        const long long o = col / sh.I, c = col - o * sh.I;
+        const int o = (int)col / (int)sh.I, c = (int)col - o * (int)sh.I;  // 32-bit: ncol < 2^31
         const long long off = xbase + o * sh.xo + (long long)(l0 + l) * sh.xl + c;
         if (MODE == kFA) v.x = static_cast<const double*>(Xv)[off];
         else v = static_cast<const double2*>(Xv)[off];
       }
-      Xs[l][j] = v;
+      xr[e] = v;
     }
-    for (int idx = tid; idx < 32 * 8; idx += 128) {
-      const int a = idx >> 3, b = idx & 7;  // kFA: a = k (row/2), b = l; kFE: a = l (row), b = k
+#pragma unroll
+    for (int e = 0; e < ME; ++e) {
+      const int idx = tid + 128 * e, a = idx / kMrK, b = idx - a * kMrK;  // kFA: a = k, b = l; kFE: a = l, b = k
       double2 m = make_double2(0.0, 0.0);
       if (MODE == kFA) {
         const int k = row0 / 2 + a;
         if (a < 16 && k < sh.K && l0 + b < sh.L) m = T[(long long)k * Lt + l0 + b];
       } else {
         const int l = row0 + a, k = l0 + b;
-        if (l < sh.K && k < sh.L) {
-          const double2 t = T[(long long)k * Lt + l];
-          const double w = (k == 0) ? 1.0 : 2.0;
-          m = make_double2(w * t.x, w * t.y);
-        }
+        if (l < sh.K && k < sh.L) m = T[(long long)k * Lt + l];  // Hermitian weight applied at the store
       }
-      Ms[a][b] = m;
+      mr[e] = m;
+    }
+  };
+  gload(0);
+  for (int l0 = 0, c = 0; l0 < sh.L; l0 += kMrK, ++c) {
+    const int buf = c & 1;
+#pragma unroll
+    for (int e = 0; e < XE; ++e) {
+      const int idx = tid + 128 * e, l = idx / kMrCols, j = idx - l * kMrCols;
+      Xs[buf][l][j] = xr[e];
+    }
+#pragma unroll
+    for (int e = 0; e < ME; ++e) {
+      const int idx = tid + 128 * e, a = idx / kMrK, b = idx - a * kMrK;
+      double2 m = mr[e];
+      if (MODE != kFA && l0 + b > 0) {  // kFE: w_k = 2 for k2 > 0 (both halves of the spectrum)
+        m.x *= 2.0;
+        m.y *= 2.0;
+      }
+      Ms[buf][a][b ^ (a & 7)] = m;
     }
     __syncthreads();
-    constexpr int KS = (MODE == kFA) ? 2 : 4;  // k-steps of 4 real k per staged chunk
+    if (l0 + kMrK < sh.L) gload(l0 + kMrK);
+    constexpr int KS = (MODE == kFA) ? kMrK / 4 : 2 * kMrK / 4;  // k-steps of 4 real k per chunk
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int kr = ks * 4 + (lane & 3);
-      double af[2], bf[2];
+      double af[2], bf[4];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const int row = (wm * 2 + mt) * 8 + (lane >> 2);
         if (MODE == kFA) {
-          const double2 m = Ms[row >> 1][kr];
+          const double2 m = Ms[buf][row >> 1][kr ^ ((row >> 1) & 7)];
           af[mt] = (row & 1) ? m.y : m.x;
         } else {
-          const double2 m = Ms[row][kr >> 1];
+          const double2 m = Ms[buf][row][(kr >> 1) ^ (row & 7)];
           af[mt] = (kr & 1) ? m.y : m.x;
         }
       }
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int col = (wn * 2 + nt) * 8 + (lane >> 2);
+      for (int nt = 0; nt < 4; ++nt) {
+        const int col = (wn * 4 + nt) * 8 + (lane >> 2);
         if (MODE == kFA) {
-          bf[nt] = Xs[kr][col].x;
+          bf[nt] = Xs[buf][kr][col].x;
         } else {
-          const double2 x = Xs[kr >> 1][col];
+          const double2 x = Xs[buf][kr >> 1][col];
           bf[nt] = (kr & 1) ? x.y : x.x;
         }
       }
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
     const int row = row0 + (wm * 2 + mt) * 8 + (lane >> 2);
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      const long long colb = c0 + (wn * 2 + nt) * 8 + 2 * (lane & 3);
+    for (int nt = 0; nt < 4; ++nt) {
+      const long long colb = c0 + (wn * 4 + nt) * 8 + 2 * (lane & 3);
       if (MODE == kFA) {
         const double im0 = __shfl_xor_sync(0xffffffffu, acc[mt][nt][0], 4);
         const double im1 = __shfl_xor_sync(0xffffffffu, acc[mt][nt][1], 4);
@@ -417,7 +458,7 @@ __global__ void __launch_bounds__(128) k_dft_mma_r(const WinTable* __restrict__ 
         for (int h = 0; h < 2; ++h) {
           const long long col = colb + h;
           if (col >= ncol) continue;
-          const long long o = col / sh.I, c = col - o * sh.I;
+          const int o = (int)col / (int)sh.I, c = (int)col - o * (int)sh.I;
           Y[o * sh.yo + (long long)k * sh.yk + c] = make_double2(h ? acc[mt][nt][1] : acc[mt][nt][0], h ? im1 : im0);
         }
       } else {
@@ -428,7 +469,7 @@ __global__ void __launch_bounds__(128) k_dft_mma_r(const WinTable* __restrict__ 
         for (int h = 0; h < 2; ++h) {
           const long long col = colb + h;
           if (col >= ncol) continue;
-          const long long o = col / sh.I, c = col - o * sh.I, op = o / lines, line = o - op * lines;
+          const int o = (int)col / (int)sh.I, c = (int)col - o * (int)sh.I, op = o / (int)lines, line = o - op * (int)lines;
           H[((line * g.L[2] + row) * ops + op) * r + c] = acc[mt][nt][h];
         }
       }
@@ -443,7 +484,7 @@ static cudaError_t launch_dft_mma_r(const WinTable& tab, const WinTable* dtab, c
   int rtiles = 1;
   for (int w = 0; w < tab.P; ++w) {
     const DftShape sh = dft_shape(tab.w[w], MODE, r, ops);
-    ctiles = std::max(ctiles, (sh.O * sh.I + 31) / 32);
+    ctiles = std::max(ctiles, (sh.O * sh.I + kMrCols - 1) / kMrCols);
     rtiles = std::max(rtiles, ((MODE == kFA ? 2 * sh.K : sh.K) + 31) / 32);
   }
   k_dft_mma_r<MODE><<<dim3((unsigned)ctiles, (unsigned)rtiles, tab.P), 128, 0, s>>>(dtab, X, Y, tw, r, ops);
