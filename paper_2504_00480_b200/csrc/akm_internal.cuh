@@ -368,7 +368,7 @@ cudaError_t launch_interp_strip(const WinTable* dtab, const PolyParam& pp, const
 bool interp_t_supported(int d, int taps, int fp, int ops, int rc);
 cudaError_t launch_interp_t(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
                             const double* u_sorted, const int* perm, const double* H, int taps, int fp, int ops, int r,
-                            int r0, int rc, double* part, long long n, cudaStream_t s);
+                            int r0, int rc, double* part, long long n, cudaStream_t s, int bscale);
 
 // fft.cu
 cudaError_t launch_fft_forward(const WinTable& tab, const WinTable* dtab, const double* grid, double2* A1,

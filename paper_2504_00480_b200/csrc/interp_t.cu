@@ -49,13 +49,13 @@ struct ItShape {
 // share the staged footprint planes and the GEMM shape; for B = 1 (c4, c5: a bin is a cell) no
 // work is padded.
 template <int TAPS, int FP, int OPS, int RC, int MT, int WN>
-__global__ void __launch_bounds__(32 * kItWarps, 2) k_interp_t(const WinTable* __restrict__ tabp,
+__global__ void __launch_bounds__(32 * kItWarps, (OPS * RC <= 2) ? 4 : 2) k_interp_t(const WinTable* __restrict__ tabp,
                                                                const WorkItem* __restrict__ items,
                                                                const double* __restrict__ u_sorted,
                                                                const int* __restrict__ perm,
                                                                const double* __restrict__ H, int r, int r0,
                                                                double* __restrict__ part, long long n,
-                                                               const __grid_constant__ PolyParam pp) {
+                                                               const __grid_constant__ PolyParam pp, int bscale) {
   constexpr int V = OPS * RC;
   using S = ItShape<FP, V, MT, WN>;
   constexpr int N = S::N, NTW = S::NTW, LDB = S::LDB, PPC = S::PPC, LDT = S::LDT, KQF = S::KQF, KR = S::KR;
@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(32 * kItWarps, 2) k_interp_t(const WinTable* _
   const long long row_vals = (long long)OPS * r;
   const bool contiguous = (RC == r && r0 == 0);
   const long long L1g = g.L[1], L2g = g.L[2], toff = g.tap_off;
-  const int ob0 = it.bin[0] * g.B, ob1 = it.bin[1] * g.B, ob2 = it.bin[2] * g.B;  // box-local footprint origin
+  // box-local footprint origin: bin items (bscale = B) or per-cell items (bscale = 1, FP = TAPS)
+  const int ob0 = it.bin[0] * bscale, ob1 = it.bin[1] * bscale, ob2 = it.bin[2] * bscale;
   // staging of footprint plane o0 into ring slot slot_of(o0): footprint row o1 by warp
   // o1 % kItWarps, consecutive lanes on consecutive columns (contiguous H: a row (o0, o1) is one
   // run of N doubles of H; otherwise a gather per element)
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(32 * kItWarps, 2) k_interp_t(const WinTable* _
 }
 
 // instances: (TAPS, FP, OPS, RC) -> (MT, WN)
-#define AKM_IT_INSTANCES(X) X(12, 12, 1, 11, 2, 1) X(12, 13, 2, 1, 2, 1) X(12, 12, 2, 1, 2, 1)
+#define AKM_IT_INSTANCES(X) X(12, 12, 1, 11, 2, 1) X(12, 12, 2, 1, 2, 1) X(12, 12, 1, 2, 2, 1)
 
 bool interp_t_supported(int d, int taps, int fp, int ops, int rc) {
 #define AKM_IT_SUP(T, F, O, R, M, W) \
@@ -283,7 +284,7 @@ bool interp_t_supported(int d, int taps, int fp, int ops, int rc) {
 
 cudaError_t launch_interp_t(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
                             const double* u_sorted, const int* perm, const double* H, int taps, int fp, int ops, int r,
-                            int r0, int rc, double* part, long long n, cudaStream_t s) {
+                            int r0, int rc, double* part, long long n, cudaStream_t s, int bscale) {
   if (n_items <= 0) return cudaSuccess;
 #define AKM_IT_CASE(T, F, O, R, M, W)                                                                          \
   if (taps == T && fp == F && ops == O && rc == R) {                                                           \
@@ -296,7 +297,7 @@ cudaError_t launch_interp_t(const WinTable* dtab, const PolyParam& pp, const Wor
       optin_mark(attr_set);                                                                                         \
     }                                                                                                          \
     k_interp_t<T, F, O, R, M, W><<<n_items, 32 * kItWarps, smem, s>>>(dtab, items, u_sorted, perm, H, r, r0,   \
-                                                                      part, n, pp);                            \
+                                                                      part, n, pp, bscale);                    \
     return cudaGetLastError();                                                                                 \
   }
   AKM_IT_INSTANCES(AKM_IT_CASE)
