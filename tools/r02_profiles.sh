@@ -1,6 +1,7 @@
 #!/bin/bash
 # Round-2 evidence on the GPU box: bench lines for every workload, the launch list of the default
-# bench command (c4), ncu --set full captures of the c4 spreading / interpolation kernels.
+# bench command (c4), ncu --set full captures of the c4 spreading / interpolation kernels, of the c3
+# 2-D strip kernels and DFT passes, and of the c2 kernels.
 set -u
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
@@ -17,4 +18,8 @@ if [ "${NCU:-1}" = 1 ]; then
       python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches exit $?"
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_spread_v5|k_interp_mma" -s 2 -c 3 \
       -o gpurun_out/prof_c4 -f python tools/prof_run.py --config c4 --calls 2 > gpurun_out/ncu_c4.log 2>&1; echo "ncu full exit $?"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_spread|k_interp|k_dft" -s 6 -c 6 \
+      -o gpurun_out/prof_c3 -f python tools/prof_run.py --config c3 --calls 2 > gpurun_out/ncu_c3.log 2>&1; echo "ncu c3 exit $?"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_spread|k_plane|k_pencil|k_interp|k_epilogue" -s 6 -c 6 \
+      -o gpurun_out/prof_c2 -f python tools/prof_run.py --config c2 --calls 3 > gpurun_out/ncu_c2.log 2>&1; echo "ncu c2 exit $?"
 fi
