@@ -51,7 +51,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 __host__ __device__ constexpr int spread_ldf(int f) { return (f + 2) & ~1; }  // weight row: even, > f
 
-template <int MB, int NB>
+template <int MB, int NB, bool DET>
 __global__ void __launch_bounds__(kSpreadThreads, spread_minb(MB, NB)) k_spread_mma(const WinTable* __restrict__ tabp,
                                                                   const WorkItem* __restrict__ items,
                                                                   const double* __restrict__ u_sorted,
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kSpreadThreads, spread_minb(MB, NB)) k_spread_
         const double v = acc[i][j][h];
         if (col >= Nn || v == 0.0) continue;
         const int c = fdiv(col, inv_F2), o2 = col - c * F2;  // B columns are ordered (c, o2)
-        if (da.limbs) det_add(da, it.win, (toff + line + o2) * r_total + r0 + c, r0 + c, v);
+        if constexpr (DET) det_add(da, it.win, (toff + line + o2) * r_total + r0 + c, r0 + c, v);
         else atomicAdd(gbase + (toff + line + o2) * r_total + c, v);
       }
     }
@@ -320,21 +320,23 @@ cudaError_t launch_spread_mma(const WinTable* dtab, const PolyParam& pp, const W
                               int r0, int rc, int r_total, double* grid, int MB, int NB, int /*WM*/, int WN,
                               int /*PB*/, size_t smem, cudaStream_t s, const DetAcc& da) {
   if (n_items <= 0) return cudaSuccess;
-#define AKM_CASE(a, b)                                                                                         \
-  if (MB == a && NB == b) {                                                                                    \
-    static std::atomic<unsigned long long> attr_set{0};                                                                              \
-    if (!optin_done(attr_set)) {                                                                                           \
-      cudaError_t e = cudaFuncSetAttribute(k_spread_mma<a, b>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                           227 * 1024);                                                        \
-      if (e != cudaSuccess) return e;                                                                          \
-      optin_mark(attr_set);                                                                                         \
-    }                                                                                                          \
-    k_spread_mma<a, b><<<n_items, kSpreadThreads, smem, s>>>(dtab, items, u_sorted, perm, V, ldv, n, r0, rc,   \
-                                                             r_total, grid, WN, pp, da);                       \
-    return cudaGetLastError();                                                                                 \
+#define AKM_CASE1(a, b, det)                                                                                   \
+  if (MB == a && NB == b && (da.limbs != nullptr) == det) {                                                    \
+    static std::atomic<unsigned long long> attr_set{0};                                                         \
+    if (!optin_done(attr_set)) {                                                                                \
+      cudaError_t e = cudaFuncSetAttribute(k_spread_mma<a, b, det>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           227 * 1024);                                                         \
+      if (e != cudaSuccess) return e;                                                                           \
+      optin_mark(attr_set);                                                                                     \
+    }                                                                                                           \
+    k_spread_mma<a, b, det><<<n_items, kSpreadThreads, smem, s>>>(dtab, items, u_sorted, perm, V, ldv, n, r0, rc, \
+                                                                  r_total, grid, WN, pp, da);                   \
+    return cudaGetLastError();                                                                                  \
   }
+#define AKM_CASE(a, b) AKM_CASE1(a, b, false) AKM_CASE1(a, b, true)
   AKM_MMA_TILES(AKM_CASE)
 #undef AKM_CASE
+#undef AKM_CASE1
   return cudaErrorInvalidValue;
 }
 

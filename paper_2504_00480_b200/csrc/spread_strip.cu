@@ -64,7 +64,7 @@ __host__ __device__ inline SsLayout ss_layout(int F, int rc, int NB) {
 }
 }  // namespace
 
-template <int TAPS, int NB>
+template <int TAPS, int NB, bool DET>
 __global__ void __launch_bounds__(kSsThreads, 2) k_spread_strip(const WinTable* __restrict__ tabp,
                                                                const WorkItem* __restrict__ items,
                                                                const double* __restrict__ u_sorted,
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kSsThreads, 2) k_spread_strip(const WinTable* 
     if (v == 0.0) continue;
     const int o2 = fdiv(col, inv_rc), c = col - o2 * rc;
     const long long node = toff + (long long)(c1 + row) * L2 + c2 + o2;
-    if (da.limbs) det_add(da, it.win, node * r_total + r0 + c, r0 + c, v);
+    if constexpr (DET) det_add(da, it.win, node * r_total + r0 + c, r0 + c, v);
     else atomicAdd(gbase + node * r_total + c, v);
   }
 }
@@ -373,21 +373,23 @@ cudaError_t launch_spread_strip(const WinTable* dtab, const PolyParam& pp, const
                                 const DetAcc& da) {
   if (n_items <= 0) return cudaSuccess;
   const size_t smem = spread_strip_smem(F, rc, nb);
-#define AKM_SS_CASE(T, N)                                                                                       \
-  if (taps == T && nb == N) {                                                                                   \
+#define AKM_SS_CASE1(T, N, det)                                                                                 \
+  if (taps == T && nb == N && (da.limbs != nullptr) == det) {                                                    \
     static std::atomic<unsigned long long> attr_set{0};                                                         \
     if (!optin_done(attr_set)) {                                                                                \
-      cudaError_t e = cudaFuncSetAttribute(k_spread_strip<T, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                           (int)kSsSmemMax);                                                    \
+      cudaError_t e = cudaFuncSetAttribute(k_spread_strip<T, N, det>,                                          \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsSmemMax);       \
       if (e != cudaSuccess) return e;                                                                           \
       optin_mark(attr_set);                                                                                     \
     }                                                                                                           \
-    k_spread_strip<T, N><<<n_items, kSsThreads, smem, s>>>(dtab, items, u_sorted, perm, V, ldv, n, r0, rc,      \
-                                                           r_total, grid, pp, da);                              \
+    k_spread_strip<T, N, det><<<n_items, kSsThreads, smem, s>>>(dtab, items, u_sorted, perm, V, ldv, n, r0, rc, \
+                                                                r_total, grid, pp, da);                         \
     return cudaGetLastError();                                                                                  \
   }
+#define AKM_SS_CASE(T, N) AKM_SS_CASE1(T, N, false) AKM_SS_CASE1(T, N, true)
   AKM_SS_INSTANCES(AKM_SS_CASE)
 #undef AKM_SS_CASE
+#undef AKM_SS_CASE1
   return cudaErrorInvalidValue;
 }
 

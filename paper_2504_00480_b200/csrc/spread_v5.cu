@@ -49,7 +49,7 @@ __device__ __forceinline__ void v5_wait_all() { asm volatile("cp.async.wait_grou
 __host__ __device__ constexpr int v5_ldw(int fmax) { return ((fmax + 1 + 7) / 16) * 16 + 8; }  // 8 mod 16, > fmax
 }  // namespace
 
-template <int MB, int NB, bool WS>
+template <int MB, int NB, bool WS, bool DET>
 __global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_v5(const WinTable* __restrict__ tabp,
                                                              const WorkItem* __restrict__ items,
                                                              const double* __restrict__ u_sorted,
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_
         const double v = acc[i][j][h];
         if (col >= Nn || v == 0.0) continue;
         const int o2 = fdiv(col, inv_rc);
-        if (da.limbs) det_add(da, it.win, (toff + line + o2) * r_total + r0 + (col - o2 * rc), r0 + (col - o2 * rc), v);
+        if constexpr (DET) det_add(da, it.win, (toff + line + o2) * r_total + r0 + (col - o2 * rc), r0 + (col - o2 * rc), v);
         else atomicAdd(gbase + (toff + line + o2) * r_total + (col - o2 * rc), v);
       }
     }
@@ -367,24 +367,27 @@ cudaError_t launch_spread_v5(const WinTable* dtab, const PolyParam& pp, const Wo
   // SM sub-partitions slows the DMMA stream more than it hides
   static const int ws_env = getenv("AKM_V5_WS") ? atoi(getenv("AKM_V5_WS")) : -1;
   const bool ws = ws_env >= 0 ? ws_env != 0 : (MB * NB <= 12 || n_items < 2 * 148);
-#define AKM_CASE1(a, b, o)                                                                                     \
-  if (MB == a && NB == b && ws == o) {                                                                          \
-    static std::atomic<unsigned long long> attr_set{0};                                                                               \
-    if (!optin_done(attr_set)) {                                                                                            \
-      cudaError_t e = cudaFuncSetAttribute(k_spread_v5<a, b, o>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+// DET (deterministic integer-limb flush) is a template parameter: a runtime branch in the flush
+// changed the register allocation of the MMA loop (c4 spreading 6.97 -> 7.27 ms)
+#define AKM_CASE2(a, b, o, det)                                                                                \
+  if (MB == a && NB == b && ws == o && (da.limbs != nullptr) == det) {                                         \
+    static std::atomic<unsigned long long> attr_set{0};                                                         \
+    if (!optin_done(attr_set)) {                                                                                \
+      cudaError_t e = cudaFuncSetAttribute(k_spread_v5<a, b, o, det>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                            227 * 1024);                                                         \
       if (e != cudaSuccess) return e;                                                                           \
-      optin_mark(attr_set);                                                                                          \
+      optin_mark(attr_set);                                                                                     \
     }                                                                                                           \
-    k_spread_v5<a, b, o><<<n_items, o ? 2 * kV5Threads : kV5Threads, smem, s>>>(dtab, items, u_sorted, perm, V, \
-                                                                                ldv, n, r0, rc,                \
-                                                           r_total, grid, WN, pp, da);                          \
+    k_spread_v5<a, b, o, det><<<n_items, o ? 2 * kV5Threads : kV5Threads, smem, s>>>(                           \
+        dtab, items, u_sorted, perm, V, ldv, n, r0, rc, r_total, grid, WN, pp, da);                              \
     return cudaGetLastError();                                                                                  \
   }
+#define AKM_CASE1(a, b, o) AKM_CASE2(a, b, o, false) AKM_CASE2(a, b, o, true)
 #define AKM_CASE(a, b) AKM_CASE1(a, b, true) AKM_CASE1(a, b, false)
   AKM_V5_TILES(AKM_CASE)
 #undef AKM_CASE
 #undef AKM_CASE1
+#undef AKM_CASE2
   return cudaErrorInvalidValue;
 }
 
