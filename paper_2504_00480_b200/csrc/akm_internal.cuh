@@ -358,6 +358,12 @@ cudaError_t launch_spread_strip(const WinTable* dtab, const PolyParam& pp, const
                                 int r0, int rc, int r_total, double* grid, int taps, int F, int nb, cudaStream_t s,
                                 const DetAcc& da);
 
+// interp_pt.cu (small launches: one warp per point, taps over the lanes, H straight from L2)
+bool interp_pt_choose(int d, int taps, int ops, int rc, int n_items_bin);
+cudaError_t launch_interp_pt(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,
+                             const double* u_sorted, const int* perm, const double* H, int d, int taps, int ops,
+                             int r, int r0, int rc, double* part, long long n, cudaStream_t s);
+
 // interp_strip.cu (2-D windows: per bin, one DMMA GEMM per strip of 1 x B cells, K = axis-2 nodes)
 bool interp_strip_supported(int d, int taps, int F, int ops, int rc);
 cudaError_t launch_interp_strip(const WinTable* dtab, const PolyParam& pp, const WorkItem* items, int n_items,

@@ -918,6 +918,17 @@ static akm_status enqueue_finish(akm_plan* plan, const double* grid, const doubl
   while (r0 < r) {
     const int rc = interp_rc_for(r - r0);
     for (const Group& grp : plan->groups) {
+      // small launches (fewer than 2 x 148 per-bin items, c1): one warp per point (interp_pt.cu)
+      if (interp_pt_choose(grp.d, 2 * plan->m, ops, rc, grp.sl[set].interp_bin_count)) {
+        AKM_CK(launch_interp_pt(dtab, plan->poly_param,
+                                plan->items_ib[set].as<WorkItem>() + grp.sl[set].interp_bin_begin,
+                                grp.sl[set].interp_bin_count, plan->u_sorted.as<double>(), plan->perm.as<int>(),
+                                plan->H.as<double>(), grp.d, 2 * plan->m, ops, r, r0, rc, plan->part.as<double>(), n,
+                                s));
+        ++plan->launches;
+        ++plan->interp_launches;
+        continue;
+      }
       // 2-D windows: per-bin strips of 1 x B cells as DMMA GEMMs (interp_strip.cu)
       if (interp_strip_supported(grp.d, 2 * plan->m, grp.F, ops, rc)) {
         AKM_CK(launch_interp_strip(dtab, plan->poly_param,
