@@ -640,7 +640,7 @@ def test_2d_strip_interpolation_every_bin_edge(akm, m, N, B):
     enough that bins split into several 128-point items.  Gate: the exact truncated-Fourier
     operator (eq. 3.3), block and per row."""
     rng = np.random.default_rng(700 + 10 * B + m)
-    n = 3000
+    n = 20000  # > 2 x 148 per-bin items, so the launch does not take the small-launch path (interp_pt.cu)
     X = np.concatenate([rng.random((n // 2, 4)), 0.5 + 0.05 * rng.standard_normal((n - n // 2, 4))])
     windows = [(0, 1), (2, 3)]
     th = (0.9, 0.3, 0.2)
@@ -662,3 +662,33 @@ def test_2d_strip_interpolation_every_bin_edge(akm, m, N, B):
             o = out.cpu().numpy()
             assert rel(o, nd[op]) <= tol, (r, op, rel(o, nd[op]))
             assert row_max(o, nd[op]) <= 10 * tol, (r, op, row_max(o, nd[op]))
+
+
+def test_small_launch_path_matches_staged_kernels(akm, tmp_path):
+    """The per-point interpolation of small launches (interp_pt.cu, < 2 x 148 per-bin items) against
+    the staged kernels on the same inputs: 3-D (c1's shape), 2-D and 1-D windows, two operators,
+    ragged RHS.  AKM_INTERP_PT is read once per process, so each side runs in its own child."""
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {ROOT!r})\n"
+        "import paper_2504_00480_b200 as akm\n"
+        "rng = np.random.default_rng(9)\n"
+        "n = 1800\n"
+        "X = rng.random((n, 6)); V = rng.standard_normal((n, 13))\n"
+        "dev = torch.device('cuda:0')\n"
+        "p = akm.Plan(0)\n"
+        "p.set_points(torch.from_numpy(X).to(dev), [(0, 1, 2), (3, 4), (5,)], 0, 32, 2.0, 6, 1.0 / 16)\n"
+        "p.set_theta(1.0, 0.3, 0.1)\n"
+        "Vd = torch.from_numpy(V).to(dev); Y = torch.empty_like(Vd); L = torch.empty_like(Vd)\n"
+        "p.mvm_multi(Vd, Y=Y, dY_ell=L); torch.cuda.synchronize()\n"
+        "np.save(sys.argv[1], np.stack([Y.cpu().numpy(), L.cpu().numpy()]))\n")
+    outs = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, AKM_INTERP_PT=mode)
+        f = tmp_path / f"out{mode}.npy"
+        subprocess.run([sys.executable, str(script), str(f)], env=env, check=True, timeout=300)
+        outs[mode] = np.load(f)
+    assert rel(outs["1"], outs["0"]) <= 1e-12, rel(outs["1"], outs["0"])
