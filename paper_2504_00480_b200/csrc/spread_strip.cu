@@ -43,7 +43,10 @@ __device__ __forceinline__ void ss_cp4(void* dst, const void* src) {
 __device__ __forceinline__ void ss_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void ss_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-__host__ __device__ constexpr int ss_ldw(int fmax) { return ((fmax + 1 + 7) / 16) * 16 + 8; }  // 8 mod 16, > fmax
+// table row strides = 4 (mod 16) doubles: the 4 points of a half-warp's fragment reads land 4 banks
+// apart (spread_v5.cu v5_ldw)
+__host__ __device__ constexpr int ss_ldw(int fmax) { return ((fmax + 1 + 11) / 16) * 16 + 4; }  // 4 mod 16, > fmax
+__host__ __device__ constexpr int ss_vld(int rc) { return rc <= 12 ? 12 : ((rc + 11) / 16) * 16 + 4; }
 __host__ __device__ constexpr int ss_ldc(int nb) { return ((4 * nb * 8 + 15) / 16) * 16 + 8; }  // 8 mod 16
 
 struct SsLayout {
@@ -54,7 +57,7 @@ __host__ __device__ inline SsLayout ss_layout(int F, int rc, int NB) {
   const int LDW = ss_ldw(F);
   l.wb = 0;
   l.vring = l.wb + sizeof(double) * 2 * 3 * kSsPB * LDW;
-  l.uring = (l.vring + sizeof(double) * kSsRing * (kSsPB * rc + 1) + 15) & ~(size_t)15;
+  l.uring = (l.vring + sizeof(double) * kSsRing * (kSsPB * ss_vld(rc) + 1) + 15) & ~(size_t)15;
   l.cs = l.uring + sizeof(double) * kSsRing * 3 * kSsPB;
   l.cacc = (l.cs + sizeof(double) * 16 * kSsLdC + 15) & ~(size_t)15;  // double2 accesses
   l.pring = l.cacc + sizeof(double) * (size_t)F * ss_ldc(NB);
@@ -83,7 +86,8 @@ __global__ void __launch_bounds__(kSsThreads, 2) k_spread_strip(const WinTable* 
   const WinGeom& g = tab.w[it.win];
   const int F1 = g.F[1], F2 = g.F[2];
   const int LDW = ss_ldw(max(F1, F2));
-  const int VS = PB * rc + 1;
+  const int VLD = ss_vld(rc);  // ring row stride of a point's RHS values
+  const int VS = PB * VLD + 1;
   const int Nn = F2 * rc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nbatch = (it.count + PB - 1) / PB;
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(kSsThreads, 2) k_spread_strip(const WinTable* 
 #pragma unroll
   for (int a = 0; a < 3; ++a) org[a] = g.box_lo[a] + it.bin[a] * g.B;
   for (int idx = tid; idx < 2 * 3 * PB * LDW; idx += NT) Wb[idx] = 0.0;
-  for (int s = tid; s < kSsRing; s += NT) Vring[s * VS + PB * rc] = 0.0;
+  for (int s = tid; s < kSsRing; s += NT) Vring[s * VS + PB * VLD] = 0.0;
   for (int idx = tid; idx < 16 * kSsLdC; idx += NT) {
     const int k = idx / kSsLdC, q = idx - k * kSsLdC;
     Cs[idx] = (k < kPolyLen && q < TAPS) ? pp.c[q * kPolyLen + k] : 0.0;
@@ -132,8 +136,8 @@ __global__ void __launch_bounds__(kSsThreads, 2) k_spread_strip(const WinTable* 
     const int* pr = Pring + (b % kSsRing) * PB;
     for (int j = tid; j < PB * rc; j += NT) {
       const int p = fdiv(j, inv_rc), c = j - p * rc;
-      if (p < pb) ss_cp8(Vs + j, V + (long long)pr[p] * ldv + r0 + c);
-      else Vs[j] = 0.0;
+      if (p < pb) ss_cp8(Vs + p * VLD + c, V + (long long)pr[p] * ldv + r0 + c);
+      else Vs[p * VLD + c] = 0.0;
     }
   };
   // weights of batch b on the tensor core (as k_spread_v5): rows (axis a in {1, 2}, point p) =
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(kSsThreads, 2) k_spread_strip(const WinTable* 
       const int p = ks * 4 + (lane & 3);
       const double* w1 = W1 + p * LDW + cs;
       const double* w2 = W2 + p * LDW;
-      const double* vs = Vs + p * rc;
+      const double* vs = Vs + p * VLD;
       double bf[NB], af[MT];
 #pragma unroll
       for (int j = 0; j < NB; ++j) bf[j] = w2[bi[j] & 0xffff] * vs[bi[j] >> 16];
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(kSsThreads, 2) k_spread_strip(const WinTable* 
       const int p = ks * 4 + (lane & 3);
       const double* w1 = W1 + p * LDW;
       const double* w2 = W2 + p * LDW;
-      const double* vs = Vs + p * rc;
+      const double* vs = Vs + p * VLD;
       const int sq = S1[p];
       double bf[NB];
 #pragma unroll

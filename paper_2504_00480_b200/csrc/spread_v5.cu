@@ -46,7 +46,12 @@ __device__ __forceinline__ void v5_bar_arrive(int id, int count) {
 }
 __device__ __forceinline__ void v5_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-__host__ __device__ constexpr int v5_ldw(int fmax) { return ((fmax + 1 + 7) / 16) * 16 + 8; }  // 8 mod 16, > fmax
+// Row strides of the per-point tables read as fragments.  A half-warp reads 4 points (lane & 3) x 4
+// consecutive columns (lane >> 2): a stride of 4 (mod 16) doubles puts the 4 point rows 4 banks
+// apart, so the 16 reads hit 16 distinct 8-byte banks (the earlier 8 (mod 16) collided rows p and
+// p + 2: 2x the ideal shared-memory wavefronts at c4, ncu).
+__host__ __device__ constexpr int v5_ldw(int fmax) { return ((fmax + 1 + 11) / 16) * 16 + 4; }  // 4 mod 16, > fmax
+__host__ __device__ constexpr int v5_vld(int rc) { return rc <= 12 ? 12 : ((rc + 11) / 16) * 16 + 4; }  // RHS row
 }  // namespace
 
 template <int MB, int NB, bool WS, bool DET>
@@ -66,7 +71,8 @@ __global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_
   const int F1 = g.F[1];
   const int Fmax = max(g.F[0], max(F1, g.F[2]));
   const int LDW = v5_ldw(Fmax);
-  const int VS = PB * rc + 1;  // ring slot of RHS values + one zero
+  const int VLD = v5_vld(rc);      // ring row stride of a point's RHS values
+  const int VS = PB * VLD + 1;  // ring slot of RHS values + one zero
   const int M = g.F[0] * F1, Nn = g.F[2] * rc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // WS: warps 0-3 run the MMAs, warps 4-7 ("helpers") the weights and the input ring; otherwise
@@ -89,7 +95,7 @@ __global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_
   for (int a = 0; a < 3; ++a) org[a] = g.box_lo[a] + it.bin[a] * g.B;
   constexpr int NALL = WS ? 2 * NT : NT;
   for (int idx = tid; idx < 2 * 3 * PB * LDW; idx += NALL) Wb[idx] = 0.0;
-  for (int s = tid; s < kV5Ring; s += NALL) Vring[s * VS + PB * rc] = 0.0;
+  for (int s = tid; s < kV5Ring; s += NALL) Vring[s * VS + PB * VLD] = 0.0;
   for (int idx = tid; idx < 16 * kV5LdC; idx += NALL) {
     const int k = idx / kV5LdC, q = idx - k * kV5LdC;
     Cs[idx] = (k < kPolyLen && q < taps) ? pp.c[q * kPolyLen + k] : 0.0;
@@ -117,8 +123,9 @@ __global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_
     const int* pr = Pring + (b % kV5Ring) * PB;
     for (int j = ltid; j < PB * rc; j += NT) {
       const int p = fdiv(j, inv_rc), c = j - p * rc;
-      if (p < pb) v5_cp8(Vs + j, V + (long long)pr[p] * ldv + r0 + c);
-      else Vs[j] = 0.0;
+      double* dst = Vs + p * VLD + c;
+      if (p < pb) v5_cp8(dst, V + (long long)pr[p] * ldv + r0 + c);
+      else *dst = 0.0;
     }
   };
   // weights of batch b into Wb[b&1], on the tensor core: for the 3*PB (axis, point) rows,
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(WS ? 2 * kV5Threads : kV5Threads, 1) k_spread_
       const double* w0 = W0 + p * LDW;
       const double* w1 = W1 + p * LDW;
       const double* w2 = W2 + p * LDW;
-      const double* vs = Vs + p * rc;
+      const double* vs = Vs + p * VLD;
       double af[MB], bf[NB];
 #pragma unroll
       for (int i = 0; i < MB; ++i) af[i] = w0[ai[i] & 0xffff] * w1[ai[i] >> 16];
@@ -351,7 +358,7 @@ bool spread_v5_choose(int M, int Nn, int& MB, int& NB, int& WN) {
 
 size_t spread_v5_smem(int Fmax, int rc, int MB, int NB, int WN) {
   (void)MB, (void)NB, (void)WN;
-  return sizeof(double) * (2 * 3 * (size_t)kV5PB * v5_ldw(Fmax) + (size_t)kV5Ring * (kV5PB * rc + 1) +
+  return sizeof(double) * (2 * 3 * (size_t)kV5PB * v5_ldw(Fmax) + (size_t)kV5Ring * (kV5PB * v5_vld(rc) + 1) +
                            (size_t)kV5Ring * 3 * kV5PB + 16 * kV5LdC) +
          sizeof(int) * (size_t)kV5Ring * kV5PB;
 }
