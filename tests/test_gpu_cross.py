@@ -184,3 +184,21 @@ def test_cross_strided_blocks(akm):
     plan.cross_mvm(2200, Vw[:, 1:4], Yhost[:, 1:4])
     assert rel(Yhost[:, 1:4], want) <= 1e-6 and np.isnan(Yhost[:, 0]).all() and np.isnan(Yhost[:, 4:]).all()
     plan.close()
+
+
+def test_cross_2d_windows_past_the_small_launch_threshold(akm):
+    """2-D windows at sizes where the strip kernels run (spreading over the class-0 sources only,
+    interpolation at the class-1 targets only; > 2 x 148 per-bin items, so not the per-point
+    small-launch path), Gaussian windows (method error ~1e-15 here, so the 1e-6 gate tests the
+    implementation), 11 RHS, two length scales: against the dense cross oracle on 512 sampled target
+    rows."""
+    rng = np.random.default_rng(77)
+    n_src, n_t = 30000, 12000
+    X = rng.random((n_src + n_t, 4))
+    V = rng.standard_normal((n_src, 11))
+    rows = np.sort(rng.choice(n_t, 512, replace=False))
+    for ell in (0.3, 0.15):
+        theta = (1.0, ell, 0.1)
+        got = gpu_cross(akm, X, n_src, [(0, 1), (2, 3)], 0, theta, V, N=64, m=8)
+        want = dense_cross(X[:n_src], X[n_src:][rows], [(0, 1), (2, 3)], 0, theta, V)
+        assert rel(got[rows], want) <= 1e-6, (ell, rel(got[rows], want))
