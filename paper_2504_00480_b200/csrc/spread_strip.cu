@@ -188,8 +188,10 @@ __global__ void __launch_bounds__(kSsThreads, 2) k_spread_strip(const WinTable* 
         if (q0 + 1 < TAPS) wrow[s + q0 + 1] = c0[t][1];
         if (q0 + 8 < TAPS) wrow[s + q0 + 8] = c1[t][0];
         if (q0 + 9 < TAPS) wrow[s + q0 + 9] = c1[t][1];
-        for (int o = j4; o < s; o += 4) wrow[o] = 0.0;
-        for (int o = s + TAPS + j4; o < Fa; o += 4) wrow[o] = 0.0;
+        if (a == 2) {  // axis 1 rows are read only at the point's own taps (rows relative to its strip)
+          for (int o = j4; o < s; o += 4) wrow[o] = 0.0;
+          for (int o = s + TAPS + j4; o < Fa; o += 4) wrow[o] = 0.0;
+        }
       } else {
         for (int o = j4; o < Fa; o += 4) wrow[o] = 0.0;
       }
