@@ -826,7 +826,7 @@ static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv,
     int M = 1;
     for (int t = 0; t < d - 1; ++t) M *= F;
     int r0 = 0;
-    // one-warp-per-SMSP kernel (spread_v5.cu) for every 2-D / 3-D window group, k_spread_mma for 1-D
+    // 2-D groups: strips (spread_strip.cu); 3-D: spread_v5.cu; k_spread_mma for 1-D
     // windows; AKM_SPREAD_V5=0/1 forces either kernel (A/B measurement)
     static const int v5_env = getenv("AKM_SPREAD_V5") ? atoi(getenv("AKM_SPREAD_V5")) : -1;
     const bool v5 = v5_env >= 0 ? v5_env != 0 : d >= 2;

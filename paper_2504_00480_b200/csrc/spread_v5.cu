@@ -1,10 +1,10 @@
 // spread_v5.cu -- adjoint NFFT gridding (NFFT step 1 transposed, App. A), the kernel
-// for every 2-D and 3-D window group (plan.cu; k_spread_mma serves 1-D windows, or all windows
-// under AKM_SPREAD_V5=0).
+// for 3-D window groups (plan.cu; 2-D groups take k_spread_strip in spread_strip.cu unless
+// AKM_SPREAD_STRIP=0, 1-D windows k_spread_mma, or all windows under AKM_SPREAD_V5=0).
 //
 // Same GEMM as spread_mma.cu (C[(o0,o1),(o2,c)] = sum_p (w0 w1)[p] (w2 v)[p] on DMMA), but:
-//   * 4 MMA warps per CTA and one CTA per SM: every SM sub-partition has exactly one MMA warp, so
-//     each can hold up to 9 x 5 DMMA accumulator tiles (tools/microbench/dmma_occupancy.cu: one warp
+//   * 4 MMA warps per CTA (two CTAs per SM at <= 255 registers: one or two MMA warps per SM
+//     sub-partition), so each warp can hold up to 9 x 5 DMMA accumulator tiles (tools/microbench/dmma_occupancy.cu: one warp
 //     per sub-partition keeps the DMMA pipe busy);
 //   * fragments are formed on the fly (A = W0 * W1, B = W2 * V: one independent DMUL each) from
 //     the per-point weight rows, so there are no operand panels and no staging phase for them;
