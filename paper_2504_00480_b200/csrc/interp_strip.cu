@@ -31,6 +31,7 @@ __device__ __forceinline__ void is_cp8(double* dst, const double* src) {
 }
 
 constexpr int kIsThreads = 128;  // one point per thread in the prologue; 4 warps share the m-tiles
+// (the per-bin items hold <= 128 points: plan.cu ch_ib, as for k_interp_bin's one point per thread)
 
 struct IsLayout {
   int KP;   // staged K rows (axis-2 footprint nodes, rounded up to a multiple of 4; padding rows zero)

@@ -27,6 +27,7 @@ namespace akm {
 
 namespace {
 constexpr int kSsPB = 32;
+static_assert(kSsPB == 32, "k_spread_strip reads one point's strip per lane (S1[lane]) and ballots over a batch");
 constexpr int kSsWarps = 4;
 constexpr int kSsThreads = 32 * kSsWarps;
 constexpr int kSsRing = 5;
