@@ -204,6 +204,8 @@ constexpr int kMmaK = 16;  // complex l per staged chunk (32 real k)
 constexpr int kMmaTM = 2, kMmaTN = 4;  // DMMA tiles per warp along m and n (2 x 2 warps per CTA)
 constexpr int kMmaRows = 2 * kMmaTM * 8, kMmaCols = 2 * kMmaTN * 8;  // real rows / columns per CTA
 constexpr int kMmaXE = kMmaK * kMmaCols / 128, kMmaME = (kMmaRows / 2) * kMmaK / 128;  // loads per thread
+constexpr int kMmaLdB = kMmaCols + 4, kMmaLdA = 2 * kMmaK + 4;  // smem row strides (= 4 mod 16)
+constexpr size_t kMmaSmem = sizeof(double) * (2 * 2 * kMmaK * kMmaLdB + 2 * kMmaRows * kMmaLdA);
 // FUSED_D (kFD, every window without an axis 0): the input is A2 itself times the multiplier
 // D_op[k0 = 0][k1][k2] (the FC1 copy and the FC2 multiply folded into the load).
 template <int MODE, bool FUSED_D = false>
@@ -223,8 +225,11 @@ __global__ void __launch_bounds__(128) k_dft_mma(const WinTable* __restrict__ ta
   const long long ybase = (MODE == kFB ? g.a2_off : g.c2_off) * r + (long long)o * sh.yo;
   const double2* T = tw + g.tw_off[1];
   const int Lt = g.L[1];
-  __shared__ double2 Xs[2][kMmaK][kMmaCols];
-  __shared__ double2 Ms[2][CK][kMmaK + 1];
+  // operands stored in their real form, so a fragment is one 8-byte load: Br[2l + p][col] = component
+  // p of X[l][col], Ar[2k + q][2l + p] = the 2x2 real block of M[k][l]; row strides = 4 (mod 16)
+  extern __shared__ __align__(16) double dft_sm[];
+  double* Br = dft_sm;                               // [2][2 kMmaK][kMmaLdB]
+  double* Ar = dft_sm + 2 * 2 * kMmaK * kMmaLdB;     // [2][kMmaRows][kMmaLdA]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wm = warp >> 1, wn = warp & 1;
   double acc[kMmaTM][kMmaTN][2];
 #pragma unroll
@@ -269,30 +274,32 @@ __global__ void __launch_bounds__(128) k_dft_mma(const WinTable* __restrict__ ta
         v.x *= dr[e];
         v.y *= dr[e];
       }
-      Xs[buf][l][j] = v;
+      double* bb = Br + (buf * 2 * kMmaK + 2 * l) * kMmaLdB + j;
+      bb[0] = v.x;
+      bb[kMmaLdB] = v.y;
     }
 #pragma unroll
     for (int e = 0; e < kMmaME; ++e) {
       const int idx = tid + 128 * e, k = idx / kMmaK, l = idx - k * kMmaK;
-      Ms[buf][k][l] = (MODE == kFB) ? mr[e] : make_double2(mr[e].x, -mr[e].y);  // kFD: conj(T[l][k])
+      const double2 m = (MODE == kFB) ? mr[e] : make_double2(mr[e].x, -mr[e].y);  // kFD: conj(T[l][k])
+      double* ab = Ar + (buf * kMmaRows + 2 * k) * kMmaLdA + 2 * l;
+      ab[0] = m.x;
+      ab[1] = -m.y;
+      ab[kMmaLdA] = m.y;
+      ab[kMmaLdA + 1] = m.x;
     }
     __syncthreads();  // chunk c visible; buffer buf ^ 1 (chunk c - 1) free for the next store
     if (l0 + kMmaK < sh.L) gload(l0 + kMmaK);
 #pragma unroll
     for (int ks = 0; ks < 2 * kMmaK / 4; ++ks) {
-      const int kr = ks * 4 + (lane & 3), ll = kr >> 1, p = kr & 1;
+      const int kr = ks * 4 + (lane & 3);
       double af[kMmaTM], bf[kMmaTN];
 #pragma unroll
-      for (int mt = 0; mt < kMmaTM; ++mt) {
-        const int row = (wm * kMmaTM + mt) * 8 + (lane >> 2), q = row & 1;
-        const double2 m = Ms[buf][row >> 1][ll];
-        af[mt] = (q == 0) ? (p == 0 ? m.x : -m.y) : (p == 0 ? m.y : m.x);
-      }
+      for (int mt = 0; mt < kMmaTM; ++mt)
+        af[mt] = Ar[(buf * kMmaRows + (wm * kMmaTM + mt) * 8 + (lane >> 2)) * kMmaLdA + kr];
 #pragma unroll
-      for (int nt = 0; nt < kMmaTN; ++nt) {
-        const double2 x = Xs[buf][ll][(wn * kMmaTN + nt) * 8 + (lane >> 2)];
-        bf[nt] = p == 0 ? x.x : x.y;
-      }
+      for (int nt = 0; nt < kMmaTN; ++nt)
+        bf[nt] = Br[(buf * 2 * kMmaK + kr) * kMmaLdB + (wn * kMmaTN + nt) * 8 + (lane >> 2)];
 #pragma unroll
       for (int mt = 0; mt < kMmaTM; ++mt)
 #pragma unroll
@@ -327,7 +334,14 @@ static cudaError_t launch_dft_mma(const WinTable& tab, const WinTable* dtab, con
     O = std::max(O, sh.O);
     ktiles = std::max(ktiles, (sh.K + kMmaRows / 2 - 1) / (kMmaRows / 2));
   }
-  k_dft_mma<MODE, FUSED_D><<<dim3((unsigned)itiles, (unsigned)(O * ktiles), tab.P), 128, 0, s>>>(
+  static std::atomic<unsigned long long> attr{0};
+  if (!optin_done(attr)) {
+    cudaError_t e = cudaFuncSetAttribute(k_dft_mma<MODE, FUSED_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kMmaSmem);
+    if (e != cudaSuccess) return e;
+    optin_mark(attr);
+  }
+  k_dft_mma<MODE, FUSED_D><<<dim3((unsigned)itiles, (unsigned)(O * ktiles), tab.P), 128, kMmaSmem, s>>>(
       dtab, X, Y, tw, r, ops, ktiles, D, dslot0);
   return cudaGetLastError();
 }
