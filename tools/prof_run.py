@@ -29,6 +29,8 @@ def main():
     outs = {op: torch.empty_like(Vd) for op in wl.ops}
     plan = akm.Plan(0)
     plan.set_points(Xd, wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
+    if "reg_eps_I" in (wl.extra or {}):  # c3r: kappa_R with the near-field correction
+        plan.set_regularization(wl.extra["reg_eps_I"], wl.extra["reg_p"])
     plan.set_theta(wl.sigma_f, wl.ell, wl.sigma_eps)
     for _ in range(a.calls):
         plan.mvm_multi(Vd, Y=outs.get("K"), dY_ell=outs.get("dell"), dY_sf=outs.get("dsf"))
