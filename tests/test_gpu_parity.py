@@ -692,3 +692,23 @@ def test_small_launch_path_matches_staged_kernels(akm, tmp_path):
         subprocess.run([sys.executable, str(script), str(f)], env=env, check=True, timeout=300)
         outs[mode] = np.load(f)
     assert rel(outs["1"], outs["0"]) <= 1e-12, rel(outs["1"], outs["0"])
+
+
+@pytest.mark.parametrize("family", [0, 1])
+def test_mixed_windows_past_the_small_launch_threshold(akm, family):
+    """One product over 3-D, 2-D and 1-D windows at a size where every group takes its production
+    kernels (k_spread_v5 / k_spread_strip / k_spread_mma, k_interp_mma or k_interp_t / k_interp_strip /
+    1-D interpolation; > 2 x 148 per-bin items, so not the per-point small-launch path), 13 RHS in
+    ragged chunks, three operators: against the exact eq. 3.3 operator on 512 sampled rows."""
+    rng = np.random.default_rng(800 + family)
+    n = 30000
+    X = rng.random((n, 6))
+    V = rng.standard_normal((n, 13))
+    windows = [(0, 1, 2), (3, 4), (5,)]
+    th = (0.9, 0.3, 0.2)
+    out, _ = gpu_apply(akm, X, windows, family, th, V, N=32, m=6, ops=("K", "dell", "dsf"))
+    rows = np.sort(rng.choice(n, 512, replace=False))
+    nd = F.additive_fastsum(X, windows, family, th, V, 32, 1.0 / 16, ops=("K", "dell", "dsf"), rows=rows)
+    for op in ("K", "dell", "dsf"):
+        assert rel(out[op][rows], nd[op]) <= 1e-9, (op, rel(out[op][rows], nd[op]))
+        assert row_max(out[op][rows], nd[op]) <= 1e-8, (op, row_max(out[op][rows], nd[op]))
