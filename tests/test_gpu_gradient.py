@@ -32,9 +32,11 @@ def _inputs(n, n_z, seed=0):
     return wl, X, np.ascontiguousarray(V[:, 0]), np.ascontiguousarray(V[:, 1:])
 
 
-def _gpu(akm, wl, X, theta, y, Z, cg, host=False):
+def _gpu(akm, wl, X, theta, y, Z, cg, host=False, deterministic=False):
     plan = akm.Plan(0)
     dev = torch.device("cuda:0")
+    if deterministic:
+        plan.set_deterministic(True)
     plan.set_points(torch.from_numpy(X).to(dev), wl.windows, wl.family, wl.N, wl.sigma_over, wl.m, wl.eps_B)
     plan.set_theta(*theta)
     if host:
@@ -106,10 +108,14 @@ def test_gradient_unconverged_theta_within_cg_noise_floor(akm, theta):
 def test_gradient_host_inputs_and_zero_iterations(akm):
     wl, X, y, Z = _inputs(1500, 3, seed=2)
     theta = (1.0, 0.5, 0.3)
-    a = _gpu(akm, wl, X, theta, y, Z, 20)
-    b = _gpu(akm, wl, X, theta, y, Z, 20, host=True)
+    # host and device inputs run the same kernels: bitwise equal in deterministic mode (integer-limb
+    # spreading); with float atomics the arrival order differs and 20 unconverged CG steps amplify it
+    a = _gpu(akm, wl, X, theta, y, Z, 20, deterministic=True)
+    b = _gpu(akm, wl, X, theta, y, Z, 20, host=True, deterministic=True)
+    c = _gpu(akm, wl, X, theta, y, Z, 20)
     for j in ("sf", "ell", "se"):
-        assert a["grad"][j] == pytest.approx(b["grad"][j], rel=1e-7)   # atomic-order noise x CG
+        assert a["grad"][j] == b["grad"][j]
+        assert c["grad"][j] == pytest.approx(a["grad"][j], rel=1e-5)
     # no iterations: alpha = Khat^{-1} z = 0, and with Rademacher probes the M terms cancel -> 0
     z = _gpu(akm, wl, X, theta, y, Z, 0)
     for j in ("sf", "ell", "se"):
