@@ -833,7 +833,7 @@ static akm_status enqueue_spread(akm_plan* plan, const double* V, long long ldv,
     while (v5 && r0 < r) {
       // 2-D windows: strips of 1 x B cells as their own GEMMs (spread_strip.cu), when a tile exists
       if (d == 2 && spread_strip_nb(d, 2 * plan->m, F, 1) > 0) {
-        static const int ss_rcmax = getenv("AKM_SS_RCMAX") ? atoi(getenv("AKM_SS_RCMAX")) : 12;
+        static const int ss_rcmax = getenv("AKM_SS_RCMAX") ? std::max(1, atoi(getenv("AKM_SS_RCMAX"))) : 12;
         int rc = std::min(ss_rcmax, r - r0);
         while (rc > 1 && spread_strip_nb(d, 2 * plan->m, F, rc) == 0) --rc;
         if (rc < r - r0 && rc > (r - r0 + 1) / 2) rc = (r - r0 + 1) / 2;
