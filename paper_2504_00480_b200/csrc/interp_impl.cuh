@@ -190,10 +190,10 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(const WinTable* __restric
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) wa[mt] = w0s[warp * 16 + mt * 8 + (lane >> 2)][o0];
     const double* bbase = cur + (lane & 3) * LDH + (lane >> 2);
-    // rows in groups of G: first all A values of the group (a burst of DMULs), then its DMMAs (a
-    // burst with no scalar FP64 in between -- interleaving them stalls the DMMAs behind DMULs that
-    // other warps' DMMA streams starve).  Warps without points skip the MMAs.
-    constexpr int G = (T1 % 4 == 0) ? 4 : 1;
+    // rows in groups of G: first the A values of the group (DMULs), then its DMMAs.  With the
+    // TMA-staged planes one row per group measures fastest (c4 interpolation G = 1 / 2 / 3 / 4 / 6:
+    // 10.80 / 10.84 / 10.88 / 10.94 / 10.92 ms).  Warps without points skip the MMAs.
+    constexpr int G = 1;
     if (wact) {
 #pragma unroll 1
       for (int g0 = 0; g0 < T1; g0 += G) {
