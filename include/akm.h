@@ -117,6 +117,27 @@ akm_status akm_kernel_deriv_mvm(akm_plan* plan, int32_t which, const double* V, 
 akm_status akm_kernel_mvm_multi(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y,
                                 double* dY_ell, double* dY_sf, int64_t ldy, void* stream);
 
+/* Streaming form of akm_kernel_mvm_multi for a sequence of independent batches held in PINNED host
+ * memory (the batched K^V throughput of BASELINE.json's metric, fed from the host).  Same operation,
+ * arguments and outputs as akm_kernel_mvm_multi; V, Y, dY_ell, dY_sf must be page-locked host
+ * buffers (cudaHostAlloc / cudaHostRegister / torch pin_memory), else INVALID_ARG.  The call only
+ * enqueues: V goes to one of two library-owned device slots on a copy-in stream, the product runs on
+ * `stream` (ordered after earlier work there, so it shares the plan's workspaces safely), and the
+ * outputs come back on a copy-out stream.  Consecutive calls therefore overlap batch k's
+ * device-to-host copy and batch k+1's host-to-device copy with the products.  Batches under 4 MiB
+ * of V (env AKM_PIPE_SPLIT_MIN_BYTES) keep their copies on `stream` (the stream handshakes would
+ * cost more than the overlap hides); the call still returns without blocking.  The copy-in is NOT
+ * ordered after earlier work on `stream` (only after the product two calls back, which used the same
+ * slot): the caller must not write V, nor read or write the outputs, until akm_pipeline_wait.
+ * Errors as akm_kernel_mvm_multi. */
+akm_status akm_kernel_mvm_pipelined(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y,
+                                    double* dY_ell, double* dY_sf, int64_t ldy, void* stream);
+
+/* Make `stream` wait (stream-ordered, no host block) until every akm_kernel_mvm_pipelined call
+ * issued so far has finished its copies: after it, synchronising `stream` means the host outputs
+ * are complete and the host inputs may be reused.  No-op without pipelined calls. */
+akm_status akm_pipeline_wait(akm_plan* plan, void* stream);
+
 /* Cross product for prediction (posterior mean / variance use K_{*X} V,
  * P:947):  Yt = sigma_f^2 sum_w K_w(X_t, X_s) V  (no noise term).
  * The points of the last akm_set_points are read as [sources X_s = rows 0 .. n_src-1; targets

@@ -36,7 +36,7 @@ ABI_SYMBOLS = ("akm_create", "akm_set_points", "akm_set_theta", "akm_kernel_mvm"
                "akm_get_bounds", "akm_set_bounds", "akm_set_radius", "akm_set_bin_override", "akm_grid_size",
                "akm_spread_grid", "akm_mvm_from_grid", "akm_set_regularization", "akm_set_preconditioner",
                "akm_precond_apply", "akm_precond_landmarks", "akm_objective", "akm_gradient",
-               "akm_gradient_columns", "akm_set_deterministic")
+               "akm_gradient_columns", "akm_set_deterministic", "akm_kernel_mvm_pipelined", "akm_pipeline_wait")
 AKM_MAX_PROBES = 31
 
 
@@ -95,6 +95,10 @@ def _load():
     lib.akm_kernel_deriv_mvm.restype = st
     lib.akm_kernel_mvm_multi.argtypes = [P, P, i64, i32, P, P, P, i64, P]
     lib.akm_kernel_mvm_multi.restype = st
+    lib.akm_kernel_mvm_pipelined.argtypes = [P, P, i64, i32, P, P, P, i64, P]
+    lib.akm_kernel_mvm_pipelined.restype = st
+    lib.akm_pipeline_wait.argtypes = [P, P]
+    lib.akm_pipeline_wait.restype = st
     lib.akm_kernel_cross_mvm.argtypes = [P, i64, P, i64, i32, P, i64, P]
     lib.akm_kernel_cross_mvm.restype = st
     lib.akm_gradient_diag.argtypes = [P, P, P, i64, i32, i32, P, P, P]
@@ -310,6 +314,22 @@ def akm_kernel_mvm_multi(plan, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
     ldy = lds.pop() if lds else r
     _check(plan, _lib.akm_kernel_mvm_multi(plan, pv, ldv, r, outs[0][0], outs[1][0], outs[2][0], ldy,
                                            _stream(stream, kv, *[o[5] for o in outs])))
+
+
+def akm_kernel_mvm_pipelined(plan, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
+    """Streaming host batches (include/akm.h): V and the outputs are pinned host blocks; the call only
+    enqueues, and the outputs are complete after akm_pipeline_wait(plan, stream) and a sync."""
+    (pv, ldv, n, r, kv), outs = _same_block(plan, V, [("Y", Y), ("dY_ell", dY_ell), ("dY_sf", dY_sf)])
+    lds = {o[1] for o in outs if o[0] is not None}
+    if len(lds) > 1:
+        raise ValueError("all outputs of akm_kernel_mvm_pipelined must share one leading dimension")
+    ldy = lds.pop() if lds else r
+    _check(plan, _lib.akm_kernel_mvm_pipelined(plan, pv, ldv, r, outs[0][0], outs[1][0], outs[2][0], ldy,
+                                               _stream(stream, kv, *[o[5] for o in outs])))
+
+
+def akm_pipeline_wait(plan, stream=None):
+    _check(plan, _lib.akm_pipeline_wait(plan, _stream(stream)))
 
 
 def akm_kernel_cross_mvm(plan, n_src, V, Yt, stream=None):
@@ -576,6 +596,13 @@ class Plan:
     def mvm_multi(self, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
         akm_kernel_mvm_multi(self.handle, V, Y, dY_ell, dY_sf, stream)
         return Y, dY_ell, dY_sf
+
+    def mvm_pipelined(self, V, Y=None, dY_ell=None, dY_sf=None, stream=None):
+        akm_kernel_mvm_pipelined(self.handle, V, Y, dY_ell, dY_sf, stream)
+        return Y, dY_ell, dY_sf
+
+    def pipeline_wait(self, stream=None):
+        akm_pipeline_wait(self.handle, stream)
 
     def cross_mvm(self, n_src, V, Yt, stream=None):
         akm_kernel_cross_mvm(self.handle, n_src, V, Yt, stream)

@@ -178,6 +178,17 @@ struct akm_plan {
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   bool use_graphs = true;
 
+  // akm_kernel_mvm_pipelined: two device slots (V in, outputs out) and the copy streams; slot j's
+  // events order the copy-in after the product that last read V[j], the product after the copy-out
+  // that last read O[j], and the copy-out after its product
+  struct Pipe {
+    cudaStream_t cin = nullptr, cout = nullptr;
+    DevBuf V[2], O[2][3];
+    cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
+    bool live[2] = {false, false};
+    int next = 0, last = -1;
+  } pipe;
+
   // profiling (akm_set_profiling / akm_get_stage_times): a ring of event sets, drained lazily
   // e[0] spread start, e[1] spread end, e[5] finish start (== e[1] unless the grids were exchanged
   // between akm_spread_grid and akm_mvm_from_grid), e[2] DFT end, e[3] interpolation end, e[4] end
@@ -223,6 +234,11 @@ struct akm_plan {
     if (own_stream) cudaStreamDestroy(own_stream);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
+    if (pipe.cin) cudaStreamDestroy(pipe.cin);
+    if (pipe.cout) cudaStreamDestroy(pipe.cout);
+    for (int j = 0; j < 2; ++j)
+      for (cudaEvent_t e : {pipe.in_done[j], pipe.comp_done[j], pipe.out_done[j]})
+        if (e) cudaEventDestroy(e);
   }
 
   akm_status fail(akm_status st, const char* fmt, ...) {
@@ -1159,6 +1175,94 @@ static akm_status mvm_entry(akm_plan* plan, const double* V, long long ldv, int 
     }
   }
   if (any_host) AKM_CK(cudaStreamSynchronize(s));
+  return AKM_OK;
+}
+
+// Streaming host batches (include/akm.h akm_kernel_mvm_pipelined): copy-in | product | copy-out on
+// three streams over two device slots, so batch k's outputs go back while batch k+1 is computed.
+akm_status akm_kernel_mvm_pipelined(akm_plan* plan, const double* V, int64_t ldv, int32_t r, double* Y,
+                                    double* dY_ell, double* dY_sf, int64_t ldy, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (!plan->have_points || !plan->have_theta)
+    return plan->fail(AKM_ERR_STATE, "kernel_mvm_pipelined called before set_points and set_theta");
+  if (r < 1 || ldv < r || ldy < r) return plan->fail(AKM_ERR_INVALID_ARG, "bad r/ldv/ldy (r=%d ldv=%lld ldy=%lld)", r, (long long)ldv, (long long)ldy);
+  double* outs[3] = {Y, dY_ell, dY_sf};
+  if (!Y && !dY_ell && !dY_sf) return plan->fail(AKM_ERR_INVALID_ARG, "no output requested");
+  const long long n = plan->n;
+  AKM_CK(cudaSetDevice(plan->device));
+  if (n == 0) return AKM_OK;
+  if (!V || !is_pinned_host(V)) return plan->fail(AKM_ERR_INVALID_ARG, "kernel_mvm_pipelined: V must be pinned host memory");
+  for (int k = 0; k < 3; ++k)
+    if (outs[k] && !is_pinned_host(outs[k]))
+      return plan->fail(AKM_ERR_INVALID_ARG, "kernel_mvm_pipelined: outputs must be pinned host memory");
+  auto& P = plan->pipe;
+  const cudaStream_t s = S(stream);
+  if (!P.cin) {
+    AKM_CK(cudaStreamCreateWithFlags(&P.cin, cudaStreamNonBlocking));
+    AKM_CK(cudaStreamCreateWithFlags(&P.cout, cudaStreamNonBlocking));
+    for (int j = 0; j < 2; ++j) {
+      AKM_CK(cudaEventCreateWithFlags(&P.in_done[j], cudaEventDisableTiming));
+      AKM_CK(cudaEventCreateWithFlags(&P.comp_done[j], cudaEventDisableTiming));
+      AKM_CK(cudaEventCreateWithFlags(&P.out_done[j], cudaEventDisableTiming));
+    }
+  }
+  const int j = P.next;
+  const size_t blk = sizeof(double) * (size_t)n * r;
+  bool grow = P.V[j].bytes < blk;
+  for (int k = 0; k < 3; ++k) grow = grow || (outs[k] && P.O[j][k].bytes < blk);
+  if (grow) {  // a slot in flight is never freed under its copies or product
+    AKM_CK(cudaStreamSynchronize(P.cin));
+    AKM_CK(cudaStreamSynchronize(P.cout));
+    AKM_CK(cudaStreamSynchronize(s));
+    AKM_CK(P.V[j].ensure(blk));
+    for (int k = 0; k < 3; ++k)
+      if (outs[k]) AKM_CK(P.O[j][k].ensure(blk));
+  }
+  double* Vd = P.V[j].as<double>();
+  double* od[3];
+  for (int k = 0; k < 3; ++k) od[k] = outs[k] ? P.O[j][k].as<double>() : nullptr;
+  // small batches (< 4 MiB of V: copies of a few microseconds) keep the copies on the caller's
+  // stream: the cross-stream event handshakes cost more than the overlap hides (c1 / c2 measured
+  // 10% / 1% slower through the copy streams); the host still does not block
+  const char* split_env = std::getenv("AKM_PIPE_SPLIT_MIN_BYTES");  // tests force either mode
+  const bool split = blk >= (split_env ? (size_t)std::atoll(split_env) : (size_t)4 << 20);
+  const cudaStream_t cin = split ? P.cin : s, cout = split ? P.cout : s;
+  // copy-in: slot j is free once the product two calls back has read it
+  if (split && P.live[j]) AKM_CK(cudaStreamWaitEvent(cin, P.comp_done[j], 0));
+  AKM_CK(copy_rows(Vd, sizeof(double) * r, V, sizeof(double) * ldv, sizeof(double) * r, n, cudaMemcpyHostToDevice, cin));
+  // product on the caller's stream (after its earlier work: the plan's workspaces stay ordered)
+  if (split) {
+    AKM_CK(cudaEventRecord(P.in_done[j], cin));
+    AKM_CK(cudaStreamWaitEvent(s, P.in_done[j], 0));
+  }
+  // O[j] is free once the copy-out two calls back has read it (a no-op when that ran on s)
+  if (P.live[j]) AKM_CK(cudaStreamWaitEvent(s, P.out_done[j], 0));
+  akm_status st = run_mvm(plan, Vd, r, r, od[0], od[1], od[2], r, s);
+  if (st != AKM_OK) return st;
+  AKM_CK(cudaEventRecord(P.comp_done[j], s));
+  // copy-out
+  if (split) AKM_CK(cudaStreamWaitEvent(cout, P.comp_done[j], 0));
+  for (int k = 0; k < 3; ++k)
+    if (outs[k])
+      AKM_CK(copy_rows(outs[k], sizeof(double) * ldy, od[k], sizeof(double) * r, sizeof(double) * r, n,
+                       cudaMemcpyDeviceToHost, cout));
+  AKM_CK(cudaEventRecord(P.out_done[j], cout));
+  P.live[j] = true;
+  P.last = j;
+  P.next = j ^ 1;
+  return AKM_OK;
+}
+
+akm_status akm_pipeline_wait(akm_plan* plan, void* stream) {
+  if (!plan) return AKM_ERR_INVALID_ARG;
+  plan->err.clear();
+  if (plan->pipe.last < 0) return AKM_OK;
+  AKM_CK(cudaSetDevice(plan->device));
+  // each slot's last copy-out follows every earlier use of that slot (the product of a call waits for
+  // the copy-out two calls back), and each copy-out follows its product and copy-in
+  for (int j = 0; j < 2; ++j)
+    if (plan->pipe.live[j]) AKM_CK(cudaStreamWaitEvent(S(stream), plan->pipe.out_done[j], 0));
   return AKM_OK;
 }
 
