@@ -395,7 +395,10 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   // S0 on the device (binsort.cu): statistics of every candidate bin edge -> B per window (host, the
   // cost model below) -> bin-major layout, bin starts, work items and the point sort on the device
   const long long total_pts = n * P;
-  long long ch_s = total_pts / (148 * 2);
+  // spreading items of at most ch_s points: about AKM_CHS_WAVES (default 2) items per SM when the
+  // points spread evenly (A/B switch; the clamp below decides at c4 / c5)
+  static const int chs_waves = getenv("AKM_CHS_WAVES") ? std::max(1, atoi(getenv("AKM_CHS_WAVES"))) : 2;
+  long long ch_s = total_pts / (148LL * chs_waves);
   ch_s = std::max(32LL, std::min(4096LL, ch_s));
   const int ch_i = 128;   // per-cell interpolation items (64 thr x 2 pts, or 8 warps x 16 pts on DMMA)
   const int ch_ib = 128;  // per-bin interpolation items: up to 128 points of one bin
