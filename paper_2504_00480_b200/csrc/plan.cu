@@ -399,7 +399,11 @@ static akm_status rebuild_bins(akm_plan* plan, cudaStream_t s) {
   // points spread evenly (A/B switch; the clamp below decides at c4 / c5)
   static const int chs_waves = getenv("AKM_CHS_WAVES") ? std::max(1, atoi(getenv("AKM_CHS_WAVES"))) : 2;
   long long ch_s = total_pts / (148LL * chs_waves);
-  ch_s = std::max(32LL, std::min(4096LL, ch_s));
+  static const long long chs_max = getenv("AKM_CHS_MAX") ? std::max(32LL, atoll(getenv("AKM_CHS_MAX"))) : 8192LL;
+  // 8192: every item costs ~15-25 us of prologue and flush per launch (measured: c4 spreading 7.14 /
+  // 7.01 / 6.91 / 6.85 / 6.83 ms at caps 1024 / 2048 / 4096 / 8192 / 16384, x4 7.13 / 6.99 / 6.89 / 6.80 /
+  // 6.82), and the larger-first order keeps the tail short
+  ch_s = std::max(32LL, std::min(chs_max, ch_s));
   const int ch_i = 128;   // per-cell interpolation items (64 thr x 2 pts, or 8 warps x 16 pts on DMMA)
   const int ch_ib = 128;  // per-bin interpolation items: up to 128 points of one bin
   // item set 0: the square product over all points; set 1: the cross product (spread the class-0
